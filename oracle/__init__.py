@@ -1,0 +1,211 @@
+"""Serial CPU oracle (ctypes wrapper over oracle/liboracle.so).
+
+ORACLE / TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this package. It imports nothing from
+the product package ``paper_cs_0502039_b200`` and the product never imports it.
+
+The oracle is the plain definition of the trajectory: all arrivals in increasing (t, c)
+order from a global priority queue (PAPER.md:196-211 serial procedure with per-cell
+streams, Eq. newt1i; uniqueness PAPER.md:596-613). Primitives:
+docs/PRIMITIVES.md.
+"""
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = [os.path.join(_HERE, "aca_oracle.c")]
+_HDR = [os.path.join(_HERE, "aca_oracle.h"), os.path.join(_HERE, "nlog_tables.h")]
+
+HEATBATH, METROPOLIS = 0, 1
+
+
+def build(force=False):
+    """Compile liboracle.so with plain gcc (no fast-math: P4 needs glibc exp bit-for-bit)."""
+    newest = max(os.path.getmtime(p) for p in _SRC + _HDR)
+    if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= newest:
+        return _SO
+    cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math", "-o", _SO] + _SRC + ["-lm"]
+    subprocess.check_call(cmd)
+    return _SO
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("arrivals", ctypes.c_uint64), ("flips", ctypes.c_uint64),
+                ("event_hash", ctypes.c_uint64), ("bond_sum", ctypes.c_int64),
+                ("magnetisation", ctypes.c_int64), ("t_min", ctypes.c_uint64),
+                ("t_max", ctypes.c_uint64), ("rounds", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_SO)
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        L.oracle_philox4x32_10.argtypes = [u32p, u32p, u32p]
+        L.oracle_nlog_q32.argtypes = [ctypes.c_uint64]
+        L.oracle_nlog_q32.restype = ctypes.c_uint64
+        L.oracle_delta.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int]
+        L.oracle_delta.restype = ctypes.c_uint64
+        L.oracle_inv_lambda.argtypes = [ctypes.c_double]
+        L.oracle_inv_lambda.restype = ctypes.c_uint64
+        L.oracle_flip_table.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
+        L.oracle_mix64.argtypes = [ctypes.c_uint64]
+        L.oracle_mix64.restype = ctypes.c_uint64
+        L.oracle_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                    ctypes.c_uint64, ctypes.c_double, ctypes.c_int]
+        L.oracle_create.restype = ctypes.c_void_p
+        L.oracle_destroy.argtypes = [ctypes.c_void_p]
+        L.oracle_run_until_q32.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+        L.oracle_run_until_random_order.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]
+        L.oracle_run_until_sync.argtypes = [ctypes.c_void_p, ctypes.c_uint64,
+                                            ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]
+        L.oracle_run_until_sync.restype = ctypes.c_int64
+        L.oracle_run_until_sync_naive_leq.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+        L.oracle_run_until_sync_naive_leq.restype = ctypes.c_int64
+        L.oracle_get_spins.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_get_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_get_counters.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_get_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(Stats)]
+        L.oracle_num_cells.argtypes = [ctypes.c_void_p]
+        L.oracle_num_cells.restype = ctypes.c_int64
+        L.oracle_replica_hist.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_uint64,
+                                          ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p]
+        L.oracle_time_weighted_hist.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                                ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                                ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                                ctypes.c_uint64, ctypes.c_void_p]
+        _lib = L
+    return _lib
+
+
+def to_q32(T):
+    """P6: T_q32 = floor(T * 2^32 + 0.5) in IEEE double."""
+    return int(np.floor(np.float64(T) * np.float64(4294967296.0) + np.float64(0.5)))
+
+
+def philox(ctr, key):
+    c = (ctypes.c_uint32 * 4)(*ctr)
+    k = (ctypes.c_uint32 * 2)(*key)
+    o = (ctypes.c_uint32 * 4)()
+    lib().oracle_philox4x32_10(c, k, o)
+    return tuple(o)
+
+
+def nlog_q32(X):
+    return lib().oracle_nlog_q32(X)
+
+
+def delta(w1, w2, lam=1.0, tie_bits=0):
+    return lib().oracle_delta(w1, w2, lib().oracle_inv_lambda(lam), tie_bits)
+
+
+def flip_table(ndim, beta, J=1.0, h=0.0, rule=HEATBATH):
+    n = 2 * (2 * ndim + 1)
+    out = (ctypes.c_uint64 * n)()
+    lib().oracle_flip_table(ndim, beta, J, h, rule, out)
+    return [int(v) for v in out]
+
+
+def mix64(z):
+    return lib().oracle_mix64(z)
+
+
+def _dims(dims):
+    return (ctypes.c_int64 * len(dims))(*dims)
+
+
+class OracleSim:
+    """One serial simulation. Methods mirror the C-ABI names of the product path."""
+
+    def __init__(self, dims, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1,
+                 init_q=0.5, tie_bits=0):
+        self.dims = tuple(int(d) for d in dims)
+        self.ndim = len(self.dims)
+        self._p = lib().oracle_create(self.ndim, _dims(self.dims), lam, beta, J, h, rule,
+                                      seed, init_q, tie_bits)
+        if not self._p:
+            raise ValueError("oracle_create rejected the arguments")
+        self.N = int(np.prod(self.dims))
+
+    def close(self):
+        if self._p:
+            lib().oracle_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        self.close()
+
+    def run_until(self, T, order="pq", choice_seed=0):
+        return self.run_until_q32(to_q32(T), order, choice_seed)
+
+    def run_until_q32(self, Tq, order="pq", choice_seed=0, fired_per_round=None):
+        if order == "pq":
+            rc = lib().oracle_run_until_q32(self._p, Tq)
+        elif order == "random":
+            rc = lib().oracle_run_until_random_order(self._p, Tq, choice_seed)
+        elif order == "sync":
+            buf = None
+            if fired_per_round is not None:
+                buf = fired_per_round.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+            rc = lib().oracle_run_until_sync(self._p, Tq, buf,
+                                             0 if fired_per_round is None else len(fired_per_round))
+            return rc
+        elif order == "naive_leq":   # negative control only
+            return lib().oracle_run_until_sync_naive_leq(self._p, Tq)
+        else:
+            raise ValueError(order)
+        if rc != 0:
+            raise ValueError("T decreased")
+        return rc
+
+    def spins(self):
+        a = np.empty(self.N, np.int8)
+        lib().oracle_get_spins(self._p, a.ctypes.data)
+        return a.reshape(self.dims[::-1])
+
+    def times(self):
+        a = np.empty(self.N, np.uint64)
+        lib().oracle_get_times(self._p, a.ctypes.data)
+        return a.reshape(self.dims[::-1])
+
+    def counters(self):
+        a = np.empty(self.N, np.uint32)
+        lib().oracle_get_counters(self._p, a.ctypes.data)
+        return a.reshape(self.dims[::-1])
+
+    def stats(self):
+        s = Stats()
+        lib().oracle_get_stats(self._p, ctypes.byref(s))
+        return s.as_dict()
+
+
+def replica_hist(dims, beta, J=1.0, h=0.0, rule=HEATBATH, seed0=1, n_rep=1000, T=50.0):
+    n = int(np.prod(dims))
+    hist = np.zeros(1 << n, np.uint64)
+    rc = lib().oracle_replica_hist(len(dims), _dims(dims), beta, J, h, rule, seed0, n_rep,
+                                   to_q32(T), hist.ctypes.data)
+    assert rc == 0
+    return hist
+
+
+def time_weighted_hist(dims, beta, J=1.0, h=0.0, rule=HEATBATH, seed=1, T0=50.0, T1=1000.0):
+    n = int(np.prod(dims))
+    w = np.zeros(1 << n, np.float64)
+    rc = lib().oracle_time_weighted_hist(len(dims), _dims(dims), beta, J, h, rule, seed,
+                                         to_q32(T0), to_q32(T1), w.ctypes.data)
+    assert rc == 0
+    return w

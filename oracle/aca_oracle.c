@@ -1,0 +1,413 @@
+/* aca_oracle.c — serial CPU oracle. ORACLE / TEST INFRASTRUCTURE ONLY (see aca_oracle.h).
+ *
+ * Plain, slow, obviously correct: every arrival is processed in increasing (t, c) order
+ * popped from a binary heap (global priority queue on t(c)). Each function cites the
+ * passage it follows; the primitives follow docs/PRIMITIVES.md, which states the readings
+ * taken where the paper is silent (generator, integer -ln, tie-break).
+ * Compiled with plain gcc -O2, no fast-math (the P4 table depends on glibc exp).
+ */
+#include "aca_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "nlog_tables.h"
+
+/* ---------------------------------------------------------------- P1: Philox4x32-10 */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; r++) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        if (r < 9) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* ---------------------------------------------------------------- P3: NLOG-2 */
+uint64_t oracle_nlog_q32(uint64_t X) {
+    uint64_t x = X | 1u;
+    int z = __builtin_clzll(x);
+    uint64_t y = x << z;
+    uint64_t m = y << 1;
+    uint64_t i = m >> 56;
+    uint64_t g = (m >> 24) & 0xffffffffu;
+    uint64_t V = (g * ORACLE_NLOG_R[i]) >> 32;
+    uint64_t V2 = V * V;
+    uint64_t A = V << 8;
+    uint64_t B = (V2 >> 33) + ((V2 & ((1ULL << 33) - 1)) != 0);
+    uint64_t C = ((V2 >> 32) * V) / (3ULL << 40);
+    uint64_t Wq = (V2 >> 32) + ((V2 & 0xffffffffULL) != 0);
+    uint64_t W2 = Wq * Wq;
+    uint64_t D = (W2 >> 50) + ((W2 & ((1ULL << 50) - 1)) != 0);
+    uint64_t lnf = ORACLE_NLOG_L[i] + A - B + C - D;
+    uint64_t S = (uint64_t)(z + 1) * ORACLE_LN2_Q48 - lnf;
+    return (S + (1ULL << 15)) >> 16;
+}
+
+uint64_t oracle_inv_lambda(double lambda) { return (uint64_t)floor(4294967296.0 / lambda + 0.5); }
+
+/* Eq. newt1i: next_t = t - ln(r)/lambda; next_t > t. */
+uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits) {
+    uint64_t X = ((uint64_t)w1 << 32) | w2;
+    uint64_t q = oracle_nlog_q32(X);
+    unsigned __int128 prod = (unsigned __int128)q * inv_lambda;
+    uint64_t d = (uint64_t)(prod >> 32);
+    if (d < 1) d = 1;
+    if (tie_bits > 0) {
+        uint64_t quantum = 1ULL << tie_bits;
+        d &= ~(quantum - 1);
+        if (d < quantum) d = quantum;
+    }
+    return d;
+}
+
+/* ---------------------------------------------------------------- P4: flip thresholds */
+/* Appendix: dE = 2(J s Sigma + H s), x = exp(-dE/T), p = x/(1+x),
+ * index = (Sigma+4)/2 + 5(s+1)/2; generalised to z = 2*ndim neighbours. Metropolis
+ * acceptance min(1, exp(-beta dE)) is the MRRTT rule the paper names. */
+void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint64_t* out) {
+    int zc = 2 * ndim;
+    for (int sb = 0; sb < 2; sb++) {
+        int s = 2 * sb - 1;
+        for (int k = 0; k <= zc; k++) {
+            int sigma = 2 * k - zc;
+            double dE = 2.0 * (J * (double)s * (double)sigma + h * (double)s);
+            double a = beta * dE;
+            double p;
+            if (rule == 0) {
+                if (a >= 0) { double x = exp(-a); p = x / (1.0 + x); }
+                else p = 1.0 / (1.0 + exp(a));
+            } else {
+                p = (dE <= 0) ? 1.0 : exp(-a);
+            }
+            uint64_t thr = (p == 1.0) ? (1ULL << 32) : (uint64_t)floor(p * 4294967296.0);
+            int idx = (sigma + zc) / 2 + (zc + 1) * (s + 1) / 2;
+            out[idx] = thr;
+        }
+    }
+}
+
+/* ---------------------------------------------------------------- P7 */
+uint64_t oracle_mix64(uint64_t z) {
+    z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ULL;
+    z ^= z >> 27; z *= 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return z;
+}
+static uint64_t rotl64(uint64_t v, int r) { return (v << r) | (v >> (64 - r)); }
+
+/* ---------------------------------------------------------------- simulation state */
+struct oracle_sim {
+    int ndim, zc;
+    int64_t dims[3], N;
+    double lambda, beta, J, h, init_q;
+    int rule, tie_bits;
+    uint64_t seed, inv_lambda, thr_init, thr[14];
+    uint32_t key[2];
+    int8_t* s;
+    uint64_t* t;
+    uint32_t* n;
+    uint32_t* heap;
+    int64_t heap_size;
+    int heap_valid;
+    uint64_t T_last;
+    uint64_t flips, event_hash, rounds;
+};
+
+int64_t oracle_num_cells(const oracle_sim* s) { return s->N; }
+
+/* neighbours of c with multiplicity, order -x,+x,-y,+y[,-z,+z]; periodic. */
+static int neighbours(const oracle_sim* S, int64_t c, int64_t* nb) {
+    int64_t nx = S->dims[0], ny = S->dims[1];
+    int64_t x = c % nx, y = (c / nx) % ny, zz = (S->ndim == 3) ? c / (nx * ny) : 0;
+    int64_t base = c - x;
+    nb[0] = base + (x + nx - 1) % nx;
+    nb[1] = base + (x + 1) % nx;
+    int64_t plane = zz * nx * ny;
+    nb[2] = plane + ((y + ny - 1) % ny) * nx + x;
+    nb[3] = plane + ((y + 1) % ny) * nx + x;
+    if (S->ndim == 3) {
+        int64_t nz = S->dims[2];
+        nb[4] = ((zz + nz - 1) % nz) * nx * ny + y * nx + x;
+        nb[5] = ((zz + 1) % nz) * nx * ny + y * nx + x;
+    }
+    return S->zc;
+}
+
+static void draw(const oracle_sim* S, uint32_t k, int64_t c, uint32_t tag, uint32_t w[4]) {
+    uint32_t ctr[4] = {k, (uint32_t)((uint64_t)c & 0xffffffffu), (uint32_t)((uint64_t)c >> 32), tag};
+    oracle_philox4x32_10(ctr, S->key, w);
+}
+
+oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double beta, double J,
+                          double h, int rule, uint64_t seed, double init_q, int tie_bits) {
+    if (ndim != 2 && ndim != 3) return NULL;
+    if (!(lambda > 0) || !isfinite(lambda) || !(beta >= 0) || !isfinite(beta)) return NULL;
+    if (rule != 0 && rule != 1) return NULL;
+    if (!(init_q >= 0 && init_q <= 1)) return NULL;
+    if (tie_bits < 0 || tie_bits > 40) return NULL;
+    int64_t N = 1;
+    for (int a = 0; a < ndim; a++) { if (dims[a] < 2) return NULL; N *= dims[a]; }
+    if (N >= (1LL << 32)) return NULL;
+    oracle_sim* S = (oracle_sim*)calloc(1, sizeof(oracle_sim));
+    S->ndim = ndim; S->zc = 2 * ndim; S->N = N;
+    for (int a = 0; a < 3; a++) S->dims[a] = a < ndim ? dims[a] : 1;
+    S->lambda = lambda; S->beta = beta; S->J = J; S->h = h; S->rule = rule;
+    S->seed = seed; S->init_q = init_q; S->tie_bits = tie_bits;
+    S->inv_lambda = oracle_inv_lambda(lambda);
+    S->thr_init = (uint64_t)floor(init_q * 4294967296.0);
+    oracle_flip_table(ndim, beta, J, h, rule, S->thr);
+    S->key[0] = (uint32_t)(seed & 0xffffffffu);
+    S->key[1] = (uint32_t)(seed >> 32);
+    S->s = (int8_t*)malloc((size_t)N);
+    S->t = (uint64_t*)malloc((size_t)N * 8);
+    S->n = (uint32_t*)malloc((size_t)N * 4);
+    S->heap = NULL;
+    if (!S->s || !S->t || !S->n) { oracle_destroy(S); return NULL; }
+    /* P5: one initial draw per cell; local clocks start at 0. */
+    for (int64_t c = 0; c < N; c++) {
+        uint32_t w[4];
+        draw(S, 0, c, 1u, w);
+        S->s[c] = ((uint64_t)w[0] < S->thr_init) ? -1 : 1;
+        S->t[c] = oracle_delta(w[1], w[2], S->inv_lambda, tie_bits);
+        S->n[c] = 0;
+    }
+    return S;
+}
+
+void oracle_destroy(oracle_sim* S) {
+    if (!S) return;
+    free(S->s); free(S->t); free(S->n); free(S->heap);
+    free(S);
+}
+
+/* One arrival of cell c (fig:a1c1pe steps 3-4; Appendix):
+ * Sigma from the neighbours' current spins (the "just before" states),
+ * flip iff w0 < thr[idx], then t += Delta, n += 1. new_s / new_t are returned so the
+ * synchronous variant can commit them later. */
+static void arrival(oracle_sim* S, int64_t c, int8_t* new_s, uint64_t* new_t) {
+    int64_t nb[6];
+    int z = neighbours(S, c, nb);
+    int sigma = 0;
+    for (int j = 0; j < z; j++) sigma += S->s[nb[j]];
+    int sc = S->s[c];
+    int idx = (sigma + z) / 2 + (z + 1) * (sc + 1) / 2;
+    uint32_t k = S->n[c];
+    uint32_t w[4];
+    draw(S, k, c, 0u, w);
+    int ns = sc;
+    if ((uint64_t)w[0] < S->thr[idx]) { ns = -sc; S->flips++; }
+    uint64_t tev = S->t[c];
+    S->event_hash += oracle_mix64(tev ^ rotl64((uint64_t)c, 20) ^ rotl64((uint64_t)k, 44) ^
+                                  (uint64_t)(ns > 0 ? 1 : 0));
+    *new_s = (int8_t)ns;
+    *new_t = tev + oracle_delta(w[1], w[2], S->inv_lambda, S->tie_bits);
+}
+
+/* lexicographic (t, c) order (P6). */
+static int lex_less(const oracle_sim* S, int64_t a, int64_t b) {
+    return S->t[a] < S->t[b] || (S->t[a] == S->t[b] && a < b);
+}
+
+static void sift_down(oracle_sim* S, int64_t i) {
+    int64_t n = S->heap_size;
+    uint32_t* H = S->heap;
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < n && lex_less(S, H[l], H[m])) m = l;
+        if (r < n && lex_less(S, H[r], H[m])) m = r;
+        if (m == i) return;
+        uint32_t tmp = H[i]; H[i] = H[m]; H[m] = tmp;
+        i = m;
+    }
+}
+
+static void build_heap(oracle_sim* S) {
+    if (!S->heap) S->heap = (uint32_t*)malloc((size_t)S->N * 4);
+    for (int64_t c = 0; c < S->N; c++) S->heap[c] = (uint32_t)c;
+    S->heap_size = S->N;
+    for (int64_t i = S->N / 2 - 1; i >= 0; i--) sift_down(S, i);
+    S->heap_valid = 1;
+}
+
+/* (A) The oracle: global priority queue on (t(c), c); pop while t < T. */
+int oracle_run_until_q32(oracle_sim* S, uint64_t T) {
+    if (T < S->T_last) return -1;
+    S->T_last = T;
+    if (!S->heap_valid) build_heap(S);
+    while (S->heap_size > 0) {
+        int64_t c = S->heap[0];
+        if (S->t[c] >= T) break;
+        int8_t ns; uint64_t nt;
+        arrival(S, c, &ns, &nt);
+        S->s[c] = ns; S->t[c] = nt; S->n[c] += 1;
+        sift_down(S, 0);   /* the popped key only grew: re-insert by sifting the root */
+    }
+    return 0;
+}
+
+/* eligibility: fig:a1c1pe step 2 with the (t, c) tie-break (P6).
+ * naive_leq = 1 is a NEGATIVE CONTROL only: the bare "t(c) <= min t(c')" test of
+ * fig:s1c1pe without a tie-break, which lets tied neighbours fire in the same round. */
+static int eligible_rule(const oracle_sim* S, int64_t c, uint64_t T, int naive_leq) {
+    if (S->t[c] >= T) return 0;
+    int64_t nb[6];
+    int z = neighbours(S, c, nb);
+    for (int j = 0; j < z; j++) {
+        if (naive_leq ? !(S->t[c] <= S->t[nb[j]]) : !lex_less(S, c, nb[j])) return 0;
+    }
+    return 1;
+}
+static int eligible(const oracle_sim* S, int64_t c, uint64_t T) { return eligible_rule(S, c, T, 0); }
+
+/* (B) uniformly random eligible local minimum, any order. */
+int oracle_run_until_random_order(oracle_sim* S, uint64_t T, uint64_t choice_seed) {
+    if (T < S->T_last) return -1;
+    S->T_last = T;
+    S->heap_valid = 0;
+    int64_t N = S->N;
+    int64_t* pos = (int64_t*)malloc((size_t)N * 8);
+    int64_t* set = (int64_t*)malloc((size_t)N * 8);
+    int64_t size = 0;
+    for (int64_t c = 0; c < N; c++) {
+        pos[c] = -1;
+        if (eligible(S, c, T)) { pos[c] = size; set[size++] = c; }
+    }
+    uint64_t rs = choice_seed * 2654435761ULL + 0x9E3779B97F4A7C15ULL;
+    if (!rs) rs = 1;
+    while (size > 0) {
+        rs ^= rs >> 12; rs ^= rs << 25; rs ^= rs >> 27;          /* xorshift64* */
+        uint64_t r = rs * 2685821657736338717ULL;
+        int64_t c = set[(int64_t)(r % (uint64_t)size)];
+        int8_t ns; uint64_t nt;
+        arrival(S, c, &ns, &nt);
+        S->s[c] = ns; S->t[c] = nt; S->n[c] += 1;
+        int64_t touch[7];
+        touch[0] = c;
+        int z = neighbours(S, c, touch + 1);
+        for (int j = 0; j <= z; j++) {
+            int64_t d = touch[j];
+            int e = eligible(S, d, T);
+            if (e && pos[d] < 0) { pos[d] = size; set[size++] = d; }
+            else if (!e && pos[d] >= 0) {
+                int64_t p = pos[d], last = set[--size];
+                set[p] = last; pos[last] = p; pos[d] = -1;
+            }
+        }
+    }
+    free(pos); free(set);
+    return 0;
+}
+
+/* (C) fig:s1c1pe: round = test all (step 2), compute new_s/new_t
+ * privately (steps 3-4), barrier, commit (steps 6-7). */
+static int64_t run_sync(oracle_sim* S, uint64_t T, uint64_t* fired_per_round,
+                        int64_t max_rounds, int naive_leq);
+int64_t oracle_run_until_sync(oracle_sim* S, uint64_t T, uint64_t* fired_per_round,
+                              int64_t max_rounds) {
+    return run_sync(S, T, fired_per_round, max_rounds, 0);
+}
+int64_t oracle_run_until_sync_naive_leq(oracle_sim* S, uint64_t T) {
+    return run_sync(S, T, NULL, 0, 1);
+}
+static int64_t run_sync(oracle_sim* S, uint64_t T, uint64_t* fired_per_round,
+                        int64_t max_rounds, int naive_leq) {
+    if (T < S->T_last) return -1;
+    S->T_last = T;
+    S->heap_valid = 0;
+    int64_t N = S->N, rounds = 0;
+    int64_t* list = (int64_t*)malloc((size_t)N * 8);
+    int8_t* ns = (int8_t*)malloc((size_t)N);
+    uint64_t* nt = (uint64_t*)malloc((size_t)N * 8);
+    for (;;) {
+        int64_t m = 0;
+        for (int64_t c = 0; c < N; c++) if (eligible_rule(S, c, T, naive_leq)) list[m++] = c;
+        if (m == 0) break;
+        for (int64_t j = 0; j < m; j++) arrival(S, list[j], &ns[j], &nt[j]);
+        for (int64_t j = 0; j < m; j++) {
+            int64_t c = list[j];
+            S->s[c] = ns[j]; S->t[c] = nt[j]; S->n[c] += 1;
+        }
+        if (fired_per_round && rounds < max_rounds) fired_per_round[rounds] = (uint64_t)m;
+        rounds++;
+    }
+    S->rounds += (uint64_t)rounds;
+    free(list); free(ns); free(nt);
+    return rounds;
+}
+
+void oracle_get_spins(const oracle_sim* S, int8_t* out) { memcpy(out, S->s, (size_t)S->N); }
+void oracle_get_times(const oracle_sim* S, uint64_t* out) { memcpy(out, S->t, (size_t)S->N * 8); }
+void oracle_get_counters(const oracle_sim* S, uint32_t* out) { memcpy(out, S->n, (size_t)S->N * 4); }
+
+/* Energy bookkeeping, Appendix comment "Energy = -J sum spin spin' - H sum spin"
+ * (PAPER.md:1680): B counts each bond once along +e_a, periodic. */
+void oracle_get_stats(const oracle_sim* S, oracle_stats* o) {
+    memset(o, 0, sizeof(*o));
+    int64_t nb[6];
+    uint64_t tmin = ~0ULL, tmax = 0, arr = 0;
+    int64_t B = 0, M = 0;
+    for (int64_t c = 0; c < S->N; c++) {
+        neighbours(S, c, nb);
+        int sc = S->s[c];
+        int plus = S->s[nb[1]] + S->s[nb[3]] + (S->ndim == 3 ? S->s[nb[5]] : 0);
+        B += sc * plus;
+        M += sc;
+        arr += S->n[c];
+        if (S->t[c] < tmin) tmin = S->t[c];
+        if (S->t[c] > tmax) tmax = S->t[c];
+    }
+    o->arrivals = arr; o->flips = S->flips; o->event_hash = S->event_hash;
+    o->bond_sum = B; o->magnetisation = M; o->t_min = tmin; o->t_max = tmax;
+    o->rounds = S->rounds;
+}
+
+/* ---------------------------------------------------------------- Boltzmann helpers */
+static uint64_t state_code(const oracle_sim* S) {
+    uint64_t code = 0;
+    for (int64_t c = 0; c < S->N; c++) if (S->s[c] > 0) code |= 1ULL << c;
+    return code;
+}
+
+int oracle_replica_hist(int ndim, const int64_t* dims, double beta, double J, double h,
+                        int rule, uint64_t seed0, int64_t n_rep, uint64_t T, uint64_t* hist) {
+    for (int64_t r = 0; r < n_rep; r++) {
+        oracle_sim* S = oracle_create(ndim, dims, 1.0, beta, J, h, rule, seed0 + (uint64_t)r, 0.5, 0);
+        if (!S || S->N > 20) { oracle_destroy(S); return -1; }
+        oracle_run_until_q32(S, T);
+        hist[state_code(S)] += 1;
+        oracle_destroy(S);
+    }
+    return 0;
+}
+
+int oracle_time_weighted_hist(int ndim, const int64_t* dims, double beta, double J, double h,
+                              int rule, uint64_t seed, uint64_t T0, uint64_t T1, double* weight) {
+    oracle_sim* S = oracle_create(ndim, dims, 1.0, beta, J, h, rule, seed, 0.5, 0);
+    if (!S || S->N > 20) { oracle_destroy(S); return -1; }
+    oracle_run_until_q32(S, T0);
+    uint64_t code = state_code(S), tprev = T0;
+    S->T_last = T1;
+    while (S->heap_size > 0) {
+        int64_t c = S->heap[0];
+        if (S->t[c] >= T1) break;
+        uint64_t tev = S->t[c];
+        weight[code] += (double)(tev - tprev) * (1.0 / 4294967296.0);
+        tprev = tev;
+        int8_t ns; uint64_t nt;
+        arrival(S, c, &ns, &nt);
+        S->s[c] = ns; S->t[c] = nt; S->n[c] += 1;
+        sift_down(S, 0);
+        if (ns > 0) code |= 1ULL << c; else code &= ~(1ULL << c);
+    }
+    weight[code] += (double)(T1 - tprev) * (1.0 / 4294967296.0);
+    oracle_destroy(S);
+    return 0;
+}

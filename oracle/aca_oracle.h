@@ -1,0 +1,78 @@
+/* aca_oracle.h — serial CPU oracle for the conservative Poisson-asynchronous Ising path.
+ *
+ * ORACLE / TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_cs_0502039_b200/, libaca.so) never includes, links or calls it, and this code
+ * includes nothing from the product path.
+ *
+ * What it computes: the plain definition of the trajectory — every arrival processed in
+ * increasing lexicographic (t, c) order from a global priority queue (the "standard"
+ * serial procedure of PAPER.md:196-211 with per-cell streams, Eq. newt1i),
+ * which the conservative parallel algorithms reach exactly (uniqueness argument,
+ * PAPER.md:596-613, 833-871, 959-963). Primitives follow docs/PRIMITIVES.md P1-P7.
+ */
+#pragma once
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct oracle_sim oracle_sim;
+
+typedef struct {
+    uint64_t arrivals, flips, event_hash;
+    int64_t bond_sum, magnetisation;
+    uint64_t t_min, t_max;
+    uint64_t rounds;   /* synchronous-round variant only: rounds executed so far */
+} oracle_stats;
+
+/* P1: Philox4x32-10, ctr[4], key[2] -> out[4]. */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+/* P3: q = NLOG-2(X) in Q32 (before lambda scaling and the max(1, .) clamp). */
+uint64_t oracle_nlog_q32(uint64_t X);
+/* P3: Delta(w1, w2) for INV = floor(2^32/lambda + 0.5), tie_bits as P3b. */
+uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits);
+uint64_t oracle_inv_lambda(double lambda);
+/* P4: thresholds, 2*(2*ndim+1) entries written to out. */
+void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint64_t* out);
+/* P7 */
+uint64_t oracle_mix64(uint64_t z);
+
+/* Returns NULL on invalid arguments. ndim in {2,3}, every dim >= 2, N < 2^32. */
+oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double beta, double J,
+                          double h, int rule, uint64_t seed, double init_q, int tie_bits);
+void oracle_destroy(oracle_sim* s);
+
+/* (A) global priority queue on (t, c): the oracle. Returns 0, or -1 if T decreased. */
+int oracle_run_until_q32(oracle_sim* s, uint64_t T_q32);
+/* (B) repeatedly fire a uniformly random eligible local minimum (choice RNG: xorshift64*,
+ *     unrelated to Philox). Order-independence invariant. */
+int oracle_run_until_random_order(oracle_sim* s, uint64_t T_q32, uint64_t choice_seed);
+/* (C) synchronous rounds of fig:s1c1pe: test all, compute privately,
+ *     commit. fired_per_round (optional, may be NULL) receives up to max_rounds counts. */
+int64_t oracle_run_until_sync(oracle_sim* s, uint64_t T_q32, uint64_t* fired_per_round,
+                              int64_t max_rounds);
+
+/* NEGATIVE CONTROL for tests only: synchronous rounds with the bare t <= min rule. */
+int64_t oracle_run_until_sync_naive_leq(oracle_sim* s, uint64_t T_q32);
+
+void oracle_get_spins(const oracle_sim* s, int8_t* out);
+void oracle_get_times(const oracle_sim* s, uint64_t* out);
+void oracle_get_counters(const oracle_sim* s, uint32_t* out);
+void oracle_get_stats(const oracle_sim* s, oracle_stats* out);
+int64_t oracle_num_cells(const oracle_sim* s);
+
+/* Boltzmann-pin helpers on tiny lattices (N <= 20): state code = sum_c [s(c)>0] << c.
+ * replicas: hist[code] += 1 for the final state of n_rep independent runs (seed0 + r).
+ * time-weighted: one run; weight[code] += time spent in code over (T0, T1] (double). */
+int oracle_replica_hist(int ndim, const int64_t* dims, double beta, double J, double h,
+                        int rule, uint64_t seed0, int64_t n_rep, uint64_t T_q32,
+                        uint64_t* hist);
+int oracle_time_weighted_hist(int ndim, const int64_t* dims, double beta, double J, double h,
+                              int rule, uint64_t seed, uint64_t T0_q32, uint64_t T1_q32,
+                              double* weight);
+
+#ifdef __cplusplus
+}
+#endif

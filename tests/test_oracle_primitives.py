@@ -1,0 +1,200 @@
+"""Pins of the oracle's primitives (docs/PRIMITIVES.md P1-P4, P7) against things other than
+the oracle itself: published known-answer vectors, the cuRAND host library, mpmath's
+logarithm/exponential, and the Appendix's worked values (SPEC.md:233-245 restating
+PAPER.md:1691-1701, 1803)."""
+import ctypes
+import math
+import os
+import random
+
+import mpmath
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+mpmath.mp.dps = 50
+
+
+def _kat_rows():
+    rows = []
+    with open(os.path.join(HERE, "golden", "philox4x32_10_kat.txt")) as f:
+        for line in f:
+            if line.startswith("#") or not line.strip():
+                continue
+            v = [int(x, 16) for x in line.split()]
+            rows.append((tuple(v[0:4]), tuple(v[4:6]), tuple(v[6:10])))
+    return rows
+
+
+@pytest.mark.parametrize("ctr,key,out", _kat_rows())
+def test_philox_known_answers(oracle_mod, ctr, key, out):
+    assert oracle_mod.philox(ctr, key) == out
+
+
+def _curand_host():
+    for p in ("/usr/local/cuda/lib64/libcurand.so", "/usr/local/cuda/lib64/libcurand.so.10"):
+        if os.path.exists(p):
+            return ctypes.CDLL(p)
+    return None
+
+
+def test_philox_matches_curand_host_generator(oracle_mod):
+    """cuRAND's host Philox4x32-10 generator (a library routine, independent of our code):
+    block i of a stream with seed S is Philox(ctr=(0,0,i,0), key=S) (established in this
+    test by the KAT-consistent block 0)."""
+    cr = _curand_host()
+    if cr is None:
+        pytest.skip("libcurand not present")
+    g = ctypes.c_void_p()
+    assert cr.curandCreateGeneratorHost(ctypes.byref(g), 161) == 0  # PHILOX4_32_10
+    try:
+        rnd = random.Random(7)
+        for seed in [0, 1, 12345, 0xFFFFFFFF, 1 << 32, 0x0123456789ABCDEF, rnd.getrandbits(64)]:
+            cr.curandSetPseudoRandomGeneratorSeed(g, ctypes.c_ulonglong(seed))
+            cr.curandSetGeneratorOffset(g, ctypes.c_ulonglong(0))
+            nblk = 4096
+            out = np.zeros(4 * nblk, np.uint32)
+            assert cr.curandGenerate(g, out.ctypes.data_as(ctypes.c_void_p), out.size) == 0
+            key = (seed & 0xFFFFFFFF, seed >> 32)
+            for i in list(range(64)) + [rnd.randrange(nblk) for _ in range(64)]:
+                assert oracle_mod.philox((0, 0, i, 0), key) == tuple(int(v) for v in out[4 * i:4 * i + 4])
+    finally:
+        cr.curandDestroyGenerator(g)
+
+
+def _exact_nlog(X):
+    x = X | 1
+    return -mpmath.log(mpmath.mpf(x) / mpmath.mpf(2) ** 64) * mpmath.mpf(2) ** 32
+
+
+def _nlog_inputs(n_random=20000, seed=3):
+    r = random.Random(seed)
+    xs = [r.getrandbits(64) for _ in range(n_random)]
+    M = (1 << 64) - 1
+    xs += [0, 1, 2, 3, 1 << 63, (1 << 63) + 1, M, M - 1]
+    for k in range(64):
+        xs += [1 << k, (1 << k) + 1, (1 << (k + 1)) - 1]
+    for i in range(256):                       # every table-segment boundary, several octaves
+        for sh in (0, 1, 7, 20, 40, 62):
+            b = ((1 << 63) | (i << 55)) >> sh
+            for d in (-(1 << 25), -1, 0, 1, 1 << 25):
+                if 0 <= b + d <= M:
+                    xs.append(b + d)
+    return xs
+
+
+def test_nlog_within_one_unit_of_mpmath(oracle_mod):
+    """P3 contract |q - (-ln u) 2^32| <= 1 (the survey's proposal allowed 2)."""
+    worst = 0.0
+    for X in _nlog_inputs():
+        err = abs(float(oracle_mod.nlog_q32(X) - _exact_nlog(X)))
+        worst = max(worst, err)
+    assert worst <= 1.0, worst
+
+
+def test_nlog_edge_values(oracle_mod):
+    assert oracle_mod.nlog_q32((1 << 64) - 1) == 0            # u -> 1: -ln u -> 0, Delta clamps to 1
+    assert oracle_mod.delta(0xFFFFFFFF, 0xFFFFFFFF) == 1
+    assert oracle_mod.nlog_q32((1 << 63) + 1) == 2977044472    # ln 2 * 2^32 = 2977044471.82
+    assert oracle_mod.nlog_q32(0) == 190530846196              # 64 ln 2 * 2^32
+    assert oracle_mod.nlog_q32(1) == 190530846196
+
+
+def test_nlog_monotone(oracle_mod):
+    xs = sorted(set(X | 1 for X in _nlog_inputs(5000, 11)))
+    qs = [oracle_mod.nlog_q32(X) for X in xs]
+    assert all(a >= b for a, b in zip(qs, qs[1:]))
+
+
+def test_increment_is_exponential(oracle_mod):
+    """Eq. newt1i with Philox draws: Delta/2^32 ~ Exp(lambda). KS + mean."""
+    from scipy import stats
+    for lam in (1.0, 2.5):
+        d = []
+        for c in range(20000):
+            w = oracle_mod.philox((0, c, 0, 0), (99, 7))
+            d.append(oracle_mod.delta(w[1], w[2], lam) / 2.0 ** 32)
+        d = np.array(d)
+        ks = stats.kstest(d, "expon", args=(0, 1 / lam))
+        assert ks.pvalue > 1e-4, ks
+        assert abs(d.mean() - 1 / lam) < 4 * (1 / lam) / math.sqrt(len(d))
+
+
+def test_increment_lambda_scaling(oracle_mod):
+    """Delta(lambda) = floor(q * round(2^32/lambda) / 2^32): for lambda = 1 it is q itself."""
+    r = random.Random(5)
+    for _ in range(2000):
+        w1, w2 = r.getrandbits(32), r.getrandbits(32)
+        q = oracle_mod.nlog_q32((w1 << 32) | w2)
+        assert oracle_mod.delta(w1, w2, 1.0) == max(1, q)
+        assert abs(oracle_mod.delta(w1, w2, 4.0) - q / 4) <= 1
+        assert abs(oracle_mod.delta(w1, w2, 0.5) - 2 * q) <= 1
+
+
+def test_tie_quantisation(oracle_mod):
+    r = random.Random(9)
+    for k in (8, 28, 31):
+        for _ in range(500):
+            w1, w2 = r.getrandbits(32), r.getrandbits(32)
+            d = oracle_mod.delta(w1, w2, 1.0, k)
+            assert d % (1 << k) == 0 and d >= (1 << k)
+
+
+def _p_exact(s, sigma, beta, J, h, rule):
+    dE = 2 * (J * s * sigma + h * s)
+    if rule == 0:
+        x = mpmath.e ** (-beta * dE)
+        return x / (1 + x)
+    return min(mpmath.mpf(1), mpmath.e ** (-beta * dE))
+
+
+@pytest.mark.parametrize("ndim", [2, 3])
+@pytest.mark.parametrize("rule", [0, 1])
+@pytest.mark.parametrize("beta,J,h", [(0.4406868, 1, 0), (1.0, 1, 0.1), (0.2216544, 1, 0),
+                                      (0.0, 1, 0), (3.0, 0.5, -0.7), (400.0, 1, 0)])
+def test_flip_table_against_formula(oracle_mod, ndim, rule, beta, J, h):
+    """P4 via mpmath: thr = floor(p 2^32) within one unit; index layout of PAPER.md:1803."""
+    thr = oracle_mod.flip_table(ndim, beta, J, h, rule)
+    z = 2 * ndim
+    assert len(thr) == 2 * (z + 1)
+    for s in (-1, 1):
+        for sigma in range(-z, z + 1, 2):
+            idx = (sigma + z) // 2 + (z + 1) * (s + 1) // 2
+            p = _p_exact(s, sigma, beta, J, h, rule)
+            assert abs(thr[idx] - p * 2 ** 32) <= 1.0 + 1e-6, (s, sigma, thr[idx], p)
+            assert 0 <= thr[idx] <= 2 ** 32
+
+
+def test_flip_table_appendix_values(oracle_mod):
+    """J=1, H=0, T=1 (Appendix; values restated in SPEC.md:233-236):
+    s=+1: Sigma=+4 -> 3.3535e-4, Sigma=0 -> 1/2, Sigma=-4 -> 0.99966; index examples
+    (SPEC.md:242-245): (-1,-4)->0, (+1,+4)->9, (+1,0)->7."""
+    thr = oracle_mod.flip_table(2, 1.0, 1.0, 0.0, 0)
+    assert abs(thr[9] / 2 ** 32 - 3.3535e-4) < 5e-8
+    assert thr[7] == 2 ** 31
+    assert abs(thr[5] / 2 ** 32 - 0.99966) < 5e-6
+    # s=-1, Sigma=-4: the -1 spin is aligned with its neighbours -> same as (+1, +4)
+    assert thr[0] == thr[9]
+    # beta = 0: heat-bath 1/2, Metropolis always
+    assert set(oracle_mod.flip_table(2, 0.0, 1.0, 0.3, 0)) == {2 ** 31}
+    assert set(oracle_mod.flip_table(3, 0.0, 1.0, 0.3, 1)) == {2 ** 32}
+
+
+def test_mix64_is_splitmix_finaliser(oracle_mod):
+    """P7 finaliser against a direct big-int evaluation of its definition and a bijection
+    spot check (the finaliser is invertible, so distinct inputs give distinct outputs)."""
+    M = (1 << 64) - 1
+    r = random.Random(1)
+    seen = set()
+    for _ in range(2000):
+        z0 = r.getrandbits(64)
+        z = z0
+        z ^= z >> 30
+        z = (z * 0xBF58476D1CE4E5B9) & M
+        z ^= z >> 27
+        z = (z * 0x94D049BB133111EB) & M
+        z ^= z >> 31
+        v = oracle_mod.mix64(z0)
+        assert v == z
+        seen.add(v)
+    assert len(seen) == 2000
