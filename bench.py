@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the conservative Poisson-asynchronous Ising path (BASELINE.json metric:
+Poisson arrivals processed/s at 1/2/4/8 B200; achieved HBM GB/s vs peak).
+
+One step = the whole hot path on one batch of synthetic input: P5 initialisation on the
+device (aca_reset), aca_run_until(T) (all in-tile rounds / outer rounds / halo exchanges),
+aca_get_stats (device reductions of B, M, arrivals). Default workload: config 3 (2-D
+16384^2 heat-bath at beta_c, T = 20, row strips across the GPUs) — the configuration the
+metric's 1->8 GPU scaling and HBM target are quoted on. State (3.2 GB) >> L2 (126 MB).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+Under torchrun (N > 1) each rank owns a row strip; time = max over ranks; rank 0 prints.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "Poisson arrivals processed/sec"
+UNIT = "arrivals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--seed", type=int, default=workloads.TIMING_SEED)
+    ap.add_argument("--rounds", type=int, default=0, help="in-tile rounds per launch (0 = library default)")
+    ap.add_argument("--tile", type=str, default="", help="e.g. 64x64 or 32x16x8")
+    ap.add_argument("--launches-per-check", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-hash", action="store_true", help="skip the P7 event hash (diagnostics only)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks during the timed region
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy b.copy_(a))"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_tag):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        return d.get(kernel_tag, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def algorithmic_bytes_per_cell(ndim, tile):
+    """Per launch (in-place, 1-cell halo): read word (8 B) + counter (4 B), write both back,
+    plus the halo words of the tile faces. DESIGN.md 'Roofline'."""
+    if ndim == 2:
+        tx, ty = tile[0], tile[1]
+        halo = 8.0 * 2 * (tx + ty) / (tx * ty)
+    else:
+        tx, ty, tz = tile
+        halo = 8.0 * 2 * (tx * ty + ty * tz + tx * tz) / (tx * ty * tz)
+    return 24.0 + halo
+
+
+def oracle_sample(cfg, seconds_target=10.0):
+    """The oracle as it stands on a bounded sample of the workload: same physics (beta, h,
+    rule, init, T) on a smaller lattice, single thread. Returns (arrivals/s, sample text)."""
+    import oracle
+    dims = tuple(cfg["dims"])
+    if len(dims) == 2:
+        side = 1024 if seconds_target >= 8 else 512
+        sdims = (min(dims[0], side), min(dims[1], side // 2 if seconds_target >= 8 else side // 2))
+    else:
+        side = 64 if seconds_target >= 8 else 48
+        sdims = tuple(min(d, side) for d in dims)
+    T = cfg["T"]
+    o = oracle.OracleSim(sdims, lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
+                         seed=1, init_q=cfg["init_q"])
+    t0 = time.perf_counter()
+    o.run_until(T)
+    dt = time.perf_counter() - t0
+    arr = o.stats()["arrivals"]
+    return arr / dt, arr, dt, "oracle (serial PQ, 1 thread) on %s lattice, same beta/h/rule/init, T=%g: %d arrivals in %.2f s" % (
+        "x".join(map(str, sdims)), T, arr, dt)
+
+
+def cpu_name():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (serial CPU) as the reference arm, rank 0 only."""
+    if rank != 0:
+        return
+    cfg = workloads.config(args.config)
+    for _ in range(args.warmup):
+        oracle_sample(cfg, 2.0)
+    tot_arr, tot_t, sample = 0, 0.0, ""
+    for _ in range(args.steps):
+        _, arr, dt, sample = oracle_sample(cfg, 2.0)
+        tot_arr += arr
+        tot_t += dt
+    v = tot_arr / tot_t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": {"workload": args.config + ": " + cfg["note"], "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_name(), "host_cores": os.cpu_count()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_cs_0502039_b200 as aca
+    from paper_cs_0502039_b200 import dist as adist
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = workloads.config(args.config)
+    dims = tuple(cfg["dims"])
+    ndim = len(dims)
+    tile = tuple(int(x) for x in args.tile.split("x")) if args.tile else tuple(cfg["tile"])
+    opts = dict(init_q=cfg["init_q"], device=local, tile=tile, event_hash=0 if args.no_hash else 1)
+    if args.rounds:
+        opts["rounds_per_launch"] = args.rounds
+    if args.launches_per_check:
+        opts["launches_per_check"] = args.launches_per_check
+    stream = torch.cuda.Stream()            # non-default stream: the library captures CUDA graphs on it
+    torch.cuda.set_stream(stream)
+    opts["stream"] = stream.cuda_stream
+    if world > 1:
+        adist.partition(dims, world)
+        uid = aca.aca_nccl_unique_id() if rank == 0 else bytes(128)
+        opts.update(world=world, rank=rank, nccl_id=adist.broadcast_bytes(uid))
+    sim = aca.Sim(dims, lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
+                  seed=args.seed, **opts)
+    n_local = aca.aca_num_cells(sim.handle)
+
+    def step(seed):
+        sim.reset(seed)
+        sim.run_until(cfg["T"])
+        return sim.stats()
+
+    for w in range(args.warmup):
+        step(args.seed + 1000 + w)
+    torch.cuda.synchronize()
+    st0 = sim.stats()
+    clocks = ClockSampler(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    arrivals = tested = fired = launches = kl = 0
+    ks = 0.0
+    for k in range(args.steps):
+        st = step(args.seed + k)
+        arrivals += st["arrivals"]
+        tested += st["cells_tested"]
+        fired += st["cells_fired"]
+        launches += st["launches"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    st1 = sim.stats()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    ks = st1["kernel_seconds"] - st0["kernel_seconds"]
+    kl = st1["kernel_launches"] - st0["kernel_launches"]
+    if world > 1:
+        elapsed = adist.reduce_max(elapsed)
+        arrivals = adist.reduce_sum_int(arrivals)
+    value = arrivals / elapsed
+
+    # roofline of the dominant kernel (the tile kernel): algorithmic bytes / mean launch time
+    peak, peak_src = peaks()
+    bpc = algorithmic_bytes_per_cell(ndim, tile)
+    mean_launch = ks / max(1, launches)
+    achieved = (n_local * bpc / mean_launch) / 1e9 if mean_launch > 0 else None
+    tag = "tile_kernel_%dd" % ndim
+    traffic = ncu_traffic(tag)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "kernel": tag, "peak_source": peak_src,
+            "algorithmic_bytes_per_cell_per_launch": bpc, "cells_per_launch": n_local,
+            "mean_launch_ms": mean_launch * 1e3, "launches_per_step": launches / args.steps,
+            "kernel_share_of_step": ks / elapsed if elapsed else None}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
+                       "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
+                       "tile": list(tile), "rounds_per_launch": args.rounds or 8,
+                       "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
+                       "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
+                       "event_hash": not args.no_hash},
+            "roofline": roof,
+            "firing_fraction": fired / tested if tested else None,
+            "arrivals_per_cell_per_launch": (fired / launches / n_local) if launches else None,
+            "gpu_launches": int(kl + 2 * args.steps),
+            "clocks": clk}
+
+    # end-to-end through the public API with host buffers: H2D of the initial spins,
+    # run, stats, D2H of the final spins, every step
+    if not args.no_e2e:
+        import torch as _t
+        host_in = _t.from_numpy(workloads.host_spins((n_local,), seed=7)).pin_memory()
+        host_out = _t.empty(n_local, dtype=_t.int8).pin_memory()
+        e_arr = 0
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            sim.reset(args.seed + k)
+            aca.aca_set_spins(sim.handle, host_in)
+            sim.run_until(cfg["T"])
+            e_arr += sim.stats()["arrivals"]
+            aca.aca_get_spins(sim.handle, host_out)
+        torch.cuda.synchronize()
+        et = time.perf_counter() - t0
+        if world > 1:
+            et = adist.reduce_max(et)
+            e_arr = adist.reduce_sum_int(e_arr)
+        line["e2e"] = {"value": e_arr / et, "unit": UNIT, "h2d_bytes_per_step": int(n_local),
+                       "d2h_bytes_per_step": int(n_local) + 8 * 13}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, arr, dt, sample = oracle_sample(cfg)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                                "cpu": cpu_name(), "host_cores": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/* aca.h — C ABI of the B200-native conservative simulator of Poisson-asynchronous
+ * cellular arrays (Lubachevsky, "Efficient Parallel Simulations of Asynchronous Cellular
+ * Arrays", arXiv cs/0502039; the reference text is PAPER.md).
+ *
+ * The calls follow the paper's problem statement: a periodic lattice of cells, each with a
+ * state s(c) and a local time t(c); Poisson arrivals of rate lambda
+ * (Eq. newt1i); next_state from the neighbourhood just before the arrival
+ * (Eq. newst), here continuous-time Glauber / Metropolis Ising
+ * (Appendix); simulate until end_time
+ * (fig:a1c1pe). All arithmetic on the path is integer and follows
+ * docs/PRIMITIVES.md (P1 Philox4x32-10, P3 NLOG-2, P4 threshold table, P5 init, P6 (t, c)
+ * tie-break, P7 event hash), so results are bit-identical to the serial oracle for every
+ * tile shape, rounds-per-launch and shard count.
+ *
+ * Conventions
+ *   - Return codes: ACA_OK (0) or a negative ACA_E* code; aca_last_error() then returns a
+ *     thread-local message. No function throws across the ABI.
+ *   - Host buffers passed to getters/setters are owned by the caller; `count` must equal
+ *     the number of cells of the handle (whole lattice; for a multi-process handle the
+ *     rank's own rows), else ACA_EINVAL. Layout: row-major, x fastest:
+ *     c = y*nx + x (2-D), c = (z*ny + y)*nx + x (3-D).
+ *   - All device memory is owned by the library (cudaMalloc at create, freed by destroy).
+ *   - Getters synchronise the handle's stream. One handle per host thread at a time.
+ *   - There is no CPU fallback: without a CUDA device aca_create returns ACA_ENODEV.
+ */
+#ifndef ACA_H
+#define ACA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aca_sim aca_sim; /* opaque, library-owned */
+
+enum { ACA_HEATBATH = 0, ACA_METROPOLIS = 1 };
+
+enum {
+    ACA_OK = 0,
+    ACA_EINVAL = -1, /* invalid argument (message names it) */
+    ACA_ENOMEM = -2, /* device or host allocation failed */
+    ACA_ECUDA = -3,  /* a CUDA call failed (message has the CUDA error string) */
+    ACA_ENCCL = -4,  /* NCCL unavailable or a NCCL call failed */
+    ACA_ESTATE = -5, /* call out of order (e.g. T decreased) or invariant violated */
+    ACA_ERANGE = -6, /* times would overflow the packed 64-bit word */
+    ACA_ENODEV = -7  /* no CUDA device */
+};
+
+typedef struct {
+    uint32_t struct_size;       /* = sizeof(aca_options); checked */
+    double init_q;              /* P5: probability that s0(c) = -1 (default 0.5) */
+    int32_t tile[3];            /* CTA tile (x, y, z); 0 = default (64x64, 32x16x8) */
+    int32_t rounds_per_launch;  /* R_max in-tile rounds per launch (0 = default 8) */
+    int32_t launches_per_check; /* K launches between host checks of termination (0 = 16) */
+    int32_t tie_bits;           /* P3b tie-stress quantisation (0 = off) */
+    int32_t sync_rounds;        /* 1: exact fig:s1c1pe two-phase rounds */
+    int32_t device;             /* CUDA device ordinal; -1 = current device */
+    int32_t shards;             /* virtual row/plane shards on this device (default 1) */
+    int32_t rank, world;        /* multi-process strips: this rank of `world` (default 0, 1) */
+    const void* nccl_id;        /* world > 1: 128-byte ncclUniqueId shared by all ranks */
+    void* stream;               /* cudaStream_t to run on; NULL = library-owned stream */
+    int32_t event_hash;         /* 1 (default): accumulate the P7 event hash */
+    int32_t whole_lattice;      /* 1: one CTA holds the whole lattice with periodic
+                                   addressing and runs to completion in one launch
+                                   (small lattices, config 1); 0 = auto, -1 = never */
+} aca_options;
+
+typedef struct {
+    uint64_t arrivals;      /* sum_c n(c) */
+    uint64_t flips;         /* arrivals that changed the spin */
+    uint64_t event_hash;    /* P7 */
+    int64_t bond_sum;       /* B = sum_c s(c) sum_a s(c + e_a) (periodic) */
+    int64_t magnetisation;  /* M = sum_c s(c) */
+    uint64_t t_min, t_max;  /* over pending arrival times, Q32 */
+    uint64_t launches;      /* tile-kernel launches that did work */
+    uint64_t inner_rounds;  /* sum over launches of the max in-tile rounds executed */
+    uint64_t cells_tested;  /* eligibility tests of cells with t < T */
+    uint64_t cells_fired;   /* = arrivals processed by the kernels */
+    double gpu_seconds;     /* CUDA-event time inside aca_run_until calls */
+    double kernel_seconds;  /* CUDA-event time of the kernel batches alone */
+    uint64_t kernel_launches; /* every tile-kernel launch issued (incl. no-op tail) */
+} aca_stats;
+
+/* Fill *opt with defaults (struct_size set). */
+int aca_default_options(aca_options* opt);
+
+/* Create a simulation and initialise it on the device (P5: one Philox draw per cell).
+ * ndim in {2, 3}; dims[a] >= 2; periodic must be 1;
+ * lambda > 0 finite; beta >= 0 finite; rule ACA_HEATBATH or ACA_METROPOLIS;
+ * opt may be NULL (defaults). On success *out owns device memory until aca_destroy. */
+int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, double lambda,
+               double beta, double J, double h, int rule, uint64_t seed, const aca_options* opt);
+
+/* Process every arrival with t < T (strict). T_q32 = floor(T*2^32 + 0.5).
+ * Successive calls must have non-decreasing T (else ACA_ESTATE) and compose exactly. */
+int aca_run_until(aca_sim* s, double T);
+int aca_run_until_q32(aca_sim* s, uint64_t T_q32);
+
+/* Copy the current state to caller-owned host memory (count = cells). */
+int aca_get_spins(aca_sim* s, int8_t* out, size_t count);
+int aca_get_times(aca_sim* s, uint64_t* out, size_t count);   /* pending arrival, Q32 */
+int aca_get_counters(aca_sim* s, uint32_t* out, size_t count); /* n(c) */
+/* Statistics (device reductions; synchronises). */
+int aca_get_stats(aca_sim* s, aca_stats* out);
+/* P4 table: count = 10 (2-D) or 14 (3-D), index (Sigma+z)/2 + (z+1)(s+1)/2. */
+int aca_get_flip_table(const aca_sim* s, uint64_t* thr, size_t count);
+
+/* Replace the state from host arrays (checkpoint / resume). Every t must be >= 1 and
+ * below the packed-word limit, spins +-1. */
+int aca_set_state(aca_sim* s, const int8_t* spins, const uint64_t* times,
+                  const uint32_t* counters, size_t count);
+/* Replace only the spins (user-supplied initial configuration); times/counters keep
+ * their P5 values. */
+int aca_set_spins(aca_sim* s, const int8_t* spins, size_t count);
+
+/* Re-initialise (P5) with `seed`: fresh state, counters and statistics, T back to 0.
+ * Used to repeat a workload without re-allocating (benchmark steps). Asynchronous. */
+int aca_reset(aca_sim* s, uint64_t seed);
+
+void aca_destroy(aca_sim* s);
+const char* aca_last_error(void);
+
+/* Multi-process setup: write a fresh 128-byte ncclUniqueId (rank 0 calls this and shares
+ * the bytes with the other ranks, e.g. through torch.distributed). NCCL is resolved at run
+ * time from the process (the library does not link it); ACA_ENCCL if unavailable. */
+int aca_nccl_unique_id(void* out128);
+
+/* Number of cells of the handle (rank-local for multi-process handles). */
+int64_t aca_num_cells(const aca_sim* s);
+
+/* ---- Self-test hooks (device primitives through the ABI; host buffers, n elements) ----
+ * P1: out[4n] = our Philox(ctr[4i..], key[2i..]); ref[4n] = cuRAND's device
+ *     curand_Philox4x32_10 on the same inputs (library reference for the pin). */
+int aca_selftest_philox(uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out,
+                        uint32_t* ref);
+/* P3: q[i] = NLOG-2(X[i]); delta[i] = Delta(X[i]) for inv_lambda, tie_bits. */
+int aca_selftest_nlog(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* delta,
+                      uint64_t inv_lambda, int tie_bits);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ACA_H */

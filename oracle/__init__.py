@@ -88,6 +88,10 @@ def lib():
                                                 ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                                 ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                                 ctypes.c_uint64, ctypes.c_void_p]
+        L.oracle_nlog_batch.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_cell_time_counter.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                               ctypes.c_uint64, ctypes.c_int,
+                                               ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)]
         _lib = L
     return _lib
 
@@ -107,6 +111,22 @@ def philox(ctr, key):
 
 def nlog_q32(X):
     return lib().oracle_nlog_q32(X)
+
+
+def nlog_batch(X):
+    X = np.ascontiguousarray(X, np.uint64)
+    q = np.empty_like(X)
+    lib().oracle_nlog_batch(X.size, X.ctypes.data, q.ctypes.data)
+    return q
+
+
+def cell_time_counter(seed, c, T, lam=1.0, tie_bits=0):
+    """(t, n) of cell c after run_until(T) from its own stream (state independence)."""
+    t = ctypes.c_uint64()
+    n = ctypes.c_uint32()
+    lib().oracle_cell_time_counter(seed, c, to_q32(T), lib().oracle_inv_lambda(lam), tie_bits,
+                                   ctypes.byref(t), ctypes.byref(n))
+    return t.value, n.value
 
 
 def delta(w1, w2, lam=1.0, tie_bits=0):

@@ -411,3 +411,28 @@ int oracle_time_weighted_hist(int ndim, const int64_t* dims, double beta, double
     oracle_destroy(S);
     return 0;
 }
+
+/* ---------------------------------------------------------------- per-cell closed forms */
+void oracle_nlog_batch(int64_t n, const uint64_t* X, uint64_t* q) {
+    for (int64_t i = 0; i < n; i++) q[i] = oracle_nlog_q32(X[i]);
+}
+
+/* Arrival times are state-independent for Ising: cell c's pending
+ * time and counter after run_until(T) follow from its own stream alone. */
+void oracle_cell_time_counter(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_t inv_lambda,
+                              int tie_bits, uint64_t* t_out, uint32_t* n_out) {
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {0, (uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 1u};
+    uint32_t w[4];
+    oracle_philox4x32_10(ctr, key, w);
+    uint64_t t = oracle_delta(w[1], w[2], inv_lambda, tie_bits);
+    uint32_t k = 0;
+    while (t < T_q32) {
+        uint32_t ce[4] = {k, (uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 0u};
+        oracle_philox4x32_10(ce, key, w);
+        t += oracle_delta(w[1], w[2], inv_lambda, tie_bits);
+        k++;
+    }
+    *t_out = t;
+    *n_out = k;
+}

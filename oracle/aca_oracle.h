@@ -2,7 +2,7 @@
  *
  * ORACLE / TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
  * cpu_baseline / --impl reference legs may load this library. The product path
- * (paper_cs_0502039_b200/, libaca.so) never includes, links or calls it, and this code
+ * (the CUDA package and its shared library) never includes, links or calls it, and this code
  * includes nothing from the product path.
  *
  * What it computes: the plain definition of the trajectory — every arrival processed in
@@ -72,6 +72,11 @@ int oracle_replica_hist(int ndim, const int64_t* dims, double beta, double J, do
 int oracle_time_weighted_hist(int ndim, const int64_t* dims, double beta, double J, double h,
                               int rule, uint64_t seed, uint64_t T0_q32, uint64_t T1_q32,
                               double* weight);
+
+/* Batch P3, and the per-cell closed form of (t, n) after run_until(T). */
+void oracle_nlog_batch(int64_t n, const uint64_t* X, uint64_t* q);
+void oracle_cell_time_counter(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_t inv_lambda,
+                              int tie_bits, uint64_t* t_out, uint32_t* n_out);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,288 @@
+"""Python binding of libaca.so (include/aca.h) — argument marshalling only.
+
+Every step of the simulation runs in the CUDA kernels behind the C ABI; this module only
+converts arguments (ctypes) and raises on non-zero return codes. There is no CPU fallback:
+if libaca.so is missing or no CUDA device is present the calls fail loudly.
+
+Names follow the C ABI: aca_create, aca_run_until, aca_get_spins/times/counters/stats, ...
+`Sim` is a small convenience wrapper over the same calls.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_PKG, "libaca.so")
+
+ACA_HEATBATH, ACA_METROPOLIS = 0, 1
+ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: "ACA_ENCCL",
+          -5: "ACA_ESTATE", -6: "ACA_ERANGE", -7: "ACA_ENODEV"}
+
+# symbols declared in include/aca.h (checked by tests/test_abi.py)
+EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
+           "aca_get_times", "aca_get_counters", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
+           "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
+           "aca_selftest_nlog"]
+
+
+class AcaError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("%s: %s" % (ERRORS.get(code, code), msg))
+        self.code = code
+
+
+class aca_options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("init_q", ctypes.c_double),
+                ("tile", ctypes.c_int32 * 3), ("rounds_per_launch", ctypes.c_int32),
+                ("launches_per_check", ctypes.c_int32), ("tie_bits", ctypes.c_int32),
+                ("sync_rounds", ctypes.c_int32), ("device", ctypes.c_int32), ("shards", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("stream", ctypes.c_void_p), ("event_hash", ctypes.c_int32),
+                ("whole_lattice", ctypes.c_int32)]
+
+
+class aca_stats(ctypes.Structure):
+    _fields_ = [("arrivals", ctypes.c_uint64), ("flips", ctypes.c_uint64), ("event_hash", ctypes.c_uint64),
+                ("bond_sum", ctypes.c_int64), ("magnetisation", ctypes.c_int64), ("t_min", ctypes.c_uint64),
+                ("t_max", ctypes.c_uint64), ("launches", ctypes.c_uint64), ("inner_rounds", ctypes.c_uint64),
+                ("cells_tested", ctypes.c_uint64), ("cells_fired", ctypes.c_uint64),
+                ("gpu_seconds", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
+                ("kernel_launches", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def library_path():
+    return _SO
+
+
+def lib():
+    """Load libaca.so (building it first if the sources are newer and nvcc is present)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_SO):
+        from . import _build
+        _build.build()
+    L = ctypes.CDLL(_SO)
+    vp, i64p = ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64)
+    L.aca_default_options.argtypes = [ctypes.POINTER(aca_options)]
+    L.aca_create.argtypes = [ctypes.POINTER(vp), ctypes.c_int, i64p, ctypes.c_int, ctypes.c_double,
+                             ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_uint64,
+                             ctypes.POINTER(aca_options)]
+    L.aca_run_until.argtypes = [vp, ctypes.c_double]
+    L.aca_run_until_q32.argtypes = [vp, ctypes.c_uint64]
+    for n in ("aca_get_spins", "aca_get_times", "aca_get_counters", "aca_set_spins"):
+        getattr(L, n).argtypes = [vp, vp, ctypes.c_size_t]
+    L.aca_get_stats.argtypes = [vp, ctypes.POINTER(aca_stats)]
+    L.aca_get_flip_table.argtypes = [vp, vp, ctypes.c_size_t]
+    L.aca_set_state.argtypes = [vp, vp, vp, vp, ctypes.c_size_t]
+    L.aca_reset.argtypes = [vp, ctypes.c_uint64]
+    L.aca_nccl_unique_id.argtypes = [vp]
+    L.aca_destroy.argtypes = [vp]
+    L.aca_destroy.restype = None
+    L.aca_last_error.restype = ctypes.c_char_p
+    L.aca_num_cells.argtypes = [vp]
+    L.aca_num_cells.restype = ctypes.c_int64
+    L.aca_selftest_philox.argtypes = [ctypes.c_uint64, vp, vp, vp, vp]
+    L.aca_selftest_nlog.argtypes = [ctypes.c_uint64, vp, vp, vp, ctypes.c_uint64, ctypes.c_int]
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != 0:
+        raise AcaError(rc, lib().aca_last_error().decode())
+    return rc
+
+
+def aca_default_options(**kw):
+    o = aca_options()
+    _check(lib().aca_default_options(ctypes.byref(o)))
+    for k, v in kw.items():
+        if k == "tile":
+            for i, t in enumerate(v):
+                o.tile[i] = int(t)
+        elif k == "nccl_id" and isinstance(v, (bytes, bytearray)):
+            o._nccl_buf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(v))   # kept alive with o
+            o.nccl_id = ctypes.cast(o._nccl_buf, ctypes.c_void_p)
+        else:
+            setattr(o, k, v)
+    return o
+
+
+def aca_create(dims, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=ACA_HEATBATH, seed=1, periodic=1, options=None):
+    dims = [int(d) for d in dims]
+    arr = (ctypes.c_int64 * len(dims))(*dims)
+    p = ctypes.c_void_p()
+    opt = options if options is not None else aca_default_options()
+    _check(lib().aca_create(ctypes.byref(p), len(dims), arr, periodic, lam, beta, J, h, rule, seed,
+                            ctypes.byref(opt)))
+    return p
+
+
+def aca_run_until(p, T):
+    return _check(lib().aca_run_until(p, float(T)))
+
+
+def aca_run_until_q32(p, Tq):
+    return _check(lib().aca_run_until_q32(p, int(Tq)))
+
+
+def aca_num_cells(p):
+    return int(lib().aca_num_cells(p))
+
+
+def _ptr(a):
+    if hasattr(a, "data_ptr"):          # torch tensor (e.g. pinned host buffer)
+        return ctypes.c_void_p(a.data_ptr())
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def aca_get_spins(p, out=None):
+    n = aca_num_cells(p)
+    out = np.empty(n, np.int8) if out is None else out
+    _check(lib().aca_get_spins(p, _ptr(out), n))
+    return out
+
+
+def aca_get_times(p, out=None):
+    n = aca_num_cells(p)
+    out = np.empty(n, np.uint64) if out is None else out
+    _check(lib().aca_get_times(p, _ptr(out), n))
+    return out
+
+
+def aca_get_counters(p, out=None):
+    n = aca_num_cells(p)
+    out = np.empty(n, np.uint32) if out is None else out
+    _check(lib().aca_get_counters(p, _ptr(out), n))
+    return out
+
+
+def aca_get_stats(p):
+    s = aca_stats()
+    _check(lib().aca_get_stats(p, ctypes.byref(s)))
+    return s.as_dict()
+
+
+def aca_get_flip_table(p, ndim):
+    n = 2 * (2 * ndim + 1)
+    a = (ctypes.c_uint64 * n)()
+    _check(lib().aca_get_flip_table(p, a, n))
+    return [int(v) for v in a]
+
+
+def aca_set_state(p, spins, times, counters):
+    spins = np.ascontiguousarray(spins, np.int8).ravel()
+    times = np.ascontiguousarray(times, np.uint64).ravel()
+    counters = np.ascontiguousarray(counters, np.uint32).ravel()
+    _check(lib().aca_set_state(p, _ptr(spins), _ptr(times), _ptr(counters), spins.size))
+
+
+def aca_set_spins(p, spins):
+    if not hasattr(spins, "data_ptr"):
+        spins = np.ascontiguousarray(spins, np.int8).ravel()
+        n = spins.size
+    else:
+        n = spins.numel()
+    _check(lib().aca_set_spins(p, _ptr(spins), n))
+
+
+def aca_reset(p, seed):
+    return _check(lib().aca_reset(p, int(seed)))
+
+
+def aca_nccl_unique_id():
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().aca_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def aca_destroy(p):
+    if p:
+        lib().aca_destroy(p)
+
+
+def aca_selftest_philox(ctr, key):
+    ctr = np.ascontiguousarray(ctr, np.uint32)
+    key = np.ascontiguousarray(key, np.uint32)
+    n = ctr.shape[0]
+    out = np.empty((n, 4), np.uint32)
+    ref = np.empty((n, 4), np.uint32)
+    _check(lib().aca_selftest_philox(n, _ptr(ctr), _ptr(key), _ptr(out), _ptr(ref)))
+    return out, ref
+
+
+def aca_selftest_nlog(X, lam=1.0, tie_bits=0):
+    X = np.ascontiguousarray(X, np.uint64)
+    q = np.empty_like(X)
+    d = np.empty_like(X)
+    inv = int(np.floor(4294967296.0 / lam + 0.5))
+    _check(lib().aca_selftest_nlog(X.size, _ptr(X), _ptr(q), _ptr(d), inv, tie_bits))
+    return q, d
+
+
+class Sim:
+    """Convenience wrapper: one aca_sim handle."""
+
+    def __init__(self, dims, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=ACA_HEATBATH, seed=1, **opts):
+        self.dims = tuple(int(d) for d in dims)
+        self.ndim = len(self.dims)
+        self.options = aca_default_options(**opts)
+        self._p = aca_create(self.dims, lam, beta, J, h, rule, seed, options=self.options)
+
+    @property
+    def handle(self):
+        return self._p
+
+    def close(self):
+        if self._p:
+            aca_destroy(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run_until(self, T):
+        aca_run_until(self._p, T)
+
+    def reset(self, seed):
+        aca_reset(self._p, seed)
+
+    def run_until_q32(self, Tq):
+        aca_run_until_q32(self._p, Tq)
+
+    def _shape(self, a):
+        n = aca_num_cells(self._p)
+        full = int(np.prod(self.dims))
+        return a.reshape(self.dims[::-1]) if n == full else a
+
+    def spins(self):
+        return self._shape(aca_get_spins(self._p))
+
+    def times(self):
+        return self._shape(aca_get_times(self._p))
+
+    def counters(self):
+        return self._shape(aca_get_counters(self._p))
+
+    def stats(self):
+        return aca_get_stats(self._p)
+
+    def flip_table(self):
+        return aca_get_flip_table(self._p, self.ndim)
+
+    def set_state(self, spins, times, counters):
+        aca_set_state(self._p, spins, times, counters)
+
+    def set_spins(self, spins):
+        aca_set_spins(self._p, spins)

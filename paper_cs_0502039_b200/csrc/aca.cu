@@ -1,0 +1,913 @@
+// aca.cu — C-ABI runtime of the B200 path (include/aca.h). Host side: validation, P4 table,
+// device allocation, shard/halo bookkeeping, the outer-round loop (CUDA-graph replay of K
+// launches, device-side termination), statistics and getters. Every step of the method
+// runs in the kernels of aca_kernels.cuh; nothing here computes a trajectory.
+#include <cuda_runtime.h>
+#include <curand_kernel.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/aca.h"
+#include "aca_kernels.cuh"
+#include "nlog_tables.cuh"
+
+using namespace aca;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(ACA_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),    \
+                        __FILE__, __LINE__);                                                  \
+    } while (0)
+
+// ---------------------------------------------------------------- NCCL (resolved at runtime)
+// The library never links NCCL; when world > 1 it resolves the symbols of the libnccl that
+// the process already loaded (torch's), so the halo exchange uses the same NCCL as the
+// process group that distributed the ncclUniqueId.
+typedef struct { char internal[128]; } ncclUniqueId_t;
+typedef void* ncclComm_t;
+typedef int (*ncclCommInitRank_fn)(ncclComm_t*, int, ncclUniqueId_t, int);
+typedef int (*ncclCommDestroy_fn)(ncclComm_t);
+typedef int (*ncclSend_fn)(const void*, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*ncclRecv_fn)(void*, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*ncclGroup_fn)(void);
+typedef int (*ncclAllReduce_fn)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef const char* (*ncclGetErrorString_fn)(int);
+typedef int (*ncclGetUniqueId_fn)(ncclUniqueId_t*);
+struct NcclApi {
+    ncclCommInitRank_fn init = nullptr;
+    ncclCommDestroy_fn destroy = nullptr;
+    ncclSend_fn send = nullptr;
+    ncclRecv_fn recv = nullptr;
+    ncclGroup_fn gstart = nullptr, gend = nullptr;
+    ncclAllReduce_fn allreduce = nullptr;
+    ncclGetErrorString_fn errstr = nullptr;
+    ncclGetUniqueId_fn uid = nullptr;
+    bool ok = false;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen(nullptr, RTLD_NOW);
+        auto sym = [&](const char* n) -> void* {
+            void* p = h ? dlsym(h, n) : nullptr;
+            if (!p) {
+                static void* lib = nullptr;
+                if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+                if (lib) p = dlsym(lib, n);
+            }
+            return p;
+        };
+        api.init = (ncclCommInitRank_fn)sym("ncclCommInitRank");
+        api.destroy = (ncclCommDestroy_fn)sym("ncclCommDestroy");
+        api.send = (ncclSend_fn)sym("ncclSend");
+        api.recv = (ncclRecv_fn)sym("ncclRecv");
+        api.gstart = (ncclGroup_fn)sym("ncclGroupStart");
+        api.gend = (ncclGroup_fn)sym("ncclGroupEnd");
+        api.allreduce = (ncclAllReduce_fn)sym("ncclAllReduce");
+        api.errstr = (ncclGetErrorString_fn)sym("ncclGetErrorString");
+        api.uid = (ncclGetUniqueId_fn)sym("ncclGetUniqueId");
+        api.ok = api.init && api.destroy && api.send && api.recv && api.gstart && api.gend && api.allreduce;
+    }
+    return api;
+}
+constexpr int NCCL_UINT8 = 1, NCCL_UINT64 = 5, NCCL_INT64 = 4, NCCL_SUM = 0, NCCL_MIN = 3, NCCL_MAX = 2;
+
+struct Shard {
+    Geo g{};
+    unsigned long long* words = nullptr;
+    unsigned int* cnt = nullptr;
+    unsigned long long* halo_lo = nullptr;  // 1 row (2-D) / plane (3-D)
+    unsigned long long* halo_hi = nullptr;
+    Ctl* ctl = nullptr;
+    size_t n = 0;          // owned cells
+    size_t face = 0;       // cells of one row / plane of the sharded axis
+    int tiles_x = 1, tiles_y = 1, tiles_z = 1;
+};
+
+}  // namespace
+
+struct aca_sim {
+    int ndim = 2;
+    int64_t dims[3] = {1, 1, 1};
+    int64_t N = 0;          // whole lattice
+    double lambda = 1, beta = 0, J = 1, h = 0;
+    int rule = 0;
+    uint64_t seed = 0;
+    aca_options opt{};
+    int device = 0;
+    int SH = 1;
+    unsigned long long inv_lambda = 1ull << 32;
+    unsigned long long thr[14] = {};
+    unsigned long long thr_init = 0;
+    unsigned long long max_delta = 0;
+    uint64_t T_last = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    unsigned long long* d_lr = nullptr;
+    std::vector<Shard> shards;
+    int G = 1;                     // shards on this device
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    int tile[3] = {64, 64, 1};
+    int rounds = 8;
+    int K = 16;
+    bool whole = false;
+    bool sync = false;
+    size_t smem_tile = 0, smem_whole = 0;
+    void* kern = nullptr;          // selected tile/whole kernel
+    int nthreads = 256;
+    cudaGraphExec_t graph = nullptr;
+    int graph_rounds = 0;
+    Ctl* h_ctl = nullptr;          // pinned mirror (per shard)
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t evb[2][3] = {};    // per in-flight batch: start, end of kernels, end of ctl copy
+    unsigned long long* d_flag = nullptr;
+    unsigned long long* h_flag = nullptr;
+    double gpu_seconds = 0;
+    double kernel_seconds = 0;
+    uint64_t kernel_launches = 0;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    StatAcc* d_stat = nullptr;
+    StatAcc* h_stat = nullptr;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- P4 table (host, double)
+// Appendix PAPER.md:1691-1701 generalised (docs/PRIMITIVES.md P4).
+void flip_table(int ndim, double beta, double J, double h, int rule, unsigned long long* out) {
+    const int zc = 2 * ndim;
+    for (int sb = 0; sb < 2; ++sb) {
+        const int s = 2 * sb - 1;
+        for (int k = 0; k <= zc; ++k) {
+            const int sigma = 2 * k - zc;
+            const double dE = 2.0 * (J * (double)s * (double)sigma + h * (double)s);
+            const double a = beta * dE;
+            double p;
+            if (rule == ACA_HEATBATH) {
+                if (a >= 0) {
+                    const double x = std::exp(-a);
+                    p = x / (1.0 + x);
+                } else {
+                    p = 1.0 / (1.0 + std::exp(a));
+                }
+            } else {
+                p = (dE <= 0) ? 1.0 : std::exp(-a);
+            }
+            const unsigned long long thr =
+                (p == 1.0) ? (1ull << 32) : (unsigned long long)std::floor(p * 4294967296.0);
+            out[(sigma + zc) / 2 + (zc + 1) * (s + 1) / 2] = thr;
+        }
+    }
+}
+
+int bits_for(uint64_t v) {
+    int b = 0;
+    while (v) { ++b; v >>= 1; }
+    return b < 1 ? 1 : b;
+}
+
+// ---------------------------------------------------------------- kernel registry
+struct TileKey { int ndim, tx, ty, tz, nt; bool sync; void* fn; };
+
+#define TK(ND, TX, TY, TZ, NT)                                                                 \
+    {ND, TX, TY, TZ, NT, false, (void*)tile_kernel<ND, TX, TY, TZ, NT, false>},                \
+    {ND, TX, TY, TZ, NT, true, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}
+
+const TileKey kTiles[] = {
+    TK(2, 32, 32, 1, 256), TK(2, 64, 32, 1, 256), TK(2, 64, 64, 1, 256), TK(2, 128, 64, 1, 512),
+    TK(2, 128, 128, 1, 1024), TK(3, 8, 8, 8, 128), TK(3, 16, 16, 16, 256), TK(3, 32, 16, 8, 256),
+    TK(3, 32, 32, 8, 512),
+};
+
+constexpr int WHOLE_NT = 1024;
+
+size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
+    const size_t slots = (size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1);
+    return (slots + 512 + 16 + nt / 32) * 8;
+}
+size_t whole_smem(int64_t n, bool sync) {
+    return (size_t)n * 8 + (512 + 16 + WHOLE_NT / 32) * 8 + (sync ? (size_t)n * 8 : 0) + (size_t)n * 4;
+}
+
+KParams make_params(const aca_sim* S, const Shard& sh) {
+    KParams P{};
+    P.g = sh.g;
+    P.words = sh.words;
+    P.cnt = sh.cnt;
+    P.halo_lo = sh.halo_lo;
+    P.halo_hi = sh.halo_hi;
+    P.ctl = sh.ctl;
+    P.lr = S->d_lr;
+    P.key0 = (uint32_t)(S->seed & 0xffffffffu);
+    P.key1 = (uint32_t)(S->seed >> 32);
+    P.inv_lambda = S->inv_lambda;
+    P.tie_bits = S->opt.tie_bits;
+    P.rounds = S->rounds;
+    P.do_hash = S->opt.event_hash;
+    P.tiles_x = sh.tiles_x;
+    P.tiles_y = sh.tiles_y;
+    P.tiles_z = sh.tiles_z;
+    for (int i = 0; i < 14; ++i) P.thr[i] = S->thr[i];
+    return P;
+}
+
+// exchange of the sharded-axis boundary rows/planes (virtual shards: D2D copies;
+// multi-process: NCCL send/recv to ring neighbours)
+int exchange(aca_sim* S) {
+    if (S->world > 1) {
+        NcclApi& api = nccl();
+        Shard& sh = S->shards[0];
+        const int up = (S->rank + 1) % S->world, dn = (S->rank + S->world - 1) % S->world;
+        const size_t bytes = sh.face * 8;
+        const unsigned long long* first = sh.words;
+        const unsigned long long* last = sh.words + (sh.n - sh.face);
+        api.gstart();
+        api.send(first, bytes, NCCL_UINT8, dn, S->comm, S->stream);   // my first row -> below's halo_hi
+        api.send(last, bytes, NCCL_UINT8, up, S->comm, S->stream);    // my last row -> above's halo_lo
+        api.recv(sh.halo_hi, bytes, NCCL_UINT8, up, S->comm, S->stream);
+        api.recv(sh.halo_lo, bytes, NCCL_UINT8, dn, S->comm, S->stream);
+        int r = api.gend();
+        if (r != 0) return fail(ACA_ENCCL, "NCCL halo exchange failed: %d", r);
+        return ACA_OK;
+    }
+    if (S->G == 1) return ACA_OK;
+    for (int s = 0; s < S->G; ++s) {
+        Shard& a = S->shards[s];
+        Shard& up = S->shards[(s + 1) % S->G];
+        Shard& dn = S->shards[(s + S->G - 1) % S->G];
+        CK(cudaMemcpyAsync(dn.halo_hi, a.words, a.face * 8, cudaMemcpyDeviceToDevice, S->stream));
+        CK(cudaMemcpyAsync(up.halo_lo, a.words + (a.n - a.face), a.face * 8, cudaMemcpyDeviceToDevice,
+                           S->stream));
+    }
+    return ACA_OK;
+}
+
+int launch_round(aca_sim* S) {
+    int rc = exchange(S);
+    if (rc) return rc;
+    for (auto& sh : S->shards) {
+        KParams P = make_params(S, sh);
+        void* args[] = {&P};
+        dim3 grid = S->whole ? dim3(1) : dim3(sh.tiles_x * sh.tiles_y * sh.tiles_z);
+        CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->whole ? S->smem_whole : S->smem_tile,
+                            S->stream));
+    }
+    return ACA_OK;
+}
+
+int build_graph(aca_sim* S) {
+    if (S->graph) return ACA_OK;
+    if (S->world > 1) return ACA_OK;   // NCCL path: direct launches
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return ACA_OK;
+    }
+    int rc = ACA_OK;
+    for (int k = 0; k < S->K && rc == ACA_OK; ++k) rc = launch_round(S);
+    cudaError_t e = cudaStreamEndCapture(S->stream, &g);
+    if (rc != ACA_OK || e != cudaSuccess) {
+        cudaGetLastError();
+        if (g) cudaGraphDestroy(g);
+        return ACA_OK;   // fall back to direct launches (same kernels)
+    }
+    e = cudaGraphInstantiate(&S->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        S->graph = nullptr;
+    }
+    S->graph_rounds = S->K;
+    return ACA_OK;
+}
+
+int sync_ctl(aca_sim* S) {
+    for (size_t i = 0; i < S->shards.size(); ++i)
+        CK(cudaMemcpyAsync(&S->h_ctl[i], S->shards[i].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, S->stream));
+    CK(cudaStreamSynchronize(S->stream));
+    return ACA_OK;
+}
+
+int ensure_scratch(aca_sim* S, size_t bytes) {
+    if (S->scratch_bytes >= bytes) return ACA_OK;
+    if (S->scratch) cudaFree(S->scratch);
+    S->scratch = nullptr;
+    S->scratch_bytes = 0;
+    CK(cudaMalloc(&S->scratch, bytes));
+    S->scratch_bytes = bytes;
+    return ACA_OK;
+}
+
+int check_count(const aca_sim* S, size_t count, const void* p) {
+    if (!S) return fail(ACA_EINVAL, "null handle");
+    if (!p) return fail(ACA_EINVAL, "null buffer");
+    size_t n = 0;
+    for (auto& sh : S->shards) n += sh.n;
+    if (count != n) return fail(ACA_EINVAL, "count %zu != number of cells %zu", count, n);
+    return ACA_OK;
+}
+
+constexpr size_t CHUNK = (size_t)1 << 25;   // cells per getter chunk (256 MB of u64)
+
+// P5 initial state on the device + zeroed control blocks.
+int init_state(aca_sim* S) {
+    const uint32_t k0 = (uint32_t)(S->seed & 0xffffffffu), k1 = (uint32_t)(S->seed >> 32);
+    for (auto& sh : S->shards) {
+        CK(cudaMemsetAsync(sh.ctl, 0, sizeof(Ctl), S->stream));
+        init_kernel<<<1184, 256, 0, S->stream>>>(sh.words, sh.cnt, sh.g, S->d_lr, k0, k1, S->thr_init, S->inv_lambda,
+                                                  S->opt.tie_bits, (unsigned long long)sh.n);
+        CK(cudaGetLastError());
+    }
+    S->T_last = 0;
+    return ACA_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char* aca_last_error(void) { return g_err.c_str(); }
+
+int aca_default_options(aca_options* o) {
+    if (!o) return fail(ACA_EINVAL, "null options");
+    memset(o, 0, sizeof *o);
+    o->struct_size = sizeof(aca_options);
+    o->init_q = 0.5;
+    o->device = -1;
+    o->shards = 1;
+    o->rank = 0;
+    o->world = 1;
+    o->event_hash = 1;
+    return ACA_OK;
+}
+
+int64_t aca_num_cells(const aca_sim* S) {
+    if (!S) return -1;
+    int64_t n = 0;
+    for (auto& sh : S->shards) n += (int64_t)sh.n;
+    return n;
+}
+
+void aca_destroy(aca_sim* S) {
+    if (!S) return;
+    if (S->stream) cudaStreamSynchronize(S->stream);
+    if (S->graph) cudaGraphExecDestroy(S->graph);
+    for (auto& sh : S->shards) {
+        cudaFree(sh.words);
+        cudaFree(sh.cnt);
+        cudaFree(sh.halo_lo);
+        cudaFree(sh.halo_hi);
+        cudaFree(sh.ctl);
+    }
+    if (S->comm && nccl().ok) nccl().destroy(S->comm);
+    cudaFree(S->d_lr);
+    cudaFree(S->scratch);
+    cudaFree(S->d_stat);
+    if (S->h_ctl) cudaFreeHost(S->h_ctl);
+    if (S->h_stat) cudaFreeHost(S->h_stat);
+    if (S->ev0) cudaEventDestroy(S->ev0);
+    if (S->ev1) cudaEventDestroy(S->ev1);
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+            if (S->evb[a][b]) cudaEventDestroy(S->evb[a][b]);
+    cudaFree(S->d_flag);
+    if (S->h_flag) cudaFreeHost(S->h_flag);
+    if (S->own_stream && S->stream) cudaStreamDestroy(S->stream);
+    delete S;
+}
+
+int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, double lambda, double beta,
+               double J, double h, int rule, uint64_t seed, const aca_options* opt_in) {
+    if (!out) return fail(ACA_EINVAL, "null out");
+    *out = nullptr;
+    if (ndim != 2 && ndim != 3) return fail(ACA_EINVAL, "ndim must be 2 or 3 (got %d)", ndim);
+    if (!dims) return fail(ACA_EINVAL, "null dims");
+    if (periodic != 1) return fail(ACA_EINVAL, "only periodic boundaries are supported (periodic=1)");
+    if (!(lambda > 0) || !std::isfinite(lambda)) return fail(ACA_EINVAL, "lambda must be > 0 and finite");
+    if (!(lambda >= 1.0 / 4294967296.0 * 2) || lambda > 4294967296.0)
+        return fail(ACA_EINVAL, "lambda outside [2^-31, 2^32]");
+    if (!(beta >= 0) || !std::isfinite(beta)) return fail(ACA_EINVAL, "beta must be >= 0 and finite");
+    if (!std::isfinite(J) || !std::isfinite(h)) return fail(ACA_EINVAL, "J and h must be finite");
+    if (rule != ACA_HEATBATH && rule != ACA_METROPOLIS) return fail(ACA_EINVAL, "rule must be 0 or 1");
+    aca_options opt;
+    aca_default_options(&opt);
+    if (opt_in) {
+        if (opt_in->struct_size != sizeof(aca_options))
+            return fail(ACA_EINVAL, "aca_options.struct_size %u != %zu", opt_in->struct_size, sizeof(aca_options));
+        opt = *opt_in;
+    }
+    if (!(opt.init_q >= 0 && opt.init_q <= 1)) return fail(ACA_EINVAL, "init_q must be in [0, 1]");
+    if (opt.tie_bits < 0 || opt.tie_bits > 40) return fail(ACA_EINVAL, "tie_bits must be in [0, 40]");
+    if (opt.shards < 1) opt.shards = 1;
+    if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(ACA_EINVAL, "bad rank/world");
+    if (opt.world > 1 && opt.shards != 1) return fail(ACA_EINVAL, "multi-process handles use shards = 1");
+    if (opt.world > 1 && !opt.nccl_id) return fail(ACA_EINVAL, "world > 1 needs nccl_id");
+    if (opt.rounds_per_launch < 0 || opt.launches_per_check < 0) return fail(ACA_EINVAL, "negative counts");
+
+    int64_t N = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (dims[a] < 2) return fail(ACA_EINVAL, "every dimension must be >= 2 (dims[%d]=%lld)", a, (long long)dims[a]);
+        if (dims[a] > (1 << 30)) return fail(ACA_EINVAL, "dimension too large");
+        N *= dims[a];
+        if (N > (int64_t)1 << 40) return fail(ACA_EINVAL, "lattice too large");
+    }
+    const int saxis = ndim - 1;                       // sharded axis
+    const int parts = opt.world > 1 ? opt.world : opt.shards;
+    if (dims[saxis] % parts != 0 || dims[saxis] / parts < 1)
+        return fail(ACA_EINVAL, "%d shards do not divide the sharded axis (%lld)", parts, (long long)dims[saxis]);
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(ACA_ENODEV, "no CUDA device (the library has no CPU fallback)");
+    }
+
+    aca_sim* S = new aca_sim();
+    S->ndim = ndim;
+    for (int a = 0; a < ndim; ++a) S->dims[a] = dims[a];
+    S->N = N;
+    S->lambda = lambda; S->beta = beta; S->J = J; S->h = h; S->rule = rule; S->seed = seed;
+    S->opt = opt;
+    S->device = opt.device >= 0 ? opt.device : -1;
+    if (S->device < 0) {
+        if (cudaGetDevice(&S->device) != cudaSuccess) { delete S; return fail(ACA_ECUDA, "cudaGetDevice"); }
+    }
+    if (cudaSetDevice(S->device) != cudaSuccess) { delete S; return fail(ACA_ECUDA, "cudaSetDevice(%d)", S->device); }
+    S->rank = opt.world > 1 ? opt.rank : 0;
+    S->world = opt.world;
+    S->G = opt.world > 1 ? 1 : opt.shards;
+    S->sync = opt.sync_rounds != 0;
+    S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 8;
+    S->K = opt.launches_per_check > 0 ? opt.launches_per_check : 16;
+
+    // P3 constants, P4 table, P5 threshold, packing
+    S->inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
+    flip_table(ndim, beta, J, h, rule, S->thr);
+    S->thr_init = (unsigned long long)std::floor(opt.init_q * 4294967296.0);
+    uint64_t max_rank = 0;
+    for (int a = 0; a < ndim; ++a) max_rank += (uint64_t)(dims[a] - 1);
+    S->SH = bits_for(max_rank) + 1;
+    {
+        const unsigned __int128 p = (unsigned __int128)190530846196ull * S->inv_lambda;
+        S->max_delta = (unsigned long long)(p >> 32) + 1 + (opt.tie_bits ? (1ull << opt.tie_bits) : 0ull);
+        if (S->SH >= 40 || S->max_delta >= (1ull << (64 - S->SH))) {
+            delete S;
+            return fail(ACA_ERANGE, "lattice/lambda leave no room for times in the packed word");
+        }
+    }
+
+    int rc = ACA_OK;
+    auto bail = [&](int code) { aca_destroy(S); return code; };
+    if (opt.stream) {
+        S->stream = (cudaStream_t)opt.stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&S->stream, cudaStreamNonBlocking) != cudaSuccess)
+            return bail(fail(ACA_ECUDA, "cudaStreamCreate"));
+        S->own_stream = true;
+    }
+    if (cudaMalloc(&S->d_lr, sizeof(ACA_NLOG_LR)) != cudaSuccess) return bail(fail(ACA_ENOMEM, "cudaMalloc lr"));
+    if (cudaMemcpy(S->d_lr, ACA_NLOG_LR, sizeof(ACA_NLOG_LR), cudaMemcpyHostToDevice) != cudaSuccess)
+        return bail(fail(ACA_ECUDA, "copy nlog table"));
+    if (cudaMalloc(&S->d_stat, sizeof(StatAcc)) != cudaSuccess) return bail(fail(ACA_ENOMEM, "cudaMalloc stat"));
+    if (cudaMallocHost(&S->h_stat, sizeof(StatAcc)) != cudaSuccess) return bail(fail(ACA_ENOMEM, "pinned stat"));
+    if (cudaEventCreate(&S->ev0) != cudaSuccess || cudaEventCreate(&S->ev1) != cudaSuccess)
+        return bail(fail(ACA_ECUDA, "cudaEventCreate"));
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 3; ++b)
+            if (cudaEventCreate(&S->evb[a][b]) != cudaSuccess) return bail(fail(ACA_ECUDA, "cudaEventCreate"));
+    if (cudaMalloc(&S->d_flag, 8) != cudaSuccess || cudaMallocHost(&S->h_flag, 8) != cudaSuccess)
+        return bail(fail(ACA_ENOMEM, "flag"));
+
+    // kernel selection
+    int dev_smem = 0;
+    cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, S->device);
+    const bool single = (S->G == 1 && S->world == 1);
+    S->whole = false;
+    if (single && opt.whole_lattice >= 0) {
+        const bool fits = whole_smem(N, S->sync) <= (size_t)dev_smem;
+        if (opt.whole_lattice == 1 && !fits) return bail(fail(ACA_EINVAL, "lattice too large for whole_lattice"));
+        S->whole = fits && (opt.whole_lattice == 1 || N <= 8192);
+    }
+    if (S->whole) {
+        S->kern = S->sync ? (void*)whole_kernel<WHOLE_NT, true> : (void*)whole_kernel<WHOLE_NT, false>;
+        S->nthreads = WHOLE_NT;
+        S->smem_whole = whole_smem(N, S->sync);
+        S->rounds = 1 << 30;
+        if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem_whole) != cudaSuccess)
+            return bail(fail(ACA_ECUDA, "smem attribute (whole)"));
+    } else {
+        int tx = opt.tile[0], ty = opt.tile[1], tz = opt.tile[2];
+        if (tx == 0 && ty == 0 && tz == 0) {
+            if (ndim == 2) { tx = 64; ty = 64; tz = 1; }
+            else { tx = 32; ty = 16; tz = 8; }
+        }
+        if (ndim == 2) tz = 1;
+        const TileKey* sel = nullptr;
+        for (const auto& k : kTiles)
+            if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz && k.sync == S->sync) sel = &k;
+        if (!sel) return bail(fail(ACA_EINVAL, "unsupported tile %dx%dx%d for ndim %d", tx, ty, tz, ndim));
+        S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
+        S->kern = sel->fn;
+        S->nthreads = sel->nt;
+        S->smem_tile = tile_smem(ndim, tx, ty, tz, sel->nt);
+        if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem_tile) != cudaSuccess)
+            return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
+    }
+
+    // shards
+    const int64_t local = dims[saxis] / parts;
+    S->shards.resize(S->G);
+    for (int s = 0; s < S->G; ++s) {
+        Shard& sh = S->shards[s];
+        const int part = S->world > 1 ? S->rank : s;
+        Geo& g = sh.g;
+        g.ndim = ndim;
+        g.nx = (int)dims[0];
+        g.NY = (int)dims[1];
+        g.NZ = ndim == 3 ? (int)dims[2] : 1;
+        g.ny = ndim == 2 ? (int)local : (int)dims[1];
+        g.nz = ndim == 3 ? (int)local : 1;
+        g.y0 = ndim == 2 ? (int)(part * local) : 0;
+        g.z0 = ndim == 3 ? (int)(part * local) : 0;
+        g.sharded = parts > 1;
+        g.SH = S->SH;
+        sh.n = (size_t)g.nx * g.ny * g.nz;
+        sh.face = ndim == 2 ? (size_t)g.nx : (size_t)g.nx * g.ny;
+        sh.tiles_x = (g.nx + S->tile[0] - 1) / S->tile[0];
+        sh.tiles_y = (g.ny + S->tile[1] - 1) / S->tile[1];
+        sh.tiles_z = ndim == 3 ? (g.nz + S->tile[2] - 1) / S->tile[2] : 1;
+        if (cudaMalloc(&sh.words, sh.n * 8) != cudaSuccess || cudaMalloc(&sh.cnt, sh.n * 4) != cudaSuccess ||
+            cudaMalloc(&sh.ctl, sizeof(Ctl)) != cudaSuccess)
+            return bail(fail(ACA_ENOMEM, "device allocation of %zu cells failed", sh.n));
+        if (g.sharded) {
+            if (cudaMalloc(&sh.halo_lo, sh.face * 8) != cudaSuccess || cudaMalloc(&sh.halo_hi, sh.face * 8) != cudaSuccess)
+                return bail(fail(ACA_ENOMEM, "halo allocation failed"));
+        }
+    }
+    if (int r = init_state(S)) return bail(r);
+    if (cudaMallocHost(&S->h_ctl, 2 * sizeof(Ctl) * S->shards.size()) != cudaSuccess)
+        return bail(fail(ACA_ENOMEM, "pinned ctl"));
+
+    if (S->world > 1) {
+        NcclApi& api = nccl();
+        if (!api.ok) return bail(fail(ACA_ENCCL, "NCCL symbols not found in the process (load torch.distributed nccl first)"));
+        ncclUniqueId_t id;
+        memcpy(&id, opt.nccl_id, sizeof id);
+        int r = api.init(&S->comm, S->world, id, S->rank);
+        if (r != 0) return bail(fail(ACA_ENCCL, "ncclCommInitRank failed: %d", r));
+    }
+    if (cudaStreamSynchronize(S->stream) != cudaSuccess) return bail(fail(ACA_ECUDA, "init sync: %s", cudaGetErrorString(cudaGetLastError())));
+    (void)rc;
+    *out = S;
+    return ACA_OK;
+}
+
+int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
+    if (!S) return fail(ACA_EINVAL, "null handle");
+    if (Tq < S->T_last) return fail(ACA_ESTATE, "T decreased (%llu < %llu)", (unsigned long long)Tq, (unsigned long long)S->T_last);
+    if (Tq >= (1ull << (64 - S->SH)) - S->max_delta)
+        return fail(ACA_ERANGE, "T too large for the packed time field (%d bits)", 64 - S->SH);
+    S->T_last = Tq;
+    CK(cudaSetDevice(S->device));
+    // reset per-call control words
+    for (size_t i = 0; i < S->shards.size(); ++i) {
+        S->h_ctl[i].wlim = (unsigned long long)Tq << S->SH;
+        S->h_ctl[i].done = 0;
+        CK(cudaMemcpyAsync(&S->shards[i].ctl->wlim, &S->h_ctl[i].wlim, sizeof(unsigned long long),
+                           cudaMemcpyHostToDevice, S->stream));
+        CK(cudaMemsetAsync(&S->shards[i].ctl->done, 0, sizeof(unsigned int), S->stream));
+    }
+    int rc = build_graph(S);
+    if (rc) return rc;
+    CK(cudaEventRecord(S->ev0, S->stream));
+    const size_t nsh = S->shards.size();
+    // One batch = K outer rounds (a CUDA-graph replay) followed by a copy of the control
+    // blocks to pinned memory. Two batches are kept in flight so the GPU never idles while
+    // the host inspects the previous batch; batches issued after termination are no-ops
+    // (every launch returns at its first instruction when ctl->done is set).
+    auto issue = [&](int slot) -> int {
+        CK(cudaEventRecord(S->evb[slot][0], S->stream));
+        if (S->graph) {
+            CK(cudaGraphLaunch(S->graph, S->stream));
+            S->kernel_launches += (uint64_t)S->graph_rounds * nsh;
+        } else {
+            for (int k = 0; k < S->K; ++k) {
+                int r = launch_round(S);
+                if (r) return r;
+                S->kernel_launches += nsh;
+            }
+        }
+        CK(cudaEventRecord(S->evb[slot][1], S->stream));
+        for (size_t i = 0; i < nsh; ++i)
+            CK(cudaMemcpyAsync(&S->h_ctl[slot * nsh + i], S->shards[i].ctl, sizeof(Ctl), cudaMemcpyDeviceToHost,
+                               S->stream));
+        CK(cudaEventRecord(S->evb[slot][2], S->stream));
+        return ACA_OK;
+    };
+    auto retire = [&](int slot, bool* done) -> int {
+        CK(cudaEventSynchronize(S->evb[slot][2]));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, S->evb[slot][0], S->evb[slot][1]));
+        S->kernel_seconds += ms * 1e-3;
+        bool d = true;
+        for (size_t i = 0; i < nsh; ++i) d = d && S->h_ctl[slot * nsh + i].done;
+        *done = d;
+        return ACA_OK;
+    };
+    const bool pipelined = S->world == 1;
+    rc = issue(0);
+    if (rc) return rc;
+    int outstanding = -1;      // pipelined: slot issued but not yet retired
+    for (int iter = 1;; ++iter) {
+        const int cur = iter & 1, prev = cur ^ 1;
+        if (pipelined) {
+            rc = issue(cur);
+            if (rc) return rc;
+            outstanding = cur;
+        }
+        bool done = false;
+        rc = retire(pipelined ? prev : 0, &done);
+        if (rc) return rc;
+        if (S->world > 1) {
+            // every rank must agree: all-reduce of the local "still active" flag
+            NcclApi& api = nccl();
+            unsigned long long* d = S->d_flag;
+            *S->h_flag = done ? 0ull : 1ull;
+            CK(cudaMemcpyAsync(d, S->h_flag, 8, cudaMemcpyHostToDevice, S->stream));
+            int r = api.allreduce(d, d, 1, NCCL_UINT64, NCCL_SUM, S->comm, S->stream);
+            if (r != 0) return fail(ACA_ENCCL, "allreduce failed: %d", r);
+            CK(cudaMemcpyAsync(S->h_flag, d, 8, cudaMemcpyDeviceToHost, S->stream));
+            CK(cudaStreamSynchronize(S->stream));
+            done = (*S->h_flag == 0);
+            if (!done) {
+                rc = issue(0);
+                if (rc) return rc;
+            }
+        }
+        if (done) break;
+        if (iter > (1 << 26)) return fail(ACA_ESTATE, "no termination");
+    }
+    if (outstanding >= 0) {   // account the trailing (no-op) batch
+        bool dummy;
+        rc = retire(outstanding, &dummy);
+        if (rc) return rc;
+    }
+    CK(cudaEventRecord(S->ev1, S->stream));
+    CK(cudaEventSynchronize(S->ev1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
+    S->gpu_seconds += ms * 1e-3;
+    // copy the final control blocks into slot 0 for getters
+    return sync_ctl(S);
+}
+
+int aca_nccl_unique_id(void* out128) {
+    if (!out128) return fail(ACA_EINVAL, "null buffer");
+    NcclApi& api = nccl();
+    if (!api.ok || !api.uid) return fail(ACA_ENCCL, "NCCL not available in this process");
+    ncclUniqueId_t id;
+    int r = api.uid(&id);
+    if (r != 0) return fail(ACA_ENCCL, "ncclGetUniqueId failed: %d", r);
+    memcpy(out128, &id, sizeof id);
+    return ACA_OK;
+}
+
+int aca_reset(aca_sim* S, uint64_t seed) {
+    if (!S) return fail(ACA_EINVAL, "null handle");
+    CK(cudaSetDevice(S->device));
+    S->seed = seed;
+    return init_state(S);
+}
+
+int aca_run_until(aca_sim* S, double T) {
+    if (!S) return fail(ACA_EINVAL, "null handle");
+    if (!(T >= 0) || !std::isfinite(T)) return fail(ACA_EINVAL, "T must be finite and >= 0");
+    const double tq = std::floor(T * 4294967296.0 + 0.5);
+    if (tq >= 18446744073709551616.0) return fail(ACA_ERANGE, "T too large");
+    return aca_run_until_q32(S, (uint64_t)tq);
+}
+
+static int get_words(aca_sim* S, int8_t* spins, uint64_t* times, size_t count) {
+    int rc = check_count(S, count, spins ? (const void*)spins : (const void*)times);
+    if (rc) return rc;
+    CK(cudaSetDevice(S->device));
+    rc = ensure_scratch(S, CHUNK * (times ? 8 : 1));
+    if (rc) return rc;
+    size_t off = 0;
+    for (auto& sh : S->shards) {
+        for (size_t b = 0; b < sh.n; b += CHUNK) {
+            const size_t m = std::min(CHUNK, sh.n - b);
+            unpack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, spins ? (int8_t*)S->scratch : nullptr,
+                                                      times ? (unsigned long long*)S->scratch : nullptr, S->SH, m);
+            CK(cudaGetLastError());
+            if (spins) CK(cudaMemcpyAsync(spins + off + b, S->scratch, m, cudaMemcpyDeviceToHost, S->stream));
+            else CK(cudaMemcpyAsync(times + off + b, S->scratch, m * 8, cudaMemcpyDeviceToHost, S->stream));
+            CK(cudaStreamSynchronize(S->stream));
+        }
+        off += sh.n;
+    }
+    return ACA_OK;
+}
+
+int aca_get_spins(aca_sim* S, int8_t* out, size_t count) { return get_words(S, out, nullptr, count); }
+int aca_get_times(aca_sim* S, uint64_t* out, size_t count) { return get_words(S, nullptr, out, count); }
+
+int aca_get_counters(aca_sim* S, uint32_t* out, size_t count) {
+    int rc = check_count(S, count, out);
+    if (rc) return rc;
+    CK(cudaSetDevice(S->device));
+    size_t off = 0;
+    for (auto& sh : S->shards) {
+        CK(cudaMemcpyAsync(out + off, sh.cnt, sh.n * 4, cudaMemcpyDeviceToHost, S->stream));
+        off += sh.n;
+    }
+    CK(cudaStreamSynchronize(S->stream));
+    return ACA_OK;
+}
+
+int aca_get_flip_table(const aca_sim* S, uint64_t* thr, size_t count) {
+    if (!S || !thr) return fail(ACA_EINVAL, "null argument");
+    const size_t n = 2 * (2 * S->ndim + 1);
+    if (count != n) return fail(ACA_EINVAL, "flip table has %zu entries", n);
+    for (size_t i = 0; i < n; ++i) thr[i] = S->thr[i];
+    return ACA_OK;
+}
+
+int aca_get_stats(aca_sim* S, aca_stats* o) {
+    if (!S || !o) return fail(ACA_EINVAL, "null argument");
+    CK(cudaSetDevice(S->device));
+    memset(o, 0, sizeof *o);
+    StatAcc init{0, 0, 0, ~0ull, 0};
+    *S->h_stat = init;
+    CK(cudaMemcpyAsync(S->d_stat, S->h_stat, sizeof(StatAcc), cudaMemcpyHostToDevice, S->stream));
+    int rc = exchange(S);      // make halos current for the bond sum across shard boundaries
+    if (rc) return rc;
+    for (auto& sh : S->shards) {
+        KParams P = make_params(S, sh);
+        stats_kernel<256><<<592, 256, 0, S->stream>>>(P, S->d_stat, (unsigned long long)sh.n);
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(S->h_stat, S->d_stat, sizeof(StatAcc), cudaMemcpyDeviceToHost, S->stream));
+    rc = sync_ctl(S);
+    if (rc) return rc;
+    o->bond_sum = S->h_stat->bond;
+    o->magnetisation = S->h_stat->mag;
+    o->arrivals = S->h_stat->arrivals;
+    o->t_min = S->h_stat->tmin;
+    o->t_max = S->h_stat->tmax;
+    for (size_t i = 0; i < S->shards.size(); ++i) {
+        const Ctl& c = S->h_ctl[i];
+        o->flips += c.flips;
+        o->event_hash += c.hash;
+        o->launches += c.launches;
+        o->inner_rounds += c.inner_rounds;
+        o->cells_tested += c.tested;
+        o->cells_fired += c.fired;
+    }
+    o->gpu_seconds = S->gpu_seconds;
+    o->kernel_seconds = S->kernel_seconds;
+    o->kernel_launches = S->kernel_launches;
+    return ACA_OK;
+}
+
+int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const uint32_t* counters, size_t count) {
+    int rc = check_count(S, count, spins);
+    if (rc) return rc;
+    if (!times || !counters) return fail(ACA_EINVAL, "null times/counters");
+    const uint64_t lim = (1ull << (64 - S->SH)) - S->max_delta;
+    for (size_t i = 0; i < count; ++i) {
+        if (spins[i] != 1 && spins[i] != -1) return fail(ACA_EINVAL, "spin %zu is not +-1", i);
+        if (times[i] < 1 || times[i] >= lim) return fail(ACA_ERANGE, "time %zu out of range", i);
+    }
+    CK(cudaSetDevice(S->device));
+    rc = ensure_scratch(S, CHUNK * 9);
+    if (rc) return rc;
+    unsigned long long* dt = (unsigned long long*)S->scratch;
+    int8_t* ds = (int8_t*)(dt + CHUNK);
+    size_t off = 0;
+    for (auto& sh : S->shards) {
+        CK(cudaMemcpyAsync(sh.cnt, counters + off, sh.n * 4, cudaMemcpyHostToDevice, S->stream));
+        for (size_t b = 0; b < sh.n; b += CHUNK) {
+            const size_t m = std::min(CHUNK, sh.n - b);
+            CK(cudaMemcpyAsync(dt, times + off + b, m * 8, cudaMemcpyHostToDevice, S->stream));
+            CK(cudaMemcpyAsync(ds, spins + off + b, m, cudaMemcpyHostToDevice, S->stream));
+            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, ds, dt, sh.g, (unsigned long long)m,
+                                                    (unsigned long long)b);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(S->stream));
+        }
+        off += sh.n;
+    }
+    S->T_last = 0;
+    return ACA_OK;
+}
+
+int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
+    int rc = check_count(S, count, spins);
+    if (rc) return rc;
+    CK(cudaSetDevice(S->device));
+    rc = ensure_scratch(S, CHUNK);
+    if (rc) return rc;
+    size_t off = 0;
+    for (auto& sh : S->shards) {
+        for (size_t b = 0; b < sh.n; b += CHUNK) {
+            const size_t m = std::min(CHUNK, sh.n - b);
+            CK(cudaMemcpyAsync(S->scratch, spins + off + b, m, cudaMemcpyHostToDevice, S->stream));
+            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, (const int8_t*)S->scratch, nullptr, sh.g,
+                                                    (unsigned long long)m, (unsigned long long)b);
+            CK(cudaGetLastError());
+        }
+        off += sh.n;
+    }
+    CK(cudaStreamSynchronize(S->stream));
+    return ACA_OK;
+}
+
+// ---------------------------------------------------------------- self-test hooks
+}  // extern "C"
+
+namespace {
+__global__ void philox_test_kernel(uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out, uint32_t* ref) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const u32x4 r = philox4x32_10(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3], key[2 * i], key[2 * i + 1]);
+        out[4 * i] = r.x; out[4 * i + 1] = r.y; out[4 * i + 2] = r.z; out[4 * i + 3] = r.w;
+        uint4 c = make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]);
+        uint2 k = make_uint2(key[2 * i], key[2 * i + 1]);
+        const uint4 q = curand_Philox4x32_10(c, k);
+        ref[4 * i] = q.x; ref[4 * i + 1] = q.y; ref[4 * i + 2] = q.z; ref[4 * i + 3] = q.w;
+    }
+}
+__global__ void nlog_test_kernel(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* d, const unsigned long long* lr_g,
+                                 unsigned long long inv_lambda, int tie_bits) {
+    __shared__ unsigned long long lr[512];
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        q[i] = nlog_q32(X[i], lr, ACA_LN2_Q48);
+        d[i] = delta_q32((uint32_t)(X[i] >> 32), (uint32_t)X[i], lr, ACA_LN2_Q48, inv_lambda, tie_bits);
+    }
+}
+}  // namespace
+
+extern "C" {
+int aca_selftest_philox(uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out, uint32_t* ref) {
+    if (!ctr || !key || !out || !ref) return fail(ACA_EINVAL, "null buffer");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
+    uint32_t *dc = nullptr, *dk = nullptr, *do_ = nullptr, *dr = nullptr;
+    CK(cudaMalloc(&dc, n * 16)); CK(cudaMalloc(&dk, n * 8)); CK(cudaMalloc(&do_, n * 16)); CK(cudaMalloc(&dr, n * 16));
+    CK(cudaMemcpy(dc, ctr, n * 16, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dk, key, n * 8, cudaMemcpyHostToDevice));
+    philox_test_kernel<<<592, 256>>>(n, dc, dk, do_, dr);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, do_, n * 16, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ref, dr, n * 16, cudaMemcpyDeviceToHost));
+    cudaFree(dc); cudaFree(dk); cudaFree(do_); cudaFree(dr);
+    return ACA_OK;
+}
+
+int aca_selftest_nlog(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* delta, uint64_t inv_lambda, int tie_bits) {
+    if (!X || !q || !delta) return fail(ACA_EINVAL, "null buffer");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
+    uint64_t *dx = nullptr, *dq = nullptr, *dd = nullptr;
+    unsigned long long* dlr = nullptr;
+    CK(cudaMalloc(&dx, n * 8)); CK(cudaMalloc(&dq, n * 8)); CK(cudaMalloc(&dd, n * 8));
+    CK(cudaMalloc(&dlr, sizeof(ACA_NLOG_LR)));
+    CK(cudaMemcpy(dlr, ACA_NLOG_LR, sizeof(ACA_NLOG_LR), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dx, X, n * 8, cudaMemcpyHostToDevice));
+    nlog_test_kernel<<<592, 256>>>(n, dx, dq, dd, dlr, inv_lambda, tie_bits);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(q, dq, n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(delta, dd, n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dx); cudaFree(dq); cudaFree(dd); cudaFree(dlr);
+    return ACA_OK;
+}
+}  // extern "C"

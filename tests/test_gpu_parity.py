@@ -1,0 +1,198 @@
+"""GPU parity: the CUDA path through the C ABI against the serial oracle, element by element
+(bit-exact: spins, every t(c), every n(c), and the integer statistics B, M, arrivals,
+flips, P7 event hash). Sizes span several tiles and ragged tails; edge cases: 2x2 (doubled
+neighbours), forced ties (P3b), run_until composition, every tile shape / rounds-per-launch /
+virtual shard count (the trajectory is invariant)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+STAT_KEYS = ("arrivals", "flips", "event_hash", "bond_sum", "magnetisation", "t_min", "t_max")
+
+
+@pytest.fixture(scope="module")
+def aca():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_cs_0502039_b200 as aca
+    return aca
+
+
+def run_pair(aca, oracle_mod, dims, Ts, beta=0.4406868, J=1.0, h=0.0, lam=1.0, rule=0, seed=1,
+             init_q=0.5, tie_bits=0, **opts):
+    g = aca.Sim(dims, lam=lam, beta=beta, J=J, h=h, rule=rule, seed=seed, init_q=init_q, tie_bits=tie_bits, **opts)
+    o = oracle_mod.OracleSim(dims, lam=lam, beta=beta, J=J, h=h, rule=rule, seed=seed, init_q=init_q,
+                             tie_bits=tie_bits)
+    assert g.flip_table() == oracle_mod.flip_table(len(dims), beta, J, h, rule)
+    for T in Ts:
+        g.run_until(T)
+        o.run_until(T)
+    return g, o
+
+
+def assert_same(g, o):
+    gs, gt, gn = g.spins(), g.times(), g.counters()
+    os_, ot, on = o.spins(), o.times(), o.counters()
+    bad_s = np.argwhere(gs != os_)
+    assert bad_s.size == 0, ("spins differ at", bad_s[:5])
+    assert np.array_equal(gt, ot), ("times differ at", np.argwhere(gt != ot)[:5])
+    assert np.array_equal(gn, on), ("counters differ at", np.argwhere(gn != on)[:5])
+    sg, so = g.stats(), o.stats()
+    for k in STAT_KEYS:
+        assert sg[k] == so[k], (k, sg[k], so[k])
+    assert sg["cells_fired"] == so["arrivals"]
+
+
+def test_philox_matches_curand_device_and_oracle(aca, oracle_mod):
+    rng = np.random.default_rng(1)
+    n = 1 << 20
+    ctr = rng.integers(0, 2 ** 32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+    key = rng.integers(0, 2 ** 32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
+    ctr[:16] = [[0, 0, 0, 0], [0xFFFFFFFF] * 4] * 8
+    key[:16] = [[0, 0], [0xFFFFFFFF] * 2] * 8
+    out, ref = aca.aca_selftest_philox(ctr, key)
+    assert np.array_equal(out, ref)
+    for i in list(range(16)) + list(rng.integers(0, n, 2000)):
+        assert tuple(int(v) for v in out[i]) == oracle_mod.philox(tuple(int(v) for v in ctr[i]),
+                                                                  tuple(int(v) for v in key[i]))
+
+
+def test_nlog_bit_identical_to_oracle(aca, oracle_mod):
+    rng = np.random.default_rng(2)
+    X = rng.integers(0, 2 ** 63, size=1 << 20, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, 1 << 20).astype(np.uint64)
+    edges = [0, 1, 2, 3, 2 ** 63, 2 ** 63 + 1, 2 ** 64 - 1, 2 ** 64 - 2] + [2 ** k for k in range(64)]
+    for i in range(256):
+        edges += [((1 << 63) | (i << 55)) >> s for s in (0, 5, 33, 62)]
+    X = np.concatenate([np.array(edges, np.uint64), X])
+    q, d = aca.aca_selftest_nlog(X)
+    assert np.array_equal(q, oracle_mod.nlog_batch(X))
+    for lam, tb in ((1.0, 0), (2.5, 0), (0.3, 0), (1.0, 28)):
+        q, d = aca.aca_selftest_nlog(X[:5000], lam, tb)
+        want = [oracle_mod.delta(int(x) >> 32, int(x) & 0xFFFFFFFF, lam, tb) for x in X[:5000]]
+        assert list(d) == want
+
+
+@pytest.mark.parametrize("dims", [(2, 2), (3, 3), (5, 7), (2, 5), (16, 16), (13, 7)])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_small_whole_lattice(aca, oracle_mod, dims, rule):
+    g, o = run_pair(aca, oracle_mod, dims, [3.0, 10.0], beta=0.44, rule=rule, h=0.1 * rule, seed=7)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 2), (4, 4, 4), (3, 2, 5), (8, 8, 8)])
+def test_small_whole_lattice_3d(aca, oracle_mod, dims):
+    g, o = run_pair(aca, oracle_mod, dims, [5.0], beta=0.2216544, seed=3)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("sync", [0, 1])
+def test_config1_exact(aca, oracle_mod, sync):
+    """Config 1: 64x64 heat-bath at beta_c, T = 10, one CTA (one cell per PE rule)."""
+    g, o = run_pair(aca, oracle_mod, (64, 64), [10.0], beta=0.4406868, seed=1, sync_rounds=sync)
+    assert_same(g, o)
+    st = g.stats()
+    assert st["launches"] == 1            # whole run_until in one launch
+    assert abs(st["arrivals"] - 40960) < 5 * 202
+
+
+@pytest.mark.parametrize("tile", [(64, 64), (32, 32), (64, 32), (128, 64), (128, 128)])
+def test_tiled_2d_ragged(aca, oracle_mod, tile):
+    """Several tiles plus ragged tails in x and y."""
+    g, o = run_pair(aca, oracle_mod, (200, 150), [2.0, 6.0], beta=0.40, rule=1, seed=11, tile=tile,
+                    whole_lattice=-1)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("rounds", [1, 3, 8, 64])
+def test_rounds_per_launch_invariance(aca, oracle_mod, rounds):
+    g, o = run_pair(aca, oracle_mod, (256, 192), [5.0], seed=5, rounds_per_launch=rounds, whole_lattice=-1)
+    assert_same(g, o)
+
+
+def test_sync_rounds_tiled(aca, oracle_mod):
+    g, o = run_pair(aca, oracle_mod, (192, 128), [4.0], seed=9, sync_rounds=1, whole_lattice=-1)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("tile", [(32, 16, 8), (16, 16, 16), (8, 8, 8), (32, 32, 8)])
+def test_tiled_3d_ragged(aca, oracle_mod, tile):
+    g, o = run_pair(aca, oracle_mod, (40, 24, 20), [3.0], beta=0.2216544, seed=13, tile=tile, whole_lattice=-1)
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("tie_bits", [28, 31])
+def test_forced_ties(aca, oracle_mod, tie_bits):
+    g, o = run_pair(aca, oracle_mod, (128, 96), [6.0], beta=0.44, seed=17, tie_bits=tie_bits, whole_lattice=-1)
+    assert_same(g, o)
+    g, o = run_pair(aca, oracle_mod, (6, 5), [6.0], beta=0.44, seed=17, tie_bits=tie_bits)
+    assert_same(g, o)
+    g, o = run_pair(aca, oracle_mod, (12, 10, 8), [4.0], beta=0.22, seed=17, tie_bits=tie_bits, whole_lattice=-1,
+                    tile=(8, 8, 8))
+    assert_same(g, o)
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+def test_virtual_shards(aca, oracle_mod, shards):
+    """G row strips (2-D) / z slabs (3-D) on one device with halo exchange each outer round:
+    the multi-GPU partition and halo logic with the transport replaced by device copies."""
+    g, o = run_pair(aca, oracle_mod, (128, 64 * shards // 2), [4.0], seed=19, shards=shards)
+    assert_same(g, o)
+    g, o = run_pair(aca, oracle_mod, (32, 16, 8 * shards), [3.0], beta=0.22, seed=19, shards=shards,
+                    tile=(16, 16, 16))
+    assert_same(g, o)
+
+
+def test_run_until_composition(aca, oracle_mod):
+    g, o = run_pair(aca, oracle_mod, (160, 96), [0.0, 0.5, 2.0, 2.0, 7.25], seed=23, whole_lattice=-1)
+    assert_same(g, o)
+    g2, _ = run_pair(aca, oracle_mod, (160, 96), [7.25], seed=23, whole_lattice=-1)
+    assert np.array_equal(g.spins(), g2.spins()) and g.stats()["event_hash"] == g2.stats()["event_hash"]
+    import paper_cs_0502039_b200 as pkg
+    with pytest.raises(pkg.AcaError):
+        g.run_until(1.0)
+
+
+def test_lambda_and_field(aca, oracle_mod):
+    g, o = run_pair(aca, oracle_mod, (96, 80), [1.5, 3.0], lam=2.5, beta=0.7, h=-0.3, J=0.8, rule=0, seed=29,
+                    whole_lattice=-1)
+    assert_same(g, o)
+
+
+def test_init_minority(aca, oracle_mod):
+    """Config 5's initial state (all +1 but an i.i.d. 5 %) at beta = 1, h = 0.1 Metropolis."""
+    g, o = run_pair(aca, oracle_mod, (256, 128), [10.0], beta=1.0, h=0.1, rule=1, init_q=0.05, seed=31,
+                    whole_lattice=-1)
+    assert_same(g, o)
+
+
+def test_set_state_roundtrip(aca, oracle_mod):
+    g = aca.Sim((64, 48), beta=0.5, seed=3, whole_lattice=-1)
+    g.run_until(2.0)
+    s, t, n = g.spins().copy(), g.times().copy(), g.counters().copy()
+    g2 = aca.Sim((64, 48), beta=0.5, seed=3, whole_lattice=-1)
+    g2.set_state(s, t, n)
+    g.run_until(5.0)
+    g2.run_until(5.0)
+    assert np.array_equal(g.spins(), g2.spins()) and np.array_equal(g.times(), g2.times())
+
+
+def test_set_spins_user_initial_state(aca, oracle_mod):
+    import workloads
+    sp = workloads.host_spins((64, 64), seed=5)
+    g = aca.Sim((64, 64), beta=0.44, seed=3, whole_lattice=-1)
+    g.set_spins(sp)
+    assert np.array_equal(g.spins().ravel(), sp)
+
+
+def test_config2_scaled(aca, oracle_mod):
+    """Config 2's physics (Metropolis beta 0.40, 64x64 tiles) on 512x512 to T = 8."""
+    g, o = run_pair(aca, oracle_mod, (512, 512), [8.0], beta=0.40, rule=1, seed=1, tile=(64, 64))
+    assert_same(g, o)
+
+
+def test_config4_scaled(aca, oracle_mod):
+    """Config 4's physics (3-D heat-bath at beta 0.2216544) on 64^3 to T = 3, 2 shards."""
+    g, o = run_pair(aca, oracle_mod, (64, 64, 64), [3.0], beta=0.2216544, seed=1, shards=2)
+    assert_same(g, o)
