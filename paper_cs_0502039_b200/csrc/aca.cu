@@ -193,24 +193,27 @@ int bits_for(uint64_t v) {
 }
 
 // ---------------------------------------------------------------- kernel registry
-struct TileKey { int ndim, tx, ty, tz, nt; bool sync; void* fn; };
+constexpr size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
+    return ((size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32) * 8;
+}
+constexpr size_t tile2_smem(int ndim, int tx, int ty, int tz, int nt) {
+    return tile_smem(ndim, tx, ty, tz, nt) + (size_t)tx * ty * tz * (4 + 2);
+}
 
-#define TK(ND, TX, TY, TZ, NT)                                                                 \
-    {ND, TX, TY, TZ, NT, false, (void*)tile_kernel<ND, TX, TY, TZ, NT, false>},                \
-    {ND, TX, TY, TZ, NT, true, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}
+struct TileKey { int ndim, tx, ty, tz, nt; bool sync; void* fn; size_t smem; };
+
+// async (default): compacted tile2_kernel; sync_rounds: two-barrier fig:s1c1pe tile_kernel
+#define TK(ND, TX, TY, TZ, NT, MB)                                                                   \
+    {ND, TX, TY, TZ, NT, false, (void*)tile2_kernel<ND, TX, TY, TZ, NT, MB>, tile2_smem(ND, TX, TY, TZ, NT)}, \
+    {ND, TX, TY, TZ, NT, true, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>, tile_smem(ND, TX, TY, TZ, NT)}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256), TK(2, 64, 32, 1, 256), TK(2, 64, 64, 1, 256), TK(2, 128, 64, 1, 512),
-    TK(2, 128, 128, 1, 1024), TK(3, 8, 8, 8, 128), TK(3, 16, 16, 16, 256), TK(3, 32, 16, 8, 256),
-    TK(3, 32, 32, 8, 512),
+    TK(2, 32, 32, 1, 256, 4), TK(2, 64, 32, 1, 256, 4), TK(2, 64, 64, 1, 256, 3), TK(2, 128, 64, 1, 512, 1),
+    TK(3, 8, 8, 8, 128, 8), TK(3, 16, 16, 16, 256, 2), TK(3, 32, 16, 8, 256, 2), TK(3, 32, 32, 8, 512, 1),
 };
 
 constexpr int WHOLE_NT = 1024;
 
-size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
-    const size_t slots = (size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1);
-    return (slots + 512 + 16 + nt / 32) * 8;
-}
 size_t whole_smem(int64_t n, bool sync) {
     return (size_t)n * 8 + (512 + 16 + WHOLE_NT / 32) * 8 + (sync ? (size_t)n * 8 : 0) + (size_t)n * 4;
 }
@@ -536,7 +539,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
         S->kern = sel->fn;
         S->nthreads = sel->nt;
-        S->smem_tile = tile_smem(ndim, tx, ty, tz, sel->nt);
+        S->smem_tile = sel->smem;
         if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem_tile) != cudaSuccess)
             return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
     }

@@ -305,6 +305,156 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds);
 }
 
+// ------------------------------------------------------------ tile kernel, compacted
+// Same method and semantics as tile_kernel<..., SYNC=false>, organised for SIMT efficiency:
+// per round every warp (i) tests its 512 cells against the current words — the test is a
+// 32-bit compare of the high halves, with a full 64-bit compare only on a high-half tie —
+// (ii) compacts the eligible cells into a warp-private queue with __ballot_sync, and
+// (iii) fires them with all 32 lanes busy (Philox + NLOG + hash are ~90 % of the work; in
+// the uncompacted kernel they ran with ~10 % of the lanes active).
+// Correctness of firing after compaction: a queued cell c was a local minimum when
+// tested; its word cannot change until it fires, so no neighbour can pass its own test
+// (it would need a word below c's) — c's neighbourhood is frozen until c fires.
+template <int NDIM, int TX, int TY, int TZ, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) tile2_kernel(const KParams P) {
+    constexpr int SX = TX + 2, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
+    constexpr int NSLOT = SX * SY * SZ;
+    constexpr int NCELL = TX * TY * TZ;
+    constexpr int NW = NT / 32;
+    constexpr int CPW = NCELL / NW;        // cells per warp
+    constexpr int JPL = CPW / 32;          // cells per lane
+    static_assert(NCELL % NT == 0 && CPW % 32 == 0, "tile/block mismatch");
+    constexpr int Z = 2 * NDIM;
+    constexpr int SXY = SX * SY;
+
+    if (*(volatile unsigned int*)&P.ctl->done) return;
+
+    extern __shared__ __align__(16) unsigned long long smem[];
+    unsigned long long* S = smem;                                   // NSLOT words
+    unsigned long long* lr = S + NSLOT;                             // 512
+    unsigned long long* thr = lr + 512;                             // 16
+    unsigned long long* red = thr + 16;                             // NW
+    unsigned int* Nc = (unsigned int*)(red + NW);                   // NCELL counters
+    unsigned short* Q = (unsigned short*)(Nc + NCELL);              // NW * CPW queue
+
+    const Geo& g = P.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bt = blockIdx.x;
+    const int tx = bt % P.tiles_x;
+    const int ty = (bt / P.tiles_x) % P.tiles_y;
+    const int tz = bt / (P.tiles_x * P.tiles_y);
+    const int x0 = tx * TX, y0 = ty * TY, z0 = tz * TZ;
+    const bool full_tile = x0 + TX <= g.nx && y0 + TY <= g.ny && (NDIM == 2 || z0 + TZ <= g.nz);
+
+    for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
+    if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
+    for (int i = tid; i < NSLOT; i += NT) {
+        const int lx = i % SX - 1, ly = (i / SX) % SY - 1, lz = (NDIM == 3) ? i / SXY - 1 : 0;
+        const int out = (lx < 0 || lx >= TX) + (ly < 0 || ly >= TY) + ((NDIM == 3) && (lz < 0 || lz >= TZ));
+        if (out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
+    }
+    for (int o = tid; o < NCELL; o += NT) {
+        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+        const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+        unsigned int nv = 0;
+        if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
+            const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
+            nv = P.cnt[gi];
+        }
+        Nc[o] = nv;
+    }
+    __syncthreads();
+
+    volatile unsigned long long* VS = S;
+    const volatile unsigned int* VH = (const volatile unsigned int*)S;   // VH[2s+1] = high half of S[s]
+    const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
+    unsigned short* q = Q + warp * CPW;
+    const int wbase = warp * CPW;
+    unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0;
+    unsigned int rounds = 0;
+
+    for (int r = 0; r < P.rounds; ++r) {
+        // (i)+(ii): test and compact
+        int cnt = 0;
+#pragma unroll 4
+        for (int j = 0; j < JPL; ++j) {
+            const int o = wbase + lane + 32 * j;
+            const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+            const int s = (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 1;
+            bool e = false;
+            const unsigned long long w = VS[s];
+            bool valid = full_tile || (x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz));
+            if (valid && w < wlim) {
+                ++tested;
+                const unsigned int oh = (unsigned int)(w >> 32);
+                const unsigned int a = VH[2 * (s - 1) + 1], b = VH[2 * (s + 1) + 1];
+                const unsigned int c = VH[2 * (s - SX) + 1], d = VH[2 * (s + SX) + 1];
+                bool lt = oh < a && oh < b && oh < c && oh < d;
+                bool gt = oh > a || oh > b || oh > c || oh > d;
+                if (NDIM == 3) {
+                    const unsigned int ee = VH[2 * (s - SXY) + 1], ff = VH[2 * (s + SXY) + 1];
+                    lt = lt && oh < ee && oh < ff;
+                    gt = gt || oh > ee || oh > ff;
+                }
+                if (lt) {
+                    e = true;
+                } else if (!gt) {   // a tie in the high halves: decide on the full words
+                    e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
+                    if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+                }
+            }
+            const unsigned int m = __ballot_sync(0xffffffffu, e);
+            if (e) q[cnt + __popc(m & ((1u << lane) - 1u))] = (unsigned short)o;
+            cnt += __popc(m);
+        }
+        __syncwarp();
+        // (iii): fire the queued cells with the whole warp
+        for (int i = lane; i < cnt; i += 32) {
+            const int o = q[i];
+            const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+            const int s = (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 1;
+            const unsigned long long w = VS[s];
+            const volatile unsigned int* VL = (const volatile unsigned int*)S;
+            uint32_t ones = (VL[2 * (s - 1)] & 1u) + (VL[2 * (s + 1)] & 1u) + (VL[2 * (s - SX)] & 1u) +
+                            (VL[2 * (s + SX)] & 1u);
+            if (NDIM == 3) ones += (VL[2 * (s - SXY)] & 1u) + (VL[2 * (s + SXY)] & 1u);
+            const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+            const unsigned long long cid = NDIM == 2
+                ? (unsigned long long)(gy + g.y0) * g.nx + gx
+                : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
+            const unsigned int k = Nc[o];
+            const FireOut f = fire(w, ones, Z, k, cid, g.SH, thr, lr, P.key0, P.key1, P.inv_lambda,
+                                   P.tie_bits, P.do_hash);
+            VS[s] = f.wnew;
+            Nc[o] = k + 1;
+            hacc += f.h;
+            flips += f.flip;
+            ++fired;
+        }
+        ++rounds;
+        if (__syncthreads_count(cnt > 0) == 0) break;
+    }
+
+    unsigned long long active = 0;
+    for (int o = tid; o < NCELL; o += NT) {
+        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+        const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+        if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
+            const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
+            const unsigned long long w = S[(lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 1];
+            P.words[gi] = w;
+            P.cnt[gi] = Nc[o];
+            active += w < wlim;
+        }
+    }
+    const unsigned long long s_act = block_sum<NT>(active, red);
+    const unsigned long long s_fir = block_sum<NT>(fired, red);
+    const unsigned long long s_flp = block_sum<NT>(flips, red);
+    const unsigned long long s_tst = block_sum<NT>(tested, red);
+    const unsigned long long s_hsh = block_sum<NT>(hacc, red);
+    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds);
+}
+
 // ------------------------------------------------------------ whole-lattice kernel
 // One CTA holds the entire (small) lattice in shared memory with true periodic addressing
 // and runs rounds until no cell has t < T: the whole run_until in one launch. This is the

@@ -97,7 +97,7 @@ def test_config1_exact(aca, oracle_mod, sync):
     assert abs(st["arrivals"] - 40960) < 5 * 202
 
 
-@pytest.mark.parametrize("tile", [(64, 64), (32, 32), (64, 32), (128, 64), (128, 128)])
+@pytest.mark.parametrize("tile", [(64, 64), (32, 32), (64, 32), (128, 64)])
 def test_tiled_2d_ragged(aca, oracle_mod, tile):
     """Several tiles plus ragged tails in x and y."""
     g, o = run_pair(aca, oracle_mod, (200, 150), [2.0, 6.0], beta=0.40, rule=1, seed=11, tile=tile,
