@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--rounds", type=int, default=0, help="in-tile rounds per launch (0 = library default)")
     ap.add_argument("--tile", type=str, default="", help="e.g. 64x64 or 32x16x8")
     ap.add_argument("--launches-per-check", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=0, help="tile kernel variant (ablation; 0 = default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true", help="skip the P7 event hash (diagnostics only)")
@@ -214,6 +215,8 @@ def main():
         opts["rounds_per_launch"] = args.rounds
     if args.launches_per_check:
         opts["launches_per_check"] = args.launches_per_check
+    if args.variant:
+        opts["variant"] = args.variant
     stream = torch.cuda.Stream()            # non-default stream: the library captures CUDA graphs on it
     torch.cuda.set_stream(stream)
     opts["stream"] = stream.cuda_stream
@@ -280,7 +283,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
                        "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
-                       "tile": list(tile), "rounds_per_launch": args.rounds or 8,
+                       "tile": list(tile), "rounds_per_launch": args.rounds or 8, "variant": args.variant,
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
                        "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
                        "event_hash": not args.no_hash},

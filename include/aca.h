@@ -65,6 +65,9 @@ typedef struct {
     int32_t whole_lattice;      /* 1: one CTA holds the whole lattice with periodic
                                    addressing and runs to completion in one launch
                                    (small lattices, config 1); 0 = auto, -1 = never */
+    int32_t variant;            /* tile kernel (ablations): 0 = persistent, TMA-staged,
+                                   compacted (default); 1 = compacted, one CTA per tile;
+                                   2 = uncompacted. All give identical results. */
 } aca_options;
 
 typedef struct {

@@ -39,7 +39,7 @@ class aca_options(ctypes.Structure):
                 ("sync_rounds", ctypes.c_int32), ("device", ctypes.c_int32), ("shards", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("event_hash", ctypes.c_int32),
-                ("whole_lattice", ctypes.c_int32)]
+                ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32)]
 
 
 class aca_stats(ctypes.Structure):

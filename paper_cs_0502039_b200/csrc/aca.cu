@@ -138,6 +138,7 @@ struct aca_sim {
     bool whole = false;
     bool sync = false;
     size_t smem_tile = 0, smem_whole = 0;
+    int persistent_ctas = 0;       // > 0: grid size of the persistent tile kernel
     void* kern = nullptr;          // selected tile/whole kernel
     int nthreads = 256;
     cudaGraphExec_t graph = nullptr;
@@ -200,12 +201,21 @@ constexpr size_t tile2_smem(int ndim, int tx, int ty, int tz, int nt) {
     return tile_smem(ndim, tx, ty, tz, nt) + (size_t)tx * ty * tz * (4 + 2);
 }
 
-struct TileKey { int ndim, tx, ty, tz, nt; bool sync; void* fn; size_t smem; };
+constexpr size_t tile3_smem(int ndim, int tx, int ty, int tz, int nt) {
+    return ((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32 + 2) * 8 +
+           (size_t)tx * ty * tz * (4 + 2);
+}
 
-// async (default): compacted tile2_kernel; sync_rounds: two-barrier fig:s1c1pe tile_kernel
-#define TK(ND, TX, TY, TZ, NT, MB)                                                                   \
-    {ND, TX, TY, TZ, NT, false, (void*)tile2_kernel<ND, TX, TY, TZ, NT, MB>, tile2_smem(ND, TX, TY, TZ, NT)}, \
-    {ND, TX, TY, TZ, NT, true, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>, tile_smem(ND, TX, TY, TZ, NT)}
+// Variants: 0 = persistent TMA-staged compacted kernel (default), 1 = compacted, one CTA
+// per tile, 2 = uncompacted asynchronous, 3 = two-barrier fig:s1c1pe rounds (sync_rounds).
+struct TileKey { int ndim, tx, ty, tz, nt; void* fn[4]; size_t smem[4]; };
+
+#define TK(ND, TX, TY, TZ, NT, MB)                                                                  \
+    {ND, TX, TY, TZ, NT,                                                                            \
+     {(void*)tile3_kernel<ND, TX, TY, TZ, NT, MB>, (void*)tile2_kernel<ND, TX, TY, TZ, NT, MB>,     \
+      (void*)tile_kernel<ND, TX, TY, TZ, NT, false>, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}, \
+     {tile3_smem(ND, TX, TY, TZ, NT), tile2_smem(ND, TX, TY, TZ, NT), tile_smem(ND, TX, TY, TZ, NT), \
+      tile_smem(ND, TX, TY, TZ, NT)}}
 
 const TileKey kTiles[] = {
     TK(2, 32, 32, 1, 256, 4), TK(2, 64, 32, 1, 256, 4), TK(2, 64, 64, 1, 256, 3), TK(2, 128, 64, 1, 512, 1),
@@ -277,7 +287,8 @@ int launch_round(aca_sim* S) {
     for (auto& sh : S->shards) {
         KParams P = make_params(S, sh);
         void* args[] = {&P};
-        dim3 grid = S->whole ? dim3(1) : dim3(sh.tiles_x * sh.tiles_y * sh.tiles_z);
+        const int ntiles = sh.tiles_x * sh.tiles_y * sh.tiles_z;
+        dim3 grid = S->whole ? dim3(1) : dim3(S->persistent_ctas > 0 ? std::min(ntiles, S->persistent_ctas) : ntiles);
         CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->whole ? S->smem_whole : S->smem_tile,
                             S->stream));
     }
@@ -534,14 +545,23 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         if (ndim == 2) tz = 1;
         const TileKey* sel = nullptr;
         for (const auto& k : kTiles)
-            if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz && k.sync == S->sync) sel = &k;
+            if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz) sel = &k;
         if (!sel) return bail(fail(ACA_EINVAL, "unsupported tile %dx%dx%d for ndim %d", tx, ty, tz, ndim));
+        if (opt.variant < 0 || opt.variant > 2) return bail(fail(ACA_EINVAL, "variant must be 0, 1 or 2"));
+        const int v = S->sync ? 3 : opt.variant;
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
-        S->kern = sel->fn;
+        S->kern = sel->fn[v];
         S->nthreads = sel->nt;
-        S->smem_tile = sel->smem;
+        S->smem_tile = sel->smem[v];
         if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem_tile) != cudaSuccess)
             return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
+        if (v == 0) {   // persistent: as many CTAs as fit on the device at once
+            int nsm = 0, occ = 0;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, S->nthreads, S->smem_tile) != cudaSuccess || occ < 1)
+                return bail(fail(ACA_ECUDA, "occupancy query failed"));
+            S->persistent_ctas = nsm * occ;
+        }
     }
 
     // shards

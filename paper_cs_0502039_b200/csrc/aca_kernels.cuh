@@ -82,6 +82,39 @@ __device__ __forceinline__ unsigned long long ld_word(const KParams& P, int gx, 
     return P.words[((size_t)gz * g.ny + y) * g.nx + x];
 }
 
+// v in [-n, 2n): one conditional add/sub instead of an integer division
+__device__ __forceinline__ int wrap1(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+
+// ---------------------------------------------------------------- TMA bulk-copy helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}"
+        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// global -> shared bulk copy (size % 16 == 0, both addresses 16-B aligned), completes on bar
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// order earlier generic-proxy accesses of shared memory before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Block-wide sum of (u64) into ctl via one atomic per CTA.
 template <int NT>
 __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* red) {
@@ -453,6 +486,268 @@ __global__ void __launch_bounds__(NT, MINB) tile2_kernel(const KParams P) {
     const unsigned long long s_tst = block_sum<NT>(tested, red);
     const unsigned long long s_hsh = block_sum<NT>(hacc, red);
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds);
+}
+
+// ------------------------------------------------------------ persistent TMA tile kernel
+// tile2's rounds inside a persistent CTA that walks the tiles (tile = blockIdx.x + k*gridDim.x).
+// Staging of a full tile: the tile's own rows of words and counters arrive by TMA bulk
+// copies (cp.async.bulk, one mbarrier, ~48 KB in flight per CTA: no other CTA writes these
+// rows, so a bulk copy is safe); the face halo — words other CTAs may be updating in place —
+// is read with ordinary 8-byte loads (single-copy atomic, so a (t, s) pair is never torn).
+// Write-back uses 16-byte vector stores. Smem row stride TX+4 puts the interior of every
+// row on a 16-byte boundary. Ragged / odd-width tiles take the generic per-word path.
+__device__ __forceinline__ unsigned long long ld_word1(const KParams& P, int gx, int gy, int gz) {
+    const Geo& g = P.g;
+    const int x = wrap1(gx, g.nx);
+    if (g.ndim == 2) {
+        if (!g.sharded) return P.words[(size_t)wrap1(gy, g.ny) * g.nx + x];
+        if (gy < 0) return P.halo_lo[x];
+        if (gy >= g.ny) return P.halo_hi[x];
+        return P.words[(size_t)gy * g.nx + x];
+    }
+    const int y = wrap1(gy, g.ny);
+    if (!g.sharded) return P.words[((size_t)wrap1(gz, g.nz) * g.ny + y) * g.nx + x];
+    if (gz < 0) return P.halo_lo[(size_t)y * g.nx + x];
+    if (gz >= g.nz) return P.halo_hi[(size_t)y * g.nx + x];
+    return P.words[((size_t)gz * g.ny + y) * g.nx + x];
+}
+
+template <int NDIM, int TX, int TY, int TZ, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) tile3_kernel(const KParams P) {
+    constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
+    constexpr int SXY = SX * SY;
+    constexpr int NSLOT = SXY * SZ;
+    constexpr int NCELL = TX * TY * TZ;
+    constexpr int NROWS = TY * TZ;
+    constexpr int NW = NT / 32;
+    constexpr int CPW = NCELL / NW;
+    constexpr int JPL = CPW / 32;
+    constexpr int Z = 2 * NDIM;
+    constexpr int NHALO = NDIM == 2 ? 2 * (TX + TY) : 2 * (TX * TY + TX * TZ + TY * TZ);
+    static_assert(NCELL % NT == 0 && CPW % 32 == 0 && TX % 4 == 0, "tile/block mismatch");
+
+    if (*(volatile unsigned int*)&P.ctl->done) return;
+
+    extern __shared__ __align__(128) unsigned long long smem[];
+    unsigned long long* S = smem;                                   // NSLOT words
+    unsigned long long* lr = S + NSLOT;                             // 512
+    unsigned long long* thr = lr + 512;                             // 16
+    unsigned long long* red = thr + 16;                             // NW
+    unsigned long long* bar = red + NW;                             // 1 (+1 pad)
+    unsigned int* Nc = (unsigned int*)(bar + 2);                    // NCELL counters (16-B aligned)
+    unsigned short* Q = (unsigned short*)(Nc + NCELL);              // NW * CPW queue
+
+    const Geo& g = P.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
+    if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
+    if (tid == 0) mbar_init(bar, 1);
+    __syncthreads();
+
+    auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2; };
+    volatile unsigned long long* VS = S;
+    const volatile unsigned int* VH = (const volatile unsigned int*)S;   // [2s+1]: high half, [2s]: low half
+    const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
+    unsigned short* q = Q + warp * CPW;
+    const int wbase = warp * CPW;
+    const int ntiles = P.tiles_x * P.tiles_y * P.tiles_z;
+    const bool vec_ok = (g.nx % 4) == 0;
+    unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0, active = 0;
+    unsigned int rounds_max = 0;
+    uint32_t parity = 0;
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int tx = tile % P.tiles_x;
+        const int ty = (tile / P.tiles_x) % P.tiles_y;
+        const int tz = tile / (P.tiles_x * P.tiles_y);
+        const int x0 = tx * TX, y0 = ty * TY, z0 = tz * TZ;
+        const bool full = x0 + TX <= g.nx && y0 + TY <= g.ny && (NDIM == 2 || z0 + TZ <= g.nz);
+        const bool fast = full && vec_ok;
+
+        // ------------------------------------------------ stage
+        if (fast) {
+            if (warp == 0) {
+                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)NROWS * TX * 12u);
+                __syncwarp();
+                fence_proxy_async();
+                for (int row = lane; row < NROWS; row += 32) {
+                    const int ly = row % TY, lz = row / TY;
+                    const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
+                                                : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
+                    bulk_g2s(&S[slot(0, ly, lz)], P.words + gi, TX * 8, bar);
+                    bulk_g2s(&Nc[row * TX], P.cnt + gi, TX * 4, bar);
+                }
+            }
+            for (int h = tid; h < NHALO; h += NT) {
+                int lx, ly, lz = 0;
+                if (NDIM == 2) {
+                    if (h < TX) { lx = h; ly = -1; }
+                    else if (h < 2 * TX) { lx = h - TX; ly = TY; }
+                    else if (h < 2 * TX + TY) { lx = -1; ly = h - 2 * TX; }
+                    else { lx = TX; ly = h - 2 * TX - TY; }
+                } else {
+                    int r = h;
+                    if (r < 2 * TX * TY) { lz = r < TX * TY ? -1 : TZ; r %= TX * TY; lx = r % TX; ly = r / TX; }
+                    else if ((r -= 2 * TX * TY) < 2 * TX * TZ) {
+                        ly = r < TX * TZ ? -1 : TY; r %= TX * TZ; lx = r % TX; lz = r / TX;
+                    } else {
+                        r -= 2 * TX * TZ;
+                        lx = r < TY * TZ ? -1 : TX; r %= TY * TZ; ly = r % TY; lz = r / TY;
+                    }
+                }
+                S[slot(lx, ly, lz)] = ld_word1(P, x0 + lx, y0 + ly, z0 + lz);
+            }
+            mbar_wait(bar, parity);
+            parity ^= 1u;
+        } else {
+            for (int i = tid; i < NSLOT; i += NT) {
+                const int lx = i % SX - 2, ly = (i / SX) % SY - 1, lz = (NDIM == 3) ? i / SXY - 1 : 0;
+                if (lx < -1 || lx > TX) continue;
+                const int out = (lx < 0 || lx >= TX) + (ly < 0 || ly >= TY) + ((NDIM == 3) && (lz < 0 || lz >= TZ));
+                if (out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
+            }
+            for (int o = tid; o < NCELL; o += NT) {
+                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+                unsigned int nv = 0;
+                if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
+                    const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
+                    nv = P.cnt[gi];
+                }
+                Nc[o] = nv;
+            }
+        }
+        __syncthreads();
+
+        // ------------------------------------------------ rounds
+        // Lane `lane` of warp `warp` owns cells o_j = warp*CPW + lane + 32 j. With FASTMAP the
+        // slot of o_j is s_0 + const(j): all shared-memory addresses become immediates.
+        constexpr bool FASTMAP = (TX % 32 == 0) && (CPW % TX == 0) && (TY % (CPW / TX == 0 ? 1 : CPW / TX) == 0);
+        constexpr int LPR = TX / 32 > 0 ? TX / 32 : 1;                  // lane-groups per row
+        int s0 = 0;
+        if (FASTMAP) {
+            const int row0 = warp * (CPW / TX);
+            s0 = slot(lane, row0 % TY, row0 / TY);
+        }
+        unsigned int rounds = 0;
+        for (int r = 0; r < P.rounds; ++r) {
+            uint32_t emask = 0, amask = 0;
+#pragma unroll
+            for (int j = 0; j < JPL; ++j) {
+                int s;
+                bool valid = true;
+                if (FASTMAP) {
+                    s = s0 + (j / LPR) * SX + 32 * (j % LPR);
+                    if (!full) {
+                        const int o = wbase + lane + 32 * j;
+                        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                        valid = x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz);
+                    }
+                } else {
+                    const int o = wbase + lane + 32 * j;
+                    const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                    s = slot(lx, ly, lz);
+                    valid = full || (x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz));
+                }
+                const unsigned long long w = VS[s];
+                const bool act = valid && w < wlim;
+                if (act) {
+                    const unsigned int oh = (unsigned int)(w >> 32);
+                    unsigned int mn = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]),
+                                          min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
+                    if (NDIM == 3) mn = min(mn, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
+                    bool e = oh < mn;
+                    if (oh == mn) {   // tie in the high halves: decide on the full words
+                        e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
+                        if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+                    }
+                    emask |= (uint32_t)e << j;
+                }
+                amask |= (uint32_t)act << j;
+            }
+            tested += __popc(amask);
+            // compaction: warp-exclusive scan of the per-lane counts
+            const int mine = __popc(emask);
+            int incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            const int cnt = __shfl_sync(0xffffffffu, incl, 31);
+            int pos = incl - mine;
+            while (emask) {
+                const int j = __ffs(emask) - 1;
+                emask &= emask - 1u;
+                q[pos++] = (unsigned short)(wbase + lane + 32 * j);
+            }
+            __syncwarp();
+            for (int i = lane; i < cnt; i += 32) {
+                const int o = q[i];
+                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                const int s = slot(lx, ly, lz);
+                const unsigned long long w = VS[s];
+                uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
+                                (VH[2 * (s + SX)] & 1u);
+                if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
+                const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+                const unsigned long long cid = NDIM == 2
+                    ? (unsigned long long)(gy + g.y0) * g.nx + gx
+                    : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
+                const unsigned int k = Nc[o];
+                const FireOut f = fire(w, ones, Z, k, cid, g.SH, thr, lr, P.key0, P.key1, P.inv_lambda,
+                                       P.tie_bits, P.do_hash);
+                VS[s] = f.wnew;
+                Nc[o] = k + 1;
+                hacc += f.h;
+                flips += f.flip;
+                ++fired;
+            }
+            ++rounds;
+            if (__syncthreads_count(cnt > 0) == 0) break;
+        }
+        rounds_max = rounds > rounds_max ? rounds : rounds_max;
+        __syncthreads();
+
+        // ------------------------------------------------ write back
+        if (fast) {
+            for (int idx = tid; idx < NROWS * (TX / 2); idx += NT) {
+                const int row = idx / (TX / 2), m2 = 2 * (idx % (TX / 2));
+                const int ly = row % TY, lz = row / TY;
+                const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
+                                            : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&S[slot(m2, ly, lz)]);
+                *reinterpret_cast<ulonglong2*>(P.words + gi + m2) = v;
+                active += (v.x < wlim) + (v.y < wlim);
+            }
+            for (int idx = tid; idx < NROWS * (TX / 4); idx += NT) {
+                const int row = idx / (TX / 4), m4 = 4 * (idx % (TX / 4));
+                const int ly = row % TY, lz = row / TY;
+                const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
+                                            : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
+                *reinterpret_cast<uint4*>(P.cnt + gi + m4) = *reinterpret_cast<const uint4*>(&Nc[row * TX + m4]);
+            }
+        } else {
+            for (int o = tid; o < NCELL; o += NT) {
+                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+                if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
+                    const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
+                    const unsigned long long w = S[slot(lx, ly, lz)];
+                    P.words[gi] = w;
+                    P.cnt[gi] = Nc[o];
+                    active += w < wlim;
+                }
+            }
+        }
+        __syncthreads();   // smem is rewritten by the next tile's staging
+    }
+    const unsigned long long s_act = block_sum<NT>(active, red);
+    const unsigned long long s_fir = block_sum<NT>(fired, red);
+    const unsigned long long s_flp = block_sum<NT>(flips, red);
+    const unsigned long long s_tst = block_sum<NT>(tested, red);
+    const unsigned long long s_hsh = block_sum<NT>(hacc, red);
+    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max);
 }
 
 // ------------------------------------------------------------ whole-lattice kernel
