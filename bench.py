@@ -122,15 +122,15 @@ def ncu_traffic(kernel_tag):
 
 
 def algorithmic_bytes_per_cell(ndim, tile):
-    """Per launch (in-place, 1-cell halo): read word (8 B) + counter (4 B), write both back,
-    plus the halo words of the tile faces. DESIGN.md 'Roofline'."""
+    """Per launch (in place, 1-cell halo): read each cell's packed word (t, rank, n, s: 8 B)
+    and write it back (8 B), plus the halo words of the tile faces. DESIGN.md 'Roofline'."""
     if ndim == 2:
         tx, ty = tile[0], tile[1]
         halo = 8.0 * 2 * (tx + ty) / (tx * ty)
     else:
         tx, ty, tz = tile
         halo = 8.0 * 2 * (tx * ty + ty * tz + tx * tz) / (tx * ty * tz)
-    return 24.0 + halo
+    return 16.0 + halo
 
 
 def oracle_sample(cfg, seconds_target=10.0):
@@ -283,7 +283,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
                        "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
-                       "tile": list(tile), "rounds_per_launch": args.rounds or 8, "variant": args.variant,
+                       "tile": list(tile), "rounds_per_launch": args.rounds or 3, "variant": args.variant,
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
                        "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
                        "event_hash": not args.no_hash},

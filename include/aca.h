@@ -65,9 +65,10 @@ typedef struct {
     int32_t whole_lattice;      /* 1: one CTA holds the whole lattice with periodic
                                    addressing and runs to completion in one launch
                                    (small lattices, config 1); 0 = auto, -1 = never */
-    int32_t variant;            /* tile kernel (ablations): 0 = persistent, TMA-staged,
-                                   compacted (default); 1 = compacted, one CTA per tile;
-                                   2 = uncompacted. All give identical results. */
+    int32_t variant;            /* tile kernel (ablations): 0 = persistent, double-buffered
+                                   TMA staging, compacted firing (default); 1 = compacted,
+                                   one CTA per tile; 2 = uncompacted; 3 = persistent,
+                                   single-buffered TMA. All give identical results. */
 } aca_options;
 
 typedef struct {
@@ -84,6 +85,7 @@ typedef struct {
     double gpu_seconds;     /* CUDA-event time inside aca_run_until calls */
     double kernel_seconds;  /* CUDA-event time of the kernel batches alone */
     uint64_t kernel_launches; /* every tile-kernel launch issued (incl. no-op tail) */
+    int32_t time_bits, counter_bits, rank_bits; /* current split of the packed state word */
 } aca_stats;
 
 /* Fill *opt with defaults (struct_size set). */
@@ -105,6 +107,10 @@ int aca_run_until_q32(aca_sim* s, uint64_t T_q32);
 int aca_get_spins(aca_sim* s, int8_t* out, size_t count);
 int aca_get_times(aca_sim* s, uint64_t* out, size_t count);   /* pending arrival, Q32 */
 int aca_get_counters(aca_sim* s, uint32_t* out, size_t count); /* n(c) */
+/* Sampled cells: for i < m, cell idx[i] (row-major, handle-local) -> spins[i], times[i],
+ * counters[i]; any output pointer may be NULL. Gathered on the device (no full copy). */
+int aca_get_cells(aca_sim* s, const int64_t* idx, size_t m, int8_t* spins, uint64_t* times,
+                  uint32_t* counters);
 /* Statistics (device reductions; synchronises). */
 int aca_get_stats(aca_sim* s, aca_stats* out);
 /* P4 table: count = 10 (2-D) or 14 (3-D), index (Sigma+z)/2 + (z+1)(s+1)/2. */

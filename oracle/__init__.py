@@ -92,6 +92,12 @@ def lib():
         L.oracle_cell_time_counter.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                                ctypes.c_uint64, ctypes.c_int,
                                                ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)]
+        L.oracle_window_cell.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                         ctypes.c_uint64, ctypes.c_double, ctypes.c_int, ctypes.c_uint64,
+                                         ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, ctypes.c_int,
+                                         ctypes.POINTER(ctypes.c_int8), ctypes.POINTER(ctypes.c_uint64),
+                                         ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
         _lib = L
     return _lib
 
@@ -229,3 +235,15 @@ def time_weighted_hist(dims, beta, J=1.0, h=0.0, rule=HEATBATH, seed=1, T0=50.0,
                                          to_q32(T0), to_q32(T1), w.ctypes.data)
     assert rc == 0
     return w
+
+
+def window_cell(dims, center, T, radius, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1, init_q=0.5,
+                tie_bits=0, refine=True):
+    """Exact (s, t, n, exact) of the cell at `center` (x, y[, z]) after run_until(T), from a
+    box of the given radius (light-cone oracle; see aca_oracle.c). exact=False: enlarge."""
+    so, to, no, ex = ctypes.c_int8(), ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_int()
+    rc = lib().oracle_window_cell(len(dims), _dims(dims), lam, beta, J, h, rule, seed, init_q, tie_bits,
+                                  to_q32(T), _dims(center), radius, 1 if refine else 0, ctypes.byref(so),
+                                  ctypes.byref(to), ctypes.byref(no), ctypes.byref(ex))
+    assert rc == 0
+    return so.value, to.value, no.value, bool(ex.value)

@@ -436,3 +436,125 @@ void oracle_cell_time_counter(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_
     *t_out = t;
     *n_out = k;
 }
+
+/* ---------------------------------------------------------------- window (light-cone) oracle
+ * Exact (s, t, n) of one cell of a lattice too large to simulate whole. A box of radius
+ * `radius` around the cell is simulated in (t, c) order with the cells' true global ids and
+ * streams; times and counters are exact everywhere (state-independent).
+ * A cell's spin is exact unless information from outside the box can have reached it: a
+ * cell becomes "unknown" when it processes an arrival whose flip decision depends on an
+ * unknown neighbour spin (a neighbour outside the box or itself unknown). With refine = 1 a
+ * decision that comes out the same for every possible value of the unknown spins stays
+ * exact (e.g. a rejection at low temperature). Causality (fig:amcgen):
+ * known spins are the true spins. *exact_out = 0 if the target ended unknown (enlarge the box). */
+typedef struct { uint64_t t; uint64_t gc; int64_t lc; } wev;
+
+static int wev_less(const wev* a, const wev* b) { return a->t < b->t || (a->t == b->t && a->gc < b->gc); }
+
+int oracle_window_cell(int ndim, const int64_t* dims, double lambda, double beta, double J, double h, int rule,
+                       uint64_t seed, double init_q, int tie_bits, uint64_t T, const int64_t* center,
+                       int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
+                       int* exact_out) {
+    int64_t D[3] = {1, 1, 1}, W[3] = {1, 1, 1}, lo[3] = {0, 0, 0};
+    int fullax[3] = {1, 1, 1};
+    int64_t NW = 1;
+    for (int a = 0; a < ndim; a++) {
+        D[a] = dims[a];
+        if (2 * radius + 1 >= D[a]) { W[a] = D[a]; lo[a] = 0; fullax[a] = 1; }
+        else { W[a] = 2 * radius + 1; lo[a] = center[a] - radius; fullax[a] = 0; }
+        NW *= W[a];
+    }
+    int zc = 2 * ndim;
+    uint64_t thr[14];
+    oracle_flip_table(ndim, beta, J, h, rule, thr);
+    uint64_t inv = oracle_inv_lambda(lambda);
+    uint64_t thr_init = (uint64_t)floor(init_q * 4294967296.0);
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    int8_t* s = (int8_t*)malloc((size_t)NW);
+    uint8_t* unk = (uint8_t*)calloc((size_t)NW, 1);
+    uint64_t* t = (uint64_t*)malloc((size_t)NW * 8);
+    uint32_t* n = (uint32_t*)calloc((size_t)NW, 4);
+    uint64_t* gid = (uint64_t*)malloc((size_t)NW * 8);
+    int64_t* nb = (int64_t*)malloc((size_t)NW * 6 * 8);    /* -1: outside the box */
+    wev* heap = (wev*)malloc((size_t)NW * sizeof(wev));
+    if (!s || !unk || !t || !n || !gid || !nb || !heap) return -1;
+    for (int64_t l = 0; l < NW; l++) {
+        int64_t lx = l % W[0], ly = (l / W[0]) % W[1], lz = l / (W[0] * W[1]);
+        int64_t L[3] = {lx, ly, lz}, G[3];
+        for (int a = 0; a < 3; a++) G[a] = (((lo[a] + L[a]) % D[a]) + D[a]) % D[a];
+        gid[l] = (uint64_t)((G[2] * D[1] + G[1]) * D[0] + G[0]);
+        for (int a = 0; a < ndim; a++) {
+            for (int dir = 0; dir < 2; dir++) {
+                int64_t M[3] = {L[0], L[1], L[2]};
+                M[a] += dir ? 1 : -1;
+                int64_t r;
+                if (fullax[a]) { M[a] = (M[a] + W[a]) % W[a]; r = (M[2] * W[1] + M[1]) * W[0] + M[0]; }
+                else if (M[a] < 0 || M[a] >= W[a]) r = -1;
+                else r = (M[2] * W[1] + M[1]) * W[0] + M[0];
+                nb[l * 6 + 2 * a + dir] = r;
+            }
+        }
+        uint32_t ctr[4] = {0, (uint32_t)(gid[l] & 0xffffffffu), (uint32_t)(gid[l] >> 32), 1u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        s[l] = ((uint64_t)w[0] < thr_init) ? -1 : 1;
+        t[l] = oracle_delta(w[1], w[2], inv, tie_bits);
+    }
+    /* binary heap of (t, global id, local id) */
+    int64_t hn = 0;
+    for (int64_t l = 0; l < NW; l++) {
+        wev e = {t[l], gid[l], l};
+        int64_t i = hn++;
+        heap[i] = e;
+        while (i > 0) {
+            int64_t p = (i - 1) / 2;
+            if (!wev_less(&heap[i], &heap[p])) break;
+            wev tmp = heap[i]; heap[i] = heap[p]; heap[p] = tmp; i = p;
+        }
+    }
+    while (hn > 0 && heap[0].t < T) {
+        int64_t c = heap[0].lc;
+        int known = 0, u = 0;
+        for (int j = 0; j < zc; j++) {
+            int64_t m = nb[c * 6 + j];
+            if (m < 0 || unk[m]) u++; else known += s[m];
+        }
+        uint32_t ctr[4] = {n[c], (uint32_t)(gid[c] & 0xffffffffu), (uint32_t)(gid[c] >> 32), 0u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        if (!unk[c]) {
+            int sc = s[c];
+            if (u == 0) {
+                int idx = (known + zc) / 2 + (zc + 1) * (sc + 1) / 2;
+                if ((uint64_t)w[0] < thr[idx]) s[c] = (int8_t)-sc;
+            } else if (refine) {
+                int f0 = -1, same = 1;
+                for (int k = 0; k <= u; k++) {
+                    int sigma = known + 2 * k - u;
+                    int idx = (sigma + zc) / 2 + (zc + 1) * (sc + 1) / 2;
+                    int f = (uint64_t)w[0] < thr[idx];
+                    if (f0 < 0) f0 = f; else if (f != f0) same = 0;
+                }
+                if (same) { if (f0) s[c] = (int8_t)-sc; }
+                else unk[c] = 1;
+            } else {
+                unk[c] = 1;
+            }
+        }
+        t[c] += oracle_delta(w[1], w[2], inv, tie_bits);
+        n[c] += 1;
+        heap[0].t = t[c];
+        int64_t i = 0;
+        for (;;) {
+            int64_t l = 2 * i + 1, r = l + 1, m = i;
+            if (l < hn && wev_less(&heap[l], &heap[m])) m = l;
+            if (r < hn && wev_less(&heap[r], &heap[m])) m = r;
+            if (m == i) break;
+            wev tmp = heap[i]; heap[i] = heap[m]; heap[m] = tmp; i = m;
+        }
+    }
+    int64_t L[3] = {0, 0, 0};
+    for (int a = 0; a < ndim; a++) L[a] = fullax[a] ? center[a] : radius;
+    int64_t tc = (L[2] * W[1] + L[1]) * W[0] + L[0];
+    *s_out = s[tc]; *t_out = t[tc]; *n_out = n[tc]; *exact_out = !unk[tc];
+    free(s); free(unk); free(t); free(n); free(gid); free(nb); free(heap);
+    return 0;
+}

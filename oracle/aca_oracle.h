@@ -78,6 +78,13 @@ void oracle_nlog_batch(int64_t n, const uint64_t* X, uint64_t* q);
 void oracle_cell_time_counter(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_t inv_lambda,
                               int tie_bits, uint64_t* t_out, uint32_t* n_out);
 
+/* Window (light-cone) oracle: exact (s, t, n) of the cell at `center` after run_until(T) on
+ * a lattice too large to simulate whole; *exact_out = 0 when the box was too small. */
+int oracle_window_cell(int ndim, const int64_t* dims, double lambda, double beta, double J, double h, int rule,
+                       uint64_t seed, double init_q, int tie_bits, uint64_t T_q32, const int64_t* center,
+                       int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
+                       int* exact_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: 
 
 # symbols declared in include/aca.h (checked by tests/test_abi.py)
 EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
-           "aca_get_times", "aca_get_counters", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
+           "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
            "aca_selftest_nlog"]
 
@@ -48,7 +48,8 @@ class aca_stats(ctypes.Structure):
                 ("t_max", ctypes.c_uint64), ("launches", ctypes.c_uint64), ("inner_rounds", ctypes.c_uint64),
                 ("cells_tested", ctypes.c_uint64), ("cells_fired", ctypes.c_uint64),
                 ("gpu_seconds", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
-                ("kernel_launches", ctypes.c_uint64)]
+                ("kernel_launches", ctypes.c_uint64), ("time_bits", ctypes.c_int32),
+                ("counter_bits", ctypes.c_int32), ("rank_bits", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -80,6 +81,7 @@ def lib():
     for n in ("aca_get_spins", "aca_get_times", "aca_get_counters", "aca_set_spins"):
         getattr(L, n).argtypes = [vp, vp, ctypes.c_size_t]
     L.aca_get_stats.argtypes = [vp, ctypes.POINTER(aca_stats)]
+    L.aca_get_cells.argtypes = [vp, vp, ctypes.c_size_t, vp, vp, vp]
     L.aca_get_flip_table.argtypes = [vp, vp, ctypes.c_size_t]
     L.aca_set_state.argtypes = [vp, vp, vp, vp, ctypes.c_size_t]
     L.aca_reset.argtypes = [vp, ctypes.c_uint64]
@@ -163,6 +165,16 @@ def aca_get_counters(p, out=None):
     out = np.empty(n, np.uint32) if out is None else out
     _check(lib().aca_get_counters(p, _ptr(out), n))
     return out
+
+
+def aca_get_cells(p, idx):
+    idx = np.ascontiguousarray(idx, np.int64)
+    m = idx.size
+    s = np.empty(m, np.int8)
+    t = np.empty(m, np.uint64)
+    n = np.empty(m, np.uint32)
+    _check(lib().aca_get_cells(p, _ptr(idx), m, _ptr(s), _ptr(t), _ptr(n)))
+    return s, t, n
 
 
 def aca_get_stats(p):
@@ -277,6 +289,9 @@ class Sim:
 
     def stats(self):
         return aca_get_stats(self._p)
+
+    def cells(self, idx):
+        return aca_get_cells(self._p, idx)
 
     def flip_table(self):
         return aca_get_flip_table(self._p, self.ndim)

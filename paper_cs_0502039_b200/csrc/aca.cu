@@ -1,11 +1,13 @@
 // aca.cu — C-ABI runtime of the B200 path (include/aca.h). Host side: validation, P4 table,
-// device allocation, shard/halo bookkeeping, the outer-round loop (CUDA-graph replay of K
-// launches, device-side termination), statistics and getters. Every step of the method
-// runs in the kernels of aca_kernels.cuh; nothing here computes a trajectory.
+// device allocation, the packed-word layout, shard/halo bookkeeping, the outer-round loop
+// (CUDA-graph replay of K launches, device-side termination, two batches in flight),
+// statistics and getters. Every step of the method runs in the kernels of aca_kernels.cuh;
+// nothing here computes a trajectory.
 #include <cuda_runtime.h>
 #include <curand_kernel.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -53,7 +55,6 @@ typedef int (*ncclSend_fn)(const void*, size_t, int, int, ncclComm_t, cudaStream
 typedef int (*ncclRecv_fn)(void*, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*ncclGroup_fn)(void);
 typedef int (*ncclAllReduce_fn)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
-typedef const char* (*ncclGetErrorString_fn)(int);
 typedef int (*ncclGetUniqueId_fn)(ncclUniqueId_t*);
 struct NcclApi {
     ncclCommInitRank_fn init = nullptr;
@@ -62,7 +63,6 @@ struct NcclApi {
     ncclRecv_fn recv = nullptr;
     ncclGroup_fn gstart = nullptr, gend = nullptr;
     ncclAllReduce_fn allreduce = nullptr;
-    ncclGetErrorString_fn errstr = nullptr;
     ncclGetUniqueId_fn uid = nullptr;
     bool ok = false;
 };
@@ -88,18 +88,16 @@ NcclApi& nccl() {
         api.gstart = (ncclGroup_fn)sym("ncclGroupStart");
         api.gend = (ncclGroup_fn)sym("ncclGroupEnd");
         api.allreduce = (ncclAllReduce_fn)sym("ncclAllReduce");
-        api.errstr = (ncclGetErrorString_fn)sym("ncclGetErrorString");
         api.uid = (ncclGetUniqueId_fn)sym("ncclGetUniqueId");
         api.ok = api.init && api.destroy && api.send && api.recv && api.gstart && api.gend && api.allreduce;
     }
     return api;
 }
-constexpr int NCCL_UINT8 = 1, NCCL_UINT64 = 5, NCCL_INT64 = 4, NCCL_SUM = 0, NCCL_MIN = 3, NCCL_MAX = 2;
+constexpr int NCCL_UINT8 = 1, NCCL_UINT64 = 5, NCCL_SUM = 0;
 
 struct Shard {
     Geo g{};
     unsigned long long* words = nullptr;
-    unsigned int* cnt = nullptr;
     unsigned long long* halo_lo = nullptr;  // 1 row (2-D) / plane (3-D)
     unsigned long long* halo_hi = nullptr;
     Ctl* ctl = nullptr;
@@ -119,7 +117,7 @@ struct aca_sim {
     uint64_t seed = 0;
     aca_options opt{};
     int device = 0;
-    int SH = 1;
+    int RB = 1, NB = 1, TB = 1;    // packed word: time bits, rank bits, counter bits (+1 spin)
     unsigned long long inv_lambda = 1ull << 32;
     unsigned long long thr[14] = {};
     unsigned long long thr_init = 0;
@@ -137,13 +135,13 @@ struct aca_sim {
     int K = 16;
     bool whole = false;
     bool sync = false;
-    size_t smem_tile = 0, smem_whole = 0;
+    size_t smem = 0;
     int persistent_ctas = 0;       // > 0: grid size of the persistent tile kernel
     void* kern = nullptr;          // selected tile/whole kernel
     int nthreads = 256;
     cudaGraphExec_t graph = nullptr;
     int graph_rounds = 0;
-    Ctl* h_ctl = nullptr;          // pinned mirror (per shard)
+    Ctl* h_ctl = nullptr;          // pinned mirror (2 slots per shard)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t evb[2][3] = {};    // per in-flight batch: start, end of kernels, end of ctl copy
     unsigned long long* d_flag = nullptr;
@@ -197,42 +195,47 @@ int bits_for(uint64_t v) {
 constexpr size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
     return ((size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32) * 8;
 }
-constexpr size_t tile2_smem(int ndim, int tx, int ty, int tz, int nt) {
-    return tile_smem(ndim, tx, ty, tz, nt) + (size_t)tx * ty * tz * (4 + 2);
+constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf) {
+    return ((((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~(size_t)15) * nbuf + 512 + 16 +
+            nt / 32 + 2) * 8 + (size_t)tx * ty * tz * 2;
 }
 
-constexpr size_t tile3_smem(int ndim, int tx, int ty, int tz, int nt) {
-    return ((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32 + 2) * 8 +
-           (size_t)tx * ty * tz * (4 + 2);
-}
+// Kernel variants (identical results; ablations): 0 = persistent TMA-staged compacted kernel
+// (default), 1 = uncompacted one-CTA-per-tile kernel, 2 = persistent, double-buffered TMA.
+// Slot NVARIANT = two-barrier fig:s1c1pe rounds (sync_rounds = 1).
+constexpr int NVARIANT = 3;
+struct TileKey { int ndim, tx, ty, tz, nt; void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1]; };
 
-// Variants: 0 = persistent TMA-staged compacted kernel (default), 1 = compacted, one CTA
-// per tile, 2 = uncompacted asynchronous, 3 = two-barrier fig:s1c1pe rounds (sync_rounds).
-struct TileKey { int ndim, tx, ty, tz, nt; void* fn[4]; size_t smem[4]; };
-
-#define TK(ND, TX, TY, TZ, NT, MB)                                                                  \
-    {ND, TX, TY, TZ, NT,                                                                            \
-     {(void*)tile3_kernel<ND, TX, TY, TZ, NT, MB>, (void*)tile2_kernel<ND, TX, TY, TZ, NT, MB>,     \
-      (void*)tile_kernel<ND, TX, TY, TZ, NT, false>, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}, \
-     {tile3_smem(ND, TX, TY, TZ, NT), tile2_smem(ND, TX, TY, TZ, NT), tile_smem(ND, TX, TY, TZ, NT), \
-      tile_smem(ND, TX, TY, TZ, NT)}}
+#define TK(ND, TX, TY, TZ, NT, MB, MBD)                                                              \
+    {ND, TX, TY, TZ, NT,                                                                             \
+     {(void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false>, (void*)tile_kernel<ND, TX, TY, TZ, NT, false>, \
+      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBD, true>, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}, \
+     {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
+      tile_smem(ND, TX, TY, TZ, NT)},                                                                \
+     {true, false, true, false}}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256, 4), TK(2, 64, 32, 1, 256, 4), TK(2, 64, 64, 1, 256, 3), TK(2, 128, 64, 1, 512, 1),
-    TK(3, 8, 8, 8, 128, 8), TK(3, 16, 16, 16, 256, 2), TK(3, 32, 16, 8, 256, 2), TK(3, 32, 32, 8, 512, 1),
+    TK(2, 32, 32, 1, 256, 4, 4), TK(2, 64, 32, 1, 256, 4, 3), TK(2, 64, 64, 1, 256, 3, 2), TK(2, 128, 64, 1, 512, 1, 1),
+    TK(3, 8, 8, 8, 128, 8, 4), TK(3, 16, 16, 16, 256, 2, 1), TK(3, 32, 16, 8, 256, 2, 1), TK(3, 32, 32, 8, 512, 1, 1),
 };
 
 constexpr int WHOLE_NT = 1024;
-
 size_t whole_smem(int64_t n, bool sync) {
-    return (size_t)n * 8 + (512 + 16 + WHOLE_NT / 32) * 8 + (sync ? (size_t)n * 8 : 0) + (size_t)n * 4;
+    return (size_t)n * 8 + (512 + 16 + WHOLE_NT / 32) * 8 + (sync ? (size_t)n * 8 : 0);
+}
+
+void set_geo_layout(aca_sim* S) {
+    for (auto& sh : S->shards) {
+        sh.g.RB = S->RB;
+        sh.g.NB = S->NB;
+        sh.g.TSH = S->RB + S->NB + 1;
+    }
 }
 
 KParams make_params(const aca_sim* S, const Shard& sh) {
     KParams P{};
     P.g = sh.g;
     P.words = sh.words;
-    P.cnt = sh.cnt;
     P.halo_lo = sh.halo_lo;
     P.halo_hi = sh.halo_hi;
     P.ctl = sh.ctl;
@@ -289,10 +292,14 @@ int launch_round(aca_sim* S) {
         void* args[] = {&P};
         const int ntiles = sh.tiles_x * sh.tiles_y * sh.tiles_z;
         dim3 grid = S->whole ? dim3(1) : dim3(S->persistent_ctas > 0 ? std::min(ntiles, S->persistent_ctas) : ntiles);
-        CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->whole ? S->smem_whole : S->smem_tile,
-                            S->stream));
+        CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->smem, S->stream));
     }
     return ACA_OK;
+}
+
+void drop_graph(aca_sim* S) {
+    if (S->graph) cudaGraphExecDestroy(S->graph);
+    S->graph = nullptr;
 }
 
 int build_graph(aca_sim* S) {
@@ -354,11 +361,61 @@ int init_state(aca_sim* S) {
     const uint32_t k0 = (uint32_t)(S->seed & 0xffffffffu), k1 = (uint32_t)(S->seed >> 32);
     for (auto& sh : S->shards) {
         CK(cudaMemsetAsync(sh.ctl, 0, sizeof(Ctl), S->stream));
-        init_kernel<<<1184, 256, 0, S->stream>>>(sh.words, sh.cnt, sh.g, S->d_lr, k0, k1, S->thr_init, S->inv_lambda,
+        init_kernel<<<1184, 256, 0, S->stream>>>(sh.words, sh.g, S->d_lr, k0, k1, S->thr_init, S->inv_lambda,
                                                   S->opt.tie_bits, (unsigned long long)sh.n);
         CK(cudaGetLastError());
     }
     S->T_last = 0;
+    return ACA_OK;
+}
+
+// Device reductions over all shards (the halos are refreshed first for the bond sum).
+int device_stats(aca_sim* S) {
+    StatAcc init{0, 0, 0, ~0ull, 0, 0};
+    *S->h_stat = init;
+    CK(cudaMemcpyAsync(S->d_stat, S->h_stat, sizeof(StatAcc), cudaMemcpyHostToDevice, S->stream));
+    int rc = exchange(S);
+    if (rc) return rc;
+    for (auto& sh : S->shards) {
+        KParams P = make_params(S, sh);
+        stats_kernel<256><<<592, 256, 0, S->stream>>>(P, S->d_stat, (unsigned long long)sh.n);
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(S->h_stat, S->d_stat, sizeof(StatAcc), cudaMemcpyDeviceToHost, S->stream));
+    CK(cudaStreamSynchronize(S->stream));
+    return ACA_OK;
+}
+
+// Choose the (t, n) split of the packed word for horizon Tq: the fewest time bits that hold
+// Tq + max_delta, every remaining bit for the counter (capped at 31); repack if it changed.
+int fit_layout(aca_sim* S, uint64_t Tq) {
+    const unsigned long long tmax = (unsigned long long)Tq + S->max_delta;
+    if (tmax < (unsigned long long)Tq) return fail(ACA_ERANGE, "time horizon overflows 64 bits");
+    const int tb = bits_for(tmax);
+    int nb = 63 - S->RB - tb;
+    if (nb > 31) nb = 31;
+    if (nb < 1) return fail(ACA_ERANGE, "lattice rank bits (%d) + time bits (%d) leave no room for the counter", S->RB, tb);
+    if (nb == S->NB) return ACA_OK;
+    if (nb < S->NB) {   // shrinking the counter field: every current counter must fit
+        int rc = device_stats(S);
+        if (rc) return rc;
+        if (S->h_stat->nmax >= (1ull << nb) - 1ull)
+            return fail(ACA_ERANGE, "event counters (max %llu) do not fit the %d bits left by T", S->h_stat->nmax, nb);
+    }
+    Geo a = S->shards[0].g;
+    const int old_nb = S->NB;
+    S->NB = nb;
+    S->TB = 63 - S->RB - nb;
+    set_geo_layout(S);
+    for (auto& sh : S->shards) {
+        Geo ga = sh.g;
+        ga.NB = old_nb;
+        ga.TSH = S->RB + old_nb + 1;
+        repack_kernel<<<1184, 256, 0, S->stream>>>(sh.words, ga, sh.g, (unsigned long long)sh.n);
+        CK(cudaGetLastError());
+    }
+    (void)a;
+    drop_graph(S);   // kernel parameters (layout) changed
     return ACA_OK;
 }
 
@@ -392,10 +449,9 @@ int64_t aca_num_cells(const aca_sim* S) {
 void aca_destroy(aca_sim* S) {
     if (!S) return;
     if (S->stream) cudaStreamSynchronize(S->stream);
-    if (S->graph) cudaGraphExecDestroy(S->graph);
+    drop_graph(S);
     for (auto& sh : S->shards) {
         cudaFree(sh.words);
-        cudaFree(sh.cnt);
         cudaFree(sh.halo_lo);
         cudaFree(sh.halo_hi);
         cudaFree(sh.ctl);
@@ -444,6 +500,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (opt.world > 1 && opt.shards != 1) return fail(ACA_EINVAL, "multi-process handles use shards = 1");
     if (opt.world > 1 && !opt.nccl_id) return fail(ACA_EINVAL, "world > 1 needs nccl_id");
     if (opt.rounds_per_launch < 0 || opt.launches_per_check < 0) return fail(ACA_EINVAL, "negative counts");
+    if (opt.variant < 0 || opt.variant >= NVARIANT) return fail(ACA_EINVAL, "variant must be in [0, %d)", NVARIANT);
 
     int64_t N = 1;
     for (int a = 0; a < ndim; ++a) {
@@ -478,26 +535,27 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->world = opt.world;
     S->G = opt.world > 1 ? 1 : opt.shards;
     S->sync = opt.sync_rounds != 0;
-    S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 8;
+    S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 3;
     S->K = opt.launches_per_check > 0 ? opt.launches_per_check : 16;
 
-    // P3 constants, P4 table, P5 threshold, packing
+    // P3 constants, P4 table, P5 threshold, packed-word layout
     S->inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
     flip_table(ndim, beta, J, h, rule, S->thr);
     S->thr_init = (unsigned long long)std::floor(opt.init_q * 4294967296.0);
     uint64_t max_rank = 0;
     for (int a = 0; a < ndim; ++a) max_rank += (uint64_t)(dims[a] - 1);
-    S->SH = bits_for(max_rank) + 1;
+    S->RB = bits_for(max_rank);
     {
         const unsigned __int128 p = (unsigned __int128)190530846196ull * S->inv_lambda;
         S->max_delta = (unsigned long long)(p >> 32) + 1 + (opt.tie_bits ? (1ull << opt.tie_bits) : 0ull);
-        if (S->SH >= 40 || S->max_delta >= (1ull << (64 - S->SH))) {
-            delete S;
-            return fail(ACA_ERANGE, "lattice/lambda leave no room for times in the packed word");
-        }
+        const int tb = bits_for(S->max_delta);
+        int nb = 63 - S->RB - tb;
+        if (nb > 31) nb = 31;
+        if (nb < 1) { delete S; return fail(ACA_ERANGE, "lattice/lambda leave no room in the packed word"); }
+        S->NB = nb;
+        S->TB = 63 - S->RB - nb;
     }
 
-    int rc = ACA_OK;
     auto bail = [&](int code) { aca_destroy(S); return code; };
     if (opt.stream) {
         S->stream = (cudaStream_t)opt.stream;
@@ -532,10 +590,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (S->whole) {
         S->kern = S->sync ? (void*)whole_kernel<WHOLE_NT, true> : (void*)whole_kernel<WHOLE_NT, false>;
         S->nthreads = WHOLE_NT;
-        S->smem_whole = whole_smem(N, S->sync);
+        S->smem = whole_smem(N, S->sync);
         S->rounds = 1 << 30;
-        if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem_whole) != cudaSuccess)
-            return bail(fail(ACA_ECUDA, "smem attribute (whole)"));
     } else {
         int tx = opt.tile[0], ty = opt.tile[1], tz = opt.tile[2];
         if (tx == 0 && ty == 0 && tz == 0) {
@@ -547,22 +603,23 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         for (const auto& k : kTiles)
             if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz) sel = &k;
         if (!sel) return bail(fail(ACA_EINVAL, "unsupported tile %dx%dx%d for ndim %d", tx, ty, tz, ndim));
-        if (opt.variant < 0 || opt.variant > 2) return bail(fail(ACA_EINVAL, "variant must be 0, 1 or 2"));
-        const int v = S->sync ? 3 : opt.variant;
+        const int v = S->sync ? NVARIANT : opt.variant;
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
         S->kern = sel->fn[v];
         S->nthreads = sel->nt;
-        S->smem_tile = sel->smem[v];
-        if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem_tile) != cudaSuccess)
-            return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
-        if (v == 0) {   // persistent: as many CTAs as fit on the device at once
+        S->smem = sel->smem[v];
+        if (sel->persistent[v]) {   // persistent: as many CTAs as fit on the device at once
+            if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
+                return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
             int nsm = 0, occ = 0;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, S->nthreads, S->smem_tile) != cudaSuccess || occ < 1)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, S->nthreads, S->smem) != cudaSuccess || occ < 1)
                 return bail(fail(ACA_ECUDA, "occupancy query failed"));
             S->persistent_ctas = nsm * occ;
         }
     }
+    if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
+        return bail(fail(ACA_ECUDA, "smem attribute"));
 
     // shards
     const int64_t local = dims[saxis] / parts;
@@ -580,20 +637,19 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         g.y0 = ndim == 2 ? (int)(part * local) : 0;
         g.z0 = ndim == 3 ? (int)(part * local) : 0;
         g.sharded = parts > 1;
-        g.SH = S->SH;
         sh.n = (size_t)g.nx * g.ny * g.nz;
         sh.face = ndim == 2 ? (size_t)g.nx : (size_t)g.nx * g.ny;
         sh.tiles_x = (g.nx + S->tile[0] - 1) / S->tile[0];
         sh.tiles_y = (g.ny + S->tile[1] - 1) / S->tile[1];
         sh.tiles_z = ndim == 3 ? (g.nz + S->tile[2] - 1) / S->tile[2] : 1;
-        if (cudaMalloc(&sh.words, sh.n * 8) != cudaSuccess || cudaMalloc(&sh.cnt, sh.n * 4) != cudaSuccess ||
-            cudaMalloc(&sh.ctl, sizeof(Ctl)) != cudaSuccess)
+        if (cudaMalloc(&sh.words, sh.n * 8) != cudaSuccess || cudaMalloc(&sh.ctl, sizeof(Ctl)) != cudaSuccess)
             return bail(fail(ACA_ENOMEM, "device allocation of %zu cells failed", sh.n));
         if (g.sharded) {
             if (cudaMalloc(&sh.halo_lo, sh.face * 8) != cudaSuccess || cudaMalloc(&sh.halo_hi, sh.face * 8) != cudaSuccess)
                 return bail(fail(ACA_ENOMEM, "halo allocation failed"));
         }
     }
+    set_geo_layout(S);
     if (int r = init_state(S)) return bail(r);
     if (cudaMallocHost(&S->h_ctl, 2 * sizeof(Ctl) * S->shards.size()) != cudaSuccess)
         return bail(fail(ACA_ENOMEM, "pinned ctl"));
@@ -606,8 +662,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         int r = api.init(&S->comm, S->world, id, S->rank);
         if (r != 0) return bail(fail(ACA_ENCCL, "ncclCommInitRank failed: %d", r));
     }
-    if (cudaStreamSynchronize(S->stream) != cudaSuccess) return bail(fail(ACA_ECUDA, "init sync: %s", cudaGetErrorString(cudaGetLastError())));
-    (void)rc;
+    if (cudaStreamSynchronize(S->stream) != cudaSuccess)
+        return bail(fail(ACA_ECUDA, "init sync: %s", cudaGetErrorString(cudaGetLastError())));
     *out = S;
     return ACA_OK;
 }
@@ -615,19 +671,18 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
 int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
     if (!S) return fail(ACA_EINVAL, "null handle");
     if (Tq < S->T_last) return fail(ACA_ESTATE, "T decreased (%llu < %llu)", (unsigned long long)Tq, (unsigned long long)S->T_last);
-    if (Tq >= (1ull << (64 - S->SH)) - S->max_delta)
-        return fail(ACA_ERANGE, "T too large for the packed time field (%d bits)", 64 - S->SH);
-    S->T_last = Tq;
     CK(cudaSetDevice(S->device));
-    // reset per-call control words
+    int rc = fit_layout(S, Tq);
+    if (rc) return rc;
+    S->T_last = Tq;
+    const int TSH = S->RB + S->NB + 1;
     for (size_t i = 0; i < S->shards.size(); ++i) {
-        S->h_ctl[i].wlim = (unsigned long long)Tq << S->SH;
-        S->h_ctl[i].done = 0;
+        S->h_ctl[i].wlim = (unsigned long long)Tq << TSH;
         CK(cudaMemcpyAsync(&S->shards[i].ctl->wlim, &S->h_ctl[i].wlim, sizeof(unsigned long long),
                            cudaMemcpyHostToDevice, S->stream));
         CK(cudaMemsetAsync(&S->shards[i].ctl->done, 0, sizeof(unsigned int), S->stream));
     }
-    int rc = build_graph(S);
+    rc = build_graph(S);
     if (rc) return rc;
     CK(cudaEventRecord(S->ev0, S->stream));
     const size_t nsh = S->shards.size();
@@ -707,8 +762,12 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, S->ev0, S->ev1));
     S->gpu_seconds += ms * 1e-3;
-    // copy the final control blocks into slot 0 for getters
-    return sync_ctl(S);
+    rc = sync_ctl(S);
+    if (rc) return rc;
+    for (size_t i = 0; i < nsh; ++i)
+        if (S->h_ctl[i].overflow)
+            return fail(ACA_ERANGE, "an event counter filled its %d-bit field; the run stopped early", S->NB);
+    return ACA_OK;
 }
 
 int aca_nccl_unique_id(void* out128) {
@@ -726,6 +785,7 @@ int aca_reset(aca_sim* S, uint64_t seed) {
     if (!S) return fail(ACA_EINVAL, "null handle");
     CK(cudaSetDevice(S->device));
     S->seed = seed;
+    drop_graph(S);   // the key is a kernel parameter
     return init_state(S);
 }
 
@@ -737,21 +797,24 @@ int aca_run_until(aca_sim* S, double T) {
     return aca_run_until_q32(S, (uint64_t)tq);
 }
 
-static int get_words(aca_sim* S, int8_t* spins, uint64_t* times, size_t count) {
-    int rc = check_count(S, count, spins ? (const void*)spins : (const void*)times);
+static int get_fields(aca_sim* S, int8_t* spins, uint64_t* times, uint32_t* counters, size_t count) {
+    const void* any = spins ? (const void*)spins : times ? (const void*)times : (const void*)counters;
+    int rc = check_count(S, count, any);
     if (rc) return rc;
     CK(cudaSetDevice(S->device));
-    rc = ensure_scratch(S, CHUNK * (times ? 8 : 1));
+    const size_t esz = times ? 8 : counters ? 4 : 1;
+    rc = ensure_scratch(S, CHUNK * esz);
     if (rc) return rc;
     size_t off = 0;
     for (auto& sh : S->shards) {
         for (size_t b = 0; b < sh.n; b += CHUNK) {
             const size_t m = std::min(CHUNK, sh.n - b);
             unpack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, spins ? (int8_t*)S->scratch : nullptr,
-                                                      times ? (unsigned long long*)S->scratch : nullptr, S->SH, m);
+                                                      times ? (unsigned long long*)S->scratch : nullptr,
+                                                      counters ? (unsigned int*)S->scratch : nullptr, sh.g, m);
             CK(cudaGetLastError());
-            if (spins) CK(cudaMemcpyAsync(spins + off + b, S->scratch, m, cudaMemcpyDeviceToHost, S->stream));
-            else CK(cudaMemcpyAsync(times + off + b, S->scratch, m * 8, cudaMemcpyDeviceToHost, S->stream));
+            void* dst = spins ? (void*)(spins + off + b) : times ? (void*)(times + off + b) : (void*)(counters + off + b);
+            CK(cudaMemcpyAsync(dst, S->scratch, m * esz, cudaMemcpyDeviceToHost, S->stream));
             CK(cudaStreamSynchronize(S->stream));
         }
         off += sh.n;
@@ -759,19 +822,38 @@ static int get_words(aca_sim* S, int8_t* spins, uint64_t* times, size_t count) {
     return ACA_OK;
 }
 
-int aca_get_spins(aca_sim* S, int8_t* out, size_t count) { return get_words(S, out, nullptr, count); }
-int aca_get_times(aca_sim* S, uint64_t* out, size_t count) { return get_words(S, nullptr, out, count); }
+int aca_get_spins(aca_sim* S, int8_t* out, size_t count) { return get_fields(S, out, nullptr, nullptr, count); }
+int aca_get_times(aca_sim* S, uint64_t* out, size_t count) { return get_fields(S, nullptr, out, nullptr, count); }
+int aca_get_counters(aca_sim* S, uint32_t* out, size_t count) { return get_fields(S, nullptr, nullptr, out, count); }
 
-int aca_get_counters(aca_sim* S, uint32_t* out, size_t count) {
-    int rc = check_count(S, count, out);
-    if (rc) return rc;
+int aca_get_cells(aca_sim* S, const int64_t* idx, size_t m, int8_t* spins, uint64_t* times, uint32_t* counters) {
+    if (!S || (m && !idx)) return fail(ACA_EINVAL, "null argument");
+    if (m == 0) return ACA_OK;
+    const int64_t n = aca_num_cells(S);
+    for (size_t i = 0; i < m; ++i)
+        if (idx[i] < 0 || idx[i] >= n) return fail(ACA_EINVAL, "cell index %lld out of range", (long long)idx[i]);
     CK(cudaSetDevice(S->device));
-    size_t off = 0;
+    int rc = ensure_scratch(S, m * 16);
+    if (rc) return rc;
+    int64_t* didx = (int64_t*)S->scratch;
+    unsigned long long* dw = (unsigned long long*)(didx + m);
+    CK(cudaMemcpyAsync(didx, idx, m * 8, cudaMemcpyHostToDevice, S->stream));
+    int64_t base = 0;
     for (auto& sh : S->shards) {
-        CK(cudaMemcpyAsync(out + off, sh.cnt, sh.n * 4, cudaMemcpyDeviceToHost, S->stream));
-        off += sh.n;
+        gather_kernel<<<(unsigned)((m + 255) / 256), 256, 0, S->stream>>>(sh.words, didx, (unsigned long long)m, base,
+                                                                         (long long)sh.n, dw);
+        CK(cudaGetLastError());
+        base += (int64_t)sh.n;
     }
+    std::vector<unsigned long long> hw(m);
+    CK(cudaMemcpyAsync(hw.data(), dw, m * 8, cudaMemcpyDeviceToHost, S->stream));
     CK(cudaStreamSynchronize(S->stream));
+    const Geo& g = S->shards[0].g;
+    for (size_t i = 0; i < m; ++i) {
+        if (spins) spins[i] = (hw[i] & 1ull) ? 1 : -1;
+        if (times) times[i] = w_time(hw[i], g);
+        if (counters) counters[i] = w_count(hw[i], g);
+    }
     return ACA_OK;
 }
 
@@ -787,17 +869,8 @@ int aca_get_stats(aca_sim* S, aca_stats* o) {
     if (!S || !o) return fail(ACA_EINVAL, "null argument");
     CK(cudaSetDevice(S->device));
     memset(o, 0, sizeof *o);
-    StatAcc init{0, 0, 0, ~0ull, 0};
-    *S->h_stat = init;
-    CK(cudaMemcpyAsync(S->d_stat, S->h_stat, sizeof(StatAcc), cudaMemcpyHostToDevice, S->stream));
-    int rc = exchange(S);      // make halos current for the bond sum across shard boundaries
+    int rc = device_stats(S);
     if (rc) return rc;
-    for (auto& sh : S->shards) {
-        KParams P = make_params(S, sh);
-        stats_kernel<256><<<592, 256, 0, S->stream>>>(P, S->d_stat, (unsigned long long)sh.n);
-        CK(cudaGetLastError());
-    }
-    CK(cudaMemcpyAsync(S->h_stat, S->d_stat, sizeof(StatAcc), cudaMemcpyDeviceToHost, S->stream));
     rc = sync_ctl(S);
     if (rc) return rc;
     o->bond_sum = S->h_stat->bond;
@@ -817,6 +890,9 @@ int aca_get_stats(aca_sim* S, aca_stats* o) {
     o->gpu_seconds = S->gpu_seconds;
     o->kernel_seconds = S->kernel_seconds;
     o->kernel_launches = S->kernel_launches;
+    o->time_bits = S->TB;
+    o->counter_bits = S->NB;
+    o->rank_bits = S->RB;
     return ACA_OK;
 }
 
@@ -824,24 +900,36 @@ int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const 
     int rc = check_count(S, count, spins);
     if (rc) return rc;
     if (!times || !counters) return fail(ACA_EINVAL, "null times/counters");
-    const uint64_t lim = (1ull << (64 - S->SH)) - S->max_delta;
+    CK(cudaSetDevice(S->device));
+    uint64_t tmax = 0;
+    uint32_t nmax = 0;
     for (size_t i = 0; i < count; ++i) {
         if (spins[i] != 1 && spins[i] != -1) return fail(ACA_EINVAL, "spin %zu is not +-1", i);
-        if (times[i] < 1 || times[i] >= lim) return fail(ACA_ERANGE, "time %zu out of range", i);
+        if (times[i] < 1) return fail(ACA_ERANGE, "time %zu must be >= 1", i);
+        tmax = std::max<uint64_t>(tmax, times[i]);
+        nmax = std::max(nmax, counters[i]);
     }
-    CK(cudaSetDevice(S->device));
-    rc = ensure_scratch(S, CHUNK * 9);
+    // layout able to hold the largest time (plus one more increment) and counter
+    const int tb = bits_for(tmax + S->max_delta);
+    int nb = std::min(31, 63 - S->RB - tb);
+    if (nb < 1 || (uint64_t)nmax >= (1ull << nb) - 1ull) return fail(ACA_ERANGE, "state does not fit the packed word");
+    S->NB = nb;
+    S->TB = 63 - S->RB - nb;
+    set_geo_layout(S);
+    drop_graph(S);
+    rc = ensure_scratch(S, CHUNK * 13);
     if (rc) return rc;
     unsigned long long* dt = (unsigned long long*)S->scratch;
-    int8_t* ds = (int8_t*)(dt + CHUNK);
+    unsigned int* dn = (unsigned int*)(dt + CHUNK);
+    int8_t* ds = (int8_t*)(dn + CHUNK);
     size_t off = 0;
     for (auto& sh : S->shards) {
-        CK(cudaMemcpyAsync(sh.cnt, counters + off, sh.n * 4, cudaMemcpyHostToDevice, S->stream));
         for (size_t b = 0; b < sh.n; b += CHUNK) {
             const size_t m = std::min(CHUNK, sh.n - b);
             CK(cudaMemcpyAsync(dt, times + off + b, m * 8, cudaMemcpyHostToDevice, S->stream));
+            CK(cudaMemcpyAsync(dn, counters + off + b, m * 4, cudaMemcpyHostToDevice, S->stream));
             CK(cudaMemcpyAsync(ds, spins + off + b, m, cudaMemcpyHostToDevice, S->stream));
-            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, ds, dt, sh.g, (unsigned long long)m,
+            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, ds, dt, dn, sh.g, (unsigned long long)m,
                                                     (unsigned long long)b);
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(S->stream));
@@ -863,7 +951,7 @@ int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
         for (size_t b = 0; b < sh.n; b += CHUNK) {
             const size_t m = std::min(CHUNK, sh.n - b);
             CK(cudaMemcpyAsync(S->scratch, spins + off + b, m, cudaMemcpyHostToDevice, S->stream));
-            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, (const int8_t*)S->scratch, nullptr, sh.g,
+            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, (const int8_t*)S->scratch, nullptr, nullptr, sh.g,
                                                     (unsigned long long)m, (unsigned long long)b);
             CK(cudaGetLastError());
         }
@@ -873,9 +961,9 @@ int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
     return ACA_OK;
 }
 
-// ---------------------------------------------------------------- self-test hooks
 }  // extern "C"
 
+// ---------------------------------------------------------------- self-test hooks
 namespace {
 __global__ void philox_test_kernel(uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out, uint32_t* ref) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {

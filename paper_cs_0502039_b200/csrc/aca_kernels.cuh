@@ -1,20 +1,25 @@
 // aca_kernels.cuh — sm_100a kernels of the conservative Poisson-asynchronous Ising path.
 //
-// State in HBM (one shard = a run of rows (2-D) or planes (3-D) of the lattice):
-//   words[c] : u64 packed word  (t << SH) | (rank(c) << 1) | [s(c) = +1]
-//   cnt[c]   : u32 event counter n(c)
-// rank(c) = x + y (+ z) in global coordinates. For every neighbour pair it orders the two
-// cells exactly as their row-major ids do (along an axis the ids grow with the coordinate,
-// and the periodic pair (n-1, 0) is ordered the same way by both), so one unsigned 64-bit
-// compare `w(c) < w(c')` is the lexicographic (t, c) test of P6, and the spin rides in the
-// same word: a (t, s) pair is read and written by one 8-byte access and is never torn.
+// State in HBM: ONE u64 word per cell (a shard = a run of rows (2-D) / planes (3-D)):
 //
-// Correctness of in-place updates (no ping-pong): every word a CTA observes for a
-// neighbour is a value that neighbour really held, and each cell's word only grows. A cell
-// fires only when its word is below every observed neighbour word; by the stale-read
-// argument of fig:amcgen and the uniqueness argument of fig:a1c1pe
-// the neighbour's state at the firing time equals the observed one, so
-// any interleaving of CTAs (and of threads inside a CTA) yields the unique trajectory.
+//     word = t << TSH | rank(c) << (NB + 1) | n << 1 | [s(c) = +1]        TSH = RB + NB + 1
+//
+// t: pending arrival time (Q32), n: event counter (NB bits), rank(c) = x + y (+ z) in global
+// coordinates (RB bits). For every neighbour pair rank orders the two cells exactly as their
+// row-major ids do (along an axis the id grows with the coordinate, and the periodic pair
+// (n-1, 0) is ordered the same way by both), and ranks of neighbours always differ, so the
+// bits below the rank never decide a comparison: one unsigned 64-bit compare
+// `word(c) < word(c')` is the lexicographic (t, c) test of P6. A cell's whole state
+// (t, n, s) is read and written by one 8-byte access and can never be observed torn.
+// The host chooses the (t, n) split per run_until(T) and repacks when T grows; a counter
+// that would overflow its field raises ctl->overflow (ACA_ERANGE) instead of wrapping.
+//
+// In-place updates (no ping-pong): every word a CTA observes for a neighbour is a value that
+// neighbour really held, and words only grow. A cell fires only when its word is below every
+// observed neighbour word; by the stale-read argument of fig:amcgen and the
+// uniqueness argument of fig:a1c1pe the neighbour's state at the firing
+// time equals the observed one, so any interleaving of CTAs and threads yields the unique
+// trajectory.
 #pragma once
 #include <stdint.h>
 
@@ -24,7 +29,7 @@
 namespace aca {
 
 struct Ctl {                            // device control block, one per shard
-    unsigned long long wlim;            // T_q32 << SH: fire iff word < wlim  (t < T)
+    unsigned long long wlim;            // T_q32 << TSH: fire iff word < wlim  (t < T)
     unsigned long long active_accum;    // cells with t < T after this launch (accumulating)
     unsigned long long active_last;     // value of the last completed launch
     unsigned long long fired, flips, tested, hash;
@@ -32,7 +37,7 @@ struct Ctl {                            // device control block, one per shard
     unsigned int done;                  // set when a launch ends with no active cell
     unsigned int ticket;                // last-CTA detection
     unsigned int rounds_max;            // max in-tile rounds over CTAs of this launch
-    unsigned int pad;
+    unsigned int overflow;              // an event counter reached its field maximum
 };
 
 struct Geo {
@@ -41,13 +46,21 @@ struct Geo {
     int NY, NZ;              // global extents of y and z
     int y0, z0;              // global offset of the shard along the sharded axis
     int sharded;             // 0: periodic wrap inside the storage; 1: halo buffers
-    int SH;                  // packing shift = rank bits + 1
+    int RB, NB, TSH;         // rank bits, counter bits, time shift (= RB + NB + 1)
 };
+
+__device__ __host__ __forceinline__ unsigned long long w_time(unsigned long long w, const Geo& g) { return w >> g.TSH; }
+__device__ __host__ __forceinline__ unsigned int w_count(unsigned long long w, const Geo& g) {
+    return (unsigned int)((w >> 1) & ((1ull << g.NB) - 1ull));
+}
+__device__ __host__ __forceinline__ unsigned long long w_pack(unsigned long long t, unsigned long long rank,
+                                                              unsigned long long n, unsigned long long sb, const Geo& g) {
+    return (t << g.TSH) | (rank << (g.NB + 1)) | (n << 1) | sb;
+}
 
 struct KParams {
     Geo g;
     unsigned long long* words;
-    unsigned int* cnt;
     const unsigned long long* halo_lo;   // sharded axis: row/plane just below the shard
     const unsigned long long* halo_hi;   // ... and just above
     Ctl* ctl;
@@ -65,30 +78,31 @@ __device__ __forceinline__ int wrapi(int v, int n) {
     v %= n;
     return v < 0 ? v + n : v;
 }
+// v in [-n, 2n): one conditional add/sub instead of an integer division
+__device__ __forceinline__ int wrap1(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
 
-__device__ __forceinline__ unsigned long long ld_word(const KParams& P, int gx, int gy, int gz) {
+template <bool ONE>
+__device__ __forceinline__ unsigned long long ld_word_t(const KParams& P, int gx, int gy, int gz) {
     const Geo& g = P.g;
-    const int x = wrapi(gx, g.nx);
+    const int x = ONE ? wrap1(gx, g.nx) : wrapi(gx, g.nx);
     if (g.ndim == 2) {
-        if (!g.sharded) return P.words[(size_t)wrapi(gy, g.ny) * g.nx + x];
+        if (!g.sharded) return P.words[(size_t)(ONE ? wrap1(gy, g.ny) : wrapi(gy, g.ny)) * g.nx + x];
         if (gy < 0) return P.halo_lo[x];
         if (gy >= g.ny) return P.halo_hi[x];
         return P.words[(size_t)gy * g.nx + x];
     }
-    const int y = wrapi(gy, g.ny);
-    if (!g.sharded) return P.words[((size_t)wrapi(gz, g.nz) * g.ny + y) * g.nx + x];
+    const int y = ONE ? wrap1(gy, g.ny) : wrapi(gy, g.ny);
+    if (!g.sharded) return P.words[((size_t)(ONE ? wrap1(gz, g.nz) : wrapi(gz, g.nz)) * g.ny + y) * g.nx + x];
     if (gz < 0) return P.halo_lo[(size_t)y * g.nx + x];
     if (gz >= g.nz) return P.halo_hi[(size_t)y * g.nx + x];
     return P.words[((size_t)gz * g.ny + y) * g.nx + x];
 }
-
-// v in [-n, 2n): one conditional add/sub instead of an integer division
-__device__ __forceinline__ int wrap1(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+__device__ __forceinline__ unsigned long long ld_word(const KParams& P, int gx, int gy, int gz) {
+    return ld_word_t<false>(P, gx, gy, gz);
+}
 
 // ---------------------------------------------------------------- TMA bulk-copy helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -111,11 +125,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 // order earlier generic-proxy accesses of shared memory before later async-proxy (TMA) ones
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Block-wide sum of (u64) into ctl via one atomic per CTA.
+// Block-wide sum (result valid in thread 0).
 template <int NT>
 __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* red) {
 #pragma unroll
@@ -129,28 +141,36 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
 #pragma unroll
         for (int w = 0; w < NT / 32; ++w) s += red[w];
     }
-    return s;   // valid in thread 0
+    return s;
 }
 
 // One arrival of a cell (fig:a1c1pe steps 3-4; Appendix).
-// `ones` = number of +1 neighbours (with multiplicity), z = coordination number.
-struct FireOut { unsigned long long wnew; uint32_t flip; unsigned long long h; };
+// `ones` = number of +1 neighbours (with multiplicity), z = coordination number. Returns
+// ok = false (and raises ctl->overflow) when the counter field is full.
+struct FireOut { unsigned long long wnew; uint32_t flip; unsigned long long h; bool ok; };
 
-__device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int z, uint32_t k,
-                                        unsigned long long c, int SH, const unsigned long long* thr,
-                                        const unsigned long long* lr, uint32_t key0, uint32_t key1,
-                                        unsigned long long inv_lambda, int tie_bits, int do_hash) {
+__device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int z, unsigned long long c,
+                                        const Geo& g, const unsigned long long* thr, const unsigned long long* lr,
+                                        uint32_t key0, uint32_t key1, unsigned long long inv_lambda, int tie_bits,
+                                        int do_hash, Ctl* ctl) {
+    FireOut o;
+    const uint32_t k = w_count(w, g);
+    if (k == (uint32_t)((1ull << g.NB) - 1ull)) {
+        atomicOr(&ctl->overflow, 1u);
+        o.wnew = w; o.flip = 0; o.h = 0; o.ok = false;
+        return o;
+    }
     const uint32_t sb = (uint32_t)(w & 1ull);
     const uint32_t idx = ones + (uint32_t)(z + 1) * sb;          // (Sigma+z)/2 + (z+1)(s+1)/2
     const u32x4 r = philox4x32_10(k, (uint32_t)c, (uint32_t)(c >> 32), 0u, key0, key1);
     const uint32_t flip = (unsigned long long)r.x < thr[idx] ? 1u : 0u;
     const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits);
-    FireOut o;
-    o.wnew = (w + (d << SH)) ^ (unsigned long long)flip;
+    o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;   // t += d, n += 1, s ^= flip
     o.flip = flip;
     o.h = 0;
+    o.ok = true;
     if (do_hash) {
-        const unsigned long long t = w >> SH;
+        const unsigned long long t = w >> g.TSH;
         o.h = mix64(t ^ rotl64(c, 20) ^ rotl64((unsigned long long)k, 44) ^ (unsigned long long)(sb ^ flip));
     }
     return o;
@@ -160,7 +180,6 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
 __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long active, unsigned long long fired,
                                               unsigned long long flips, unsigned long long tested,
                                               unsigned long long hash, unsigned int rounds) {
-    // thread 0 only
     atomicAdd(&ctl->active_accum, active);
     if (fired) atomicAdd(&ctl->fired, fired);
     if (flips) atomicAdd(&ctl->flips, flips);
@@ -173,7 +192,7 @@ __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long activ
         __threadfence();
         const unsigned long long act = atomicAdd(&ctl->active_accum, 0ull);
         ctl->active_last = act;
-        ctl->done = (act == 0ull) ? 1u : 0u;
+        ctl->done = (act == 0ull || ctl->overflow) ? 1u : 0u;
         ctl->active_accum = 0ull;
         ctl->launches += 1ull;
         ctl->inner_rounds += atomicAdd(&ctl->rounds_max, 0u);
@@ -183,11 +202,17 @@ __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long activ
     }
 }
 
-// ------------------------------------------------------------------------ tile kernel
+__device__ __forceinline__ unsigned long long cell_id(const Geo& g, int gx, int gy, int gz) {
+    return g.ndim == 2 ? (unsigned long long)(gy + g.y0) * g.nx + gx
+                       : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
+}
+
+// ------------------------------------------------------------------------ uncompacted tile kernel
 // One CTA per tile; the tile plus a one-cell halo (faces only) is staged in shared memory;
-// up to R rounds of the local-minimum test run on-chip. SYNC = false: asynchronous in-place
-// updates (fig:a1c1pe semantics inside the tile); SYNC = true: the two
-// barriers of fig:s1c1pe, private new_s/new_t then commit.
+// up to R rounds of the local-minimum test. SYNC = false: asynchronous in-place updates
+// (fig:a1c1pe semantics inside the tile); SYNC = true: the two barriers of
+// fig:s1c1pe, private new words then commit — the exact synchronous round
+// whose firing fraction N0/N is the paper's efficiency.
 template <int NDIM, int TX, int TY, int TZ, int NT, bool SYNC>
 __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
     constexpr int SX = TX + 2, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
@@ -216,31 +241,20 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
 
     for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
-
-    // stage tile + face halo (slots with more than one coordinate outside are never read)
     for (int i = tid; i < NSLOT; i += NT) {
         const int lx = i % SX - 1, ly = (i / SX) % SY - 1, lz = (NDIM == 3) ? i / SXY - 1 : 0;
         const int out = (lx < 0 || lx >= TX) + (ly < 0 || ly >= TY) + ((NDIM == 3) && (lz < 0 || lz >= TZ));
         if (out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
     }
 
-    // owned cells of this thread: i = tid + k*NT
     unsigned long long wreg[CPT];
-    uint32_t nreg[CPT];
     uint32_t valid = 0;
     const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         const int i = tid + k * NT;
         const int lx = i % TX, ly = (i / TX) % TY, lz = i / (TX * TY);
-        const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-        const bool v = gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz);
-        nreg[k] = 0;
-        if (v) {
-            valid |= 1u << k;
-            const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
-            nreg[k] = P.cnt[gi];
-        }
+        if (x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz)) valid |= 1u << k;
     }
     __syncthreads();
 #pragma unroll
@@ -254,8 +268,6 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
 
     unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0;
     unsigned int rounds = 0;
-    const uint32_t key0 = P.key0, key1 = P.key1;
-
     for (int r = 0; r < P.rounds; ++r) {
         int any = 0;
         unsigned long long pend[SYNC ? CPT : 1];
@@ -278,16 +290,12 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
                 ones += (uint32_t)(e & 1ull) + (uint32_t)(f & 1ull);
             }
             if (!ok) continue;
-            const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-            const unsigned long long cid = NDIM == 2
-                ? (unsigned long long)(gy + g.y0) * g.nx + gx
-                : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
-            const FireOut o = fire(w, ones, Z, nreg[k], cid, g.SH, thr, lr, key0, key1, P.inv_lambda,
-                                   P.tie_bits, P.do_hash);
+            const FireOut o = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.key0, P.key1,
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+            if (!o.ok) continue;
             hacc += o.h;
             flips += o.flip;
             ++fired;
-            nreg[k] += 1;
             changed |= 1u << k;
             any = 1;
             if (SYNC) {
@@ -315,7 +323,6 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
         if (__syncthreads_count(any) == 0) break;              // barrier 2 / stall detection
     }
 
-    // write back the owned cells that changed; count cells still active
     unsigned long long active = 0;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
@@ -324,10 +331,7 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
         const int lx = i % TX, ly = (i / TX) % TY, lz = i / (TX * TY);
         const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
         const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
-        if ((changed >> k) & 1u) {
-            P.words[gi] = wreg[k];
-            P.cnt[gi] = nreg[k];
-        }
+        if ((changed >> k) & 1u) P.words[gi] = wreg[k];
         active += wreg[k] < wlim;
     }
     const unsigned long long s_act = block_sum<NT>(active, red);
@@ -338,267 +342,216 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds);
 }
 
-// ------------------------------------------------------------ tile kernel, compacted
-// Same method and semantics as tile_kernel<..., SYNC=false>, organised for SIMT efficiency:
-// per round every warp (i) tests its 512 cells against the current words — the test is a
-// 32-bit compare of the high halves, with a full 64-bit compare only on a high-half tie —
-// (ii) compacts the eligible cells into a warp-private queue with __ballot_sync, and
-// (iii) fires them with all 32 lanes busy (Philox + NLOG + hash are ~90 % of the work; in
-// the uncompacted kernel they ran with ~10 % of the lanes active).
-// Correctness of firing after compaction: a queued cell c was a local minimum when
-// tested; its word cannot change until it fires, so no neighbour can pass its own test
-// (it would need a word below c's) — c's neighbourhood is frozen until c fires.
-template <int NDIM, int TX, int TY, int TZ, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) tile2_kernel(const KParams P) {
-    constexpr int SX = TX + 2, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
-    constexpr int NSLOT = SX * SY * SZ;
-    constexpr int NCELL = TX * TY * TZ;
-    constexpr int NW = NT / 32;
-    constexpr int CPW = NCELL / NW;        // cells per warp
-    constexpr int JPL = CPW / 32;          // cells per lane
-    static_assert(NCELL % NT == 0 && CPW % 32 == 0, "tile/block mismatch");
-    constexpr int Z = 2 * NDIM;
-    constexpr int SXY = SX * SY;
-
-    if (*(volatile unsigned int*)&P.ctl->done) return;
-
-    extern __shared__ __align__(16) unsigned long long smem[];
-    unsigned long long* S = smem;                                   // NSLOT words
-    unsigned long long* lr = S + NSLOT;                             // 512
-    unsigned long long* thr = lr + 512;                             // 16
-    unsigned long long* red = thr + 16;                             // NW
-    unsigned int* Nc = (unsigned int*)(red + NW);                   // NCELL counters
-    unsigned short* Q = (unsigned short*)(Nc + NCELL);              // NW * CPW queue
-
-    const Geo& g = P.g;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int bt = blockIdx.x;
-    const int tx = bt % P.tiles_x;
-    const int ty = (bt / P.tiles_x) % P.tiles_y;
-    const int tz = bt / (P.tiles_x * P.tiles_y);
-    const int x0 = tx * TX, y0 = ty * TY, z0 = tz * TZ;
-    const bool full_tile = x0 + TX <= g.nx && y0 + TY <= g.ny && (NDIM == 2 || z0 + TZ <= g.nz);
-
-    for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
-    if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
-    for (int i = tid; i < NSLOT; i += NT) {
-        const int lx = i % SX - 1, ly = (i / SX) % SY - 1, lz = (NDIM == 3) ? i / SXY - 1 : 0;
-        const int out = (lx < 0 || lx >= TX) + (ly < 0 || ly >= TY) + ((NDIM == 3) && (lz < 0 || lz >= TZ));
-        if (out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
-    }
-    for (int o = tid; o < NCELL; o += NT) {
-        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-        const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-        unsigned int nv = 0;
-        if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
-            const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
-            nv = P.cnt[gi];
-        }
-        Nc[o] = nv;
-    }
-    __syncthreads();
-
-    volatile unsigned long long* VS = S;
-    const volatile unsigned int* VH = (const volatile unsigned int*)S;   // VH[2s+1] = high half of S[s]
-    const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
-    unsigned short* q = Q + warp * CPW;
-    const int wbase = warp * CPW;
-    unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0;
-    unsigned int rounds = 0;
-
-    for (int r = 0; r < P.rounds; ++r) {
-        // (i)+(ii): test and compact
-        int cnt = 0;
-#pragma unroll 4
-        for (int j = 0; j < JPL; ++j) {
-            const int o = wbase + lane + 32 * j;
-            const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-            const int s = (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 1;
-            bool e = false;
-            const unsigned long long w = VS[s];
-            bool valid = full_tile || (x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz));
-            if (valid && w < wlim) {
-                ++tested;
-                const unsigned int oh = (unsigned int)(w >> 32);
-                const unsigned int a = VH[2 * (s - 1) + 1], b = VH[2 * (s + 1) + 1];
-                const unsigned int c = VH[2 * (s - SX) + 1], d = VH[2 * (s + SX) + 1];
-                bool lt = oh < a && oh < b && oh < c && oh < d;
-                bool gt = oh > a || oh > b || oh > c || oh > d;
-                if (NDIM == 3) {
-                    const unsigned int ee = VH[2 * (s - SXY) + 1], ff = VH[2 * (s + SXY) + 1];
-                    lt = lt && oh < ee && oh < ff;
-                    gt = gt || oh > ee || oh > ff;
-                }
-                if (lt) {
-                    e = true;
-                } else if (!gt) {   // a tie in the high halves: decide on the full words
-                    e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
-                    if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
-                }
-            }
-            const unsigned int m = __ballot_sync(0xffffffffu, e);
-            if (e) q[cnt + __popc(m & ((1u << lane) - 1u))] = (unsigned short)o;
-            cnt += __popc(m);
-        }
-        __syncwarp();
-        // (iii): fire the queued cells with the whole warp
-        for (int i = lane; i < cnt; i += 32) {
-            const int o = q[i];
-            const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-            const int s = (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 1;
-            const unsigned long long w = VS[s];
-            const volatile unsigned int* VL = (const volatile unsigned int*)S;
-            uint32_t ones = (VL[2 * (s - 1)] & 1u) + (VL[2 * (s + 1)] & 1u) + (VL[2 * (s - SX)] & 1u) +
-                            (VL[2 * (s + SX)] & 1u);
-            if (NDIM == 3) ones += (VL[2 * (s - SXY)] & 1u) + (VL[2 * (s + SXY)] & 1u);
-            const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-            const unsigned long long cid = NDIM == 2
-                ? (unsigned long long)(gy + g.y0) * g.nx + gx
-                : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
-            const unsigned int k = Nc[o];
-            const FireOut f = fire(w, ones, Z, k, cid, g.SH, thr, lr, P.key0, P.key1, P.inv_lambda,
-                                   P.tie_bits, P.do_hash);
-            VS[s] = f.wnew;
-            Nc[o] = k + 1;
-            hacc += f.h;
-            flips += f.flip;
-            ++fired;
-        }
-        ++rounds;
-        if (__syncthreads_count(cnt > 0) == 0) break;
-    }
-
-    unsigned long long active = 0;
-    for (int o = tid; o < NCELL; o += NT) {
-        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-        const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-        if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
-            const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
-            const unsigned long long w = S[(lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 1];
-            P.words[gi] = w;
-            P.cnt[gi] = Nc[o];
-            active += w < wlim;
-        }
-    }
-    const unsigned long long s_act = block_sum<NT>(active, red);
-    const unsigned long long s_fir = block_sum<NT>(fired, red);
-    const unsigned long long s_flp = block_sum<NT>(flips, red);
-    const unsigned long long s_tst = block_sum<NT>(tested, red);
-    const unsigned long long s_hsh = block_sum<NT>(hacc, red);
-    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds);
-}
-
 // ------------------------------------------------------------ persistent TMA tile kernel
-// tile2's rounds inside a persistent CTA that walks the tiles (tile = blockIdx.x + k*gridDim.x).
-// Staging of a full tile: the tile's own rows of words and counters arrive by TMA bulk
-// copies (cp.async.bulk, one mbarrier, ~48 KB in flight per CTA: no other CTA writes these
-// rows, so a bulk copy is safe); the face halo — words other CTAs may be updating in place —
-// is read with ordinary 8-byte loads (single-copy atomic, so a (t, s) pair is never torn).
-// Write-back uses 16-byte vector stores. Smem row stride TX+4 puts the interior of every
-// row on a 16-byte boundary. Ragged / odd-width tiles take the generic per-word path.
-__device__ __forceinline__ unsigned long long ld_word1(const KParams& P, int gx, int gy, int gz) {
-    const Geo& g = P.g;
-    const int x = wrap1(gx, g.nx);
-    if (g.ndim == 2) {
-        if (!g.sharded) return P.words[(size_t)wrap1(gy, g.ny) * g.nx + x];
-        if (gy < 0) return P.halo_lo[x];
-        if (gy >= g.ny) return P.halo_hi[x];
-        return P.words[(size_t)gy * g.nx + x];
-    }
-    const int y = wrap1(gy, g.ny);
-    if (!g.sharded) return P.words[((size_t)wrap1(gz, g.nz) * g.ny + y) * g.nx + x];
-    if (gz < 0) return P.halo_lo[(size_t)y * g.nx + x];
-    if (gz >= g.nz) return P.halo_hi[(size_t)y * g.nx + x];
-    return P.words[((size_t)gz * g.ny + y) * g.nx + x];
-}
+// The production kernel. Persistent CTAs walk the tiles (the sweep direction alternates
+// between launches, so the in-place updates of tiles processed earlier in a launch propagate
+// both ways: Gauss-Seidel across tiles). Staging of a full tile: its own rows arrive by TMA
+// bulk copies (cp.async.bulk; no other CTA writes these rows), the face halo — words other
+// CTAs may be updating — by ordinary 8-byte loads (single-copy atomic). DB: the next tile's
+// rows stream into a second buffer while the current tile is processed. Per round each warp
+// (i) tests its cells: a 32-bit compare of the high halves (full 64-bit compare only on a
+// tie), (ii) compacts the eligible cells with a warp scan, (iii) fires them with all lanes
+// busy. A queued cell's neighbourhood is frozen until it fires (no neighbour can pass its
+// own test while the cell's lower word is unchanged), so compaction preserves exactness.
+struct TileStats {
+    unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0;
+};
 
-template <int NDIM, int TX, int TY, int TZ, int NT, int MINB>
-__global__ void __launch_bounds__(NT, MINB) tile3_kernel(const KParams P) {
-    constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
+template <int NDIM, int TX, int TY, int TZ, int NT, bool FULL>
+__device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned long long* S, unsigned short* Q,
+                                                    const unsigned long long* thr, const unsigned long long* lr,
+                                                    int x0, int y0, int z0, unsigned long long wlim, TileStats& st) {
+    constexpr int SX = TX + 4, SY = TY + 2;
     constexpr int SXY = SX * SY;
-    constexpr int NSLOT = SXY * SZ;
     constexpr int NCELL = TX * TY * TZ;
-    constexpr int NROWS = TY * TZ;
     constexpr int NW = NT / 32;
     constexpr int CPW = NCELL / NW;
     constexpr int JPL = CPW / 32;
     constexpr int Z = 2 * NDIM;
+    constexpr bool FASTMAP = (TX % 32 == 0) && (CPW % TX == 0) && (TY % (CPW / TX == 0 ? 1 : CPW / TX) == 0);
+    constexpr int LPR = TX / 32 > 0 ? TX / 32 : 1;
+    const Geo& g = P.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wbase = warp * CPW;
+    unsigned short* q = Q + warp * CPW;
+    volatile unsigned long long* VS = S;
+    const volatile unsigned int* VH = (const volatile unsigned int*)S;   // [2s+1]: high half, [2s]: low half
+    auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2; };
+    int s0 = 0;
+    if (FASTMAP) {
+        const int row0 = warp * (CPW / TX);
+        s0 = slot(lane, row0 % TY, row0 / TY);
+    }
+    unsigned int rounds = 0;
+    for (int r = 0; r < P.rounds; ++r) {
+        uint32_t emask = 0, amask = 0;
+#pragma unroll
+        for (int j = 0; j < JPL; ++j) {
+            int s;
+            bool valid = true;
+            if (FASTMAP) {
+                s = s0 + (j / LPR) * SX + 32 * (j % LPR);
+            } else {
+                const int o = wbase + lane + 32 * j;
+                s = slot(o % TX, (o / TX) % TY, o / (TX * TY));
+            }
+            if (!FULL) {
+                const int o = wbase + lane + 32 * j;
+                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                valid = x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz);
+            }
+            const unsigned long long w = VS[s];
+            const bool act = valid && w < wlim;
+            if (act) {
+                const unsigned int oh = (unsigned int)(w >> 32);
+                unsigned int mn = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]),
+                                      min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
+                if (NDIM == 3) mn = min(mn, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
+                bool e = oh < mn;
+                if (oh == mn) {   // tie in the high halves: decide on the full words
+                    e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
+                    if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+                }
+                emask |= (uint32_t)e << j;
+            }
+            amask |= (uint32_t)act << j;
+        }
+        st.tested += __popc(amask);
+        const int mine = __popc(emask);
+        int incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const int cnt = __shfl_sync(0xffffffffu, incl, 31);
+        int pos = incl - mine;
+        while (emask) {
+            const int j = __ffs(emask) - 1;
+            emask &= emask - 1u;
+            q[pos++] = (unsigned short)(wbase + lane + 32 * j);
+        }
+        __syncwarp();
+        for (int i = lane; i < cnt; i += 32) {
+            const int o = q[i];
+            const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+            const int s = slot(lx, ly, lz);
+            const unsigned long long w = VS[s];
+            uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
+                            (VH[2 * (s + SX)] & 1u);
+            if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
+            const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.key0, P.key1,
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+            if (!f.ok) continue;
+            VS[s] = f.wnew;
+            st.hacc += f.h;
+            st.flips += f.flip;
+            ++st.fired;
+        }
+        ++rounds;
+        if (__syncthreads_count(cnt > 0) == 0) break;
+    }
+    return rounds;
+}
+
+template <int NDIM, int TX, int TY, int TZ>
+__device__ __forceinline__ void halo_coords(int h, int& lx, int& ly, int& lz) {
+    lz = 0;
+    if (NDIM == 2) {
+        if (h < TX) { lx = h; ly = -1; }
+        else if (h < 2 * TX) { lx = h - TX; ly = TY; }
+        else if (h < 2 * TX + TY) { lx = -1; ly = h - 2 * TX; }
+        else { lx = TX; ly = h - 2 * TX - TY; }
+    } else {
+        int r = h;
+        if (r < 2 * TX * TY) { lz = r < TX * TY ? -1 : TZ; r %= TX * TY; lx = r % TX; ly = r / TX; }
+        else if ((r -= 2 * TX * TY) < 2 * TX * TZ) { ly = r < TX * TZ ? -1 : TY; r %= TX * TZ; lx = r % TX; lz = r / TX; }
+        else { r -= 2 * TX * TZ; lx = r < TY * TZ ? -1 : TX; r %= TY * TZ; ly = r % TY; lz = r / TY; }
+    }
+}
+
+template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB>
+__global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
+    constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
+    constexpr int SXY = SX * SY;
+    constexpr int NSLOT = SXY * SZ;
+    constexpr int NSLOTP = (NSLOT + 15) & ~15;          // keep each buffer 128-B aligned
+    constexpr int NB_ = DB ? 2 : 1;
+    constexpr int NCELL = TX * TY * TZ;
+    constexpr int NROWS = TY * TZ;
+    constexpr int NW = NT / 32;
     constexpr int NHALO = NDIM == 2 ? 2 * (TX + TY) : 2 * (TX * TY + TX * TZ + TY * TZ);
-    static_assert(NCELL % NT == 0 && CPW % 32 == 0 && TX % 4 == 0, "tile/block mismatch");
+    static_assert(NCELL % NT == 0 && (NCELL / NW) % 32 == 0 && TX % 4 == 0, "tile/block mismatch");
 
     if (*(volatile unsigned int*)&P.ctl->done) return;
 
     extern __shared__ __align__(128) unsigned long long smem[];
-    unsigned long long* S = smem;                                   // NSLOT words
-    unsigned long long* lr = S + NSLOT;                             // 512
+    unsigned long long* Sb = smem;                                  // NB_ x NSLOTP words
+    unsigned long long* lr = Sb + NB_ * NSLOTP;                     // 512
     unsigned long long* thr = lr + 512;                             // 16
     unsigned long long* red = thr + 16;                             // NW
-    unsigned long long* bar = red + NW;                             // 1 (+1 pad)
-    unsigned int* Nc = (unsigned int*)(bar + 2);                    // NCELL counters (16-B aligned)
-    unsigned short* Q = (unsigned short*)(Nc + NCELL);              // NW * CPW queue
+    unsigned long long* bar = red + NW;                             // 2
+    unsigned short* Q = (unsigned short*)(bar + 2);                 // NCELL
 
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
-    if (tid == 0) mbar_init(bar, 1);
+    if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
     __syncthreads();
 
     auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2; };
-    volatile unsigned long long* VS = S;
-    const volatile unsigned int* VH = (const volatile unsigned int*)S;   // [2s+1]: high half, [2s]: low half
     const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
-    unsigned short* q = Q + warp * CPW;
-    const int wbase = warp * CPW;
     const int ntiles = P.tiles_x * P.tiles_y * P.tiles_z;
-    const bool vec_ok = (g.nx % 4) == 0;
-    unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0, active = 0;
+    const bool vec_ok = (g.nx % 2) == 0;
+    const bool reverse = (*(volatile unsigned long long*)&P.ctl->launches) & 1ull;
+    TileStats st;
+    unsigned long long active = 0;
     unsigned int rounds_max = 0;
-    uint32_t parity = 0;
+    uint32_t ph = 0;   // bit b: parity of bar[b]
 
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int tx = tile % P.tiles_x;
-        const int ty = (tile / P.tiles_x) % P.tiles_y;
-        const int tz = tile / (P.tiles_x * P.tiles_y);
-        const int x0 = tx * TX, y0 = ty * TY, z0 = tz * TZ;
-        const bool full = x0 + TX <= g.nx && y0 + TY <= g.ny && (NDIM == 2 || z0 + TZ <= g.nz);
-        const bool fast = full && vec_ok;
+    auto origin = [&](int it, int& x0, int& y0, int& z0, bool& fast, bool& full) {
+        const int tile = reverse ? ntiles - 1 - it : it;
+        const int tx = tile % P.tiles_x, ty = (tile / P.tiles_x) % P.tiles_y, tz = tile / (P.tiles_x * P.tiles_y);
+        x0 = tx * TX; y0 = ty * TY; z0 = tz * TZ;
+        full = x0 + TX <= g.nx && y0 + TY <= g.ny && (NDIM == 2 || z0 + TZ <= g.nz);
+        fast = full && vec_ok;
+    };
+    auto issue = [&](int it, int b) {   // warp 0: TMA of the tile's own rows into buffer b
+        int x0, y0, z0; bool fast, full;
+        origin(it, x0, y0, z0, fast, full);
+        if (!fast) return;
+        if (lane == 0) mbar_arrive_expect_tx(&bar[b], (uint32_t)NROWS * TX * 8u);
+        __syncwarp();
+        fence_proxy_async();
+        unsigned long long* S = Sb + b * NSLOTP;
+        for (int row = lane; row < NROWS; row += 32) {
+            const int ly = row % TY, lz = row / TY;
+            const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
+                                        : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
+            bulk_g2s(&S[slot(0, ly, lz)], P.words + gi, TX * 8, &bar[b]);
+        }
+    };
 
-        // ------------------------------------------------ stage
+    if (DB && warp == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    int k = 0;
+    for (int it = blockIdx.x; it < ntiles; it += gridDim.x, ++k) {
+        const int b = DB ? (k & 1) : 0;
+        unsigned long long* S = Sb + b * NSLOTP;
+        int x0, y0, z0; bool fast, full;
+        origin(it, x0, y0, z0, fast, full);
+        if (warp == 0) {
+            if (DB) { if (it + (int)gridDim.x < ntiles) issue(it + gridDim.x, b ^ 1); }
+            else issue(it, 0);
+        }
         if (fast) {
-            if (warp == 0) {
-                if (lane == 0) mbar_arrive_expect_tx(bar, (uint32_t)NROWS * TX * 12u);
-                __syncwarp();
-                fence_proxy_async();
-                for (int row = lane; row < NROWS; row += 32) {
-                    const int ly = row % TY, lz = row / TY;
-                    const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
-                                                : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
-                    bulk_g2s(&S[slot(0, ly, lz)], P.words + gi, TX * 8, bar);
-                    bulk_g2s(&Nc[row * TX], P.cnt + gi, TX * 4, bar);
-                }
-            }
             for (int h = tid; h < NHALO; h += NT) {
-                int lx, ly, lz = 0;
-                if (NDIM == 2) {
-                    if (h < TX) { lx = h; ly = -1; }
-                    else if (h < 2 * TX) { lx = h - TX; ly = TY; }
-                    else if (h < 2 * TX + TY) { lx = -1; ly = h - 2 * TX; }
-                    else { lx = TX; ly = h - 2 * TX - TY; }
-                } else {
-                    int r = h;
-                    if (r < 2 * TX * TY) { lz = r < TX * TY ? -1 : TZ; r %= TX * TY; lx = r % TX; ly = r / TX; }
-                    else if ((r -= 2 * TX * TY) < 2 * TX * TZ) {
-                        ly = r < TX * TZ ? -1 : TY; r %= TX * TZ; lx = r % TX; lz = r / TX;
-                    } else {
-                        r -= 2 * TX * TZ;
-                        lx = r < TY * TZ ? -1 : TX; r %= TY * TZ; ly = r % TY; lz = r / TY;
-                    }
-                }
-                S[slot(lx, ly, lz)] = ld_word1(P, x0 + lx, y0 + ly, z0 + lz);
+                int lx, ly, lz;
+                halo_coords<NDIM, TX, TY, TZ>(h, lx, ly, lz);
+                S[slot(lx, ly, lz)] = ld_word_t<true>(P, x0 + lx, y0 + ly, z0 + lz);
             }
-            mbar_wait(bar, parity);
-            parity ^= 1u;
+            mbar_wait(&bar[b], (ph >> b) & 1u);
+            ph ^= 1u << b;
         } else {
             for (int i = tid; i < NSLOT; i += NT) {
                 const int lx = i % SX - 2, ly = (i / SX) % SY - 1, lz = (NDIM == 3) ? i / SXY - 1 : 0;
@@ -606,110 +559,14 @@ __global__ void __launch_bounds__(NT, MINB) tile3_kernel(const KParams P) {
                 const int out = (lx < 0 || lx >= TX) + (ly < 0 || ly >= TY) + ((NDIM == 3) && (lz < 0 || lz >= TZ));
                 if (out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
             }
-            for (int o = tid; o < NCELL; o += NT) {
-                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-                const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-                unsigned int nv = 0;
-                if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
-                    const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
-                    nv = P.cnt[gi];
-                }
-                Nc[o] = nv;
-            }
         }
         __syncthreads();
 
-        // ------------------------------------------------ rounds
-        // Lane `lane` of warp `warp` owns cells o_j = warp*CPW + lane + 32 j. With FASTMAP the
-        // slot of o_j is s_0 + const(j): all shared-memory addresses become immediates.
-        constexpr bool FASTMAP = (TX % 32 == 0) && (CPW % TX == 0) && (TY % (CPW / TX == 0 ? 1 : CPW / TX) == 0);
-        constexpr int LPR = TX / 32 > 0 ? TX / 32 : 1;                  // lane-groups per row
-        int s0 = 0;
-        if (FASTMAP) {
-            const int row0 = warp * (CPW / TX);
-            s0 = slot(lane, row0 % TY, row0 / TY);
-        }
-        unsigned int rounds = 0;
-        for (int r = 0; r < P.rounds; ++r) {
-            uint32_t emask = 0, amask = 0;
-#pragma unroll
-            for (int j = 0; j < JPL; ++j) {
-                int s;
-                bool valid = true;
-                if (FASTMAP) {
-                    s = s0 + (j / LPR) * SX + 32 * (j % LPR);
-                    if (!full) {
-                        const int o = wbase + lane + 32 * j;
-                        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-                        valid = x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz);
-                    }
-                } else {
-                    const int o = wbase + lane + 32 * j;
-                    const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-                    s = slot(lx, ly, lz);
-                    valid = full || (x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz));
-                }
-                const unsigned long long w = VS[s];
-                const bool act = valid && w < wlim;
-                if (act) {
-                    const unsigned int oh = (unsigned int)(w >> 32);
-                    unsigned int mn = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]),
-                                          min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
-                    if (NDIM == 3) mn = min(mn, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
-                    bool e = oh < mn;
-                    if (oh == mn) {   // tie in the high halves: decide on the full words
-                        e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
-                        if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
-                    }
-                    emask |= (uint32_t)e << j;
-                }
-                amask |= (uint32_t)act << j;
-            }
-            tested += __popc(amask);
-            // compaction: warp-exclusive scan of the per-lane counts
-            const int mine = __popc(emask);
-            int incl = mine;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            const int cnt = __shfl_sync(0xffffffffu, incl, 31);
-            int pos = incl - mine;
-            while (emask) {
-                const int j = __ffs(emask) - 1;
-                emask &= emask - 1u;
-                q[pos++] = (unsigned short)(wbase + lane + 32 * j);
-            }
-            __syncwarp();
-            for (int i = lane; i < cnt; i += 32) {
-                const int o = q[i];
-                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
-                const int s = slot(lx, ly, lz);
-                const unsigned long long w = VS[s];
-                uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
-                                (VH[2 * (s + SX)] & 1u);
-                if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
-                const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-                const unsigned long long cid = NDIM == 2
-                    ? (unsigned long long)(gy + g.y0) * g.nx + gx
-                    : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
-                const unsigned int k = Nc[o];
-                const FireOut f = fire(w, ones, Z, k, cid, g.SH, thr, lr, P.key0, P.key1, P.inv_lambda,
-                                       P.tie_bits, P.do_hash);
-                VS[s] = f.wnew;
-                Nc[o] = k + 1;
-                hacc += f.h;
-                flips += f.flip;
-                ++fired;
-            }
-            ++rounds;
-            if (__syncthreads_count(cnt > 0) == 0) break;
-        }
+        const unsigned int rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true>(P, S, Q, thr, lr, x0, y0, z0, wlim, st)
+                                         : tile_rounds<NDIM, TX, TY, TZ, NT, false>(P, S, Q, thr, lr, x0, y0, z0, wlim, st);
         rounds_max = rounds > rounds_max ? rounds : rounds_max;
         __syncthreads();
 
-        // ------------------------------------------------ write back
         if (fast) {
             for (int idx = tid; idx < NROWS * (TX / 2); idx += NT) {
                 const int row = idx / (TX / 2), m2 = 2 * (idx % (TX / 2));
@@ -720,13 +577,6 @@ __global__ void __launch_bounds__(NT, MINB) tile3_kernel(const KParams P) {
                 *reinterpret_cast<ulonglong2*>(P.words + gi + m2) = v;
                 active += (v.x < wlim) + (v.y < wlim);
             }
-            for (int idx = tid; idx < NROWS * (TX / 4); idx += NT) {
-                const int row = idx / (TX / 4), m4 = 4 * (idx % (TX / 4));
-                const int ly = row % TY, lz = row / TY;
-                const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
-                                            : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
-                *reinterpret_cast<uint4*>(P.cnt + gi + m4) = *reinterpret_cast<const uint4*>(&Nc[row * TX + m4]);
-            }
         } else {
             for (int o = tid; o < NCELL; o += NT) {
                 const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
@@ -735,18 +585,17 @@ __global__ void __launch_bounds__(NT, MINB) tile3_kernel(const KParams P) {
                     const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
                     const unsigned long long w = S[slot(lx, ly, lz)];
                     P.words[gi] = w;
-                    P.cnt[gi] = Nc[o];
                     active += w < wlim;
                 }
             }
         }
-        __syncthreads();   // smem is rewritten by the next tile's staging
+        __syncthreads();   // the buffer is rewritten by a later staging
     }
     const unsigned long long s_act = block_sum<NT>(active, red);
-    const unsigned long long s_fir = block_sum<NT>(fired, red);
-    const unsigned long long s_flp = block_sum<NT>(flips, red);
-    const unsigned long long s_tst = block_sum<NT>(tested, red);
-    const unsigned long long s_hsh = block_sum<NT>(hacc, red);
+    const unsigned long long s_fir = block_sum<NT>(st.fired, red);
+    const unsigned long long s_flp = block_sum<NT>(st.flips, red);
+    const unsigned long long s_tst = block_sum<NT>(st.tested, red);
+    const unsigned long long s_hsh = block_sum<NT>(st.hacc, red);
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max);
 }
 
@@ -766,14 +615,12 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
     unsigned long long* thr = lr + 512;               // 16
     unsigned long long* red = thr + 16;               // NT/32
     unsigned long long* pend = red + NT / 32;         // N (SYNC only)
-    unsigned int* ns = (unsigned int*)(pend + (SYNC ? N : 0));   // N counters
     const int tid = threadIdx.x;
     const int Z = 2 * g.ndim;
     for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
     for (int i = tid; i < N; i += NT) {
         S[i] = P.words[i];
-        ns[i] = P.cnt[i];
         if (SYNC) pend[i] = 0ull;
     }
     __syncthreads();
@@ -803,14 +650,14 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
                 ones += (uint32_t)(e & 1ull) + (uint32_t)(f & 1ull);
             }
             if (!ok) continue;
-            const FireOut o = fire(w, ones, Z, ns[i], (unsigned long long)i, g.SH, thr, lr, P.key0, P.key1,
-                                   P.inv_lambda, P.tie_bits, P.do_hash);
+            const FireOut o = fire(w, ones, Z, (unsigned long long)i, g, thr, lr, P.key0, P.key1, P.inv_lambda,
+                                   P.tie_bits, P.do_hash, P.ctl);
+            if (!o.ok) continue;
             hacc += o.h;
             flips += o.flip;
             ++fired;
-            ns[i] += 1;
             any = 1;
-            if (SYNC) pend[i] = o.wnew;   // private new_s/new_t (word 0 never occurs: t >= 1)
+            if (SYNC) pend[i] = o.wnew;   // private new word (0 never occurs: t >= 1)
             else VS[i] = o.wnew;
         }
         ++rounds;
@@ -826,7 +673,6 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
     unsigned long long active = 0;
     for (int i = tid; i < N; i += NT) {
         P.words[i] = S[i];
-        P.cnt[i] = ns[i];
         active += S[i] < wlim;
     }
     const unsigned long long s_act = block_sum<NT>(active, red);
@@ -838,77 +684,99 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
 }
 
 // ------------------------------------------------------------------------ init (P5)
-__global__ void init_kernel(unsigned long long* __restrict__ words, unsigned int* __restrict__ cnt, Geo g,
-                            const unsigned long long* __restrict__ lr_g, uint32_t key0, uint32_t key1,
-                            unsigned long long thr_init, unsigned long long inv_lambda, int tie_bits,
-                            unsigned long long n_local) {
+__device__ __forceinline__ void cell_coords(const Geo& g, unsigned long long li, unsigned long long& c,
+                                            unsigned long long& rank) {
+    const unsigned long long x = li % g.nx;
+    if (g.ndim == 2) {
+        const unsigned long long y = li / g.nx + g.y0;
+        c = y * g.nx + x;
+        rank = x + y;
+    } else {
+        const unsigned long long plane = (unsigned long long)g.nx * g.ny;
+        const unsigned long long y = (li / g.nx) % g.ny, z = li / plane + g.z0;
+        c = (z * g.NY + y) * g.nx + x;
+        rank = x + y + z;
+    }
+}
+
+__global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const unsigned long long* __restrict__ lr_g,
+                            uint32_t key0, uint32_t key1, unsigned long long thr_init, unsigned long long inv_lambda,
+                            int tie_bits, unsigned long long n_local) {
     __shared__ unsigned long long lr[512];
     for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
     __syncthreads();
-    const unsigned long long plane = (unsigned long long)g.nx * g.ny;
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n_local;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long x = i % g.nx;
         unsigned long long c, rank;
-        if (g.ndim == 2) {
-            const unsigned long long y = i / g.nx + g.y0;
-            c = y * g.nx + x;
-            rank = x + y;
-        } else {
-            const unsigned long long y = (i / g.nx) % g.ny, z = i / plane + g.z0;
-            c = (z * g.NY + y) * g.nx + x;
-            rank = x + y + z;
-        }
+        cell_coords(g, i, c, rank);
         const u32x4 r = philox4x32_10(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, key0, key1);
         const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
         const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits);
-        words[i] = (t0 << g.SH) | (rank << 1) | sb;
-        cnt[i] = 0u;
+        words[i] = w_pack(t0, rank, 0ull, sb, g);
     }
 }
 
-// Repack (t, s) from host-provided spins / times into words (aca_set_state / aca_set_spins).
-// Element i of the launch is shard-local cell base + i.
+// Build words from host-provided spins / times / counters (any may be null: keep the
+// current field). Element i of the launch is shard-local cell base + i.
 __global__ void pack_kernel(unsigned long long* __restrict__ words, const int8_t* __restrict__ spins,
-                            const unsigned long long* __restrict__ times, Geo g, unsigned long long n,
-                            unsigned long long base) {
-    const unsigned long long plane = (unsigned long long)g.nx * g.ny;
+                            const unsigned long long* __restrict__ times, const unsigned int* __restrict__ counters,
+                            Geo g, unsigned long long n, unsigned long long base) {
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long li = base + i;
-        const unsigned long long x = li % g.nx;
-        unsigned long long rank;
-        if (g.ndim == 2) rank = x + li / g.nx + g.y0;
-        else rank = x + (li / g.nx) % g.ny + li / plane + g.z0;
+        unsigned long long c, rank;
+        cell_coords(g, base + i, c, rank);
         const unsigned long long w = words[i];
-        const unsigned long long t = times ? times[i] : (w >> g.SH);
+        const unsigned long long t = times ? times[i] : w_time(w, g);
+        const unsigned long long k = counters ? counters[i] : w_count(w, g);
         const unsigned long long sb = spins ? (spins[i] > 0 ? 1ull : 0ull) : (w & 1ull);
-        words[i] = (t << g.SH) | (rank << 1) | sb;
+        words[i] = w_pack(t, rank, k, sb, g);
     }
 }
 
-// Unpack spins (int8) and times (u64) for the getters.
+// Change the (t, n) split of the words in place (from layout a to layout b).
+__global__ void repack_kernel(unsigned long long* __restrict__ words, Geo a, Geo b, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long w = words[i];
+        const unsigned long long rank = (w >> (a.NB + 1)) & ((1ull << a.RB) - 1ull);
+        words[i] = w_pack(w_time(w, a), rank, w_count(w, a), w & 1ull, b);
+    }
+}
+
+// Gather sampled cells (handle-wide indices; this shard holds [base, base + n)).
+__global__ void gather_kernel(const unsigned long long* __restrict__ words, const int64_t* __restrict__ idx,
+                              unsigned long long m, long long base, long long n, unsigned long long* __restrict__ w_out) {
+    const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const long long c = idx[i] - base;
+    if (c < 0 || c >= n) return;
+    w_out[i] = words[c];
+}
+
+// Unpack spins (int8), times (u64) or counters (u32) for the getters.
 __global__ void unpack_kernel(const unsigned long long* __restrict__ words, int8_t* __restrict__ spins,
-                              unsigned long long* __restrict__ times, int SH, unsigned long long n) {
+                              unsigned long long* __restrict__ times, unsigned int* __restrict__ counters, Geo g,
+                              unsigned long long n) {
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const unsigned long long w = words[i];
         if (spins) spins[i] = (w & 1ull) ? (int8_t)1 : (int8_t)-1;
-        if (times) times[i] = w >> SH;
+        if (times) times[i] = w_time(w, g);
+        if (counters) counters[i] = w_count(w, g);
     }
 }
 
-// Statistics over the owned cells: B (bonds along +e_a), M, sum n, t_min, t_max.
+// Statistics over the owned cells: B (bonds along +e_a), M, sum n, max n, t_min, t_max.
 struct StatAcc {
     long long bond, mag;
-    unsigned long long arrivals, tmin, tmax;
+    unsigned long long arrivals, tmin, tmax, nmax;
 };
 
 template <int NT>
 __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out, unsigned long long n_local) {
     const Geo& g = P.g;
     long long bond = 0, mag = 0;
-    unsigned long long arr = 0, tmin = ~0ull, tmax = 0;
+    unsigned long long arr = 0, tmin = ~0ull, tmax = 0, nmax = 0;
     const unsigned long long plane = (unsigned long long)g.nx * g.ny;
     for (unsigned long long i = blockIdx.x * (unsigned long long)NT + threadIdx.x; i < n_local;
          i += (unsigned long long)gridDim.x * NT) {
@@ -922,8 +790,10 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         if (g.ndim == 3) plus += (ld_word(P, x, y, z + 1) & 1ull) ? 1 : -1;
         bond += s * plus;
         mag += s;
-        arr += P.cnt[i];
-        const unsigned long long t = w >> g.SH;
+        const unsigned long long k = w_count(w, g);
+        arr += k;
+        nmax = k > nmax ? k : nmax;
+        const unsigned long long t = w_time(w, g);
         tmin = t < tmin ? t : tmin;
         tmax = t > tmax ? t : tmax;
     }
@@ -934,8 +804,10 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         arr += __shfl_xor_sync(0xffffffffu, arr, o);
         const unsigned long long a = __shfl_xor_sync(0xffffffffu, tmin, o);
         const unsigned long long b = __shfl_xor_sync(0xffffffffu, tmax, o);
+        const unsigned long long c = __shfl_xor_sync(0xffffffffu, nmax, o);
         tmin = a < tmin ? a : tmin;
         tmax = b > tmax ? b : tmax;
+        nmax = c > nmax ? c : nmax;
     }
     if ((threadIdx.x & 31) == 0) {
         atomicAdd((unsigned long long*)&out->bond, (unsigned long long)bond);
@@ -943,6 +815,7 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         atomicAdd(&out->arrivals, arr);
         atomicMin(&out->tmin, tmin);
         atomicMax(&out->tmax, tmax);
+        atomicMax(&out->nmax, nmax);
     }
 }
 

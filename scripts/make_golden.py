@@ -1,0 +1,45 @@
+"""Write tests/golden/<config>_seed<k>.json: SHA-256 digests of the final spins, times and
+counters plus the integer statistics of a FULL oracle run of a BASELINE config.
+Calls only oracle/ (the serial PQ oracle); nothing here touches the CUDA path.
+usage: python scripts/make_golden.py c2 [seed]"""
+import hashlib
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import oracle  # noqa: E402
+import workloads  # noqa: E402
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def main():
+    name = sys.argv[1]
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else workloads.PARITY_SEEDS[0]
+    cfg = workloads.config(name)
+    t0 = time.time()
+    o = oracle.OracleSim(cfg["dims"], lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
+                         seed=seed, init_q=cfg["init_q"])
+    o.run_until(cfg["T"])
+    st = o.stats()
+    st.pop("rounds")
+    out = {"config": name, "seed": seed, "dims": list(cfg["dims"]), "T": cfg["T"],
+           "generated_by": "scripts/make_golden.py (oracle/ only)", "oracle_seconds": round(time.time() - t0, 1),
+           "sha256_spins_int8": digest(o.spins()), "sha256_times_u64": digest(o.times()),
+           "sha256_counters_u32": digest(o.counters()), "stats": {k: int(v) for k, v in st.items()}}
+    path = os.path.join(ROOT, "tests", "golden", "%s_seed%d.json" % (name, seed))
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(path, out["oracle_seconds"], "s")
+
+
+if __name__ == "__main__":
+    main()

@@ -25,7 +25,11 @@ for r in rows:
         cur = (fname, int(r[0]), r[1].strip()[:90])
     if cur and r[2]:
         a = agg[cur[:2]]
-        f = lambda x: float(x) if x not in ("", "-") else 0.0
+        def f(x):
+            try:
+                return float(x)
+            except ValueError:
+                return 0.0
         a[0] += f(r[ie])
         a[1] += f(r[sm])
         a[2] = cur[2]

@@ -1,0 +1,119 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (default
+tile, rounds and kernel): configs 2-5 run to their end time on the GPU, then
+  * every sampled cell's t(c) and n(c) equal the oracle's per-cell closed form (arrival
+    times are state-independent) — exact;
+  * every sampled cell's spin equals the window (light-cone) oracle's exact value
+    (oracle.window_cell, pinned in tests/test_oracle_window.py);
+  * properties that hold at any size: B and M recomputed from the returned spins equal the
+    device statistics, sum n = arrivals = cells fired, every t >= T, sum n within 5 sigma
+    of N*lambda*T.
+Sampled cells: random ones plus lattice corners, tile corners and tile-boundary cells."""
+import math
+
+import numpy as np
+import pytest
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def aca():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_cs_0502039_b200 as aca
+    return aca
+
+
+def sample_cells(dims, tile, n_random, seed):
+    rng = np.random.default_rng(seed)
+    pts = [tuple(0 for _ in dims), tuple(d - 1 for d in dims)]
+    for _ in range(n_random):
+        pts.append(tuple(int(rng.integers(0, d)) for d in dims))
+    for _ in range(6):   # tile corners and tile-face cells
+        p = [int(rng.integers(0, d // t)) * t for d, t in zip(dims, tile)]
+        pts.append(tuple(p))
+        q = list(p)
+        q[0] = (q[0] + tile[0] - 1) % dims[0]
+        pts.append(tuple(q))
+    return pts
+
+
+def flat(c, dims):
+    i = 0
+    for a in reversed(range(len(dims))):
+        i = i * dims[a] + c[a]
+    return i
+
+
+def bond_sum(spins, ndim):
+    s = spins.astype(np.int64)
+    return int(sum((s * np.roll(s, -1, axis=ax)).sum() for ax in range(ndim)))
+
+
+def test_config2_full_digest(aca, oracle_mod):
+    """Config 2 in full (1024^2, Metropolis beta 0.40, T = 100, ~1.05e8 arrivals) against the
+    digests of a full oracle run (tests/golden/c2_seed1.json, written by
+    scripts/make_golden.py from oracle/ only): every spin, time and counter, bit for bit."""
+    import hashlib
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c2_seed1.json")
+    gold = json.load(open(path))
+    cfg = workloads.config("c2")
+    g = aca.Sim(cfg["dims"], lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
+                seed=gold["seed"], init_q=cfg["init_q"], tile=cfg["tile"])
+    g.run_until(cfg["T"])
+    dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    assert dig(g.spins()) == gold["sha256_spins_int8"]
+    assert dig(g.times()) == gold["sha256_times_u64"]
+    assert dig(g.counters()) == gold["sha256_counters_u32"]
+    st = g.stats()
+    for k, v in gold["stats"].items():
+        assert st[k] == v, k
+
+
+@pytest.mark.parametrize("name,n_random,radii", [
+    ("c3", 40, (8, 16, 32, 64)),
+    ("c4", 24, (4, 8, 12, 16)),
+    ("c5", 24, (8, 16, 32, 64, 96)),
+])
+def test_full_size_sampled_parity(aca, oracle_mod, name, n_random, radii):
+    cfg = workloads.config(name)
+    dims, T = tuple(cfg["dims"]), cfg["T"]
+    kw = dict(lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"])
+    seed = workloads.PARITY_SEEDS[0]
+    g = aca.Sim(dims, seed=seed, init_q=cfg["init_q"], tile=cfg["tile"], **kw)
+    g.run_until(T)
+    st = g.stats()
+
+    pts = sample_cells(dims, cfg["tile"], n_random, seed=7)
+    idx = np.array([flat(c, dims) for c in pts], np.int64)
+    s_g, t_g, n_g = g.cells(idx)
+    unverified = 0
+    for c, s, t, n in zip(pts, s_g, t_g, n_g):
+        t_o, n_o = oracle_mod.cell_time_counter(seed, flat(c, dims), T, cfg["lam"])
+        assert (int(t), int(n)) == (t_o, n_o), (name, c)
+        for r in radii:
+            s_o, t_w, n_w, exact = oracle_mod.window_cell(dims, c, T, r, seed=seed, init_q=cfg["init_q"], **kw)
+            assert (t_w, n_w) == (t_o, n_o)
+            if exact:
+                assert int(s) == s_o, (name, c, r)
+                break
+        else:
+            unverified += 1
+    assert unverified <= len(pts) // 10, "%d of %d sampled spins had no exact window" % (unverified, len(pts))
+
+    spins = g.spins()
+    assert st["bond_sum"] == bond_sum(spins, len(dims))
+    assert st["magnetisation"] == int(spins.astype(np.int64).sum())
+    del spins
+    counters = g.counters()
+    tot = int(counters.astype(np.int64).sum())
+    assert tot == st["arrivals"] == st["cells_fired"]
+    N = int(np.prod(dims))
+    mu = N * cfg["lam"] * T
+    assert abs(tot - mu) < 5 * math.sqrt(mu)
+    assert st["t_min"] >= oracle_mod.to_q32(T)

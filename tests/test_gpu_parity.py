@@ -107,8 +107,8 @@ def test_tiled_2d_ragged(aca, oracle_mod, tile):
 
 @pytest.mark.parametrize("variant", [0, 1, 2])
 def test_kernel_variants(aca, oracle_mod, variant):
-    """Persistent TMA kernel (0), compacted per-tile kernel (1), uncompacted kernel (2):
-    identical trajectories, 2-D (full + ragged tiles, odd width) and 3-D."""
+    """Persistent TMA kernel (0), uncompacted per-tile kernel (1), double-buffered TMA
+    kernel (2): identical trajectories, 2-D (full + ragged tiles, odd width) and 3-D."""
     for dims, tile, T in (((256, 192), (64, 64), 5.0), ((200, 150), (64, 32), 4.0), ((130, 70), (32, 32), 4.0),
                           ((64, 48, 40), (32, 16, 8), 3.0), ((40, 24, 20), (16, 16, 16), 3.0)):
         beta = 0.2216544 if len(dims) == 3 else 0.4406868
@@ -187,6 +187,38 @@ def test_set_state_roundtrip(aca, oracle_mod):
     g.run_until(5.0)
     g2.run_until(5.0)
     assert np.array_equal(g.spins(), g2.spins()) and np.array_equal(g.times(), g2.times())
+
+
+def test_packed_layout_repack(aca, oracle_mod):
+    """The (t, n) split of the packed word follows T: long horizons move bits from the counter
+    to the time field (repack in place) and the trajectory is unchanged."""
+    g, o = run_pair(aca, oracle_mod, (40, 24), [0.5, 40.0, 700.0], beta=0.44, seed=41, whole_lattice=-1,
+                    tile=(32, 32))
+    assert_same(g, o)
+    g, o = run_pair(aca, oracle_mod, (6, 7), [3.0, 1500.0], beta=0.3, seed=41)   # whole-lattice kernel
+    assert_same(g, o)
+
+
+def test_counter_overflow_is_reported(aca, oracle_mod):
+    """A counter that would overflow its packed field stops the run with ACA_ERANGE instead
+    of wrapping."""
+    import paper_cs_0502039_b200 as pkg
+    g = aca.Sim((8, 8), beta=0.4, seed=3, whole_lattice=-1, tile=(32, 32))
+    s, t, n = g.spins().copy(), g.times().copy(), g.counters().copy()
+    g.set_state(s, t, n)
+    nb = g.stats()["counter_bits"]
+    assert nb >= 9
+    n[:] = 2 ** nb - 2          # one more event fills the field, the next would overflow
+    g.set_state(s, t, n)
+    assert g.stats()["counter_bits"] == nb
+    with pytest.raises(pkg.AcaError) as ei:
+        g.run_until(float(t.max()) / 2 ** 32 + 3.0)
+    assert ei.value.code == -6
+    # a state whose counters cannot fit is refused up front
+    n[:] = 2 ** 31
+    with pytest.raises(pkg.AcaError) as ei:
+        g.set_state(s, t, n)
+    assert ei.value.code == -6
 
 
 def test_set_spins_user_initial_state(aca, oracle_mod):
