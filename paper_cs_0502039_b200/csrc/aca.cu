@@ -132,6 +132,7 @@ struct aca_sim {
     ncclComm_t comm = nullptr;
     int tile[3] = {64, 64, 1};
     int rounds = 8;
+    int round_mode = 2;            // see KParams::round_mode (ACA_ROUND_MODE overrides; experiments)
     int K = 16;
     bool whole = false;
     bool sync = false;
@@ -201,22 +202,25 @@ constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf) {
 }
 
 // Kernel variants (identical results; ablations): 0 = persistent TMA-staged compacted kernel
-// (default), 1 = uncompacted one-CTA-per-tile kernel, 2 = persistent, double-buffered TMA.
+// (default), 1 = uncompacted one-CTA-per-tile kernel, 2 = persistent, double-buffered TMA,
+// 3 = persistent TMA with register-resident synchronous rounds and CTA-wide firing.
 // Slot NVARIANT = two-barrier fig:s1c1pe rounds (sync_rounds = 1).
-constexpr int NVARIANT = 3;
+constexpr int NVARIANT = 4;
 struct TileKey { int ndim, tx, ty, tz, nt; void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1]; };
 
-#define TK(ND, TX, TY, TZ, NT, MB, MBD)                                                              \
+#define TK(ND, TX, TY, TZ, NT, MB, MBD, MBR)                                                         \
     {ND, TX, TY, TZ, NT,                                                                             \
-     {(void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false>, (void*)tile_kernel<ND, TX, TY, TZ, NT, false>, \
-      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBD, true>, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}, \
+     {(void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false>, (void*)tile_kernel<ND, TX, TY, TZ, NT, false>, \
+      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBD, true, false>,                                 \
+      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBR, false, true>, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}, \
      {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
-      tile_smem(ND, TX, TY, TZ, NT)},                                                                \
-     {true, false, true, false}}
+      tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT)},                                \
+     {true, false, true, true, false}}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256, 4, 4), TK(2, 64, 32, 1, 256, 4, 3), TK(2, 64, 64, 1, 256, 3, 2), TK(2, 128, 64, 1, 512, 1, 1),
-    TK(3, 8, 8, 8, 128, 8, 4), TK(3, 16, 16, 16, 256, 2, 1), TK(3, 32, 16, 8, 256, 2, 1), TK(3, 32, 32, 8, 512, 1, 1),
+    TK(2, 32, 32, 1, 256, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3), TK(2, 64, 64, 1, 256, 3, 2, 3),
+    TK(2, 128, 64, 1, 512, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8), TK(3, 16, 16, 16, 256, 2, 1, 2),
+    TK(3, 32, 16, 8, 256, 2, 1, 2), TK(3, 32, 32, 8, 512, 1, 1, 1),
 };
 
 constexpr int WHOLE_NT = 1024;
@@ -245,6 +249,7 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.inv_lambda = S->inv_lambda;
     P.tie_bits = S->opt.tie_bits;
     P.rounds = S->rounds;
+    P.round_mode = S->round_mode;
     P.do_hash = S->opt.event_hash;
     P.tiles_x = sh.tiles_x;
     P.tiles_y = sh.tiles_y;
@@ -537,6 +542,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->sync = opt.sync_rounds != 0;
     S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 3;
     S->K = opt.launches_per_check > 0 ? opt.launches_per_check : 16;
+    if (const char* e = getenv("ACA_ROUND_MODE")) S->round_mode = atoi(e);
 
     // P3 constants, P4 table, P5 threshold, packed-word layout
     S->inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);

@@ -69,6 +69,7 @@ struct KParams {
     unsigned long long inv_lambda;
     int tie_bits;
     int rounds;                          // R_max
+    int round_mode;                      // 0: CTA barrier per round; 1: no barrier, R rounds; 2: per-warp exit
     int do_hash;
     int tiles_x, tiles_y, tiles_z;
     unsigned long long thr[14];          // P4 table
@@ -449,7 +450,153 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             ++st.fired;
         }
         ++rounds;
-        if (__syncthreads_count(cnt > 0) == 0) break;
+        if (P.round_mode == 0) {
+            if (__syncthreads_count(cnt > 0) == 0) break;   // CTA-wide stall detection
+        } else if (P.round_mode == 2 && cnt == 0) {
+            break;                                          // this warp found nothing eligible
+        }
+    }
+    return rounds;
+}
+
+// Register-resident rounds (full tiles whose rows split evenly over the warps). Lane `lane`
+// of warp `warp` owns RW rows x CPL adjacent columns; their words live in registers. The
+// test of a round reads the row neighbours from the lane's own registers, the column
+// neighbours by warp shuffles of the 32-bit high halves (halo columns preloaded into the
+// edge lanes' registers), and only the rows at a warp edge (and 3-D plane neighbours) from
+// shared memory. All tests of a round see one snapshot (no cell fires during the test
+// phase): this is exactly the synchronous round of fig:s1c1pe, whose
+// eligible cells are pairwise non-neighbours. They are queued per warp and fired by the
+// whole CTA (all lanes busy), then each owner reloads the words of its fired cells.
+template <int NDIM, int TX, int TY, int TZ, int NT>
+struct RegMap {
+    static constexpr int NCELL = TX * TY * TZ;
+    static constexpr int NW = NT / 32;
+    static constexpr int CPW = NCELL / NW;
+    static constexpr int CPL = TX / 32;                 // columns per lane
+    static constexpr int RW = CPL > 0 ? CPW / TX : 0;   // rows per warp
+    static constexpr bool ok = (TX % 32 == 0) && (CPL == 1 || CPL == 2) && (CPW % TX == 0) && RW >= 2 &&
+                               (TY % (RW > 0 ? RW : 1) == 0) && RW * CPL <= 32;
+};
+
+template <int NDIM, int TX, int TY, int TZ, int NT>
+__device__ __forceinline__ unsigned int tile_rounds_reg(const KParams& P, unsigned long long* S, unsigned short* Q,
+                                                        unsigned int* wcnt, const unsigned long long* thr,
+                                                        const unsigned long long* lr, int x0, int y0, int z0,
+                                                        unsigned long long wlim, TileStats& st) {
+    using M = RegMap<NDIM, TX, TY, TZ, NT>;
+    constexpr int CPL = M::CPL, RW = M::RW, NW = M::NW, CPW = M::CPW;
+    constexpr int SX = TX + 4, SY = TY + 2, SXY = SX * SY;
+    constexpr int Z = 2 * NDIM;
+    const Geo& g = P.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int row0 = warp * RW;                       // first (y, z) row of this warp
+    const int ly0 = row0 % TY, lz0 = row0 / TY;
+    const int s0 = (lz0 + (NDIM == 3)) * SXY + (ly0 + 1) * SX + lane * CPL + 2;
+    volatile unsigned long long* VS = S;
+    const volatile unsigned int* VH = (const volatile unsigned int*)S;
+
+    unsigned long long w[RW][CPL];
+    unsigned int hx[RW];   // frozen halo column: lane 0 keeps the left one, lane 31 the right one
+#pragma unroll
+    for (int j = 0; j < RW; ++j) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) w[j][c] = VS[s0 + j * SX + c];
+        hx[j] = VH[2 * (s0 + j * SX + (lane == 0 ? -1 : CPL)) + 1];
+    }
+    unsigned int rounds = 0;
+    for (int r = 0; r < P.rounds; ++r) {
+        uint32_t emask = 0, ntest = 0;
+        // rows just outside the warp (other warps' rows or the tile halo) and plane neighbours
+        unsigned int up_e[CPL], dn_e[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            up_e[c] = VH[2 * (s0 - SX + c) + 1];
+            dn_e[c] = VH[2 * (s0 + RW * SX + c) + 1];
+        }
+#pragma unroll
+        for (int j = 0; j < RW; ++j) {
+            const unsigned int kl = __shfl_up_sync(0xffffffffu, (unsigned int)(w[j][CPL - 1] >> 32), 1);
+            const unsigned int kr = __shfl_down_sync(0xffffffffu, (unsigned int)(w[j][0] >> 32), 1);
+            const unsigned int left0 = lane > 0 ? kl : hx[j];
+            const unsigned int rightN = lane < 31 ? kr : hx[j];
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+                const unsigned long long wc = w[j][c];
+                const unsigned int oh = (unsigned int)(wc >> 32);
+                const unsigned int kL = c > 0 ? (unsigned int)(w[j][c - 1] >> 32) : left0;
+                const unsigned int kR = c < CPL - 1 ? (unsigned int)(w[j][c + 1] >> 32) : rightN;
+                const unsigned int kU = j > 0 ? (unsigned int)(w[j - 1][c] >> 32) : up_e[c];
+                const unsigned int kD = j < RW - 1 ? (unsigned int)(w[j + 1][c] >> 32) : dn_e[c];
+                unsigned int mn = min(min(kL, kR), min(kU, kD));
+                const int s = s0 + j * SX + c;
+                if (NDIM == 3) mn = min(mn, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
+                const bool act = wc < wlim;
+                bool e = act && oh < mn;
+                if (act && oh == mn) {   // tie in the high halves: full words from shared memory
+                    e = wc < VS[s - 1] && wc < VS[s + 1] && wc < VS[s - SX] && wc < VS[s + SX];
+                    if (NDIM == 3) e = e && wc < VS[s - SXY] && wc < VS[s + SXY];
+                }
+                emask |= (uint32_t)e << (j * CPL + c);
+                ntest += act;
+            }
+        }
+        st.tested += ntest;
+        // compaction into this warp's queue region
+        const int mine = __popc(emask);
+        int incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        int pos = warp * CPW + incl - mine;
+        uint32_t em = emask;
+        while (em) {
+            const int b = __ffs(em) - 1;
+            em &= em - 1u;
+            const int j = b / CPL, c = b % CPL;
+            const int o = (row0 + j) * TX + lane * CPL + c;   // cell index in the tile
+            Q[pos++] = (unsigned short)o;
+        }
+        if (lane == 31) wcnt[warp] = (unsigned int)incl;
+        __syncthreads();
+        // CTA-wide fire of all queued cells
+        unsigned int cw[NW];
+        unsigned int total = 0;
+#pragma unroll
+        for (int v = 0; v < NW; ++v) { cw[v] = wcnt[v]; total += cw[v]; }
+        if (total == 0) break;
+        for (unsigned int i = tid; i < total; i += NT) {
+            unsigned int acc = 0, qi = 0;
+#pragma unroll
+            for (int u = 0; u < NW; ++u) {   // queue entry i lives in warp u's region
+                if (i >= acc) qi = u * CPW + (i - acc);
+                acc += cw[u];
+            }
+            const int o = Q[qi];
+            const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+            const int s = (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2;
+            const unsigned long long wv = VS[s];
+            uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
+                            (VH[2 * (s + SX)] & 1u);
+            if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
+            const FireOut f = fire(wv, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.key0, P.key1,
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+            if (!f.ok) continue;
+            VS[s] = f.wnew;
+            st.hacc += f.h;
+            st.flips += f.flip;
+            ++st.fired;
+        }
+        ++rounds;
+        __syncthreads();
+        // owners reload the words of their fired cells
+#pragma unroll
+        for (int j = 0; j < RW; ++j)
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+                if ((emask >> (j * CPL + c)) & 1u) w[j][c] = VS[s0 + j * SX + c];
     }
     return rounds;
 }
@@ -470,7 +617,7 @@ __device__ __forceinline__ void halo_coords(int h, int& lx, int& ly, int& lz) {
     }
 }
 
-template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB>
+template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG>
 __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
     constexpr int SXY = SX * SY;
@@ -562,8 +709,18 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
         }
         __syncthreads();
 
-        const unsigned int rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true>(P, S, Q, thr, lr, x0, y0, z0, wlim, st)
-                                         : tile_rounds<NDIM, TX, TY, TZ, NT, false>(P, S, Q, thr, lr, x0, y0, z0, wlim, st);
+        unsigned int rounds = 0;
+        bool done_reg = false;
+        if constexpr (REG && RegMap<NDIM, TX, TY, TZ, NT>::ok) {
+            if (full) {
+                rounds = tile_rounds_reg<NDIM, TX, TY, TZ, NT>(P, S, Q, (unsigned int*)red, thr, lr, x0, y0, z0, wlim, st);
+                done_reg = true;
+            }
+        }
+        if (!done_reg) {
+            rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true>(P, S, Q, thr, lr, x0, y0, z0, wlim, st)
+                          : tile_rounds<NDIM, TX, TY, TZ, NT, false>(P, S, Q, thr, lr, x0, y0, z0, wlim, st);
+        }
         rounds_max = rounds > rounds_max ? rounds : rounds_max;
         __syncthreads();
 
