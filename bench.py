@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--tile", type=str, default="", help="e.g. 64x64 or 32x16x8")
     ap.add_argument("--launches-per-check", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0, help="tile kernel variant (ablation; 0 = default)")
+    ap.add_argument("--early-reject", type=int, default=-1, help="a10 early rejection (-1 = config default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true", help="skip the P7 event hash (diagnostics only)")
@@ -211,6 +212,9 @@ def main():
     ndim = len(dims)
     tile = tuple(int(x) for x in args.tile.split("x")) if args.tile else tuple(cfg["tile"])
     opts = dict(init_q=cfg["init_q"], device=local, tile=tile, event_hash=0 if args.no_hash else 1)
+    opts.update(cfg.get("opts", {}))
+    if args.early_reject >= 0:
+        opts["early_reject"] = args.early_reject
     if args.rounds:
         opts["rounds_per_launch"] = args.rounds
     if args.launches_per_check:

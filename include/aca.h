@@ -69,6 +69,9 @@ typedef struct {
                                    TMA staging, compacted firing (default); 1 = compacted,
                                    one CTA per tile; 2 = uncompacted; 3 = persistent,
                                    single-buffered TMA. All give identical results. */
+    int32_t early_reject;       /* 1: a cell may also commit arrivals that are rejected for
+                                   every possible state of the neighbours it still waits for
+                                   (exact; pays off at low temperature, config 5). 0 = off */
 } aca_options;
 
 typedef struct {
@@ -86,6 +89,10 @@ typedef struct {
     double kernel_seconds;  /* CUDA-event time of the kernel batches alone */
     uint64_t kernel_launches; /* every tile-kernel launch issued (incl. no-op tail) */
     int32_t time_bits, counter_bits, rank_bits; /* current split of the packed state word */
+    uint64_t class_hist[14];  /* BKL classes |Gamma_k| of the current configuration, index
+                                 (Sigma+z)/2 + (z+1)(s+1)/2 as the P4 table */
+    double nfold_rate;        /* lambda * sum_k |Gamma_k| p_k: the total flip rate of the BKL
+                                 n-fold way */
 } aca_stats;
 
 /* Fill *opt with defaults (struct_size set). */

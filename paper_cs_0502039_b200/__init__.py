@@ -39,7 +39,8 @@ class aca_options(ctypes.Structure):
                 ("sync_rounds", ctypes.c_int32), ("device", ctypes.c_int32), ("shards", ctypes.c_int32),
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("event_hash", ctypes.c_int32),
-                ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32)]
+                ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32),
+                ("early_reject", ctypes.c_int32)]
 
 
 class aca_stats(ctypes.Structure):
@@ -49,10 +50,13 @@ class aca_stats(ctypes.Structure):
                 ("cells_tested", ctypes.c_uint64), ("cells_fired", ctypes.c_uint64),
                 ("gpu_seconds", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
                 ("kernel_launches", ctypes.c_uint64), ("time_bits", ctypes.c_int32),
-                ("counter_bits", ctypes.c_int32), ("rank_bits", ctypes.c_int32)]
+                ("counter_bits", ctypes.c_int32), ("rank_bits", ctypes.c_int32),
+                ("class_hist", ctypes.c_uint64 * 14), ("nfold_rate", ctypes.c_double)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["class_hist"] = [int(v) for v in self.class_hist]
+        return d
 
 
 _lib = None

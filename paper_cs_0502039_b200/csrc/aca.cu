@@ -120,6 +120,8 @@ struct aca_sim {
     int RB = 1, NB = 1, TB = 1;    // packed word: time bits, rank bits, counter bits (+1 spin)
     unsigned long long inv_lambda = 1ull << 32;
     unsigned long long thr[14] = {};
+    unsigned long long thm[98] = {};   // a10 early-rejection table (see commit_loop)
+    int bulk = 1;
     unsigned long long thr_init = 0;
     unsigned long long max_delta = 0;
     uint64_t T_last = 0;
@@ -186,6 +188,32 @@ void flip_table(int ndim, double beta, double J, double h, int rule, unsigned lo
     }
 }
 
+// a10 table: thm[(s*(Z+1) + u)*(Z+1) + k] for a cell with spin bit s, u neighbours that may
+// still change before its arrival and k known +1 neighbours. u = 0: the exact threshold.
+// u > 0: the largest threshold over the u unknown spins (w0 >= it rejects in every world),
+// or "wait" (> 2^32) when early rejection is off or a rejection is less likely than 1/2
+// (a Philox draw would mostly be wasted).
+void early_table(int ndim, const unsigned long long* thr, bool enabled, unsigned long long* thm) {
+    const int Z = 2 * ndim;
+    const unsigned long long WAIT = 1ull << 33, CAP = 1ull << 31;
+    for (int i = 0; i < 98; ++i) thm[i] = WAIT;
+    for (int sb = 0; sb < 2; ++sb)
+        for (int u = 0; u <= Z; ++u)
+            for (int k = 0; k + u <= Z; ++k) {
+                unsigned long long v;
+                if (u == 0) {
+                    v = thr[k + (Z + 1) * sb];
+                } else if (!enabled) {
+                    v = WAIT;
+                } else {
+                    unsigned long long m = 0;
+                    for (int j = 0; j <= u; ++j) m = std::max(m, thr[k + j + (Z + 1) * sb]);
+                    v = m >= CAP ? WAIT : m;
+                }
+                thm[(sb * (Z + 1) + u) * (Z + 1) + k] = v;
+            }
+}
+
 int bits_for(uint64_t v) {
     int b = 0;
     while (v) { ++b; v >>= 1; }
@@ -197,7 +225,7 @@ constexpr size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
     return ((size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32) * 8;
 }
 constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf) {
-    return ((((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~(size_t)15) * nbuf + 512 + 16 +
+    return ((((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~(size_t)15) * nbuf + 512 + 16 + 112 +
             nt / 32 + 2) * 8 + (size_t)tx * ty * tz * 2;
 }
 
@@ -206,7 +234,11 @@ constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf) {
 // 3 = persistent TMA with register-resident synchronous rounds and CTA-wide firing.
 // Slot NVARIANT = two-barrier fig:s1c1pe rounds (sync_rounds = 1).
 constexpr int NVARIANT = 4;
-struct TileKey { int ndim, tx, ty, tz, nt; void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1]; };
+struct TileKey {
+    int ndim, tx, ty, tz, nt;
+    void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1];
+    void* fn_early;   // variant 0 with the a10 early-rejection path compiled in
+};
 
 #define TK(ND, TX, TY, TZ, NT, MB, MBD, MBR)                                                         \
     {ND, TX, TY, TZ, NT,                                                                             \
@@ -215,7 +247,8 @@ struct TileKey { int ndim, tx, ty, tz, nt; void* fn[NVARIANT + 1]; size_t smem[N
       (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBR, false, true>, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}, \
      {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
       tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT)},                                \
-     {true, false, true, true, false}}
+     {true, false, true, true, false},                                                               \
+     (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>}
 
 const TileKey kTiles[] = {
     TK(2, 32, 32, 1, 256, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3), TK(2, 64, 64, 1, 256, 3, 2, 3),
@@ -251,6 +284,9 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.rounds = S->rounds;
     P.round_mode = S->round_mode;
     P.do_hash = S->opt.event_hash;
+    P.early = S->opt.early_reject;
+    P.bulk = S->bulk;
+    for (int i = 0; i < 98; ++i) P.thm[i] = S->thm[i];
     P.tiles_x = sh.tiles_x;
     P.tiles_y = sh.tiles_y;
     P.tiles_z = sh.tiles_z;
@@ -547,6 +583,10 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     // P3 constants, P4 table, P5 threshold, packed-word layout
     S->inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
     flip_table(ndim, beta, J, h, rule, S->thr);
+    early_table(ndim, S->thr, opt.early_reject != 0, S->thm);
+    S->bulk = 1;   // one committed arrival per cell per fire step: longer in-thread chains
+                   // diverge within the warp (measured: bulk 4/32 are 1.8-2x slower on c5)
+    if (const char* e = getenv("ACA_BULK")) S->bulk = std::max(1, atoi(e));
     S->thr_init = (unsigned long long)std::floor(opt.init_q * 4294967296.0);
     uint64_t max_rank = 0;
     for (int a = 0; a < ndim; ++a) max_rank += (uint64_t)(dims[a] - 1);
@@ -611,7 +651,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         if (!sel) return bail(fail(ACA_EINVAL, "unsupported tile %dx%dx%d for ndim %d", tx, ty, tz, ndim));
         const int v = S->sync ? NVARIANT : opt.variant;
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
-        S->kern = sel->fn[v];
+        S->kern = (v == 0 && opt.early_reject) ? sel->fn_early : sel->fn[v];
         S->nthreads = sel->nt;
         S->smem = sel->smem[v];
         if (sel->persistent[v]) {   // persistent: as many CTAs as fit on the device at once
@@ -899,6 +939,13 @@ int aca_get_stats(aca_sim* S, aca_stats* o) {
     o->time_bits = S->TB;
     o->counter_bits = S->NB;
     o->rank_bits = S->RB;
+    const int ncls = 2 * (2 * S->ndim + 1);
+    double rate = 0;
+    for (int k = 0; k < ncls; ++k) {
+        o->class_hist[k] = S->h_stat->hist[k];
+        rate += (double)S->h_stat->hist[k] * ((double)S->thr[k] / 4294967296.0);
+    }
+    o->nfold_rate = rate * S->lambda;
     return ACA_OK;
 }
 

@@ -71,8 +71,11 @@ struct KParams {
     int rounds;                          // R_max
     int round_mode;                      // 0: CTA barrier per round; 1: no barrier, R rounds; 2: per-warp exit
     int do_hash;
+    int early;                           // a10: queue early-rejection candidates
+    int bulk;                            // max arrivals committed per cell per fire step (1 = one)
     int tiles_x, tiles_y, tiles_z;
     unsigned long long thr[14];          // P4 table
+    unsigned long long thm[98];          // a10 table, see commit_loop (2 (Z+1)^2 entries)
 };
 
 __device__ __forceinline__ int wrapi(int v, int n) {
@@ -358,10 +361,61 @@ struct TileStats {
     unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0;
 };
 
-template <int NDIM, int TX, int TY, int TZ, int NT, bool FULL>
+// Commit the pending arrivals of the cell in slot s for as long as that is exact (a10):
+//  * u = 0 (the cell is below every neighbour): an ordinary arrival, flip iff w0 < thr;
+//  * u > 0 neighbours may still change before the arrival: commit it only when the draw
+//    rejects the flip for EVERY value of those u spins (w0 >= thm = max threshold over the
+//    possible neighbour sums) — "rejected in every consistent world". The arrival then
+//    advances t and n and leaves s unchanged, which is what it does in the true trajectory
+//    whatever the u neighbours do; the other neighbours' spins are known (they cannot move
+//    before the arrival, fig:amcgen stale-read argument PAPER.md:833-871). This is the exact
+//    use of the BKL observation that most attempts are rejections.
+// thm[(s*(Z+1) + u)*(Z+1) + k] (k = known +1 neighbours) > 2^32 means "wait".
+template <int NDIM, int SX, int SXY>
+__device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned long long* VS, int s,
+                                            unsigned long long cid, const unsigned long long* thr,
+                                            const unsigned long long* thm, const unsigned long long* lr,
+                                            unsigned long long wlim, TileStats& st) {
+    constexpr int Z = 2 * NDIM;
+    const Geo& g = P.g;
+    unsigned long long w = VS[s];
+    for (int it = 0; it < P.bulk; ++it) {
+        if (w >= wlim) break;
+        const int off[6] = {-1, 1, -SX, SX, -SXY, SXY};
+        uint32_t u = 0, k = 0;
+#pragma unroll
+        for (int q = 0; q < Z; ++q) {
+            const unsigned long long nb = VS[s + off[q]];
+            const bool below = nb < w;
+            u += below;
+            k += below ? 0u : (uint32_t)(nb & 1ull);
+        }
+        const uint32_t sb = (uint32_t)(w & 1ull);
+        const unsigned long long tm = thm[(sb * (Z + 1) + u) * (Z + 1) + k];
+        if (tm > (1ull << 32)) break;                     // must wait for the u neighbours
+        const uint32_t n = w_count(w, g);
+        if (n == (uint32_t)((1ull << g.NB) - 1ull)) { atomicOr(&P.ctl->overflow, 1u); break; }
+        const u32x4 r = philox4x32_10(n, (uint32_t)cid, (uint32_t)(cid >> 32), 0u, P.key0, P.key1);
+        uint32_t flip = 0;
+        if (u == 0) flip = (unsigned long long)r.x < thr[k + (uint32_t)(Z + 1) * sb] ? 1u : 0u;
+        else if ((unsigned long long)r.x < tm) break;     // a flip is possible in some world: wait
+        const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, P.tie_bits);
+        if (P.do_hash) {
+            const unsigned long long t = w >> g.TSH;
+            st.hacc += mix64(t ^ rotl64(cid, 20) ^ rotl64((unsigned long long)n, 44) ^ (unsigned long long)(sb ^ flip));
+        }
+        w = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;
+        VS[s] = w;
+        st.flips += flip;
+        ++st.fired;
+    }
+}
+
+template <int NDIM, int TX, int TY, int TZ, int NT, bool FULL, bool EARLY>
 __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned long long* S, unsigned short* Q,
-                                                    const unsigned long long* thr, const unsigned long long* lr,
-                                                    int x0, int y0, int z0, unsigned long long wlim, TileStats& st) {
+                                                    const unsigned long long* thr, const unsigned long long* thm,
+                                                    const unsigned long long* lr, int x0, int y0, int z0,
+                                                    unsigned long long wlim, TileStats& st) {
     constexpr int SX = TX + 4, SY = TY + 2;
     constexpr int SXY = SX * SY;
     constexpr int NCELL = TX * TY * TZ;
@@ -413,6 +467,18 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                     e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
                     if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
                 }
+                if (EARLY && !e) {   // early-rejection candidate? (a10; decided in commit_loop)
+                    uint32_t u = 0, k = 0;
+                    const int off[6] = {-1, 1, -SX, SX, -SXY, SXY};
+#pragma unroll
+                    for (int q2 = 0; q2 < Z; ++q2) {
+                        const unsigned long long nb = VS[s + off[q2]];
+                        const bool below = nb < w;
+                        u += below;
+                        k += below ? 0u : (uint32_t)(nb & 1ull);
+                    }
+                    e = thm[((w & 1ull) * (Z + 1) + u) * (Z + 1) + k] <= (1ull << 32);
+                }
                 emask |= (uint32_t)e << j;
             }
             amask |= (uint32_t)act << j;
@@ -437,6 +503,10 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             const int o = q[i];
             const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
             const int s = slot(lx, ly, lz);
+            if (EARLY) {
+                commit_loop<NDIM, SX, SXY>(P, VS, s, cell_id(g, x0 + lx, y0 + ly, z0 + lz), thr, thm, lr, wlim, st);
+                continue;
+            }
             const unsigned long long w = VS[s];
             uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
                             (VH[2 * (s + SX)] & 1u);
@@ -617,7 +687,7 @@ __device__ __forceinline__ void halo_coords(int h, int& lx, int& ly, int& lz) {
     }
 }
 
-template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG>
+template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG, bool EARLY = false>
 __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
     constexpr int SXY = SX * SY;
@@ -636,7 +706,8 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     unsigned long long* Sb = smem;                                  // NB_ x NSLOTP words
     unsigned long long* lr = Sb + NB_ * NSLOTP;                     // 512
     unsigned long long* thr = lr + 512;                             // 16
-    unsigned long long* red = thr + 16;                             // NW
+    unsigned long long* thm = thr + 16;                             // 112 (a10 table)
+    unsigned long long* red = thm + 112;                            // NW
     unsigned long long* bar = red + NW;                             // 2
     unsigned short* Q = (unsigned short*)(bar + 2);                 // NCELL
 
@@ -644,6 +715,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
+    for (int i = tid; i < 112; i += NT) thm[i] = i < 98 ? P.thm[i] : ~0ull;
     if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
     __syncthreads();
 
@@ -718,8 +790,8 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
             }
         }
         if (!done_reg) {
-            rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true>(P, S, Q, thr, lr, x0, y0, z0, wlim, st)
-                          : tile_rounds<NDIM, TX, TY, TZ, NT, false>(P, S, Q, thr, lr, x0, y0, z0, wlim, st);
+            rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true, EARLY>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st)
+                          : tile_rounds<NDIM, TX, TY, TZ, NT, false, EARLY>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st);
         }
         rounds_max = rounds > rounds_max ? rounds : rounds_max;
         __syncthreads();
@@ -923,18 +995,25 @@ __global__ void unpack_kernel(const unsigned long long* __restrict__ words, int8
     }
 }
 
-// Statistics over the owned cells: B (bonds along +e_a), M, sum n, max n, t_min, t_max.
+// Statistics over the owned cells: B (bonds along +e_a), M, sum n, max n, t_min, t_max, and
+// the BKL class histogram |Gamma_k| over the (s, Sigma) classes, the
+// index of the P4 table (10 classes in 2-D, 14 in 3-D).
 struct StatAcc {
     long long bond, mag;
     unsigned long long arrivals, tmin, tmax, nmax;
+    unsigned long long hist[14];
 };
 
 template <int NT>
 __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out, unsigned long long n_local) {
     const Geo& g = P.g;
+    __shared__ unsigned int hs[14];
+    if (threadIdx.x < 14) hs[threadIdx.x] = 0;
+    __syncthreads();
     long long bond = 0, mag = 0;
     unsigned long long arr = 0, tmin = ~0ull, tmax = 0, nmax = 0;
     const unsigned long long plane = (unsigned long long)g.nx * g.ny;
+    const int Z = 2 * g.ndim;
     for (unsigned long long i = blockIdx.x * (unsigned long long)NT + threadIdx.x; i < n_local;
          i += (unsigned long long)gridDim.x * NT) {
         const unsigned long long w = P.words[i];
@@ -943,8 +1022,16 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         int y, z;
         if (g.ndim == 2) { y = (int)(i / g.nx); z = 0; }
         else { y = (int)((i / g.nx) % g.ny); z = (int)(i / plane); }
-        int plus = ((ld_word(P, x + 1, y, z) & 1ull) ? 1 : -1) + ((ld_word(P, x, y + 1, z) & 1ull) ? 1 : -1);
-        if (g.ndim == 3) plus += (ld_word(P, x, y, z + 1) & 1ull) ? 1 : -1;
+        const int ux = (int)(ld_word(P, x + 1, y, z) & 1ull), uy = (int)(ld_word(P, x, y + 1, z) & 1ull);
+        const int dx = (int)(ld_word(P, x - 1, y, z) & 1ull), dy = (int)(ld_word(P, x, y - 1, z) & 1ull);
+        int ones = ux + uy + dx + dy;
+        int plus = 2 * (ux + uy) - 2;
+        if (g.ndim == 3) {
+            const int uz = (int)(ld_word(P, x, y, z + 1) & 1ull), dz = (int)(ld_word(P, x, y, z - 1) & 1ull);
+            plus += 2 * uz - 1;
+            ones += uz + dz;
+        }
+        atomicAdd(&hs[ones + (Z + 1) * (s > 0 ? 1 : 0)], 1u);
         bond += s * plus;
         mag += s;
         const unsigned long long k = w_count(w, g);
@@ -974,6 +1061,8 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         atomicMax(&out->tmax, tmax);
         atomicMax(&out->nmax, nmax);
     }
+    __syncthreads();
+    if (threadIdx.x < 14 && hs[threadIdx.x]) atomicAdd(&out->hist[threadIdx.x], (unsigned long long)hs[threadIdx.x]);
 }
 
 }  // namespace aca

@@ -85,7 +85,7 @@ def test_full_size_sampled_parity(aca, oracle_mod, name, n_random, radii):
     dims, T = tuple(cfg["dims"]), cfg["T"]
     kw = dict(lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"])
     seed = workloads.PARITY_SEEDS[0]
-    g = aca.Sim(dims, seed=seed, init_q=cfg["init_q"], tile=cfg["tile"], **kw)
+    g = aca.Sim(dims, seed=seed, init_q=cfg["init_q"], tile=cfg["tile"], **cfg.get("opts", {}), **kw)
     g.run_until(T)
     st = g.stats()
 

@@ -117,6 +117,22 @@ def test_kernel_variants(aca, oracle_mod, variant):
         assert_same(g, o)
 
 
+@pytest.mark.parametrize("case", ["c5", "hb", "3d", "ties", "bulk"])
+def test_early_rejection_exact(aca, oracle_mod, case, monkeypatch):
+    """a10: committing arrivals that are rejected in every consistent world (and, with bulk,
+    several arrivals of one cell per step) leaves the trajectory bit-identical."""
+    if case == "bulk":
+        monkeypatch.setenv("ACA_BULK", "8")
+    kw = dict(c5=dict(dims=(256, 192), T=[20.0], beta=1.0, h=0.1, rule=1, init_q=0.05),
+              hb=dict(dims=(192, 128), T=[6.0], beta=0.6, h=0.05, rule=0),
+              bulk=dict(dims=(192, 128), T=[6.0], beta=0.4406868, rule=0),
+              ties=dict(dims=(128, 96), T=[8.0], beta=1.0, h=0.1, rule=1, init_q=0.05, tie_bits=30),
+              **{"3d": dict(dims=(48, 32, 24), T=[4.0], beta=0.5, h=0.1, rule=1, init_q=0.05)})[case]
+    dims, Ts = kw.pop("dims"), kw.pop("T")
+    g, o = run_pair(aca, oracle_mod, dims, Ts, seed=43, whole_lattice=-1, early_reject=1, **kw)
+    assert_same(g, o)
+
+
 @pytest.mark.parametrize("rounds", [1, 3, 8, 64])
 def test_rounds_per_launch_invariance(aca, oracle_mod, rounds):
     g, o = run_pair(aca, oracle_mod, (256, 192), [5.0], seed=5, rounds_per_launch=rounds, whole_lattice=-1)
@@ -240,3 +256,22 @@ def test_config4_scaled(aca, oracle_mod):
     """Config 4's physics (3-D heat-bath at beta 0.2216544) on 64^3 to T = 3, 2 shards."""
     g, o = run_pair(aca, oracle_mod, (64, 64, 64), [3.0], beta=0.2216544, seed=1, shards=2)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("dims", [(96, 80), (20, 16, 12)])
+def test_class_histogram(aca, oracle_mod, dims):
+    """BKL classes |Gamma_k| of the final configuration, recomputed with
+    numpy from the oracle's spins, and the n-fold-way rate sum_k |Gamma_k| p_k."""
+    g, o = run_pair(aca, oracle_mod, dims, [4.0], beta=1.0, h=0.1, rule=1, init_q=0.05, seed=47, whole_lattice=-1)
+    s = o.spins().astype(np.int64)
+    nd = len(dims)
+    up = (s > 0).astype(np.int64)
+    ones = sum(np.roll(up, sh, axis=ax) for ax in range(nd) for sh in (1, -1))
+    z = 2 * nd
+    idx = ones + (z + 1) * up
+    want = np.bincount(idx.ravel(), minlength=2 * (z + 1))
+    st = g.stats()
+    assert st["class_hist"][:2 * (z + 1)] == [int(v) for v in want]
+    thr = oracle_mod.flip_table(nd, 1.0, 1.0, 0.1, 1)
+    rate = sum(int(c) * t / 2 ** 32 for c, t in zip(want, thr))
+    assert abs(st["nfold_rate"] - rate) < 1e-6 * max(1.0, rate)
