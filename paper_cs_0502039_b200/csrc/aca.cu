@@ -131,6 +131,7 @@ struct aca_sim {
     std::vector<Shard> shards;
     int G = 1;                     // shards on this device
     int rank = 0, world = 1;
+    bool use_nccl = false;         // nccl_id given: halos travel by NCCL (world >= 1; world 1 = self)
     ncclComm_t comm = nullptr;
     int tile[3] = {64, 64, 1};
     int rounds = 8;
@@ -297,7 +298,7 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
 // exchange of the sharded-axis boundary rows/planes (virtual shards: D2D copies;
 // multi-process: NCCL send/recv to ring neighbours)
 int exchange(aca_sim* S) {
-    if (S->world > 1) {
+    if (S->use_nccl) {
         NcclApi& api = nccl();
         Shard& sh = S->shards[0];
         const int up = (S->rank + 1) % S->world, dn = (S->rank + S->world - 1) % S->world;
@@ -345,7 +346,7 @@ void drop_graph(aca_sim* S) {
 
 int build_graph(aca_sim* S) {
     if (S->graph) return ACA_OK;
-    if (S->world > 1) return ACA_OK;   // NCCL path: direct launches
+    if (S->use_nccl) return ACA_OK;   // NCCL path: direct launches
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
         cudaGetLastError();
@@ -538,7 +539,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (opt.tie_bits < 0 || opt.tie_bits > 40) return fail(ACA_EINVAL, "tie_bits must be in [0, 40]");
     if (opt.shards < 1) opt.shards = 1;
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(ACA_EINVAL, "bad rank/world");
-    if (opt.world > 1 && opt.shards != 1) return fail(ACA_EINVAL, "multi-process handles use shards = 1");
+    if ((opt.world > 1 || opt.nccl_id) && opt.shards != 1)
+        return fail(ACA_EINVAL, "NCCL (multi-process) handles use shards = 1");
     if (opt.world > 1 && !opt.nccl_id) return fail(ACA_EINVAL, "world > 1 needs nccl_id");
     if (opt.rounds_per_launch < 0 || opt.launches_per_check < 0) return fail(ACA_EINVAL, "negative counts");
     if (opt.variant < 0 || opt.variant >= NVARIANT) return fail(ACA_EINVAL, "variant must be in [0, %d)", NVARIANT);
@@ -574,6 +576,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (cudaSetDevice(S->device) != cudaSuccess) { delete S; return fail(ACA_ECUDA, "cudaSetDevice(%d)", S->device); }
     S->rank = opt.world > 1 ? opt.rank : 0;
     S->world = opt.world;
+    S->use_nccl = opt.nccl_id != nullptr;   // world 1 + nccl_id: the ring of one (self-exchange)
     S->G = opt.world > 1 ? 1 : opt.shards;
     S->sync = opt.sync_rounds != 0;
     S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 3;
@@ -626,7 +629,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     // kernel selection
     int dev_smem = 0;
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, S->device);
-    const bool single = (S->G == 1 && S->world == 1);
+    const bool single = (S->G == 1 && S->world == 1 && !S->use_nccl);
     S->whole = false;
     if (single && opt.whole_lattice >= 0) {
         const bool fits = whole_smem(N, S->sync) <= (size_t)dev_smem;
@@ -682,7 +685,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         g.nz = ndim == 3 ? (int)local : 1;
         g.y0 = ndim == 2 ? (int)(part * local) : 0;
         g.z0 = ndim == 3 ? (int)(part * local) : 0;
-        g.sharded = parts > 1;
+        g.sharded = parts > 1 || S->use_nccl;
         sh.n = (size_t)g.nx * g.ny * g.nz;
         sh.face = ndim == 2 ? (size_t)g.nx : (size_t)g.nx * g.ny;
         sh.tiles_x = (g.nx + S->tile[0] - 1) / S->tile[0];
@@ -700,7 +703,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (cudaMallocHost(&S->h_ctl, 2 * sizeof(Ctl) * S->shards.size()) != cudaSuccess)
         return bail(fail(ACA_ENOMEM, "pinned ctl"));
 
-    if (S->world > 1) {
+    if (S->use_nccl) {
         NcclApi& api = nccl();
         if (!api.ok) return bail(fail(ACA_ENCCL, "NCCL symbols not found in the process (load torch.distributed nccl first)"));
         ncclUniqueId_t id;
@@ -765,7 +768,7 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         *done = d;
         return ACA_OK;
     };
-    const bool pipelined = S->world == 1;
+    const bool pipelined = !S->use_nccl;
     rc = issue(0);
     if (rc) return rc;
     int outstanding = -1;      // pipelined: slot issued but not yet retired
@@ -779,7 +782,7 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         bool done = false;
         rc = retire(pipelined ? prev : 0, &done);
         if (rc) return rc;
-        if (S->world > 1) {
+        if (S->use_nccl) {
             // every rank must agree: all-reduce of the local "still active" flag
             NcclApi& api = nccl();
             unsigned long long* d = S->d_flag;

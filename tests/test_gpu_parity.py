@@ -252,6 +252,22 @@ def test_config2_scaled(aca, oracle_mod):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("dims", [(256, 192), (32, 24, 16)])
+def test_nccl_transport_ring_of_one(aca, oracle_mod, dims):
+    """The multi-process path on one GPU: a 1-rank NCCL communicator built from
+    aca_nccl_unique_id, halo rows/planes exchanged with grouped ncclSend/ncclRecv to the ring
+    neighbours (here the rank itself), termination all-reduced. Bit-exact vs the oracle."""
+    import torch  # noqa: F401  (loads libnccl into the process)
+    try:
+        uid = aca.aca_nccl_unique_id()
+    except aca.AcaError as e:
+        pytest.skip("NCCL not loadable: %s" % e)
+    beta = 0.2216544 if len(dims) == 3 else 0.4406868
+    tile = (16, 16, 16) if len(dims) == 3 else (64, 64)
+    g, o = run_pair(aca, oracle_mod, dims, [2.0, 4.0], beta=beta, seed=53, nccl_id=uid, tile=tile)
+    assert_same(g, o)
+
+
 def test_config4_scaled(aca, oracle_mod):
     """Config 4's physics (3-D heat-bath at beta 0.2216544) on 64^3 to T = 3, 2 shards."""
     g, o = run_pair(aca, oracle_mod, (64, 64, 64), [3.0], beta=0.2216544, seed=1, shards=2)
