@@ -72,6 +72,11 @@ typedef struct {
     int32_t early_reject;       /* 1: a cell may also commit arrivals that are rejected for
                                    every possible state of the neighbours it still waits for
                                    (exact; pays off at low temperature, config 5). 0 = off */
+    int32_t checkerboard;       /* persistent tile kernels: 0 (default) / 1 = each sweep is two
+                                   launches, the tiles of one checkerboard colour each (no two
+                                   tiles of a launch are adjacent, so every tile reads its
+                                   neighbours' state of the same sweep: Gauss-Seidel across
+                                   tiles); -1 = one launch over all tiles. Same results. */
 } aca_options;
 
 typedef struct {

@@ -40,7 +40,7 @@ class aca_options(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("event_hash", ctypes.c_int32),
                 ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32),
-                ("early_reject", ctypes.c_int32)]
+                ("early_reject", ctypes.c_int32), ("checkerboard", ctypes.c_int32)]
 
 
 class aca_stats(ctypes.Structure):

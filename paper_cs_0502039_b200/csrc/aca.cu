@@ -139,6 +139,7 @@ struct aca_sim {
     int K = 16;
     bool whole = false;
     bool sync = false;
+    bool phased = false;           // checkerboard sweeps (two launches per outer round)
     size_t smem = 0;
     int persistent_ctas = 0;       // > 0: grid size of the persistent tile kernel
     void* kern = nullptr;          // selected tile/whole kernel
@@ -227,34 +228,37 @@ constexpr size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
 }
 constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf) {
     return ((((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~(size_t)15) * nbuf + 512 + 16 + 112 +
-            nt / 32 + 2) * 8 + (size_t)tx * ty * tz * 2;
+            nt / 32 + 2) * 8 + ((size_t)tx * ty * tz + 64) * 2 + (size_t)tx * ty * tz / 32 * 8 + 16;
 }
 
 // Kernel variants (identical results; ablations): 0 = persistent TMA-staged compacted kernel
 // (default), 1 = uncompacted one-CTA-per-tile kernel, 2 = persistent, double-buffered TMA,
-// 3 = persistent TMA with register-resident synchronous rounds and CTA-wide firing.
+// 3 = persistent TMA with register-resident synchronous rounds and CTA-wide firing,
+// 4 = persistent TMA with work-list rounds (re-test only the cells whose neighbourhood changed).
 // Slot NVARIANT = two-barrier fig:s1c1pe rounds (sync_rounds = 1).
-constexpr int NVARIANT = 4;
+constexpr int NVARIANT = 5;
 struct TileKey {
     int ndim, tx, ty, tz, nt;
     void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1];
     void* fn_early;   // variant 0 with the a10 early-rejection path compiled in
 };
 
-#define TK(ND, TX, TY, TZ, NT, MB, MBD, MBR)                                                         \
+#define TK(ND, TX, TY, TZ, NT, MB, MBD, MBR, MBW)                                                         \
     {ND, TX, TY, TZ, NT,                                                                             \
      {(void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false>, (void*)tile_kernel<ND, TX, TY, TZ, NT, false>, \
       (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBD, true, false>,                                 \
-      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBR, false, true>, (void*)tile_kernel<ND, TX, TY, TZ, NT, true>}, \
+      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBR, false, true>,                                 \
+      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBW, false, false, false, true>,                   \
+      (void*)tile_kernel<ND, TX, TY, TZ, NT, true>},                                                 \
      {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
-      tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT)},                                \
-     {true, false, true, true, false},                                                               \
+      tma_smem(ND, TX, TY, TZ, NT, 1), tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT)}, \
+     {true, false, true, true, true, false},                                                         \
      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3), TK(2, 64, 64, 1, 256, 3, 2, 3),
-    TK(2, 128, 64, 1, 512, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8), TK(3, 16, 16, 16, 256, 2, 1, 2),
-    TK(3, 32, 16, 8, 256, 2, 1, 2), TK(3, 32, 32, 8, 512, 1, 1, 1),
+    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 64, 1, 256, 3, 2, 3, 4),
+    TK(2, 128, 64, 1, 512, 1, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8, 8), TK(3, 16, 16, 16, 256, 2, 1, 2, 2),
+    TK(3, 32, 16, 8, 256, 2, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
 };
 
 constexpr int WHOLE_NT = 1024;
@@ -280,6 +284,7 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.lr = S->d_lr;
     P.key0 = (uint32_t)(S->seed & 0xffffffffu);
     P.key1 = (uint32_t)(S->seed >> 32);
+    philox_round_keys(P.key0, P.key1, P.rk);
     P.inv_lambda = S->inv_lambda;
     P.tie_bits = S->opt.tie_bits;
     P.rounds = S->rounds;
@@ -291,6 +296,11 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.tiles_x = sh.tiles_x;
     P.tiles_y = sh.tiles_y;
     P.tiles_z = sh.tiles_z;
+    P.phase = -1;
+    {   // parity of the shard's first tile row in global tile coordinates (colouring only)
+        const int t0 = sh.g.ndim == 2 ? sh.g.y0 / S->tile[1] : sh.g.z0 / S->tile[2];
+        P.row_par0 = t0 & 1;
+    }
     for (int i = 0; i < 14; ++i) P.thr[i] = S->thr[i];
     return P;
 }
@@ -326,15 +336,23 @@ int exchange(aca_sim* S) {
     return ACA_OK;
 }
 
+// One outer round (sweep): every tile once. Checkerboard mode: two launches, colour 0 then
+// colour 1, with a halo exchange before each.
 int launch_round(aca_sim* S) {
-    int rc = exchange(S);
-    if (rc) return rc;
-    for (auto& sh : S->shards) {
-        KParams P = make_params(S, sh);
-        void* args[] = {&P};
-        const int ntiles = sh.tiles_x * sh.tiles_y * sh.tiles_z;
-        dim3 grid = S->whole ? dim3(1) : dim3(S->persistent_ctas > 0 ? std::min(ntiles, S->persistent_ctas) : ntiles);
-        CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->smem, S->stream));
+    for (int ph = S->phased ? 0 : -1; ph < (S->phased ? 2 : 0); ++ph) {
+        int rc = exchange(S);
+        if (rc) return rc;
+        for (auto& sh : S->shards) {
+            KParams P = make_params(S, sh);
+            P.phase = ph;
+            void* args[] = {&P};
+            const int ntiles = ph < 0 ? sh.tiles_x * sh.tiles_y * sh.tiles_z
+                                      : ((sh.tiles_x + 1) / 2) * sh.tiles_y * sh.tiles_z;
+            dim3 grid = S->whole ? dim3(1)
+                                 : dim3(S->persistent_ctas > 0 ? std::min(ntiles, S->persistent_ctas) : ntiles);
+            CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->smem, S->stream));
+        }
+        if (ph < 0) break;
     }
     return ACA_OK;
 }
@@ -665,6 +683,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, S->nthreads, S->smem) != cudaSuccess || occ < 1)
                 return bail(fail(ACA_ECUDA, "occupancy query failed"));
             S->persistent_ctas = nsm * occ;
+            S->phased = opt.checkerboard >= 0;
         }
     }
     if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
@@ -743,12 +762,12 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         CK(cudaEventRecord(S->evb[slot][0], S->stream));
         if (S->graph) {
             CK(cudaGraphLaunch(S->graph, S->stream));
-            S->kernel_launches += (uint64_t)S->graph_rounds * nsh;
+            S->kernel_launches += (uint64_t)S->graph_rounds * nsh * (S->phased ? 2 : 1);
         } else {
             for (int k = 0; k < S->K; ++k) {
                 int r = launch_round(S);
                 if (r) return r;
-                S->kernel_launches += nsh;
+                S->kernel_launches += nsh * (S->phased ? 2 : 1);
             }
         }
         CK(cudaEventRecord(S->evb[slot][1], S->stream));
@@ -1023,7 +1042,13 @@ int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
 namespace {
 __global__ void philox_test_kernel(uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out, uint32_t* ref) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const u32x4 r = philox4x32_10(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3], key[2 * i], key[2 * i + 1]);
+        u32x4 r = philox4x32_10(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3], key[2 * i], key[2 * i + 1]);
+        uint32_t rk[20];
+        philox_round_keys(key[2 * i], key[2 * i + 1], rk);
+        const u32x4 r2 = philox4x32_10_rk(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3], rk);
+        if (r2.x != r.x || r2.y != r.y || r2.z != r.z || r2.w != r.w) {   // both forms must agree
+            r.x = ~r.x; r.y = ~r.y; r.z = ~r.z; r.w = ~r.w;
+        }
         out[4 * i] = r.x; out[4 * i + 1] = r.y; out[4 * i + 2] = r.z; out[4 * i + 3] = r.w;
         uint4 c = make_uint4(ctr[4 * i], ctr[4 * i + 1], ctr[4 * i + 2], ctr[4 * i + 3]);
         uint2 k = make_uint2(key[2 * i], key[2 * i + 1]);

@@ -38,6 +38,7 @@ struct Ctl {                            // device control block, one per shard
     unsigned int ticket;                // last-CTA detection
     unsigned int rounds_max;            // max in-tile rounds over CTAs of this launch
     unsigned int overflow;              // an event counter reached its field maximum
+    unsigned long long active_carry;    // checkerboard: active cells of the phase-0 tiles
 };
 
 struct Geo {
@@ -66,6 +67,7 @@ struct KParams {
     Ctl* ctl;
     const unsigned long long* lr;        // device copy of ACA_NLOG_LR (512 entries)
     uint32_t key0, key1;
+    uint32_t rk[20];                     // Philox round keys of (key0, key1)
     unsigned long long inv_lambda;
     int tie_bits;
     int rounds;                          // R_max
@@ -74,6 +76,8 @@ struct KParams {
     int early;                           // a10: queue early-rejection candidates
     int bulk;                            // max arrivals committed per cell per fire step (1 = one)
     int tiles_x, tiles_y, tiles_z;
+    int phase;                           // -1: every tile; 0 / 1: tiles of that checkerboard colour
+    int row_par0;                        // parity of the shard's first tile row (global colouring)
     unsigned long long thr[14];          // P4 table
     unsigned long long thm[98];          // a10 table, see commit_loop (2 (Z+1)^2 entries)
 };
@@ -155,7 +159,7 @@ struct FireOut { unsigned long long wnew; uint32_t flip; unsigned long long h; b
 
 __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int z, unsigned long long c,
                                         const Geo& g, const unsigned long long* thr, const unsigned long long* lr,
-                                        uint32_t key0, uint32_t key1, unsigned long long inv_lambda, int tie_bits,
+                                        const uint32_t* rk, unsigned long long inv_lambda, int tie_bits,
                                         int do_hash, Ctl* ctl) {
     FireOut o;
     const uint32_t k = w_count(w, g);
@@ -166,7 +170,7 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
     }
     const uint32_t sb = (uint32_t)(w & 1ull);
     const uint32_t idx = ones + (uint32_t)(z + 1) * sb;          // (Sigma+z)/2 + (z+1)(s+1)/2
-    const u32x4 r = philox4x32_10(k, (uint32_t)c, (uint32_t)(c >> 32), 0u, key0, key1);
+    const u32x4 r = philox4x32_10_rk(k, (uint32_t)c, (uint32_t)(c >> 32), 0u, rk);
     const uint32_t flip = (unsigned long long)r.x < thr[idx] ? 1u : 0u;
     const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits);
     o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;   // t += d, n += 1, s ^= flip
@@ -181,9 +185,12 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
 }
 
 // Last-CTA bookkeeping of one launch: publish counters, decide termination.
+// Checkerboard phases: a sweep is two launches (phase 0, then phase 1); the phase-0 tiles do
+// not change during phase 1, so their active count carries over and the sweep ends (and
+// termination is decided) with phase 1.
 __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long active, unsigned long long fired,
                                               unsigned long long flips, unsigned long long tested,
-                                              unsigned long long hash, unsigned int rounds) {
+                                              unsigned long long hash, unsigned int rounds, int phase = -1) {
     atomicAdd(&ctl->active_accum, active);
     if (fired) atomicAdd(&ctl->fired, fired);
     if (flips) atomicAdd(&ctl->flips, flips);
@@ -194,12 +201,17 @@ __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long activ
     const unsigned int ticket = atomicAdd(&ctl->ticket, 1u);
     if (ticket == gridDim.x * gridDim.y * gridDim.z - 1) {
         __threadfence();
-        const unsigned long long act = atomicAdd(&ctl->active_accum, 0ull);
-        ctl->active_last = act;
-        ctl->done = (act == 0ull || ctl->overflow) ? 1u : 0u;
-        ctl->active_accum = 0ull;
-        ctl->launches += 1ull;
+        unsigned long long act = atomicAdd(&ctl->active_accum, 0ull);
         ctl->inner_rounds += atomicAdd(&ctl->rounds_max, 0u);
+        ctl->active_accum = 0ull;
+        if (phase == 0) {
+            ctl->active_carry = act;
+        } else {
+            if (phase == 1) act += ctl->active_carry;
+            ctl->active_last = act;
+            ctl->done = (act == 0ull || ctl->overflow) ? 1u : 0u;
+            ctl->launches += 1ull;
+        }
         ctl->rounds_max = 0u;
         __threadfence();
         ctl->ticket = 0u;
@@ -294,7 +306,7 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
                 ones += (uint32_t)(e & 1ull) + (uint32_t)(f & 1ull);
             }
             if (!ok) continue;
-            const FireOut o = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.key0, P.key1,
+            const FireOut o = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
                                    P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
             if (!o.ok) continue;
             hacc += o.h;
@@ -395,7 +407,7 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
         if (tm > (1ull << 32)) break;                     // must wait for the u neighbours
         const uint32_t n = w_count(w, g);
         if (n == (uint32_t)((1ull << g.NB) - 1ull)) { atomicOr(&P.ctl->overflow, 1u); break; }
-        const u32x4 r = philox4x32_10(n, (uint32_t)cid, (uint32_t)(cid >> 32), 0u, P.key0, P.key1);
+        const u32x4 r = philox4x32_10_rk(n, (uint32_t)cid, (uint32_t)(cid >> 32), 0u, P.rk);
         uint32_t flip = 0;
         if (u == 0) flip = (unsigned long long)r.x < thr[k + (uint32_t)(Z + 1) * sb] ? 1u : 0u;
         else if ((unsigned long long)r.x < tm) break;     // a flip is possible in some world: wait
@@ -511,7 +523,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
-            const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.key0, P.key1,
+            const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
                                    P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
             if (!f.ok) continue;
             VS[s] = f.wnew;
@@ -651,7 +663,7 @@ __device__ __forceinline__ unsigned int tile_rounds_reg(const KParams& P, unsign
             uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
-            const FireOut f = fire(wv, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.key0, P.key1,
+            const FireOut f = fire(wv, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
                                    P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
             if (!f.ok) continue;
             VS[s] = f.wnew;
@@ -667,6 +679,208 @@ __device__ __forceinline__ unsigned int tile_rounds_reg(const KParams& P, unsign
 #pragma unroll
             for (int c = 0; c < CPL; ++c)
                 if ((emask >> (j * CPL + c)) & 1u) w[j][c] = VS[s0 + j * SX + c];
+    }
+    return rounds;
+}
+
+// Exact local-minimum test of the cell in slot s against its observed neighbours (P6:
+// word order = (t, c) order). High halves first; the full words only on a tie.
+template <int NDIM, int SX, int SXY>
+__device__ __forceinline__ bool is_local_min(const volatile unsigned long long* VS, const volatile unsigned int* VH,
+                                             int s, unsigned long long w) {
+    const unsigned int oh = (unsigned int)(w >> 32);
+    unsigned int mn = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]), min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
+    if (NDIM == 3) mn = min(mn, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
+    if (oh != mn) return oh < mn;
+    bool e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
+    if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+    return e;
+}
+
+// Work-list rounds (full tiles). Round 0 tests every cell of the tile against one snapshot
+// and queues the local minima; every later round fires the queued cells and re-tests ONLY
+// the cells whose neighbourhood just changed — the fired cell and its in-tile neighbours —
+// queueing the new local minima for the next round (a claim bitmap keeps each cell once per
+// queue). A cell can become eligible only when it or one of its neighbours fires (words only
+// grow; the halo is frozen for the launch), so this finds what a full re-scan would find, at
+// about Z + 1 tests per arrival instead of one test per cell per round.
+// Exactness: every queued cell was a local minimum when it was queued and stays one until it
+// fires (its neighbours, being larger, cannot fire first), so a queue is a set of pairwise
+// non-adjacent eligible cells — the set of one synchronous round of fig:s1c1pe
+// — and each fires against a neighbourhood frozen until its own write
+// (stale-read argument of fig:amcgen). The loop runs until the tile's
+// frontier reaches the halo's time bound (empty queue) or R_max rounds.
+template <int NDIM, int TX, int TY, int TZ, int NT>
+__device__ __forceinline__ unsigned int tile_rounds_wl(const KParams& P, unsigned long long* S, unsigned short* Q,
+                                                       unsigned int* claim, unsigned int* qcnt,
+                                                       const unsigned long long* thr, const unsigned long long* lr,
+                                                       int x0, int y0, int z0, unsigned long long wlim, TileStats& st) {
+    constexpr int SX = TX + 4, SY = TY + 2, SXY = SX * SY;
+    constexpr int NCELL = TX * TY * TZ;
+    constexpr int NW = NT / 32;
+    constexpr int CPW = NCELL / NW;
+    constexpr int JPL = CPW / 32;
+    constexpr int Z = 2 * NDIM;
+    constexpr int QH = NCELL / 2 + 32;          // capacity of one queue (an independent set)
+    constexpr int NCW = NCELL / 32;             // words of one claim bitmap
+    static_assert(CPW % 32 == 0, "whole warps of cells");
+    const Geo& g = P.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    volatile unsigned long long* VS = S;
+    const volatile unsigned int* VH = (const volatile unsigned int*)S;
+    volatile unsigned int* VC = qcnt;
+    auto slot_of = [](int o) {   // tile cell index -> smem slot
+        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+        return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2;
+    };
+
+    for (int i = tid; i < 2 * NCW; i += NT) claim[i] = 0u;
+    if (tid < 4) qcnt[tid] = 0u;
+    __syncthreads();
+
+    // ---- round 0: full scan against one snapshot (no cell fires before the barrier)
+    {
+        const int o0 = warp * CPW + lane;
+        uint32_t emask = 0, amask = 0;
+#pragma unroll
+        for (int j = 0; j < JPL; ++j) {
+            const int o = o0 + 32 * j;   // rows of this warp, lane-contiguous columns
+            const int s = slot_of(o);
+            const unsigned long long w = VS[s];
+            const bool act = w < wlim;
+            if (act && is_local_min<NDIM, SX, SXY>(VS, VH, s, w)) emask |= 1u << j;
+            amask |= (uint32_t)act << j;
+        }
+        st.tested += __popc(amask);
+        const int mine = __popc(emask);
+        int incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        unsigned int base = 0;
+        if (lane == 31 && incl) base = atomicAdd(&qcnt[0], (unsigned int)incl);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        int pos = (int)base + incl - mine;
+        while (emask) {
+            const int j = __ffs(emask) - 1;
+            emask &= emask - 1u;
+            Q[pos++] = (unsigned short)(o0 + 32 * j);
+        }
+    }
+    __syncthreads();
+
+    // ---- fire rounds
+    const int doff[6] = {-1, 1, -TX, TX, -TX * TY, TX * TY};
+    const int soff[6] = {-1, 1, -SX, SX, -SXY, SXY};
+    unsigned int rounds = 1;
+    for (int r = 0; r < P.rounds; ++r) {
+        const int n = (int)VC[r % 3];
+        if (n == 0) break;
+        const int cur = r & 1;
+        if (tid == 0) VC[(r + 2) % 3] = 0u;                         // counter of the round after next
+        for (int i = tid; i < NCW; i += NT) claim[cur * NCW + i] = 0u;   // bitmap of this round's queue
+        const unsigned short* qin = Q + cur * QH;
+        unsigned short* qout = Q + (cur ^ 1) * QH;
+        unsigned int* cl = claim + (cur ^ 1) * NCW;
+        unsigned int* cnt_out = qcnt + (r + 1) % 3;
+        for (int b0 = warp * 32; b0 < n; b0 += NT) {
+            const int i = b0 + lane;
+            uint32_t pm = 0;
+            int ofired = 0;
+            if (i < n) {
+                const int o = qin[i];
+                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                const int s = slot_of(o);
+                const unsigned long long w = VS[s];
+                uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
+                                (VH[2 * (s + SX)] & 1u);
+                if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
+                const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
+                                       P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+                if (f.ok) {
+                    VS[s] = f.wnew;
+                    st.hacc += f.h;
+                    st.flips += f.flip;
+                    ++st.fired;
+                    // Re-test the cell itself and its in-tile neighbours (halo cells are frozen).
+                    // All loads first (independent, in flight together), then the compares;
+                    // the fired cell's new word is one of every neighbour's neighbours.
+                    const unsigned long long wn = f.wnew;
+                    const unsigned int hn = (unsigned int)(wn >> 32);
+                    unsigned long long wq[Z];
+                    bool inq[Z];
+#pragma unroll
+                    for (int q = 0; q < Z; ++q) {
+                        const int a = q >> 1;
+                        const int coord = a == 0 ? lx : (a == 1 ? ly : lz);
+                        const int ext = a == 0 ? TX : (a == 1 ? TY : TZ);
+                        inq[q] = (q & 1) ? coord != ext - 1 : coord != 0;
+                        wq[q] = VS[s + soff[q]];
+                    }
+                    unsigned int mq[Z];   // min over the high halves of x_q's other neighbours
+#pragma unroll
+                    for (int q = 0; q < Z; ++q) {
+                        unsigned int m = hn;
+                        if (inq[q]) {
+#pragma unroll
+                            for (int p = 0; p < Z; ++p)
+                                if (p != (q ^ 1)) m = min(m, VH[2 * (s + soff[q] + soff[p]) + 1]);
+                        }
+                        mq[q] = m;
+                    }
+                    uint32_t em = 0, ntest = 0;
+                    {   // the fired cell itself
+                        unsigned int m = (unsigned int)(wq[0] >> 32);
+#pragma unroll
+                        for (int q = 1; q < Z; ++q) m = min(m, (unsigned int)(wq[q] >> 32));
+                        if (wn < wlim) {
+                            ++ntest;
+                            const bool e = hn != m ? hn < m : is_local_min<NDIM, SX, SXY>(VS, VH, s, wn);
+                            em |= (uint32_t)e;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < Z; ++q) {
+                        if (!inq[q] || wq[q] >= wlim) continue;
+                        ++ntest;
+                        const unsigned int h = (unsigned int)(wq[q] >> 32);
+                        const bool e = h != mq[q] ? h < mq[q] : is_local_min<NDIM, SX, SXY>(VS, VH, s + soff[q], wq[q]);
+                        em |= (uint32_t)e << (q + 1);
+                    }
+                    st.tested += ntest;
+                    if (em) {   // rare: about one new local minimum per arrival
+#pragma unroll
+                        for (int q = 0; q <= Z; ++q) {
+                            if (!((em >> q) & 1u)) continue;
+                            const int oc = q == 0 ? o : o + doff[q - 1];
+                            const unsigned int bit = 1u << (oc & 31);
+                            if (atomicOr(&cl[oc >> 5], bit) & bit) continue;   // already queued
+                            pm |= 1u << q;
+                        }
+                    }
+                    ofired = o;
+                }
+            }
+            // warp-aggregated push into the next queue
+            const int mine = __popc(pm);
+            int incl = mine;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += v;
+            }
+            unsigned int base = 0;
+            if (lane == 31 && incl) base = atomicAdd(cnt_out, (unsigned int)incl);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            int pos = (int)base + incl - mine;
+#pragma unroll
+            for (int q = 0; q <= Z; ++q)
+                if ((pm >> q) & 1u) qout[pos++] = (unsigned short)(q == 0 ? ofired : ofired + doff[q - 1]);
+        }
+        ++rounds;
+        __syncthreads();
     }
     return rounds;
 }
@@ -687,7 +901,7 @@ __device__ __forceinline__ void halo_coords(int h, int& lx, int& ly, int& lz) {
     }
 }
 
-template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG, bool EARLY = false>
+template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG, bool EARLY = false, bool WL = false>
 __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
     constexpr int SXY = SX * SY;
@@ -709,7 +923,9 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     unsigned long long* thm = thr + 16;                             // 112 (a10 table)
     unsigned long long* red = thm + 112;                            // NW
     unsigned long long* bar = red + NW;                             // 2
-    unsigned short* Q = (unsigned short*)(bar + 2);                 // NCELL
+    unsigned short* Q = (unsigned short*)(bar + 2);                 // NCELL + 64 (WL: two queues)
+    unsigned int* claim = (unsigned int*)(Q + NCELL + 64);          // WL: 2 x NCELL/32 claim bits
+    unsigned int* qcnt = claim + 2 * (NCELL / 32);                  // WL: 4 queue counters
 
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -721,25 +937,35 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
 
     auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2; };
     const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
-    const int ntiles = P.tiles_x * P.tiles_y * P.tiles_z;
+    // work items: every tile (phase < 0), or the tiles of one checkerboard colour: item k is
+    // column pair j = k % hx of tile row k / hx, tx = 2j + ((row parity + phase) & 1)
+    const int hx = (P.tiles_x + 1) >> 1;
+    const int ntiles = P.phase < 0 ? P.tiles_x * P.tiles_y * P.tiles_z : hx * P.tiles_y * P.tiles_z;
     const bool vec_ok = (g.nx % 2) == 0;
-    const bool reverse = (*(volatile unsigned long long*)&P.ctl->launches) & 1ull;
+    const bool reverse = P.phase < 0 && ((*(volatile unsigned long long*)&P.ctl->launches) & 1ull);
     TileStats st;
     unsigned long long active = 0;
     unsigned int rounds_max = 0;
     uint32_t ph = 0;   // bit b: parity of bar[b]
 
-    auto origin = [&](int it, int& x0, int& y0, int& z0, bool& fast, bool& full) {
-        const int tile = reverse ? ntiles - 1 - it : it;
-        const int tx = tile % P.tiles_x, ty = (tile / P.tiles_x) % P.tiles_y, tz = tile / (P.tiles_x * P.tiles_y);
+    auto origin = [&](int it, int& x0, int& y0, int& z0, bool& fast, bool& full) -> bool {
+        int tx, ty, tz;
+        if (P.phase < 0) {
+            const int tile = reverse ? ntiles - 1 - it : it;
+            tx = tile % P.tiles_x; ty = (tile / P.tiles_x) % P.tiles_y; tz = tile / (P.tiles_x * P.tiles_y);
+        } else {
+            const int row = it / hx;
+            ty = row % P.tiles_y; tz = row / P.tiles_y;
+            tx = 2 * (it % hx) + ((ty + tz + P.row_par0 + P.phase) & 1);
+        }
         x0 = tx * TX; y0 = ty * TY; z0 = tz * TZ;
         full = x0 + TX <= g.nx && y0 + TY <= g.ny && (NDIM == 2 || z0 + TZ <= g.nz);
         fast = full && vec_ok;
+        return tx < P.tiles_x;
     };
     auto issue = [&](int it, int b) {   // warp 0: TMA of the tile's own rows into buffer b
         int x0, y0, z0; bool fast, full;
-        origin(it, x0, y0, z0, fast, full);
-        if (!fast) return;
+        if (!origin(it, x0, y0, z0, fast, full) || !fast) return;
         if (lane == 0) mbar_arrive_expect_tx(&bar[b], (uint32_t)NROWS * TX * 8u);
         __syncwarp();
         fence_proxy_async();
@@ -758,11 +984,12 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
         const int b = DB ? (k & 1) : 0;
         unsigned long long* S = Sb + b * NSLOTP;
         int x0, y0, z0; bool fast, full;
-        origin(it, x0, y0, z0, fast, full);
+        const bool valid = origin(it, x0, y0, z0, fast, full);
         if (warp == 0) {
             if (DB) { if (it + (int)gridDim.x < ntiles) issue(it + gridDim.x, b ^ 1); }
             else issue(it, 0);
         }
+        if (!valid) continue;   // odd tiles_x: the last column pair has one tile
         if (fast) {
             for (int h = tid; h < NHALO; h += NT) {
                 int lx, ly, lz;
@@ -783,7 +1010,12 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
 
         unsigned int rounds = 0;
         bool done_reg = false;
-        if constexpr (REG && RegMap<NDIM, TX, TY, TZ, NT>::ok) {
+        if constexpr (WL) {
+            if (full) {
+                rounds = tile_rounds_wl<NDIM, TX, TY, TZ, NT>(P, S, Q, claim, qcnt, thr, lr, x0, y0, z0, wlim, st);
+                done_reg = true;
+            }
+        } else if constexpr (REG && RegMap<NDIM, TX, TY, TZ, NT>::ok) {
             if (full) {
                 rounds = tile_rounds_reg<NDIM, TX, TY, TZ, NT>(P, S, Q, (unsigned int*)red, thr, lr, x0, y0, z0, wlim, st);
                 done_reg = true;
@@ -825,7 +1057,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     const unsigned long long s_flp = block_sum<NT>(st.flips, red);
     const unsigned long long s_tst = block_sum<NT>(st.tested, red);
     const unsigned long long s_hsh = block_sum<NT>(st.hacc, red);
-    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max);
+    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase);
 }
 
 // ------------------------------------------------------------ whole-lattice kernel
@@ -879,7 +1111,7 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
                 ones += (uint32_t)(e & 1ull) + (uint32_t)(f & 1ull);
             }
             if (!ok) continue;
-            const FireOut o = fire(w, ones, Z, (unsigned long long)i, g, thr, lr, P.key0, P.key1, P.inv_lambda,
+            const FireOut o = fire(w, ones, Z, (unsigned long long)i, g, thr, lr, P.rk, P.inv_lambda,
                                    P.tie_bits, P.do_hash, P.ctl);
             if (!o.ok) continue;
             hacc += o.h;

@@ -27,27 +27,62 @@ __device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_
     return {c0, c1, c2, c3};
 }
 
+// Same function with the ten round keys precomputed (rk[2r], rk[2r+1] = key schedule of round
+// r, see philox_round_keys). With rk in the kernel-parameter (constant) bank the key xor folds
+// into the LOP3 of each round: 2 IMAD.WIDE + 2 LOP3 per round.
+__device__ __forceinline__ u32x4 philox4x32_10_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
+                                                   const uint32_t* rk) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ rk[2 * r];
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ rk[2 * r + 1];
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+    }
+    return {c0, c1, c2, c3};
+}
+
+__host__ __device__ inline void philox_round_keys(uint32_t k0, uint32_t k1, uint32_t* rk) {
+    for (int r = 0; r < 10; ++r) {
+        rk[2 * r] = k0;
+        rk[2 * r + 1] = k1;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
 // ---------------------------------------------------------------- P3 NLOG-2
 // -ln(u) in Q32 for u = (X|1)/2^64, integer-only. `lr` points at the interleaved
-// {L[i], R[i]} table (shared memory copy of ACA_NLOG_LR).
+// {L[i], R[i]} table (shared memory copy of ACA_NLOG_LR). Every intermediate of the
+// definition in docs/PRIMITIVES.md P3 fits 32 bits except L + A, so the arithmetic is done
+// on 32-bit halves (IMAD / IMAD.HI) — the same integers as the 64-bit statement of P3:
+//   V = (g R[i]) >> 32 = umulhi(g, R[i] mod 2^32) + [i = 0] g     (R[0] = 2^32, R[i>0] < 2^32)
+//   V2 = V^2 = (v2h, v2l);  B = ceil(V2 / 2^33);  C = floor((umulhi(v2h, V) >> 8) / 3)
+//   Wq = ceil(V2 / 2^32) < 2^32;  D = ceil(Wq^2 / 2^50)
+//   lnf = L[i] + (V << 8) + C - (B + D)   (B + D < 2^32; the sum is exact modulo 2^64)
 __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long long* __restrict__ lr,
                                              uint64_t ln2_q48) {
     const uint64_t x = X | 1ull;
     const int z = __clzll((long long)x);
     const uint64_t m = (x << z) << 1;
-    const uint32_t i = (uint32_t)(m >> 56);
-    const uint64_t g = (m >> 24) & 0xffffffffull;
-    const uint64_t Li = lr[2 * i], Ri = lr[2 * i + 1];
-    const uint64_t V = (g * Ri) >> 32;                   // < 2^32
-    const uint64_t V2 = V * V;
-    const uint64_t A = V << 8;
-    const uint64_t B = (V2 >> 33) + ((V2 & ((1ull << 33) - 1)) != 0ull);
-    const uint32_t C = (uint32_t)(((V2 >> 32) * V) >> 40) / 3u;   // floor(floor(./2^40)/3)
-    const uint64_t Wq = (V2 >> 32) + ((V2 & 0xffffffffull) != 0ull);
-    const uint64_t W2 = Wq * Wq;
-    const uint64_t D = (W2 >> 50) + ((W2 & ((1ull << 50) - 1)) != 0ull);
-    const uint64_t lnf = Li + A - B + C - D;
-    const uint64_t S = (uint64_t)(z + 1) * ln2_q48 - lnf;
+    const uint32_t mh = (uint32_t)(m >> 32), ml = (uint32_t)m;
+    const uint32_t i = mh >> 24;
+    const uint32_t g = __funnelshift_r(ml, mh, 24);          // bits 24..55 of m
+    const uint64_t Li = lr[2 * i];
+    const uint32_t Rl = (uint32_t)lr[2 * i + 1];
+    const uint32_t V = i == 0u ? g : __umulhi(g, Rl);
+    const uint32_t v2l = V * V, v2h = __umulhi(V, V);
+    const uint32_t B = (v2h >> 1) + ((v2l | (v2h & 1u)) != 0u ? 1u : 0u);
+    const uint32_t C = (__umulhi(v2h, V) >> 8) / 3u;
+    const uint32_t Wq = v2h + (v2l != 0u ? 1u : 0u);
+    const uint32_t w2l = Wq * Wq, w2h = __umulhi(Wq, Wq);
+    const uint32_t D = (w2h >> 18) + ((w2l | (w2h & 0x3ffffu)) != 0u ? 1u : 0u);
+    const uint64_t lnf = Li + ((uint64_t)V << 8) + (uint64_t)C - (uint64_t)(B + D);
+    const uint64_t S = (uint64_t)(uint32_t)(z + 1) * ln2_q48 - lnf;
     return (S + (1ull << 15)) >> 16;
 }
 

@@ -105,11 +105,11 @@ def test_tiled_2d_ragged(aca, oracle_mod, tile):
     assert_same(g, o)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_kernel_variants(aca, oracle_mod, variant):
     """Persistent TMA kernel (0), uncompacted per-tile kernel (1), double-buffered TMA
-    kernel (2), register-resident synchronous rounds (3): identical trajectories, 2-D (full +
-    ragged tiles, odd width) and 3-D."""
+    kernel (2), register-resident synchronous rounds (3), work-list rounds (4): identical
+    trajectories, 2-D (full + ragged tiles, odd width) and 3-D."""
     for dims, tile, T in (((256, 192), (64, 64), 5.0), ((200, 150), (64, 32), 4.0), ((130, 70), (32, 32), 4.0),
                           ((64, 48, 40), (32, 16, 8), 3.0), ((40, 24, 20), (16, 16, 16), 3.0)):
         beta = 0.2216544 if len(dims) == 3 else 0.4406868
