@@ -450,8 +450,59 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         s0 = slot(lane, row0 % TY, row0 / TY);
     }
     unsigned int rounds = 0;
+    auto cell_slot = [&](int j) {
+        if (FASTMAP) return s0 + (j / LPR) * SX + 32 * (j % LPR);
+        const int o = wbase + lane + 32 * j;
+        return slot(o % TX, (o / TX) % TY, o / (TX * TY));
+    };
+    auto cell_valid = [&](int j) {
+        if (FULL) return true;
+        const int o = wbase + lane + 32 * j;
+        const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+        return x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz);
+    };
     for (int r = 0; r < P.rounds; ++r) {
         uint32_t emask = 0, amask = 0;
+        if constexpr (!EARLY) {
+            // Branch-free test in batches of TB cells: every load of the batch is issued before
+            // any compare (the lane's cells are independent), the 32-bit high halves decide
+            // unless they tie; tied cells are settled on the full words in a rare second pass.
+            constexpr int TB = 4;
+            static_assert(JPL % TB == 0, "cells per lane must be a multiple of the test batch");
+            uint32_t tmask = 0;
+#pragma unroll
+            for (int j0 = 0; j0 < JPL; j0 += TB) {
+                unsigned long long wv[TB];
+                unsigned int mv[TB];
+#pragma unroll
+                for (int k = 0; k < TB; ++k) wv[k] = VS[cell_slot(j0 + k)];
+#pragma unroll
+                for (int k = 0; k < TB; ++k) {
+                    const int s = cell_slot(j0 + k);
+                    unsigned int m = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]),
+                                         min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
+                    if (NDIM == 3) m = min(m, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
+                    mv[k] = m;
+                }
+#pragma unroll
+                for (int k = 0; k < TB; ++k) {
+                    const bool act = cell_valid(j0 + k) && wv[k] < wlim;
+                    const unsigned int oh = (unsigned int)(wv[k] >> 32);
+                    emask |= (uint32_t)(act && oh < mv[k]) << (j0 + k);
+                    tmask |= (uint32_t)(act && oh == mv[k]) << (j0 + k);
+                    amask |= (uint32_t)act << (j0 + k);
+                }
+            }
+            while (tmask) {   // tie in the high halves: decide on the full words
+                const int j = __ffs(tmask) - 1;
+                tmask &= tmask - 1u;
+                const int s = cell_slot(j);
+                const unsigned long long w = VS[s];
+                bool e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
+                if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+                emask |= (uint32_t)e << j;
+            }
+        } else
 #pragma unroll
         for (int j = 0; j < JPL; ++j) {
             int s;
@@ -531,6 +582,10 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             st.flips += f.flip;
             ++st.fired;
         }
+        // Every queued cell's new word must be visible to the whole warp before its next test:
+        // a queued cell is still a local minimum until its word is written, and lanes of a warp
+        // are not guaranteed to reconverge after the divergent fire loop.
+        __syncwarp();
         ++rounds;
         if (P.round_mode == 0) {
             if (__syncthreads_count(cnt > 0) == 0) break;   // CTA-wide stall detection
