@@ -77,6 +77,11 @@ typedef struct {
                                    tiles of a launch are adjacent, so every tile reads its
                                    neighbours' state of the same sweep: Gauss-Seidel across
                                    tiles); -1 = one launch over all tiles. Same results. */
+    int32_t law;                /* asynchrony law of the increments (docs/PRIMITIVES.md P3L):
+                                   0 (default) Poisson, next_t = t - ln(r)/lambda (Eq. newt1i,
+                                   PAPER.md:485-488); 1 uniform, next_t - t = r/lambda
+                                   (PAPER.md:1389-1393); 2 next_t - t = r^(1/8)/lambda
+                                   (PAPER.md:1425-1430). r from the arrival's Philox draw. */
 } aca_options;
 
 typedef struct {
@@ -159,6 +164,10 @@ int aca_selftest_philox(uint64_t n, const uint32_t* ctr, const uint32_t* key, ui
 /* P3: q[i] = NLOG-2(X[i]); delta[i] = Delta(X[i]) for inv_lambda, tie_bits. */
 int aca_selftest_nlog(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* delta,
                       uint64_t inv_lambda, int tie_bits);
+/* P3L: u[i] = unscaled increment of `law` for (w1, w2) = (X[i] >> 32, X[i] & 0xffffffff);
+ * delta[i] = the increment after 1/lambda, the clamp and P3b. ACA_EINVAL for law outside 0..2. */
+int aca_selftest_law(uint64_t n, const uint64_t* X, int law, uint64_t inv_lambda, int tie_bits, uint64_t* u,
+                     uint64_t* delta);
 
 #ifdef __cplusplus
 }

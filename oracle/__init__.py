@@ -57,6 +57,10 @@ def lib():
         L.oracle_nlog_q32.restype = ctypes.c_uint64
         L.oracle_delta.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int]
         L.oracle_delta.restype = ctypes.c_uint64
+        L.oracle_delta_law.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int, ctypes.c_int]
+        L.oracle_delta_law.restype = ctypes.c_uint64
+        L.oracle_law_q32.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_int]
+        L.oracle_law_q32.restype = ctypes.c_uint64
         L.oracle_inv_lambda.argtypes = [ctypes.c_double]
         L.oracle_inv_lambda.restype = ctypes.c_uint64
         L.oracle_flip_table.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double,
@@ -67,6 +71,8 @@ def lib():
                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                     ctypes.c_uint64, ctypes.c_double, ctypes.c_int]
         L.oracle_create.restype = ctypes.c_void_p
+        L.oracle_create_law.argtypes = L.oracle_create.argtypes + [ctypes.c_int]
+        L.oracle_create_law.restype = ctypes.c_void_p
         L.oracle_destroy.argtypes = [ctypes.c_void_p]
         L.oracle_run_until_q32.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
         L.oracle_run_until_random_order.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]
@@ -92,12 +98,16 @@ def lib():
         L.oracle_cell_time_counter.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                                ctypes.c_uint64, ctypes.c_int,
                                                ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)]
+        L.oracle_cell_time_counter_law.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                                   ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                                   ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint32)]
         L.oracle_window_cell.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_double,
                                          ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                          ctypes.c_uint64, ctypes.c_double, ctypes.c_int, ctypes.c_uint64,
                                          ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, ctypes.c_int,
                                          ctypes.POINTER(ctypes.c_int8), ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
+        L.oracle_window_cell_law.argtypes = L.oracle_window_cell.argtypes + [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -126,17 +136,24 @@ def nlog_batch(X):
     return q
 
 
-def cell_time_counter(seed, c, T, lam=1.0, tie_bits=0):
+POISSON, UNIFORM, ROOT8 = 0, 1, 2   # P3L asynchrony laws
+
+
+def cell_time_counter(seed, c, T, lam=1.0, tie_bits=0, law=POISSON):
     """(t, n) of cell c after run_until(T) from its own stream (state independence)."""
     t = ctypes.c_uint64()
     n = ctypes.c_uint32()
-    lib().oracle_cell_time_counter(seed, c, to_q32(T), lib().oracle_inv_lambda(lam), tie_bits,
-                                   ctypes.byref(t), ctypes.byref(n))
+    lib().oracle_cell_time_counter_law(seed, c, to_q32(T), lib().oracle_inv_lambda(lam), tie_bits, law,
+                                       ctypes.byref(t), ctypes.byref(n))
     return t.value, n.value
 
 
-def delta(w1, w2, lam=1.0, tie_bits=0):
-    return lib().oracle_delta(w1, w2, lib().oracle_inv_lambda(lam), tie_bits)
+def delta(w1, w2, lam=1.0, tie_bits=0, law=POISSON):
+    return lib().oracle_delta_law(w1, w2, lib().oracle_inv_lambda(lam), tie_bits, law)
+
+
+def law_q32(w1, w2, law):
+    return lib().oracle_law_q32(w1, w2, law)
 
 
 def flip_table(ndim, beta, J=1.0, h=0.0, rule=HEATBATH):
@@ -158,11 +175,11 @@ class OracleSim:
     """One serial simulation. Methods mirror the C-ABI names of the product path."""
 
     def __init__(self, dims, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1,
-                 init_q=0.5, tie_bits=0):
+                 init_q=0.5, tie_bits=0, law=POISSON):
         self.dims = tuple(int(d) for d in dims)
         self.ndim = len(self.dims)
-        self._p = lib().oracle_create(self.ndim, _dims(self.dims), lam, beta, J, h, rule,
-                                      seed, init_q, tie_bits)
+        self._p = lib().oracle_create_law(self.ndim, _dims(self.dims), lam, beta, J, h, rule,
+                                          seed, init_q, tie_bits, law)
         if not self._p:
             raise ValueError("oracle_create rejected the arguments")
         self.N = int(np.prod(self.dims))
@@ -238,12 +255,12 @@ def time_weighted_hist(dims, beta, J=1.0, h=0.0, rule=HEATBATH, seed=1, T0=50.0,
 
 
 def window_cell(dims, center, T, radius, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1, init_q=0.5,
-                tie_bits=0, refine=True):
+                tie_bits=0, refine=True, law=POISSON):
     """Exact (s, t, n, exact) of the cell at `center` (x, y[, z]) after run_until(T), from a
     box of the given radius (light-cone oracle; see aca_oracle.c). exact=False: enlarge."""
     so, to, no, ex = ctypes.c_int8(), ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_int()
-    rc = lib().oracle_window_cell(len(dims), _dims(dims), lam, beta, J, h, rule, seed, init_q, tie_bits,
-                                  to_q32(T), _dims(center), radius, 1 if refine else 0, ctypes.byref(so),
-                                  ctypes.byref(to), ctypes.byref(no), ctypes.byref(ex))
+    rc = lib().oracle_window_cell_law(len(dims), _dims(dims), lam, beta, J, h, rule, seed, init_q, tie_bits,
+                                      to_q32(T), _dims(center), radius, 1 if refine else 0, ctypes.byref(so),
+                                      ctypes.byref(to), ctypes.byref(no), ctypes.byref(ex), law)
     assert rc == 0
     return so.value, to.value, no.value, bool(ex.value)

@@ -53,10 +53,23 @@ uint64_t oracle_nlog_q32(uint64_t X) {
 
 uint64_t oracle_inv_lambda(double lambda) { return (uint64_t)floor(4294967296.0 / lambda + 0.5); }
 
-/* Eq. newt1i: next_t = t - ln(r)/lambda; next_t > t. */
-uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits) {
-    uint64_t X = ((uint64_t)w1 << 32) | w2;
-    uint64_t q = oracle_nlog_q32(X);
+/* P3L: the asynchrony law, the unscaled increment U in Q32 (docs/PRIMITIVES.md P3L):
+ *   law 0, Poisson (Eq. newt1i):        U = NLOG-2((w1 << 32) | w2) = -ln(r)
+ *   law 1, uniform on (0,1):         U = w1
+ *   law 2, next_t - t = r^(1/8):     U = floor(sqrt(sqrt(sqrt(r))) * 2^32),
+ *          r = (w1 + 0.5) * 2^-32 in IEEE double (sqrt is correctly rounded). */
+uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law) {
+    if (law == 1) return (uint64_t)w1;
+    if (law == 2) {
+        double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
+        return (uint64_t)floor(sqrt(sqrt(sqrt(r))) * 4294967296.0);
+    }
+    return oracle_nlog_q32(((uint64_t)w1 << 32) | w2);
+}
+
+/* next_t = t + U / lambda; next_t > t. */
+uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits, int law) {
+    uint64_t q = oracle_law_q32(w1, w2, law);
     unsigned __int128 prod = (unsigned __int128)q * inv_lambda;
     uint64_t d = (uint64_t)(prod >> 32);
     if (d < 1) d = 1;
@@ -66,6 +79,11 @@ uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bit
         if (d < quantum) d = quantum;
     }
     return d;
+}
+
+/* Eq. newt1i: next_t = t - ln(r)/lambda (the Poisson law). */
+uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits) {
+    return oracle_delta_law(w1, w2, inv_lambda, tie_bits, 0);
 }
 
 /* ---------------------------------------------------------------- P4: flip thresholds */
@@ -108,7 +126,7 @@ struct oracle_sim {
     int ndim, zc;
     int64_t dims[3], N;
     double lambda, beta, J, h, init_q;
-    int rule, tie_bits;
+    int rule, tie_bits, law;
     uint64_t seed, inv_lambda, thr_init, thr[14];
     uint32_t key[2];
     int8_t* s;
@@ -148,7 +166,13 @@ static void draw(const oracle_sim* S, uint32_t k, int64_t c, uint32_t tag, uint3
 
 oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double beta, double J,
                           double h, int rule, uint64_t seed, double init_q, int tie_bits) {
+    return oracle_create_law(ndim, dims, lambda, beta, J, h, rule, seed, init_q, tie_bits, 0);
+}
+
+oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, double beta, double J,
+                              double h, int rule, uint64_t seed, double init_q, int tie_bits, int law) {
     if (ndim != 2 && ndim != 3) return NULL;
+    if (law < 0 || law > 2) return NULL;
     if (!(lambda > 0) || !isfinite(lambda) || !(beta >= 0) || !isfinite(beta)) return NULL;
     if (rule != 0 && rule != 1) return NULL;
     if (!(init_q >= 0 && init_q <= 1)) return NULL;
@@ -160,7 +184,7 @@ oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double b
     S->ndim = ndim; S->zc = 2 * ndim; S->N = N;
     for (int a = 0; a < 3; a++) S->dims[a] = a < ndim ? dims[a] : 1;
     S->lambda = lambda; S->beta = beta; S->J = J; S->h = h; S->rule = rule;
-    S->seed = seed; S->init_q = init_q; S->tie_bits = tie_bits;
+    S->seed = seed; S->init_q = init_q; S->tie_bits = tie_bits; S->law = law;
     S->inv_lambda = oracle_inv_lambda(lambda);
     S->thr_init = (uint64_t)floor(init_q * 4294967296.0);
     oracle_flip_table(ndim, beta, J, h, rule, S->thr);
@@ -176,7 +200,7 @@ oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double b
         uint32_t w[4];
         draw(S, 0, c, 1u, w);
         S->s[c] = ((uint64_t)w[0] < S->thr_init) ? -1 : 1;
-        S->t[c] = oracle_delta(w[1], w[2], S->inv_lambda, tie_bits);
+        S->t[c] = oracle_delta_law(w[1], w[2], S->inv_lambda, tie_bits, law);
         S->n[c] = 0;
     }
     return S;
@@ -208,7 +232,7 @@ static void arrival(oracle_sim* S, int64_t c, int8_t* new_s, uint64_t* new_t) {
     S->event_hash += oracle_mix64(tev ^ rotl64((uint64_t)c, 20) ^ rotl64((uint64_t)k, 44) ^
                                   (uint64_t)(ns > 0 ? 1 : 0));
     *new_s = (int8_t)ns;
-    *new_t = tev + oracle_delta(w[1], w[2], S->inv_lambda, S->tie_bits);
+    *new_t = tev + oracle_delta_law(w[1], w[2], S->inv_lambda, S->tie_bits, S->law);
 }
 
 /* lexicographic (t, c) order (P6). */
@@ -421,16 +445,21 @@ void oracle_nlog_batch(int64_t n, const uint64_t* X, uint64_t* q) {
  * time and counter after run_until(T) follow from its own stream alone. */
 void oracle_cell_time_counter(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_t inv_lambda,
                               int tie_bits, uint64_t* t_out, uint32_t* n_out) {
+    oracle_cell_time_counter_law(seed, c, T_q32, inv_lambda, tie_bits, 0, t_out, n_out);
+}
+
+void oracle_cell_time_counter_law(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_t inv_lambda,
+                                  int tie_bits, int law, uint64_t* t_out, uint32_t* n_out) {
     uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
     uint32_t ctr[4] = {0, (uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 1u};
     uint32_t w[4];
     oracle_philox4x32_10(ctr, key, w);
-    uint64_t t = oracle_delta(w[1], w[2], inv_lambda, tie_bits);
+    uint64_t t = oracle_delta_law(w[1], w[2], inv_lambda, tie_bits, law);
     uint32_t k = 0;
     while (t < T_q32) {
         uint32_t ce[4] = {k, (uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 0u};
         oracle_philox4x32_10(ce, key, w);
-        t += oracle_delta(w[1], w[2], inv_lambda, tie_bits);
+        t += oracle_delta_law(w[1], w[2], inv_lambda, tie_bits, law);
         k++;
     }
     *t_out = t;
@@ -455,6 +484,14 @@ int oracle_window_cell(int ndim, const int64_t* dims, double lambda, double beta
                        uint64_t seed, double init_q, int tie_bits, uint64_t T, const int64_t* center,
                        int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
                        int* exact_out) {
+    return oracle_window_cell_law(ndim, dims, lambda, beta, J, h, rule, seed, init_q, tie_bits, T, center, radius,
+                                  refine, s_out, t_out, n_out, exact_out, 0);
+}
+
+int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double beta, double J, double h, int rule,
+                       uint64_t seed, double init_q, int tie_bits, uint64_t T, const int64_t* center,
+                       int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
+                       int* exact_out, int law) {
     int64_t D[3] = {1, 1, 1}, W[3] = {1, 1, 1}, lo[3] = {0, 0, 0};
     int fullax[3] = {1, 1, 1};
     int64_t NW = 1;
@@ -497,7 +534,7 @@ int oracle_window_cell(int ndim, const int64_t* dims, double lambda, double beta
         uint32_t ctr[4] = {0, (uint32_t)(gid[l] & 0xffffffffu), (uint32_t)(gid[l] >> 32), 1u}, w[4];
         oracle_philox4x32_10(ctr, key, w);
         s[l] = ((uint64_t)w[0] < thr_init) ? -1 : 1;
-        t[l] = oracle_delta(w[1], w[2], inv, tie_bits);
+        t[l] = oracle_delta_law(w[1], w[2], inv, tie_bits, law);
     }
     /* binary heap of (t, global id, local id) */
     int64_t hn = 0;
@@ -539,7 +576,7 @@ int oracle_window_cell(int ndim, const int64_t* dims, double lambda, double beta
                 unk[c] = 1;
             }
         }
-        t[c] += oracle_delta(w[1], w[2], inv, tie_bits);
+        t[c] += oracle_delta_law(w[1], w[2], inv, tie_bits, law);
         n[c] += 1;
         heap[0].t = t[c];
         int64_t i = 0;

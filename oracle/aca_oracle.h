@@ -34,6 +34,10 @@ uint64_t oracle_nlog_q32(uint64_t X);
 /* P3: Delta(w1, w2) for INV = floor(2^32/lambda + 0.5), tie_bits as P3b. */
 uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits);
 uint64_t oracle_inv_lambda(double lambda);
+/* P3L: asynchrony laws. law 0 Poisson (= oracle_delta), 1 uniform on (0,1), 2 r^(1/8).
+ * oracle_law_q32 is the unscaled increment U in Q32 (before 1/lambda, the clamp and P3b). */
+uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law);
+uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits, int law);
 /* P4: thresholds, 2*(2*ndim+1) entries written to out. */
 void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint64_t* out);
 /* P7 */
@@ -42,6 +46,8 @@ uint64_t oracle_mix64(uint64_t z);
 /* Returns NULL on invalid arguments. ndim in {2,3}, every dim >= 2, N < 2^32. */
 oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double beta, double J,
                           double h, int rule, uint64_t seed, double init_q, int tie_bits);
+oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, double beta, double J,
+                              double h, int rule, uint64_t seed, double init_q, int tie_bits, int law);
 void oracle_destroy(oracle_sim* s);
 
 /* (A) global priority queue on (t, c): the oracle. Returns 0, or -1 if T decreased. */
@@ -77,6 +83,8 @@ int oracle_time_weighted_hist(int ndim, const int64_t* dims, double beta, double
 void oracle_nlog_batch(int64_t n, const uint64_t* X, uint64_t* q);
 void oracle_cell_time_counter(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_t inv_lambda,
                               int tie_bits, uint64_t* t_out, uint32_t* n_out);
+void oracle_cell_time_counter_law(uint64_t seed, uint64_t c, uint64_t T_q32, uint64_t inv_lambda,
+                                  int tie_bits, int law, uint64_t* t_out, uint32_t* n_out);
 
 /* Window (light-cone) oracle: exact (s, t, n) of the cell at `center` after run_until(T) on
  * a lattice too large to simulate whole; *exact_out = 0 when the box was too small. */
@@ -84,6 +92,10 @@ int oracle_window_cell(int ndim, const int64_t* dims, double lambda, double beta
                        uint64_t seed, double init_q, int tie_bits, uint64_t T_q32, const int64_t* center,
                        int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
                        int* exact_out);
+int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double beta, double J, double h, int rule,
+                           uint64_t seed, double init_q, int tie_bits, uint64_t T_q32, const int64_t* center,
+                           int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
+                           int* exact_out, int law);
 
 #ifdef __cplusplus
 }

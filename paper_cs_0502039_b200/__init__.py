@@ -23,7 +23,8 @@ ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: 
 EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
-           "aca_selftest_nlog"]
+           "aca_selftest_nlog", "aca_selftest_law"]
+POISSON, UNIFORM, ROOT8 = 0, 1, 2   # asynchrony laws (aca_options.law)
 
 
 class AcaError(RuntimeError):
@@ -40,7 +41,8 @@ class aca_options(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("stream", ctypes.c_void_p), ("event_hash", ctypes.c_int32),
                 ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32),
-                ("early_reject", ctypes.c_int32), ("checkerboard", ctypes.c_int32)]
+                ("early_reject", ctypes.c_int32), ("checkerboard", ctypes.c_int32),
+                ("law", ctypes.c_int32)]
 
 
 class aca_stats(ctypes.Structure):
@@ -97,6 +99,7 @@ def lib():
     L.aca_num_cells.restype = ctypes.c_int64
     L.aca_selftest_philox.argtypes = [ctypes.c_uint64, vp, vp, vp, vp]
     L.aca_selftest_nlog.argtypes = [ctypes.c_uint64, vp, vp, vp, ctypes.c_uint64, ctypes.c_int]
+    L.aca_selftest_law.argtypes = [ctypes.c_uint64, vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, vp, vp]
     _lib = L
     return L
 
@@ -242,6 +245,15 @@ def aca_selftest_nlog(X, lam=1.0, tie_bits=0):
     inv = int(np.floor(4294967296.0 / lam + 0.5))
     _check(lib().aca_selftest_nlog(X.size, _ptr(X), _ptr(q), _ptr(d), inv, tie_bits))
     return q, d
+
+
+def aca_selftest_law(X, law, lam=1.0, tie_bits=0):
+    X = np.ascontiguousarray(X, np.uint64)
+    u = np.empty_like(X)
+    d = np.empty_like(X)
+    inv = int(np.floor(4294967296.0 / lam + 0.5))
+    _check(lib().aca_selftest_law(X.size, _ptr(X), int(law), inv, tie_bits, _ptr(u), _ptr(d)))
+    return u, d
 
 
 class Sim:

@@ -122,6 +122,7 @@ struct aca_sim {
     unsigned long long thr[14] = {};
     unsigned long long thm[98] = {};   // a10 early-rejection table (see commit_loop)
     int bulk = 1;
+    int defer_tail = 1;
     unsigned long long thr_init = 0;
     unsigned long long max_delta = 0;
     uint64_t T_last = 0;
@@ -226,9 +227,8 @@ int bits_for(uint64_t v) {
 constexpr size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
     return ((size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32) * 8;
 }
-constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf) {
-    return ((((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~(size_t)15) * nbuf + 512 + 16 + 112 +
-            nt / 32 + 2) * 8 + ((size_t)tx * ty * tz + 64) * 2 + (size_t)tx * ty * tz / 32 * 8 + 16;
+constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl = false, bool early = false) {
+    return tma_smem_bytes(ndim, tx, ty, tz, nt, nbuf, wl, early);
 }
 
 // Kernel variants (identical results; ablations): 0 = persistent TMA-staged compacted kernel
@@ -251,12 +251,12 @@ struct TileKey {
       (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBW, false, false, false, true>,                   \
       (void*)tile_kernel<ND, TX, TY, TZ, NT, true>},                                                 \
      {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
-      tma_smem(ND, TX, TY, TZ, NT, 1), tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT)}, \
+      tma_smem(ND, TX, TY, TZ, NT, 1), tma_smem(ND, TX, TY, TZ, NT, 1, true), tile_smem(ND, TX, TY, TZ, NT)}, \
      {true, false, true, true, true, false},                                                         \
      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 64, 1, 256, 3, 2, 3, 4),
+    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 64, 1, 256, 5, 2, 3, 4),
     TK(2, 128, 64, 1, 512, 1, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8, 8), TK(3, 16, 16, 16, 256, 2, 1, 2, 2),
     TK(3, 32, 16, 8, 256, 2, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
 };
@@ -287,11 +287,13 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     philox_round_keys(P.key0, P.key1, P.rk);
     P.inv_lambda = S->inv_lambda;
     P.tie_bits = S->opt.tie_bits;
+    P.law = S->opt.law;
     P.rounds = S->rounds;
     P.round_mode = S->round_mode;
     P.do_hash = S->opt.event_hash;
     P.early = S->opt.early_reject;
     P.bulk = S->bulk;
+    P.defer_tail = S->defer_tail;
     for (int i = 0; i < 98; ++i) P.thm[i] = S->thm[i];
     P.tiles_x = sh.tiles_x;
     P.tiles_y = sh.tiles_y;
@@ -422,7 +424,7 @@ int init_state(aca_sim* S) {
     for (auto& sh : S->shards) {
         CK(cudaMemsetAsync(sh.ctl, 0, sizeof(Ctl), S->stream));
         init_kernel<<<1184, 256, 0, S->stream>>>(sh.words, sh.g, S->d_lr, k0, k1, S->thr_init, S->inv_lambda,
-                                                  S->opt.tie_bits, (unsigned long long)sh.n);
+                                                  S->opt.tie_bits, (unsigned long long)sh.n, S->opt.law);
         CK(cudaGetLastError());
     }
     S->T_last = 0;
@@ -555,6 +557,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     }
     if (!(opt.init_q >= 0 && opt.init_q <= 1)) return fail(ACA_EINVAL, "init_q must be in [0, 1]");
     if (opt.tie_bits < 0 || opt.tie_bits > 40) return fail(ACA_EINVAL, "tie_bits must be in [0, 40]");
+    if (opt.law < 0 || opt.law > 2) return fail(ACA_EINVAL, "law must be 0 (Poisson), 1 (uniform) or 2 (r^1/8)");
     if (opt.shards < 1) opt.shards = 1;
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(ACA_EINVAL, "bad rank/world");
     if ((opt.world > 1 || opt.nccl_id) && opt.shards != 1)
@@ -608,12 +611,15 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->bulk = 1;   // one committed arrival per cell per fire step: longer in-thread chains
                    // diverge within the warp (measured: bulk 4/32 are 1.8-2x slower on c5)
     if (const char* e = getenv("ACA_BULK")) S->bulk = std::max(1, atoi(e));
+    if (const char* e = getenv("ACA_DEFER_TAIL")) S->defer_tail = atoi(e);
     S->thr_init = (unsigned long long)std::floor(opt.init_q * 4294967296.0);
     uint64_t max_rank = 0;
     for (int a = 0; a < ndim; ++a) max_rank += (uint64_t)(dims[a] - 1);
     S->RB = bits_for(max_rank);
     {
-        const unsigned __int128 p = (unsigned __int128)190530846196ull * S->inv_lambda;
+        // largest unscaled increment of the law: NLOG-2(1) for Poisson, < 2^32 otherwise
+        const unsigned long long umax = opt.law == 0 ? 190530846196ull : (1ull << 32);
+        const unsigned __int128 p = (unsigned __int128)umax * S->inv_lambda;
         S->max_delta = (unsigned long long)(p >> 32) + 1 + (opt.tie_bits ? (1ull << opt.tie_bits) : 0ull);
         const int tb = bits_for(S->max_delta);
         int nb = 63 - S->RB - tb;
@@ -675,6 +681,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         S->kern = (v == 0 && opt.early_reject) ? sel->fn_early : sel->fn[v];
         S->nthreads = sel->nt;
         S->smem = sel->smem[v];
+        if (v == 0 && opt.early_reject)   // a10 candidates need a full per-warp queue
+            S->smem = tma_smem(ndim, tx, ty, tz, sel->nt, 1, false, true);
         if (sel->persistent[v]) {   // persistent: as many CTAs as fit on the device at once
             if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
                 return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
@@ -1066,9 +1074,40 @@ __global__ void nlog_test_kernel(uint64_t n, const uint64_t* X, uint64_t* q, uin
         d[i] = delta_q32((uint32_t)(X[i] >> 32), (uint32_t)X[i], lr, ACA_LN2_Q48, inv_lambda, tie_bits);
     }
 }
+__global__ void law_test_kernel(uint64_t n, const uint64_t* X, uint64_t* u, uint64_t* d, const unsigned long long* lr_g,
+                                unsigned long long inv_lambda, int tie_bits, int law) {
+    __shared__ unsigned long long lr[512];
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    __syncthreads();
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t w1 = (uint32_t)(X[i] >> 32), w2 = (uint32_t)X[i];
+        u[i] = law_q32(w1, w2, lr, ACA_LN2_Q48, law);
+        d[i] = delta_q32(w1, w2, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
+    }
+}
 }  // namespace
 
 extern "C" {
+int aca_selftest_law(uint64_t n, const uint64_t* X, int law, uint64_t inv_lambda, int tie_bits, uint64_t* u,
+                     uint64_t* delta) {
+    if (!X || !u || !delta) return fail(ACA_EINVAL, "null buffer");
+    if (law < 0 || law > 2) return fail(ACA_EINVAL, "bad law");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
+    uint64_t *dx = nullptr, *du = nullptr, *dd = nullptr;
+    unsigned long long* dlr = nullptr;
+    CK(cudaMalloc(&dx, n * 8)); CK(cudaMalloc(&du, n * 8)); CK(cudaMalloc(&dd, n * 8));
+    CK(cudaMalloc(&dlr, sizeof(ACA_NLOG_LR)));
+    CK(cudaMemcpy(dlr, ACA_NLOG_LR, sizeof(ACA_NLOG_LR), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dx, X, n * 8, cudaMemcpyHostToDevice));
+    law_test_kernel<<<592, 256>>>(n, dx, du, dd, dlr, inv_lambda, tie_bits, law);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(u, du, n * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(delta, dd, n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dx); cudaFree(du); cudaFree(dd); cudaFree(dlr);
+    return ACA_OK;
+}
+
 int aca_selftest_philox(uint64_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out, uint32_t* ref) {
     if (!ctr || !key || !out || !ref) return fail(ACA_EINVAL, "null buffer");
     int ndev = 0;

@@ -70,11 +70,13 @@ struct KParams {
     uint32_t rk[20];                     // Philox round keys of (key0, key1)
     unsigned long long inv_lambda;
     int tie_bits;
+    int law;                             // P3L asynchrony law (0 Poisson, 1 uniform, 2 r^(1/8))
     int rounds;                          // R_max
     int round_mode;                      // 0: CTA barrier per round; 1: no barrier, R rounds; 2: per-warp exit
     int do_hash;
     int early;                           // a10: queue early-rejection candidates
     int bulk;                            // max arrivals committed per cell per fire step (1 = one)
+    int defer_tail;                      // tile_rounds: defer a partial last fire chunk to the next round
     int tiles_x, tiles_y, tiles_z;
     int phase;                           // -1: every tile; 0 / 1: tiles of that checkerboard colour
     int row_par0;                        // parity of the shard's first tile row (global colouring)
@@ -160,7 +162,7 @@ struct FireOut { unsigned long long wnew; uint32_t flip; unsigned long long h; b
 __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int z, unsigned long long c,
                                         const Geo& g, const unsigned long long* thr, const unsigned long long* lr,
                                         const uint32_t* rk, unsigned long long inv_lambda, int tie_bits,
-                                        int do_hash, Ctl* ctl) {
+                                        int do_hash, Ctl* ctl, int law = 0) {
     FireOut o;
     const uint32_t k = w_count(w, g);
     if (k == (uint32_t)((1ull << g.NB) - 1ull)) {
@@ -172,7 +174,7 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
     const uint32_t idx = ones + (uint32_t)(z + 1) * sb;          // (Sigma+z)/2 + (z+1)(s+1)/2
     const u32x4 r = philox4x32_10_rk(k, (uint32_t)c, (uint32_t)(c >> 32), 0u, rk);
     const uint32_t flip = (unsigned long long)r.x < thr[idx] ? 1u : 0u;
-    const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits);
+    const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
     o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;   // t += d, n += 1, s ^= flip
     o.flip = flip;
     o.h = 0;
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
             }
             if (!ok) continue;
             const FireOut o = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
             if (!o.ok) continue;
             hacc += o.h;
             flips += o.flip;
@@ -356,6 +358,24 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
     const unsigned long long s_tst = block_sum<NT>(tested, red);
     const unsigned long long s_hsh = block_sum<NT>(hacc, red);
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds);
+}
+
+// Shared-memory layout of tile_tma_kernel (host and device): words (NB_ buffers), the P3 table,
+// P4/a10 tables, reduction scratch, 2 mbarriers, then the fire queue(s): per-warp queues of
+// CPW/2 + 16 entries (the eligible cells of a warp form an independent set: at most one per
+// two cells of each row segment), CPW with a10 candidates, or the work-list's two CTA queues
+// plus claim bitmaps and counters.
+__host__ __device__ constexpr size_t tma_words(int ndim, int tx, int ty, int tz) {
+    return (((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~(size_t)15);
+}
+__host__ __device__ constexpr size_t tma_queue_entries(int ncell, int nt, bool wl, bool early) {
+    return wl ? (size_t)ncell + 64 : early ? (size_t)ncell : (size_t)(nt / 32) * (ncell / (nt / 32) / 2 + 16);
+}
+__host__ __device__ constexpr size_t tma_smem_bytes(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl,
+                                                    bool early) {
+    return (tma_words(ndim, tx, ty, tz) * nbuf + 512 + 16 + 112 + nt / 32 + 2) * 8 +
+           ((tma_queue_entries(tx * ty * tz, nt, wl, early) * 2 + 15) & ~(size_t)15) +
+           (wl ? (size_t)tx * ty * tz / 32 * 8 + 16 : 0);
 }
 
 // ------------------------------------------------------------ persistent TMA tile kernel
@@ -411,7 +431,7 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
         uint32_t flip = 0;
         if (u == 0) flip = (unsigned long long)r.x < thr[k + (uint32_t)(Z + 1) * sb] ? 1u : 0u;
         else if ((unsigned long long)r.x < tm) break;     // a flip is possible in some world: wait
-        const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, P.tie_bits);
+        const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, P.tie_bits, P.law);
         if (P.do_hash) {
             const unsigned long long t = w >> g.TSH;
             st.hacc += mix64(t ^ rotl64(cid, 20) ^ rotl64((unsigned long long)n, 44) ^ (unsigned long long)(sb ^ flip));
@@ -440,7 +460,8 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wbase = warp * CPW;
-    unsigned short* q = Q + warp * CPW;
+    constexpr int QW = EARLY ? CPW : CPW / 2 + 16;       // per-warp queue (see tma_smem_bytes)
+    unsigned short* q = Q + warp * QW;
     volatile unsigned long long* VS = S;
     const volatile unsigned int* VH = (const volatile unsigned int*)S;   // [2s+1]: high half, [2s]: low half
     auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2; };
@@ -562,7 +583,11 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             q[pos++] = (unsigned short)(wbase + lane + 32 * j);
         }
         __syncwarp();
-        for (int i = lane; i < cnt; i += 32) {
+        // Fire whole 32-lane chunks only; the partial tail chunk waits for the next round (its
+        // cells stay local minima, and every active cell is re-tested each round anyway). The
+        // last round, and rounds with a single (partial) chunk, fire everything.
+        const int nfire = (P.defer_tail && r < P.rounds - 1 && cnt > 32) ? (cnt & ~31) : cnt;
+        for (int i = lane; i < nfire; i += 32) {
             const int o = q[i];
             const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
             const int s = slot(lx, ly, lz);
@@ -575,7 +600,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
             const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
             if (!f.ok) continue;
             VS[s] = f.wnew;
             st.hacc += f.h;
@@ -719,7 +744,7 @@ __device__ __forceinline__ unsigned int tile_rounds_reg(const KParams& P, unsign
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
             const FireOut f = fire(wv, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
             if (!f.ok) continue;
             VS[s] = f.wnew;
             st.hacc += f.h;
@@ -853,7 +878,7 @@ __device__ __forceinline__ unsigned int tile_rounds_wl(const KParams& P, unsigne
                                 (VH[2 * (s + SX)] & 1u);
                 if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
                 const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                       P.inv_lambda, P.tie_bits, P.do_hash, P.ctl);
+                                       P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
                 if (f.ok) {
                     VS[s] = f.wnew;
                     st.hacc += f.h;
@@ -978,8 +1003,8 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     unsigned long long* thm = thr + 16;                             // 112 (a10 table)
     unsigned long long* red = thm + 112;                            // NW
     unsigned long long* bar = red + NW;                             // 2
-    unsigned short* Q = (unsigned short*)(bar + 2);                 // NCELL + 64 (WL: two queues)
-    unsigned int* claim = (unsigned int*)(Q + NCELL + 64);          // WL: 2 x NCELL/32 claim bits
+    unsigned short* Q = (unsigned short*)(bar + 2);                 // fire queue(s), see tma_smem_bytes
+    unsigned int* claim = (unsigned int*)(Q + ((tma_queue_entries(NCELL, NT, WL, EARLY) + 7) & ~(size_t)7));
     unsigned int* qcnt = claim + 2 * (NCELL / 32);                  // WL: 4 queue counters
 
     const Geo& g = P.g;
@@ -1167,7 +1192,7 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
             }
             if (!ok) continue;
             const FireOut o = fire(w, ones, Z, (unsigned long long)i, g, thr, lr, P.rk, P.inv_lambda,
-                                   P.tie_bits, P.do_hash, P.ctl);
+                                   P.tie_bits, P.do_hash, P.ctl, P.law);
             if (!o.ok) continue;
             hacc += o.h;
             flips += o.flip;
@@ -1217,7 +1242,7 @@ __device__ __forceinline__ void cell_coords(const Geo& g, unsigned long long li,
 
 __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const unsigned long long* __restrict__ lr_g,
                             uint32_t key0, uint32_t key1, unsigned long long thr_init, unsigned long long inv_lambda,
-                            int tie_bits, unsigned long long n_local) {
+                            int tie_bits, unsigned long long n_local, int law) {
     __shared__ unsigned long long lr[512];
     for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
     __syncthreads();
@@ -1227,7 +1252,7 @@ __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const
         cell_coords(g, i, c, rank);
         const u32x4 r = philox4x32_10(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, key0, key1);
         const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
-        const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits);
+        const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
         words[i] = w_pack(t0, rank, 0ull, sb, g);
     }
 }

@@ -86,10 +86,25 @@ __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long lon
     return (S + (1ull << 15)) >> 16;
 }
 
-// Eq. newt1i, next_t > t; P3b tie quantisation.
+// P3L asynchrony law: the unscaled increment U in Q32 (docs/PRIMITIVES.md P3L).
+//   0 Poisson, Eq. newt1i:   U = NLOG-2((w1 << 32) | w2)
+//   1 uniform on (0,1):    U = w1
+//   2 r^(1/8):             U = floor(sqrt(sqrt(sqrt(r))) * 2^32), r = (w1 + 0.5) 2^-32
+//     (IEEE double; sqrt is correctly rounded on the device as on the host)
+__device__ __forceinline__ uint64_t law_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr,
+                                            uint64_t ln2_q48, int law) {
+    if (law == 1) return (uint64_t)w1;
+    if (law == 2) {
+        const double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
+        return (uint64_t)(__dsqrt_rn(__dsqrt_rn(__dsqrt_rn(r))) * 4294967296.0);
+    }
+    return nlog_q32(((uint64_t)w1 << 32) | w2, lr, ln2_q48);
+}
+
+// next_t = t + U / lambda, next_t > t; P3b tie quantisation.
 __device__ __forceinline__ uint64_t delta_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr,
-                                              uint64_t ln2_q48, uint64_t inv_lambda, int tie_bits) {
-    const uint64_t q = nlog_q32(((uint64_t)w1 << 32) | w2, lr, ln2_q48);
+                                              uint64_t ln2_q48, uint64_t inv_lambda, int tie_bits, int law = 0) {
+    const uint64_t q = law_q32(w1, w2, lr, ln2_q48, law);
     uint64_t d;
     if (inv_lambda == (1ull << 32)) {
         d = q;

@@ -21,10 +21,11 @@ def aca():
 
 
 def run_pair(aca, oracle_mod, dims, Ts, beta=0.4406868, J=1.0, h=0.0, lam=1.0, rule=0, seed=1,
-             init_q=0.5, tie_bits=0, **opts):
-    g = aca.Sim(dims, lam=lam, beta=beta, J=J, h=h, rule=rule, seed=seed, init_q=init_q, tie_bits=tie_bits, **opts)
+             init_q=0.5, tie_bits=0, law=0, **opts):
+    g = aca.Sim(dims, lam=lam, beta=beta, J=J, h=h, rule=rule, seed=seed, init_q=init_q, tie_bits=tie_bits, law=law,
+                **opts)
     o = oracle_mod.OracleSim(dims, lam=lam, beta=beta, J=J, h=h, rule=rule, seed=seed, init_q=init_q,
-                             tie_bits=tie_bits)
+                             tie_bits=tie_bits, law=law)
     assert g.flip_table() == oracle_mod.flip_table(len(dims), beta, J, h, rule)
     for T in Ts:
         g.run_until(T)
@@ -72,6 +73,32 @@ def test_nlog_bit_identical_to_oracle(aca, oracle_mod):
         q, d = aca.aca_selftest_nlog(X[:5000], lam, tb)
         want = [oracle_mod.delta(int(x) >> 32, int(x) & 0xFFFFFFFF, lam, tb) for x in X[:5000]]
         assert list(d) == want
+
+
+@pytest.mark.parametrize("law", [0, 1, 2])
+def test_law_bit_identical_to_oracle(aca, oracle_mod, law):
+    """P3L asynchrony laws: the device's unscaled increment and
+    Delta equal the oracle's on random and edge inputs, for several lambda / tie settings."""
+    rng = np.random.default_rng(5 + law)
+    X = rng.integers(0, 2 ** 63, size=1 << 18, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, 1 << 18).astype(np.uint64)
+    edges = [0, 1, 2 ** 32 - 1, 2 ** 32, 2 ** 63, 2 ** 64 - 1, 2 ** 64 - 2 ** 32] + [(2 ** k) << 32 for k in range(32)]
+    X = np.concatenate([np.array(edges, np.uint64), X])
+    for lam, tb in ((1.0, 0), (2.5, 0), (0.3, 0), (1.0, 28)):
+        u, d = aca.aca_selftest_law(X[:20000], law, lam, tb)
+        want_u = [oracle_mod.law_q32(int(x) >> 32, int(x) & 0xFFFFFFFF, law) for x in X[:20000]]
+        want_d = [oracle_mod.delta(int(x) >> 32, int(x) & 0xFFFFFFFF, lam, tb, law) for x in X[:20000]]
+        assert list(u) == want_u
+        assert list(d) == want_d
+
+
+@pytest.mark.parametrize("law", [1, 2])
+def test_law_trajectories(aca, oracle_mod, law):
+    """Whole trajectories under the uniform and r^(1/8) laws: whole-lattice, tiled 2-D with
+    ragged tiles, 3-D tiles, with field and both rules."""
+    for dims, kw in (((6, 5), dict(rule=0)), ((200, 150), dict(rule=1, h=0.1, whole_lattice=-1)),
+                     ((24, 16, 12), dict(rule=0, beta=0.22, whole_lattice=-1, tile=(8, 8, 8)))):
+        g, o = run_pair(aca, oracle_mod, dims, [3.0, 6.0], seed=23, law=law, **kw)
+        assert_same(g, o)
 
 
 @pytest.mark.parametrize("dims", [(2, 2), (3, 3), (5, 7), (2, 5), (16, 16), (13, 7)])

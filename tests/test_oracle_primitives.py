@@ -198,3 +198,54 @@ def test_mix64_is_splitmix_finaliser(oracle_mod):
         assert v == z
         seen.add(v)
     assert len(seen) == 2000
+
+
+# ---------------------------------------------------------------- P3L asynchrony laws
+def test_law_uniform_is_the_raw_word(oracle_mod):
+    """Law 1, next_t - t uniform on (0,1): U = w1, i.e. (w1/2^32) is the
+    uniform variate; the increment is U/lambda clamped to >= 1 unit."""
+    r = random.Random(21)
+    for _ in range(2000):
+        w1, w2 = r.getrandbits(32), r.getrandbits(32)
+        assert oracle_mod.law_q32(w1, w2, 1) == w1
+        assert oracle_mod.delta(w1, w2, 1.0, 0, 1) == max(1, w1)
+        assert abs(oracle_mod.delta(w1, w2, 2.0, 0, 1) - w1 / 2) <= 1
+    assert oracle_mod.delta(0, 5, 1.0, 0, 1) == 1
+
+
+def test_law_root8_within_one_unit_of_mpmath(oracle_mod):
+    """Law 2, next_t - t = r^(1/8): U = floor(r^(1/8) 2^32) with
+    r = (w1 + 1/2) 2^-32, within one unit of the exact real value; monotone in w1."""
+    r = random.Random(22)
+    ws = [0, 1, 2, 3, 255, 256, 2 ** 31, 2 ** 32 - 2, 2 ** 32 - 1] + [r.getrandbits(32) for _ in range(4000)]
+    for w1 in ws:
+        exact = mpmath.floor(mpmath.root((mpmath.mpf(w1) + mpmath.mpf(0.5)) / 2 ** 32, 8) * 2 ** 32)
+        assert abs(int(oracle_mod.law_q32(w1, 0, 2)) - int(exact)) <= 1, w1
+    ws = sorted(set(ws))
+    us = [oracle_mod.law_q32(w, 0, 2) for w in ws]
+    assert all(a <= b for a, b in zip(us, us[1:]))
+    assert oracle_mod.law_q32(2 ** 32 - 1, 0, 2) == 2 ** 32 - 1     # r^(1/8) < 1 always
+
+
+def test_law_root8_distribution(oracle_mod):
+    """(U/2^32)^8 of Philox draws is Uniform(0,1) (KS); mean of U/2^32 is 8/9."""
+    from scipy import stats
+    v = []
+    for c in range(20000):
+        w = oracle_mod.philox((0, c, 0, 0), (41, 3))
+        v.append(oracle_mod.law_q32(w[1], w[2], 2) / 2.0 ** 32)
+    v = np.array(v)
+    assert stats.kstest(v ** 8, "uniform").pvalue > 1e-4
+    assert abs(v.mean() - 8 / 9) < 4 * math.sqrt(8 / 10 - (8 / 9) ** 2) / math.sqrt(len(v))
+
+
+@pytest.mark.parametrize("law", [1, 2])
+def test_law_closed_form_times(oracle_mod, law):
+    """Arrival times are state-independent under every law: the oracle's
+    final (t, n) equal each cell's own partial sums."""
+    o = oracle_mod.OracleSim((12, 10), beta=0.44, seed=5, law=law)
+    o.run_until(7.0)
+    t, n = o.times(), o.counters()
+    for c in range(120):
+        tc, nc = oracle_mod.cell_time_counter(5, c, 7.0, law=law)
+        assert (int(t.flat[c]), int(n.flat[c])) == (tc, nc)

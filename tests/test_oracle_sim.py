@@ -95,10 +95,10 @@ def test_init_rule(oracle_mod):
     assert (s0.spins() == 1).all()
 
 
-def _run_all_orders(oracle_mod, dims, T, tie_bits, seed, beta=0.4406868, rule=0, h=0.0):
+def _run_all_orders(oracle_mod, dims, T, tie_bits, seed, beta=0.4406868, rule=0, h=0.0, law=0):
     out = []
     for order, cs in (("pq", 0), ("random", 1), ("random", 2), ("sync", 0)):
-        s = oracle_mod.OracleSim(dims, beta=beta, rule=rule, h=h, seed=seed, tie_bits=tie_bits)
+        s = oracle_mod.OracleSim(dims, beta=beta, rule=rule, h=h, seed=seed, tie_bits=tie_bits, law=law)
         s.run_until(T, order=order, choice_seed=cs)
         st = s.stats()
         st.pop("rounds")
@@ -117,6 +117,18 @@ def test_order_independence(oracle_mod, dims, tie_bits):
         for a, b in zip(ref[:3], other[:3]):
             assert np.array_equal(a, b)
         assert ref[3] == other[3]
+
+
+@pytest.mark.parametrize("dims", [(16, 16), (2, 5), (4, 4, 4)])
+@pytest.mark.parametrize("law", [1, 2])
+def test_order_independence_other_laws(oracle_mod, dims, law):
+    """The uniqueness argument does not depend on the asynchrony law
+    (PAPER.md:364-410): uniform and r^(1/8) increments give one trajectory in every order."""
+    res = _run_all_orders(oracle_mod, dims, 6.0, 0, seed=77, rule=1, h=0.1, law=law)
+    for other in res[1:]:
+        for a, b in zip(res[0][:3], other[:3]):
+            assert np.array_equal(a, b)
+        assert res[0][3] == other[3]
 
 
 def test_tie_stress_really_has_ties(oracle_mod):
