@@ -156,6 +156,20 @@ int aca_nccl_unique_id(void* out128);
 /* Number of cells of the handle (rank-local for multi-process handles). */
 int64_t aca_num_cells(const aca_sim* s);
 
+/* ---- Time-only efficiency model ----
+ * Synchronous iterations of fig:s1c1pe on the local times only (valid because next_t does
+ * not depend on the states for the Ising model): each iteration every
+ * cell whose (t, c) is below all neighbours' (P6 order) draws its next increment of `law`
+ * (P3L) at rate lambda. ndim 1 (n-circle), 2 (n x n torus), 3 (periodic n^3); dims[ndim],
+ * every dim >= 2. Draws: initial t from Philox ctr (0, c, 0, 1) (P5), iteration r from ctr
+ * (r, c_lo, c_hi, 2). Outputs (host buffers, caller-owned): fired_per_round[rounds] = N0 of
+ * each iteration (its efficiency is N0/N); t_out[N] (may be NULL) = the
+ * final times; *gpu_seconds (may be NULL) = device time of the iterations. device < 0: the
+ * current device. Device memory (2 x 8N bytes) is allocated and freed inside the call.
+ * Errors: ACA_EINVAL (arguments), ACA_ENOMEM, ACA_ENODEV, ACA_ECUDA. */
+int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
+                       uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds);
+
 /* ---- Self-test hooks (device primitives through the ABI; host buffers, n elements) ----
  * P1: out[4n] = our Philox(ctr[4i..], key[2i..]); ref[4n] = cuRAND's device
  *     curand_Philox4x32_10 on the same inputs (library reference for the pin). */

@@ -108,6 +108,9 @@ def lib():
                                          ctypes.POINTER(ctypes.c_int8), ctypes.POINTER(ctypes.c_uint64),
                                          ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
         L.oracle_window_cell_law.argtypes = L.oracle_window_cell.argtypes + [ctypes.c_int]
+        L.oracle_efficiency_run.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
+                                            ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
+                                            ctypes.c_void_p]
         _lib = L
     return _lib
 
@@ -264,3 +267,14 @@ def window_cell(dims, center, T, radius, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=H
                                       ctypes.byref(to), ctypes.byref(no), ctypes.byref(ex), law)
     assert rc == 0
     return so.value, to.value, no.value, bool(ex.value)
+
+
+def efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False):
+    """Time-only model of PAPER.md:1355-1442: N0 per synchronous iteration (and final times)."""
+    n = int(np.prod(dims))
+    fired = np.zeros(rounds, np.uint64)
+    t = np.zeros(n, np.uint64) if want_times else None
+    rc = lib().oracle_efficiency_run(len(dims), _dims(dims), law, lam, seed, rounds, fired.ctypes.data,
+                                     t.ctypes.data if want_times else None)
+    assert rc == 0
+    return (fired, t) if want_times else fired

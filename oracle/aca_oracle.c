@@ -595,3 +595,59 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
     free(s); free(unk); free(t); free(n); free(gid); free(nb); free(heap);
     return 0;
 }
+
+/* ---------------------------------------------------------------- time-only efficiency model
+ * for an Ising model next_t is independent of the states, so whether a
+ * cell passes the test of fig:s1c1pe step 2 depends on the local times only. One iteration:
+ * every cell whose (t, c) is below every neighbour's (t', c') (P6 order) increments its time;
+ * all tests see the times of the previous iteration (synchronous). fired_per_round[r] = N0
+ * of iteration r; the efficiency of the iteration is N0/N.
+ * Draws: initial t(c) = Delta of Philox ctr (0, c, 0, TAG_INIT = 1) (P5); the increment of
+ * iteration r uses ctr (r, c_lo, c_hi, TAG_EFF = 2) (a cell fires at most once per iteration).
+ * ndim 1 (n-circle), 2 (torus), 3 (periodic cube); laws as P3L. Plain loops, test
+ * infrastructure only. Returns 0, or -1 on bad arguments. */
+int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
+                          uint64_t* fired_per_round, uint64_t* t_out) {
+    if (ndim < 1 || ndim > 3 || law < 0 || law > 2 || !(lambda > 0) || rounds < 0) return -1;
+    int64_t d[3] = {1, 1, 1}, N = 1;
+    for (int a = 0; a < ndim; a++) { if (dims[a] < 2) return -1; d[a] = dims[a]; N *= dims[a]; }
+    uint64_t inv = oracle_inv_lambda(lambda);
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint64_t* t = (uint64_t*)malloc((size_t)N * 8);
+    unsigned char* fire = (unsigned char*)malloc((size_t)N);
+    if (!t || !fire) { free(t); free(fire); return -1; }
+    for (int64_t c = 0; c < N; c++) {
+        uint32_t ctr[4] = {0, (uint32_t)((uint64_t)c & 0xffffffffu), (uint32_t)((uint64_t)c >> 32), 1u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        t[c] = oracle_delta_law(w[1], w[2], inv, 0, law);
+    }
+    for (int64_t r = 0; r < rounds; r++) {
+        uint64_t n0 = 0;
+        for (int64_t c = 0; c < N; c++) {          /* test: all against the same times */
+            int64_t x = c % d[0], y = (c / d[0]) % d[1], z = c / (d[0] * d[1]);
+            int ok = 1;
+            for (int a = 0; a < ndim && ok; a++) {
+                for (int s = -1; s <= 1 && ok; s += 2) {
+                    int64_t xx = x, yy = y, zz = z;
+                    if (a == 0) xx = (x + s + d[0]) % d[0];
+                    if (a == 1) yy = (y + s + d[1]) % d[1];
+                    if (a == 2) zz = (z + s + d[2]) % d[2];
+                    int64_t nb = (zz * d[1] + yy) * d[0] + xx;
+                    if (!(t[c] < t[nb] || (t[c] == t[nb] && c < nb))) ok = 0;
+                }
+            }
+            fire[c] = (unsigned char)ok;
+            n0 += (uint64_t)ok;
+        }
+        for (int64_t c = 0; c < N; c++) {          /* commit */
+            if (!fire[c]) continue;
+            uint32_t ctr[4] = {(uint32_t)r, (uint32_t)((uint64_t)c & 0xffffffffu), (uint32_t)((uint64_t)c >> 32), 2u}, w[4];
+            oracle_philox4x32_10(ctr, key, w);
+            t[c] += oracle_delta_law(w[1], w[2], inv, 0, law);
+        }
+        if (fired_per_round) fired_per_round[r] = n0;
+    }
+    if (t_out) memcpy(t_out, t, (size_t)N * 8);
+    free(t); free(fire);
+    return 0;
+}

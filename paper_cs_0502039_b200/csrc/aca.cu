@@ -17,6 +17,7 @@
 
 #include "../../include/aca.h"
 #include "aca_kernels.cuh"
+#include "aca_eff.cuh"
 #include "nlog_tables.cuh"
 
 using namespace aca;
@@ -122,7 +123,7 @@ struct aca_sim {
     unsigned long long thr[14] = {};
     unsigned long long thm[98] = {};   // a10 early-rejection table (see commit_loop)
     int bulk = 1;
-    int defer_tail = 1;
+    int defer_tail = 0;            // ablation only: deferring costs arrivals per sweep
     unsigned long long thr_init = 0;
     unsigned long long max_delta = 0;
     uint64_t T_last = 0;
@@ -251,12 +252,13 @@ struct TileKey {
       (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBW, false, false, false, true>,                   \
       (void*)tile_kernel<ND, TX, TY, TZ, NT, true>},                                                 \
      {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
-      tma_smem(ND, TX, TY, TZ, NT, 1), tma_smem(ND, TX, TY, TZ, NT, 1, true), tile_smem(ND, TX, TY, TZ, NT)}, \
+      tma_smem(ND, TX, TY, TZ, NT, 1, false, true), tma_smem(ND, TX, TY, TZ, NT, 1, true),              \
+      tile_smem(ND, TX, TY, TZ, NT)},                                                                \
      {true, false, true, true, true, false},                                                         \
      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 64, 1, 256, 5, 2, 3, 4),
+    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 64, 1, 256, 4, 2, 3, 4),
     TK(2, 128, 64, 1, 512, 1, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8, 8), TK(3, 16, 16, 16, 256, 2, 1, 2, 2),
     TK(3, 32, 16, 8, 256, 2, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
 };
@@ -1140,5 +1142,84 @@ int aca_selftest_nlog(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* delt
     CK(cudaMemcpy(delta, dd, n * 8, cudaMemcpyDeviceToHost));
     cudaFree(dx); cudaFree(dq); cudaFree(dd); cudaFree(dlr);
     return ACA_OK;
+}
+
+// ---------------------------------------------------------------- time-only efficiency model
+int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
+                       uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds) {
+    if (ndim < 1 || ndim > 3 || !dims) return fail(ACA_EINVAL, "ndim must be 1, 2 or 3");
+    if (law < 0 || law > 2) return fail(ACA_EINVAL, "law must be 0, 1 or 2");
+    if (!(lambda > 0) || !std::isfinite(lambda)) return fail(ACA_EINVAL, "lambda must be > 0");
+    if (rounds < 0 || rounds > (int64_t)1 << 31) return fail(ACA_EINVAL, "rounds out of range");
+    if (rounds > 0 && !fired_per_round) return fail(ACA_EINVAL, "null fired_per_round");
+    int64_t N = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (dims[a] < 2) return fail(ACA_EINVAL, "every dimension must be >= 2");
+        N *= dims[a];
+        if (N > (int64_t)1 << 34) return fail(ACA_EINVAL, "lattice too large");
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
+    if (device >= 0) CK(cudaSetDevice(device));
+    EffParams P{};
+    P.ndim = ndim;
+    P.nx = dims[0]; P.ny = ndim >= 2 ? dims[1] : 1; P.nz = ndim == 3 ? dims[2] : 1; P.N = N;
+    philox_round_keys((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), P.rk);
+    P.inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
+    P.law = law;
+    unsigned long long *a = nullptr, *b = nullptr, *fired = nullptr, *dlr = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto cleanup = [&]() {
+        if (st) cudaStreamSynchronize(st);
+        cudaFree(a); cudaFree(b); cudaFree(fired); cudaFree(dlr);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (st) cudaStreamDestroy(st);
+    };
+    if (cudaMalloc(&a, (size_t)N * 8) != cudaSuccess || cudaMalloc(&b, (size_t)N * 8) != cudaSuccess ||
+        cudaMalloc(&fired, (size_t)std::max<int64_t>(rounds, 1) * 8) != cudaSuccess ||
+        cudaMalloc(&dlr, sizeof(ACA_NLOG_LR)) != cudaSuccess) {
+        cleanup();
+        return fail(ACA_ENOMEM, "device allocation failed (%lld cells)", (long long)N);
+    }
+    int rc = ACA_OK;
+    do {
+        if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(ACA_ECUDA, "stream"); break; }
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaMemcpyAsync(dlr, ACA_NLOG_LR, sizeof(ACA_NLOG_LR), cudaMemcpyHostToDevice, st);
+        cudaMemsetAsync(fired, 0, (size_t)std::max<int64_t>(rounds, 1) * 8, st);
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device >= 0 ? device : 0);
+        const long long want = (N + 255) / 256;
+        const unsigned grid = (unsigned)std::min<long long>(want, (long long)nsm * 8);
+        eff_init_kernel<<<grid, 256, 0, st>>>(a, P, dlr);
+        cudaEventRecord(e0, st);
+        for (int64_t r = 0; r < rounds; ++r) {
+            const unsigned long long* tin = (r & 1) ? b : a;
+            unsigned long long* tout = (r & 1) ? a : b;
+            if (ndim == 1) eff_round_kernel<1><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+            else if (ndim == 2) eff_round_kernel<2><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+            else eff_round_kernel<3><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+        }
+        cudaEventRecord(e1, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+            rc = fail(ACA_ECUDA, "efficiency kernels failed");
+            break;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (gpu_seconds) *gpu_seconds = ms * 1e-3;
+        if (rounds > 0 && cudaMemcpy(fired_per_round, fired, (size_t)rounds * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            rc = fail(ACA_ECUDA, "copy counts");
+            break;
+        }
+        if (t_out && cudaMemcpy(t_out, (rounds & 1) ? b : a, (size_t)N * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            rc = fail(ACA_ECUDA, "copy times");
+            break;
+        }
+    } while (0);
+    cleanup();
+    return rc;
 }
 }  // extern "C"

@@ -1,0 +1,89 @@
+// aca_eff.cuh — time-only efficiency model of PAPER.md:1355-1442 on the GPU.
+//
+// For an Ising model next_t does not depend on the states, so whether a
+// cell passes the test of fig:s1c1pe step 2 is decided by the local times alone. One
+// iteration: every cell whose (t, c) is below every neighbour's (P6 order) draws its next
+// increment; all tests see the previous iteration's times (ping-pong buffers). N0 per
+// iteration is accumulated on the device; N0/N is the iteration's efficiency (PAPER.md:
+// 1338-1353). Draw of iteration r: Philox ctr (r, c_lo, c_hi, TAG_EFF = 2); initial times from
+// the P5 draw (0, c, 0, TAG_INIT = 1); laws as P3L. ndim 1 (n-circle), 2 (torus), 3.
+//
+// Bound: HBM streaming — per cell and iteration one 8-byte read (the neighbours' reads hit
+// L1/L2) and one 8-byte write.
+#pragma once
+#include "aca_prim.cuh"
+#include "nlog_tables.cuh"
+
+namespace aca {
+
+struct EffParams {
+    int ndim;
+    long long nx, ny, nz, N;
+    uint32_t rk[20];
+    unsigned long long inv_lambda;
+    int law;
+};
+
+__global__ void __launch_bounds__(256) eff_init_kernel(unsigned long long* __restrict__ t, const EffParams P,
+                                                       const unsigned long long* __restrict__ lr_g) {
+    __shared__ unsigned long long lr[512];
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    __syncthreads();
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < P.N; c += (long long)gridDim.x * blockDim.x) {
+        const u32x4 r = philox4x32_10_rk(0u, (uint32_t)c, (uint32_t)((unsigned long long)c >> 32), 1u, P.rk);
+        t[c] = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, 0, P.law);
+    }
+}
+
+__device__ __forceinline__ bool lex_below(unsigned long long t, long long c, unsigned long long tn, long long n) {
+    return t < tn || (t == tn && c < n);
+}
+
+template <int NDIM>
+__global__ void __launch_bounds__(256) eff_round_kernel(const unsigned long long* __restrict__ tin,
+                                                        unsigned long long* __restrict__ tout, const EffParams P,
+                                                        const unsigned long long* __restrict__ lr_g, uint32_t round,
+                                                        unsigned long long* __restrict__ fired) {
+    __shared__ unsigned long long lr[512];
+    __shared__ unsigned int red[8];
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    __syncthreads();
+    unsigned int n0 = 0;
+    const long long nxy = P.nx * P.ny;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < P.N; c += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long t = tin[c];
+        const long long x = c % P.nx;
+        const long long row = c - x;
+        const long long xm = row + (x == 0 ? P.nx - 1 : x - 1), xp = row + (x == P.nx - 1 ? 0 : x + 1);
+        bool ok = lex_below(t, c, __ldg(tin + xm), xm) && lex_below(t, c, __ldg(tin + xp), xp);
+        if (NDIM >= 2) {
+            const long long y = (c / P.nx) % P.ny;
+            const long long ym = c + ((y == 0 ? P.ny - 1 : y - 1) - y) * P.nx;
+            const long long yp = c + ((y == P.ny - 1 ? 0 : y + 1) - y) * P.nx;
+            ok = ok && lex_below(t, c, __ldg(tin + ym), ym) && lex_below(t, c, __ldg(tin + yp), yp);
+        }
+        if (NDIM == 3) {
+            const long long z = c / nxy;
+            const long long zm = c + ((z == 0 ? P.nz - 1 : z - 1) - z) * nxy;
+            const long long zp = c + ((z == P.nz - 1 ? 0 : z + 1) - z) * nxy;
+            ok = ok && lex_below(t, c, __ldg(tin + zm), zm) && lex_below(t, c, __ldg(tin + zp), zp);
+        }
+        unsigned long long tn = t;
+        if (ok) {
+            const u32x4 r = philox4x32_10_rk(round, (uint32_t)c, (uint32_t)((unsigned long long)c >> 32), 2u, P.rk);
+            tn = t + delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, 0, P.law);
+            ++n0;
+        }
+        tout[c] = tn;
+    }
+    for (int o = 16; o > 0; o >>= 1) n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = n0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        atomicAdd(fired + round, s);
+    }
+}
+
+}  // namespace aca

@@ -1004,7 +1004,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     unsigned long long* red = thm + 112;                            // NW
     unsigned long long* bar = red + NW;                             // 2
     unsigned short* Q = (unsigned short*)(bar + 2);                 // fire queue(s), see tma_smem_bytes
-    unsigned int* claim = (unsigned int*)(Q + ((tma_queue_entries(NCELL, NT, WL, EARLY) + 7) & ~(size_t)7));
+    unsigned int* claim = (unsigned int*)(Q + ((tma_queue_entries(NCELL, NT, WL, EARLY || REG) + 7) & ~(size_t)7));
     unsigned int* qcnt = claim + 2 * (NCELL / 32);                  // WL: 4 queue counters
 
     const Geo& g = P.g;

@@ -1,0 +1,45 @@
+"""GPU time-only efficiency model through the C ABI: bit-identical to the
+oracle's iterations (every N0 and every final time) on small arrays, and at sizes far beyond
+the oracle's reach the steady-state efficiency equals the values the paper prints
+(tests/golden/paper_efficiency.txt)."""
+import os
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("dims", [(2,), (37,), (1000,), (2, 2), (13, 7), (64, 48), (2, 2, 2), (12, 10, 8)])
+@pytest.mark.parametrize("law", [0, 1, 2])
+def test_efficiency_bit_identical(aca, oracle_mod, dims, law):
+    rounds = 150
+    f_g, t_g, _ = aca.aca_efficiency_run(dims, rounds, law=law, seed=31, want_times=True)
+    f_o, t_o = oracle_mod.efficiency_run(dims, rounds, law=law, seed=31, want_times=True)
+    assert np.array_equal(f_g, f_o)
+    assert np.array_equal(t_g, t_o)
+
+
+def _golden():
+    rows = []
+    for line in open(os.path.join(HERE, "golden", "paper_efficiency.txt")):
+        if not line.startswith("#") and line.strip():
+            nd, law, v, tol = line.split()
+            rows.append((int(nd), int(law), float(v), float(tol)))
+    return rows
+
+
+@pytest.mark.parametrize("ndim,law,value,tol", _golden())
+def test_efficiency_large_arrays_match_paper(aca, ndim, law, value, tol):
+    """1-D n = 2^24, 2-D 4096 x 4096: 400 iterations, the last 250 averaged."""
+    dims = (1 << 24,) if ndim == 1 else (4096, 4096)
+    fired, _ = aca.aca_efficiency_run(dims, 400, law=law, seed=101 + law)
+    eff = fired[150:].astype(np.float64) / np.prod(dims)
+    assert abs(eff.mean() - value) < tol, (eff.mean(), value)
+
+
+def test_efficiency_rejects_bad_arguments(aca):
+    for dims, law in (((1,), 0), ((4, 4), 3)):
+        with pytest.raises(aca.AcaError):
+            aca.aca_efficiency_run(dims, 5, law=law)
