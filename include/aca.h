@@ -156,6 +156,20 @@ int aca_nccl_unique_id(void* out128);
 /* Number of cells of the handle (rank-local for multi-process handles). */
 int64_t aca_num_cells(const aca_sim* s);
 
+/* ---- Output frames (fig:genout) ----
+ * Continue the simulation and capture the state of every cell at the frame times
+ * K dt, K = K0 .. K0 + count - 1 (the state at time t includes an arrival at exactly t,
+ * PAPER.md:355-362). Frames are filled on the device while the cells advance: each fired
+ * arrival writes the frames its new state covers. B frames (1..16) are buffered, so the
+ * local times of the cells never spread by more than about B dt (the bounded-lag window of
+ * PAPER.md:1295-1318); after each window the frames are copied to `out`. On return every
+ * arrival at or before (K0 + count - 1) dt has been processed (as aca_run_until_q32 of that
+ * time + 1 unit). out: count frames of ceil(N/8) bytes, caller-owned; frame k bit i (byte i/8,
+ * bit i%8) = 1 iff cell i (row-major; rank-local for multi-process handles) had s = +1.
+ * Errors: ACA_EINVAL (null, dt <= 0, count < 1, B outside 1..16), ACA_ESTATE (K0 dt is
+ * before the time already simulated), ACA_ERANGE (frame times overflow), run_until errors. */
+int aca_run_frames(aca_sim* s, double dt, int64_t K0, int64_t count, int B, uint8_t* out);
+
 /* ---- Time-only efficiency model ----
  * Synchronous iterations of fig:s1c1pe on the local times only (valid because next_t does
  * not depend on the states for the Ising model): each iteration every

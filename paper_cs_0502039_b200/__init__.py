@@ -23,7 +23,7 @@ ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: 
 EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
-           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run"]
+           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames"]
 POISSON, UNIFORM, ROOT8 = 0, 1, 2   # asynchrony laws (aca_options.law)
 
 
@@ -99,6 +99,7 @@ def lib():
     L.aca_num_cells.restype = ctypes.c_int64
     L.aca_selftest_philox.argtypes = [ctypes.c_uint64, vp, vp, vp, vp]
     L.aca_selftest_nlog.argtypes = [ctypes.c_uint64, vp, vp, vp, ctypes.c_uint64, ctypes.c_int]
+    L.aca_run_frames.argtypes = [vp, ctypes.c_double, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]
     L.aca_efficiency_run.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
                                      ctypes.c_int64, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     L.aca_selftest_law.argtypes = [ctypes.c_uint64, vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, vp, vp]
@@ -258,6 +259,16 @@ def aca_selftest_law(X, law, lam=1.0, tie_bits=0):
     return u, d
 
 
+def aca_run_frames(p, dt, K0, count, B=4):
+    """Frames (fig:genout): int8[count, N] of the states at times K dt, K = K0..K0+count-1."""
+    n = int(lib().aca_num_cells(p))
+    fb = (n + 7) // 8
+    bits = np.zeros(count * fb, np.uint8)
+    _check(lib().aca_run_frames(p, float(dt), int(K0), int(count), int(B), _ptr(bits)))
+    pm = np.unpackbits(bits.reshape(count, fb), axis=1, bitorder="little")[:, :n]
+    return np.where(pm > 0, 1, -1).astype(np.int8)
+
+
 def aca_efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False, device=-1):
     """Time-only efficiency model on the GPU: N0 per synchronous
     iteration (uint64[rounds]), the final times if asked, and the device seconds."""
@@ -330,6 +341,11 @@ class Sim:
 
     def set_state(self, spins, times, counters):
         aca_set_state(self._p, spins, times, counters)
+
+    def frames(self, dt, K0, count, B=4):
+        f = aca_run_frames(self._p, dt, K0, count, B)
+        n, full = aca_num_cells(self._p), int(np.prod(self.dims))
+        return f.reshape((count,) + self.dims[::-1]) if n == full else f
 
     def set_spins(self, spins):
         aca_set_spins(self._p, spins)

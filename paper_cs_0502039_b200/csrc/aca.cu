@@ -160,6 +160,9 @@ struct aca_sim {
     size_t scratch_bytes = 0;
     StatAcc* d_stat = nullptr;
     StatAcc* h_stat = nullptr;
+    FrameParams fr{};              // output frames of the current aca_run_frames chunk (nb = 0: off)
+    unsigned int* frame_ring = nullptr;
+    size_t frame_ring_bytes = 0;
 };
 
 namespace {
@@ -301,6 +304,7 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.tiles_y = sh.tiles_y;
     P.tiles_z = sh.tiles_z;
     P.phase = -1;
+    P.fr = S->fr;
     {   // parity of the shard's first tile row in global tile coordinates (colouring only)
         const int t0 = sh.g.ndim == 2 ? sh.g.y0 / S->tile[1] : sh.g.z0 / S->tile[2];
         P.row_par0 = t0 & 1;
@@ -524,6 +528,7 @@ void aca_destroy(aca_sim* S) {
     cudaFree(S->d_lr);
     cudaFree(S->scratch);
     cudaFree(S->d_stat);
+    cudaFree(S->frame_ring);
     if (S->h_ctl) cudaFreeHost(S->h_ctl);
     if (S->h_stat) cudaFreeHost(S->h_stat);
     if (S->ev0) cudaEventDestroy(S->ev0);
@@ -1167,6 +1172,10 @@ int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, ui
     philox_round_keys((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), P.rk);
     P.inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
     P.law = law;
+    const bool small = N < ((int64_t)1 << 32);   // 32-bit indices: Lemire division, compacted kernel
+    auto recip = [](unsigned long long d) { return (unsigned long long)(~0ull / d) + 1ull; };   // ceil(2^64/d), d >= 2
+    P.mx = recip((unsigned long long)P.nx);
+    P.my = recip((unsigned long long)P.ny < 2 ? 2ull : (unsigned long long)P.ny);
     unsigned long long *a = nullptr, *b = nullptr, *fired = nullptr, *dlr = nullptr;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1198,7 +1207,11 @@ int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, ui
         for (int64_t r = 0; r < rounds; ++r) {
             const unsigned long long* tin = (r & 1) ? b : a;
             unsigned long long* tout = (r & 1) ? a : b;
-            if (ndim == 1) eff_round_kernel<1><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+            if (small) {
+                if (ndim == 1) eff_round_kernel_c<1><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+                else if (ndim == 2) eff_round_kernel_c<2><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+                else eff_round_kernel_c<3><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+            } else if (ndim == 1) eff_round_kernel<1><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
             else if (ndim == 2) eff_round_kernel<2><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
             else eff_round_kernel<3><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
         }
@@ -1220,6 +1233,65 @@ int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, ui
         }
     } while (0);
     cleanup();
+    return rc;
+}
+
+// ---------------------------------------------------------------- output frames (fig:genout)
+int aca_run_frames(aca_sim* S, double dt, int64_t K0, int64_t count, int B, uint8_t* out) {
+    if (!S || !out) return fail(ACA_EINVAL, "null argument");
+    if (!(dt > 0) || !std::isfinite(dt)) return fail(ACA_EINVAL, "dt must be > 0");
+    if (K0 < 0 || count < 1) return fail(ACA_EINVAL, "K0 >= 0 and count >= 1 required");
+    if (B < 1 || B > 16) return fail(ACA_EINVAL, "B must be in [1, 16]");
+    const double dq = std::floor(dt * 4294967296.0 + 0.5);
+    if (dq < 1 || dq * (double)(K0 + count) >= 1.8e19) return fail(ACA_ERANGE, "frame times overflow");
+    const unsigned long long dtq = (unsigned long long)dq;
+    if (S->T_last > (unsigned long long)K0 * dtq + 1ull)
+        return fail(ACA_ESTATE, "frame K0 lies before the time already simulated");
+    CK(cudaSetDevice(S->device));
+    size_t nloc = 0;
+    for (auto& sh : S->shards) nloc += sh.n;
+    const size_t wpf = (nloc + 31) / 32;
+    const size_t need = (size_t)B * wpf * 4;
+    if (S->frame_ring_bytes < need) {
+        cudaFree(S->frame_ring);
+        S->frame_ring = nullptr;
+        S->frame_ring_bytes = 0;
+        CK(cudaMalloc(&S->frame_ring, need));
+        S->frame_ring_bytes = need;
+    }
+    const size_t fbytes = (nloc + 7) / 8;
+    const long long base = S->world > 1 ? (long long)(S->shards[0].g.ndim == 2
+                                                          ? (long long)S->shards[0].g.y0 * S->shards[0].g.nx
+                                                          : (long long)S->shards[0].g.z0 * S->shards[0].g.ny * S->shards[0].g.nx)
+                                        : 0;
+    int rc = ACA_OK;
+    for (int64_t K = K0; K < K0 + count && rc == ACA_OK; ) {
+        const int nb = (int)std::min<int64_t>(B, K0 + count - K);
+        CK(cudaMemsetAsync(S->frame_ring, 0, (size_t)nb * wpf * 4, S->stream));
+        S->fr.bits = S->frame_ring;
+        S->fr.t0 = (unsigned long long)K * dtq;
+        S->fr.dt = dtq;
+        S->fr.wpf = wpf;
+        S->fr.base = base;
+        S->fr.nb = nb;
+        drop_graph(S);   // kernel parameters changed
+        unsigned long long off = 0;
+        for (auto& sh : S->shards) {
+            frame_prefill_kernel<<<592, 256, 0, S->stream>>>(sh.words, sh.g, S->fr, (unsigned long long)sh.n, off);
+            CK(cudaGetLastError());
+            off += sh.n;
+        }
+        rc = aca_run_until_q32(S, (unsigned long long)(K + nb - 1) * dtq + 1ull);
+        if (rc == ACA_OK) {
+            for (int k = 0; k < nb; ++k)
+                CK(cudaMemcpyAsync(out + (size_t)(K - K0 + k) * fbytes, S->frame_ring + (size_t)k * wpf, fbytes,
+                                   cudaMemcpyDeviceToHost, S->stream));
+            CK(cudaStreamSynchronize(S->stream));
+        }
+        K += nb;
+    }
+    S->fr = FrameParams{};
+    drop_graph(S);
     return rc;
 }
 }  // extern "C"

@@ -19,6 +19,7 @@ namespace aca {
 struct EffParams {
     int ndim;
     long long nx, ny, nz, N;
+    unsigned long long mx, my;           // Lemire reciprocals ceil(2^64 / nx), ceil(2^64 / ny) (N < 2^32)
     uint32_t rk[20];
     unsigned long long inv_lambda;
     int law;
@@ -82,6 +83,103 @@ __global__ void __launch_bounds__(256) eff_round_kernel(const unsigned long long
     if (threadIdx.x == 0) {
         unsigned long long s = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        atomicAdd(fired + round, s);
+    }
+}
+
+// n / d for n, d < 2^32 with M = ceil(2^64 / d) (Lemire, Kaser, Kurz 2019: exact for 32-bit n).
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, unsigned long long M) { return (uint32_t)__umul64hi(M, n); }
+
+// Compacted iteration (N < 2^32): each warp takes chunks of 256 consecutive cells; every lane
+// tests 8 cells (coalesced), copies the non-firing ones to the output, queues the firing ones
+// (about 12 % in 2-D) in a per-warp list and the whole warp then draws their increments
+// together (one Philox + law per lane instead of a divergent branch in most warps).
+template <int NDIM>
+__global__ void __launch_bounds__(256) eff_round_kernel_c(const unsigned long long* __restrict__ tin,
+                                                          unsigned long long* __restrict__ tout, const EffParams P,
+                                                          const unsigned long long* __restrict__ lr_g, uint32_t round,
+                                                          unsigned long long* __restrict__ fired) {
+    constexpr int J = 8;
+    __shared__ unsigned long long lr[512];
+    __shared__ unsigned int red[8];
+    __shared__ uint32_t qc[8][32 * J];
+    __shared__ unsigned long long qt[8][32 * J];
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nx = (uint32_t)P.nx, ny = (uint32_t)P.ny, nz = (uint32_t)P.nz, N = (uint32_t)P.N;
+    const uint32_t nxy = nx * ny;
+    const uint32_t nchunk = (N + 32 * J - 1) / (32 * J);
+    unsigned int n0 = 0;
+    for (uint32_t ch = blockIdx.x * 8 + warp; ch < nchunk; ch += gridDim.x * 8) {
+        uint32_t fm = 0;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const uint32_t c = ch * (32 * J) + lane + 32 * j;
+            if (c >= N) continue;
+            const unsigned long long t = tin[c];
+            const uint32_t q1 = fdiv(c, P.mx);             // row index
+            const uint32_t x = c - q1 * nx, row = c - x;
+            const uint32_t xm = row + (x == 0 ? nx - 1 : x - 1), xp = row + (x == nx - 1 ? 0 : x + 1);
+            bool ok = lex_below(t, c, __ldg(tin + xm), xm) && lex_below(t, c, __ldg(tin + xp), xp);
+            if (NDIM >= 2) {
+                const uint32_t q2 = fdiv(q1, P.my);         // plane index
+                const uint32_t y = q1 - q2 * ny;
+                const uint32_t ym = y == 0 ? c + (ny - 1) * nx : c - nx;
+                const uint32_t yp = y == ny - 1 ? c - (ny - 1) * nx : c + nx;
+                ok = ok && lex_below(t, c, __ldg(tin + ym), ym) && lex_below(t, c, __ldg(tin + yp), yp);
+                if (NDIM == 3) {
+                    const uint32_t z = q2;
+                    const uint32_t zm = z == 0 ? c + (nz - 1) * nxy : c - nxy;
+                    const uint32_t zp = z == nz - 1 ? c - (nz - 1) * nxy : c + nxy;
+                    ok = ok && lex_below(t, c, __ldg(tin + zm), zm) && lex_below(t, c, __ldg(tin + zp), zp);
+                }
+            }
+            if (ok) {
+                fm |= 1u << j;
+                qt[warp][lane + 32 * j] = t;   // the firing cell's time, for the draw phase
+            } else {
+                tout[c] = t;
+            }
+        }
+        // compaction of the firing cells of this chunk
+        const int mine = __popc(fm);
+        int incl = mine;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += v;
+        }
+        const int cnt = __shfl_sync(0xffffffffu, incl, 31);
+        int pos = incl - mine;
+        unsigned long long tl[J];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < J; ++j) tl[j] = qt[warp][lane + 32 * j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            if ((fm >> j) & 1u) {
+                qc[warp][pos] = ch * (32 * J) + lane + 32 * j;
+                qt[warp][pos] = tl[j];
+                ++pos;
+            }
+        }
+        __syncwarp();
+        for (int i = lane; i < cnt; i += 32) {
+            const uint32_t c = qc[warp][i];
+            const u32x4 r = philox4x32_10_rk(round, c, 0u, 2u, P.rk);
+            tout[c] = qt[warp][i] + delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, 0, P.law);
+        }
+        __syncwarp();
+        n0 += (lane == 0) ? (unsigned int)cnt : 0u;
+    }
+    for (int o = 16; o > 0; o >>= 1) n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+    if (lane == 0) red[warp] = n0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < 8; ++w) s += red[w];
         atomicAdd(fired + round, s);
     }
 }

@@ -59,6 +59,31 @@ __device__ __host__ __forceinline__ unsigned long long w_pack(unsigned long long
     return (t << g.TSH) | (rank << (g.NB + 1)) | (n << 1) | sb;
 }
 
+// Output frames (fig:genout): the state of every cell at the frame times
+// tau_k = t0 + k dt, k = 0..nb-1, one bit per cell (+1 = 1) in frame k of `bits` (words of
+// `wpf` u32 each). A fired arrival at t_p (new spin s', next arrival t_n) owns the frames with
+// t_p <= tau_k < t_n: s' is the cell's state on [t_p, t_n) ("at time t the value is already
+// new"). Frames before the first arrival of a chunk are pre-filled on the
+// host side (frame_prefill_kernel).
+struct FrameParams {
+    unsigned int* bits;
+    unsigned long long t0, dt;           // Q32
+    unsigned long long wpf;              // u32 words per frame
+    long long base;                      // cell id of bit 0 (rank-local frames)
+    int nb;                              // frames in the window (0 = off)
+};
+
+__device__ __forceinline__ void frame_write(const FrameParams& F, unsigned long long tp, unsigned long long tn,
+                                            unsigned long long c, uint32_t splus) {
+    if (F.nb == 0 || !splus || tn <= F.t0) return;
+    const unsigned long long b = c - (unsigned long long)F.base;
+    unsigned long long tau = F.t0;
+    for (int k = 0; k < F.nb; ++k, tau += F.dt) {
+        if (tau >= tn) break;
+        if (tau >= tp) atomicOr(F.bits + (size_t)k * F.wpf + (b >> 5), 1u << (b & 31));
+    }
+}
+
 struct KParams {
     Geo g;
     unsigned long long* words;
@@ -82,6 +107,7 @@ struct KParams {
     int row_par0;                        // parity of the shard's first tile row (global colouring)
     unsigned long long thr[14];          // P4 table
     unsigned long long thm[98];          // a10 table, see commit_loop (2 (Z+1)^2 entries)
+    FrameParams fr;                      // output frames (off unless aca_run_frames)
 };
 
 __device__ __forceinline__ int wrapi(int v, int n) {
@@ -162,7 +188,7 @@ struct FireOut { unsigned long long wnew; uint32_t flip; unsigned long long h; b
 __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int z, unsigned long long c,
                                         const Geo& g, const unsigned long long* thr, const unsigned long long* lr,
                                         const uint32_t* rk, unsigned long long inv_lambda, int tie_bits,
-                                        int do_hash, Ctl* ctl, int law = 0) {
+                                        int do_hash, Ctl* ctl, int law = 0, const FrameParams* fr = nullptr) {
     FireOut o;
     const uint32_t k = w_count(w, g);
     if (k == (uint32_t)((1ull << g.NB) - 1ull)) {
@@ -177,6 +203,10 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
     const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
     o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;   // t += d, n += 1, s ^= flip
     o.flip = flip;
+    if (fr && fr->nb) {
+        const unsigned long long tp = w >> g.TSH;
+        frame_write(*fr, tp, tp + d, c, sb ^ flip);
+    }
     o.h = 0;
     o.ok = true;
     if (do_hash) {
@@ -309,7 +339,7 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
             }
             if (!ok) continue;
             const FireOut o = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
             if (!o.ok) continue;
             hacc += o.h;
             flips += o.flip;
@@ -435,6 +465,10 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
         if (P.do_hash) {
             const unsigned long long t = w >> g.TSH;
             st.hacc += mix64(t ^ rotl64(cid, 20) ^ rotl64((unsigned long long)n, 44) ^ (unsigned long long)(sb ^ flip));
+        }
+        if (P.fr.nb) {
+            const unsigned long long tp = w >> g.TSH;
+            frame_write(P.fr, tp, tp + d, cid, sb ^ flip);
         }
         w = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;
         VS[s] = w;
@@ -600,7 +634,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
             const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
             if (!f.ok) continue;
             VS[s] = f.wnew;
             st.hacc += f.h;
@@ -744,7 +778,7 @@ __device__ __forceinline__ unsigned int tile_rounds_reg(const KParams& P, unsign
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
             const FireOut f = fire(wv, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
+                                   P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
             if (!f.ok) continue;
             VS[s] = f.wnew;
             st.hacc += f.h;
@@ -878,7 +912,7 @@ __device__ __forceinline__ unsigned int tile_rounds_wl(const KParams& P, unsigne
                                 (VH[2 * (s + SX)] & 1u);
                 if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
                 const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
-                                       P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law);
+                                       P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
                 if (f.ok) {
                     VS[s] = f.wnew;
                     st.hacc += f.h;
@@ -1192,7 +1226,7 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
             }
             if (!ok) continue;
             const FireOut o = fire(w, ones, Z, (unsigned long long)i, g, thr, lr, P.rk, P.inv_lambda,
-                                   P.tie_bits, P.do_hash, P.ctl, P.law);
+                                   P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
             if (!o.ok) continue;
             hacc += o.h;
             flips += o.flip;
@@ -1254,6 +1288,42 @@ __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const
         const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
         const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
         words[i] = w_pack(t0, rank, 0ull, sb, g);
+    }
+}
+
+// Frame pre-fill at the start of a frame chunk: every arrival before the chunk is at most the
+// previous frame time, so a cell whose pending arrival t is after tau_k held its current spin
+// at tau_k. One thread per 32 cells (one u32 word of every frame; no atomics: the chunk's
+// kernels run after this one).
+__global__ void frame_prefill_kernel(const unsigned long long* __restrict__ words, Geo g, FrameParams F,
+                                     unsigned long long n, unsigned long long base_local) {
+    for (unsigned long long wi = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; wi * 32 < n;
+         wi += (unsigned long long)gridDim.x * blockDim.x) {
+        uint32_t acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0u;
+        for (int j = 0; j < 32; ++j) {
+            const unsigned long long i = wi * 32 + j;
+            if (i >= n) break;
+            const unsigned long long w = words[i];
+            if (!(w & 1ull)) continue;
+            const unsigned long long t = w_time(w, g);
+            unsigned long long tau = F.t0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k, tau += F.dt)
+                if (k < F.nb && tau < t) acc[k] |= 1u << j;
+        }
+        // this shard's cells start at bit base_local (a multiple of 32 when shards are row-aligned)
+        const unsigned long long b = base_local + wi * 32;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            if (k >= F.nb || !acc[k]) continue;
+            if ((b & 31) == 0) atomicOr(F.bits + (size_t)k * F.wpf + (b >> 5), acc[k]);
+            else {   // unaligned shard start: split over two words
+                atomicOr(F.bits + (size_t)k * F.wpf + (b >> 5), acc[k] << (b & 31));
+                atomicOr(F.bits + (size_t)k * F.wpf + (b >> 5) + 1, acc[k] >> (32 - (b & 31)));
+            }
+        }
     }
 }
 
