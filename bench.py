@@ -111,13 +111,16 @@ def peaks():
 
 
 def ncu_traffic(kernel_tag):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    """dram bytes per sweep of the dominant kernel (both checkerboard launches) from the
+    committed ncu --set full summary (profiles/ncu_full_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     if not os.path.exists(p):
         return None
     try:
-        d = json.load(open(p))
-        return d.get(kernel_tag, {}).get("dram_bytes_per_launch")
+        d = json.load(open(p)).get(kernel_tag, {})
+        if "dram_bytes_per_sweep" in d:
+            return d["dram_bytes_per_sweep"]
+        return None
     except Exception:
         return None
 
@@ -268,18 +271,23 @@ def main():
         arrivals = adist.reduce_sum_int(arrivals)
     value = arrivals / elapsed
 
-    # roofline of the dominant kernel (the tile kernel): algorithmic bytes / mean launch time
+    # roofline of the dominant kernel (the tile kernel): algorithmic bytes / mean time. `launches`
+    # (ctl) counts outer rounds = sweeps; with checkerboard sweeps a sweep is two kernel
+    # launches over half the tiles each, so bytes/sweep over sweep time = bytes/launch over
+    # launch time.
     peak, peak_src = peaks()
     bpc = algorithmic_bytes_per_cell(ndim, tile)
-    mean_launch = ks / max(1, launches)
-    achieved = (n_local * bpc / mean_launch) / 1e9 if mean_launch > 0 else None
+    mean_sweep = ks / max(1, launches)
+    kl_per_sweep = (kl / max(1, launches * 1.0)) if launches else 1.0
+    achieved = (n_local * bpc / mean_sweep) / 1e9 if mean_sweep > 0 else None
     tag = "tile_kernel_%dd" % ndim
     traffic = ncu_traffic(tag)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "kernel": tag, "peak_source": peak_src,
-            "algorithmic_bytes_per_cell_per_launch": bpc, "cells_per_launch": n_local,
-            "mean_launch_ms": mean_launch * 1e3, "launches_per_step": launches / args.steps,
+            "algorithmic_bytes_per_cell_per_sweep": bpc, "cells_per_sweep": n_local,
+            "mean_sweep_ms": mean_sweep * 1e3, "sweeps_per_step": launches / args.steps,
+            "kernel_launches_per_sweep": round(kl_per_sweep, 2),
             "kernel_share_of_step": ks / elapsed if elapsed else None}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -287,13 +295,14 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
                        "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
-                       "tile": list(tile), "rounds_per_launch": args.rounds or 3, "variant": args.variant,
+                       "tile": list(tile), "rounds_per_tile_visit": args.rounds or 4, "variant": args.variant,
+                       "sweep": "checkerboard: 2 kernel launches per outer round (tile colours 0, 1)",
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
                        "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
                        "event_hash": not args.no_hash},
             "roofline": roof,
             "firing_fraction": fired / tested if tested else None,
-            "arrivals_per_cell_per_launch": (fired / launches / n_local) if launches else None,
+            "arrivals_per_cell_per_sweep": (fired / launches / n_local) if launches else None,
             "gpu_launches": int(kl + 2 * args.steps),
             "clocks": clk}
 

@@ -52,7 +52,7 @@ typedef struct {
     uint32_t struct_size;       /* = sizeof(aca_options); checked */
     double init_q;              /* P5: probability that s0(c) = -1 (default 0.5) */
     int32_t tile[3];            /* CTA tile (x, y, z); 0 = default (64x64, 32x16x8) */
-    int32_t rounds_per_launch;  /* R_max in-tile rounds per launch (0 = default 8) */
+    int32_t rounds_per_launch;  /* R_max in-tile rounds per tile visit (0 = default 4) */
     int32_t launches_per_check; /* K launches between host checks of termination (0 = 16) */
     int32_t tie_bits;           /* P3b tie-stress quantisation (0 = off) */
     int32_t sync_rounds;        /* 1: exact fig:s1c1pe two-phase rounds */
@@ -65,10 +65,11 @@ typedef struct {
     int32_t whole_lattice;      /* 1: one CTA holds the whole lattice with periodic
                                    addressing and runs to completion in one launch
                                    (small lattices, config 1); 0 = auto, -1 = never */
-    int32_t variant;            /* tile kernel (ablations): 0 = persistent, double-buffered
-                                   TMA staging, compacted firing (default); 1 = compacted,
-                                   one CTA per tile; 2 = uncompacted; 3 = persistent,
-                                   single-buffered TMA. All give identical results. */
+    int32_t variant;            /* tile kernel (ablations; identical results): 0 = persistent,
+                                   TMA-staged, per-warp compacted firing (default); 1 = one CTA
+                                   per tile, uncompacted; 2 = 0 with double-buffered TMA; 3 =
+                                   register-resident synchronous rounds; 4 = work-list rounds
+                                   (re-test only cells whose neighbourhood changed). */
     int32_t early_reject;       /* 1: a cell may also commit arrivals that are rejected for
                                    every possible state of the neighbours it still waits for
                                    (exact; pays off at low temperature, config 5). 0 = off */

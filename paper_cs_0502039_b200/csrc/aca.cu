@@ -607,7 +607,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->use_nccl = opt.nccl_id != nullptr;   // world 1 + nccl_id: the ring of one (self-exchange)
     S->G = opt.world > 1 ? 1 : opt.shards;
     S->sync = opt.sync_rounds != 0;
-    S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 3;
+    S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 4;   // measured knee with checkerboard sweeps
     S->K = opt.launches_per_check > 0 ? opt.launches_per_check : 16;
     if (const char* e = getenv("ACA_ROUND_MODE")) S->round_mode = atoi(e);
 

@@ -67,6 +67,7 @@ def num(s):
 def main():
     tag, lpath, fpath = sys.argv[1:4]
     ktag = sys.argv[4] if len(sys.argv) > 4 else "tile_kernel_2d"
+    per_sweep = int(sys.argv[5]) if len(sys.argv) > 5 else 2   # kernel launches per sweep (checkerboard: 2)
     d = os.path.join(ROOT, "profiles", tag)
     os.makedirs(d, exist_ok=True)
     L = launches(lpath)
@@ -88,7 +89,9 @@ def main():
         wb = sum(num(c["dram__bytes_write.sum"]) for c in F) / len(F)
         summ = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
         cur = json.load(open(summ)) if os.path.exists(summ) else {}
-        cur[ktag] = {"dram_bytes_per_launch": rb + wb, "dram_read": rb, "dram_write": wb, "source": "profiles/%s" % tag}
+        cur[ktag] = {"dram_bytes_per_launch": rb + wb, "dram_read": rb, "dram_write": wb,
+                     "launches_per_sweep": per_sweep, "dram_bytes_per_sweep": (rb + wb) * per_sweep,
+                     "source": "profiles/%s" % tag}
         json.dump(cur, open(summ, "w"), indent=1)
     print("wrote", d)
 
