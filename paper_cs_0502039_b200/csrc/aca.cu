@@ -305,6 +305,8 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.tiles_z = sh.tiles_z;
     P.phase = -1;
     P.fr = S->fr;
+    P.fast = (S->opt.law == 0 && S->inv_lambda == (1ull << 32) && S->opt.tie_bits == 0 && S->fr.nb == 0 &&
+              S->N < ((int64_t)1 << 32)) ? 1 : 0;
     {   // parity of the shard's first tile row in global tile coordinates (colouring only)
         const int t0 = sh.g.ndim == 2 ? sh.g.y0 / S->tile[1] : sh.g.z0 / S->tile[2];
         P.row_par0 = t0 & 1;

@@ -108,6 +108,7 @@ struct KParams {
     unsigned long long thr[14];          // P4 table
     unsigned long long thm[98];          // a10 table, see commit_loop (2 (Z+1)^2 entries)
     FrameParams fr;                      // output frames (off unless aca_run_frames)
+    int fast;                            // fire_fast applies (law 0, lambda 1, no ties, no frames, N < 2^32)
 };
 
 __device__ __forceinline__ int wrapi(int v, int n) {
@@ -253,6 +254,38 @@ __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long activ
 __device__ __forceinline__ unsigned long long cell_id(const Geo& g, int gx, int gy, int gz) {
     return g.ndim == 2 ? (unsigned long long)(gy + g.y0) * g.nx + gx
                        : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
+}
+
+// 32-bit cell id (N < 2^32; the Philox counter word c_hi is then 0)
+__device__ __forceinline__ uint32_t cell_id32(const Geo& g, int gx, int gy, int gz) {
+    return g.ndim == 2 ? (uint32_t)(gy + g.y0) * (uint32_t)g.nx + (uint32_t)gx
+                       : ((uint32_t)(gz + g.z0) * (uint32_t)g.NY + (uint32_t)gy) * (uint32_t)g.nx + (uint32_t)gx;
+}
+
+// fire() for the common configuration (Poisson law, lambda = 1, tie_bits = 0, no output frames,
+// N < 2^32): the same integers with the general branches compiled out. The caller raises the
+// overflow flag when ok = false.
+__device__ __forceinline__ FireOut fire_fast(unsigned long long w, uint32_t ones, int z, uint32_t c, const Geo& g,
+                                             const unsigned long long* thr, const unsigned long long* lr,
+                                             const uint32_t* rk, int do_hash) {
+    FireOut o;
+    const uint32_t k = w_count(w, g);
+    o.ok = k != (uint32_t)((1ull << g.NB) - 1ull);
+    const uint32_t sb = (uint32_t)(w & 1ull);
+    const uint32_t idx = ones + (uint32_t)(z + 1) * sb;
+    const u32x4 r = philox4x32_10_rk(k, c, 0u, 0u, rk);
+    const uint32_t flip = (unsigned long long)r.x < thr[idx] ? 1u : 0u;
+    uint64_t d = nlog_q32(((uint64_t)r.y << 32) | r.z, lr, ACA_LN2_Q48);
+    d = d < 1ull ? 1ull : d;
+    o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;
+    o.flip = flip;
+    o.h = 0;
+    if (do_hash) {
+        const unsigned long long t = w >> g.TSH;
+        o.h = mix64(t ^ rotl64((unsigned long long)c, 20) ^ rotl64((unsigned long long)k, 44) ^
+                    (unsigned long long)(sb ^ flip));
+    }
+    return o;
 }
 
 // ------------------------------------------------------------------------ uncompacted tile kernel
@@ -516,6 +549,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
         return x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz);
     };
+    uint32_t fl32 = 0, fi32 = 0;   // fast-path flips / fires (folded into st at the end)
     for (int r = 0; r < P.rounds; ++r) {
         uint32_t emask = 0, amask = 0;
         if constexpr (!EARLY) {
@@ -633,6 +667,16 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
+            if (P.fast) {   // uniform: Poisson law, lambda = 1, no tie stress, no frames, N < 2^32
+                const FireOut f = fire_fast(w, ones, Z, cell_id32(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
+                                            P.do_hash);
+                if (!f.ok) { atomicOr(&P.ctl->overflow, 1u); continue; }
+                VS[s] = f.wnew;
+                st.hacc += f.h;
+                fl32 += f.flip;
+                ++fi32;
+                continue;
+            }
             const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
                                    P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
             if (!f.ok) continue;
@@ -652,6 +696,8 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             break;                                          // this warp found nothing eligible
         }
     }
+    st.flips += fl32;
+    st.fired += fi32;
     return rounds;
 }
 
