@@ -231,16 +231,18 @@ int bits_for(uint64_t v) {
 constexpr size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
     return ((size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32) * 8;
 }
-constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl = false, bool early = false) {
-    return tma_smem_bytes(ndim, tx, ty, tz, nt, nbuf, wl, early);
+constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl = false, bool early = false,
+                          int hw = 1) {
+    return tma_smem_bytes(ndim, tx, ty, tz, nt, nbuf, wl, early, hw);
 }
 
 // Kernel variants (identical results; ablations): 0 = persistent TMA-staged compacted kernel
 // (default), 1 = uncompacted one-CTA-per-tile kernel, 2 = persistent, double-buffered TMA,
 // 3 = persistent TMA with register-resident synchronous rounds and CTA-wide firing,
-// 4 = persistent TMA with work-list rounds (re-test only the cells whose neighbourhood changed).
+// 4 = persistent TMA with work-list rounds (re-test only the cells whose neighbourhood changed),
+// 5 = variant 0 with a 2-wide halo whose inner ring is simulated redundantly (2-D; 3-D = 0).
 // Slot NVARIANT = two-barrier fig:s1c1pe rounds (sync_rounds = 1).
-constexpr int NVARIANT = 5;
+constexpr int NVARIANT = 6;
 struct TileKey {
     int ndim, tx, ty, tz, nt;
     void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1];
@@ -253,11 +255,12 @@ struct TileKey {
       (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBD, true, false>,                                 \
       (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBR, false, true>,                                 \
       (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBW, false, false, false, true>,                   \
+      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, false, false, (ND == 2 ? 2 : 1)>, \
       (void*)tile_kernel<ND, TX, TY, TZ, NT, true>},                                                 \
      {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
       tma_smem(ND, TX, TY, TZ, NT, 1, false, true), tma_smem(ND, TX, TY, TZ, NT, 1, true),              \
-      tile_smem(ND, TX, TY, TZ, NT)},                                                                \
-     {true, false, true, true, true, false},                                                         \
+      tma_smem(ND, TX, TY, TZ, NT, 1, false, false, ND == 2 ? 2 : 1), tile_smem(ND, TX, TY, TZ, NT)},  \
+     {true, false, true, true, true, true, false},                                                   \
      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>}
 
 const TileKey kTiles[] = {
@@ -687,10 +690,10 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         if (!sel) return bail(fail(ACA_EINVAL, "unsupported tile %dx%dx%d for ndim %d", tx, ty, tz, ndim));
         const int v = S->sync ? NVARIANT : opt.variant;
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
-        S->kern = (v == 0 && opt.early_reject) ? sel->fn_early : sel->fn[v];
+        S->kern = ((v == 0 || v == 5) && opt.early_reject) ? sel->fn_early : sel->fn[v];
         S->nthreads = sel->nt;
         S->smem = sel->smem[v];
-        if (v == 0 && opt.early_reject)   // a10 candidates need a full per-warp queue
+        if ((v == 0 || v == 5) && opt.early_reject)   // a10 candidates need a full per-warp queue
             S->smem = tma_smem(ndim, tx, ty, tz, sel->nt, 1, false, true);
         if (sel->persistent[v]) {   // persistent: as many CTAs as fit on the device at once
             if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)

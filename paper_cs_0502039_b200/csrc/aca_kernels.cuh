@@ -428,16 +428,20 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
 // CPW/2 + 16 entries (the eligible cells of a warp form an independent set: at most one per
 // two cells of each row segment), CPW with a10 candidates, or the work-list's two CTA queues
 // plus claim bitmaps and counters.
-__host__ __device__ constexpr size_t tma_words(int ndim, int tx, int ty, int tz) {
-    return (((size_t)(tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~(size_t)15);
+__host__ __device__ constexpr size_t tma_words(int ndim, int tx, int ty, int tz, int hw = 1) {
+    return (((size_t)(tx + 4) * (ty + 2 * hw) * (ndim == 3 ? tz + 2 * hw : 1) + 15) & ~(size_t)15);
 }
-__host__ __device__ constexpr size_t tma_queue_entries(int ncell, int nt, bool wl, bool early) {
-    return wl ? (size_t)ncell + 64 : early ? (size_t)ncell : (size_t)(nt / 32) * (ncell / (nt / 32) / 2 + 16);
+// per-warp queue of tile_rounds: CPW/2 + 16 own cells (+ 64 redundant ring cells with hw = 2)
+__host__ __device__ constexpr int tile_queue_per_warp(int cpw, bool early, int hw) {
+    return early ? cpw : cpw / 2 + 16 + (hw == 2 ? 64 : 0);
+}
+__host__ __device__ constexpr size_t tma_queue_entries(int ncell, int nt, bool wl, bool early, int hw = 1) {
+    return wl ? (size_t)ncell + 64 : (size_t)(nt / 32) * tile_queue_per_warp(ncell / (nt / 32), early, hw);
 }
 __host__ __device__ constexpr size_t tma_smem_bytes(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl,
-                                                    bool early) {
-    return (tma_words(ndim, tx, ty, tz) * nbuf + 512 + 16 + 112 + nt / 32 + 2) * 8 +
-           ((tma_queue_entries(tx * ty * tz, nt, wl, early) * 2 + 15) & ~(size_t)15) +
+                                                    bool early, int hw = 1) {
+    return (tma_words(ndim, tx, ty, tz, hw) * nbuf + 512 + 16 + 112 + nt / 32 + 2) * 8 +
+           ((tma_queue_entries(tx * ty * tz, nt, wl, early, hw) * 2 + 15) & ~(size_t)15) +
            (wl ? (size_t)tx * ty * tz / 32 * 8 + 16 : 0);
 }
 
@@ -510,12 +514,35 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
     }
 }
 
-template <int NDIM, int TX, int TY, int TZ, int NT, bool FULL, bool EARLY>
+// Exact local-minimum test of the cell in slot s against its observed neighbours (P6:
+// word order = (t, c) order). High halves first; the full words only on a tie.
+template <int NDIM, int SX, int SXY>
+__device__ __forceinline__ bool is_local_min(const volatile unsigned long long* VS, const volatile unsigned int* VH,
+                                             int s, unsigned long long w) {
+    const unsigned int oh = (unsigned int)(w >> 32);
+    unsigned int mn = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]), min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
+    if (NDIM == 3) mn = min(mn, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
+    if (oh != mn) return oh < mn;
+    bool e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
+    if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+    return e;
+}
+
+// Ring cell ri of a 2-D tile with a 2-wide halo: the (TX+2) x (TY+2) frame around the tile
+// (rows -1 and TY over lx = -1..TX, then columns -1 and TX over ly = 0..TY-1).
+template <int TX, int TY>
+__device__ __forceinline__ void ring_coords(int ri, int& lx, int& ly) {
+    if (ri < 2 * (TX + 2)) { ly = ri < TX + 2 ? -1 : TY; lx = ri % (TX + 2) - 1; }
+    else { const int r2 = ri - 2 * (TX + 2); lx = r2 < TY ? -1 : TX; ly = r2 % TY; }
+}
+
+template <int NDIM, int TX, int TY, int TZ, int NT, bool FULL, bool EARLY, int HW = 1>
 __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned long long* S, unsigned short* Q,
                                                     const unsigned long long* thr, const unsigned long long* thm,
                                                     const unsigned long long* lr, int x0, int y0, int z0,
                                                     unsigned long long wlim, TileStats& st) {
-    constexpr int SX = TX + 4, SY = TY + 2;
+    static_assert(HW == 1 || (HW == 2 && NDIM == 2 && !EARLY), "2-wide halo: 2-D, no a10");
+    constexpr int SX = TX + 4, SY = TY + 2 * HW;
     constexpr int SXY = SX * SY;
     constexpr int NCELL = TX * TY * TZ;
     constexpr int NW = NT / 32;
@@ -527,11 +554,47 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wbase = warp * CPW;
-    constexpr int QW = EARLY ? CPW : CPW / 2 + 16;       // per-warp queue (see tma_smem_bytes)
+    constexpr int QW = tile_queue_per_warp(CPW, EARLY, HW);   // per-warp queue (see tma_smem_bytes)
     unsigned short* q = Q + warp * QW;
     volatile unsigned long long* VS = S;
     const volatile unsigned int* VH = (const volatile unsigned int*)S;   // [2s+1]: high half, [2s]: low half
-    auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2; };
+    auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3 ? HW : 0)) * SXY + (ly + HW) * SX + lx + 2; };
+    // 2-wide halo: the inner halo ring (cells of the neighbour tiles) is also advanced here and
+    // written back, its arrivals counted here (the owners continue from the new states). A ring
+    // cell may fire only if its owner tile is idle during this launch (the other checkerboard
+    // colour): then it and its neighbours were last written by finished launches, every state
+    // it observes precedes its pending arrival, and the stale-read argument of fig:amcgen
+    // applies; it has exactly one writer. Frozen instead: corner cells (diagonal tiles share
+    // our colour and run concurrently), the end cells of every edge (corner cells of the neighbour
+    // tile, which touch a second active tile), edges whose wrapped neighbour tile has our colour
+    // (odd tile counts), rows outside the shard (halo buffers hold one row), ragged tiles, and
+    // everything when the launch is not a checkerboard phase. Each thread owns up to two ring
+    // cells.
+    constexpr int NRING = HW == 2 ? 2 * (TX + 2) + 2 * TY : 0;
+    int rs[2] = {0, 0};
+    bool rv[2] = {false, false};
+    if constexpr (HW == 2) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int ri = tid + k * NT;
+            if (ri < NRING) {
+                int lx, ly;
+                ring_coords<TX, TY>(ri, lx, ly);
+                rs[k] = slot(lx, ly, 0);
+                const int dx = lx < 0 ? -1 : (lx >= TX ? 1 : 0), dy = ly < 0 ? -1 : (ly >= TY ? 1 : 0);
+                const int tx = x0 / TX, ty = y0 / TY;
+                bool ok = FULL && P.phase >= 0 && (dx == 0 || dy == 0);
+                // the two end cells of each edge are corner cells of the neighbour tile, adjacent
+                // to a second active tile as well: frozen, so every ring cell has one writer
+                if (dy != 0) ok = ok && lx != 0 && lx != TX - 1;
+                if (dx != 0) ok = ok && ly != 0 && ly != TY - 1;
+                if (dy != 0 && g.sharded) ok = ok && (ty + dy >= 0 && ty + dy < P.tiles_y);
+                const int ntx = wrapi(tx + dx, P.tiles_x), nty = wrapi(ty + dy, P.tiles_y);
+                ok = ok && (((ntx + nty + P.row_par0) & 1) != ((tx + ty + P.row_par0) & 1));
+                rv[k] = ok;
+            }
+        }
+    }
     int s0 = 0;
     if (FASTMAP) {
         const int row0 = warp * (CPW / TX);
@@ -591,6 +654,15 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
                 emask |= (uint32_t)e << j;
             }
+            if constexpr (HW == 2) {   // the lane's ring cells take mask bits JPL, JPL + 1
+#pragma unroll
+                for (int k = 0; k < 2; ++k) {
+                    if (!rv[k]) continue;
+                    const unsigned long long w = VS[rs[k]];
+                    const bool act = w < wlim;
+                    if (act && is_local_min<NDIM, SX, SXY>(VS, VH, rs[k], w)) emask |= 1u << (JPL + k);
+                }
+            }
         } else
 #pragma unroll
         for (int j = 0; j < JPL; ++j) {
@@ -648,7 +720,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         while (emask) {
             const int j = __ffs(emask) - 1;
             emask &= emask - 1u;
-            q[pos++] = (unsigned short)(wbase + lane + 32 * j);
+            q[pos++] = (unsigned short)(j < JPL ? wbase + lane + 32 * j : NCELL + tid + (j - JPL) * NT);
         }
         __syncwarp();
         // Fire whole 32-lane chunks only; the partial tail chunk waits for the next round (its
@@ -657,6 +729,24 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         const int nfire = (P.defer_tail && r < P.rounds - 1 && cnt > 32) ? (cnt & ~31) : cnt;
         for (int i = lane; i < nfire; i += 32) {
             const int o = q[i];
+            if (HW == 2 && o >= NCELL) {   // ring cell of an idle neighbour tile: a real arrival
+                int rlx, rly;
+                ring_coords<TX, TY>(o - NCELL, rlx, rly);
+                const int s = slot(rlx, rly, 0);
+                const unsigned long long w = VS[s];
+                const uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
+                                      (VH[2 * (s + SX)] & 1u);
+                const int gy = y0 + rly;
+                const uint32_t c = cell_id32(g, wrapi(x0 + rlx, g.nx), g.sharded ? gy : wrapi(gy, g.ny), 0);
+                const FireOut f = fire(w, ones, Z, (unsigned long long)c, g, thr, lr, P.rk, P.inv_lambda, P.tie_bits,
+                                       P.do_hash, P.ctl, P.law, &P.fr);
+                if (!f.ok) continue;
+                VS[s] = f.wnew;
+                st.hacc += f.h;
+                st.flips += f.flip;
+                ++st.fired;
+                continue;
+            }
             const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
             const int s = slot(lx, ly, lz);
             if (EARLY) {
@@ -698,6 +788,22 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
     }
     st.flips += fl32;
     st.fired += fi32;
+    if constexpr (HW == 2) {
+        // The ring cells this tile advanced are written back: their owner tiles are idle in this
+        // launch (single writer, words only grow) and will continue from these states, so the
+        // global state stays one in which every neighbour's last arrival precedes a cell's
+        // pending arrival. Other warps may still be firing ring cells: wait for all of them.
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (!rv[k]) continue;
+            int lx, ly;
+            ring_coords<TX, TY>(tid + k * NT, lx, ly);
+            const int gy = y0 + ly;
+            const size_t gi = (size_t)(g.sharded ? gy : wrapi(gy, g.ny)) * g.nx + wrapi(x0 + lx, g.nx);
+            P.words[gi] = VS[rs[k]];
+        }
+    }
     return rounds;
 }
 
@@ -843,19 +949,6 @@ __device__ __forceinline__ unsigned int tile_rounds_reg(const KParams& P, unsign
     return rounds;
 }
 
-// Exact local-minimum test of the cell in slot s against its observed neighbours (P6:
-// word order = (t, c) order). High halves first; the full words only on a tie.
-template <int NDIM, int SX, int SXY>
-__device__ __forceinline__ bool is_local_min(const volatile unsigned long long* VS, const volatile unsigned int* VH,
-                                             int s, unsigned long long w) {
-    const unsigned int oh = (unsigned int)(w >> 32);
-    unsigned int mn = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]), min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
-    if (NDIM == 3) mn = min(mn, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
-    if (oh != mn) return oh < mn;
-    bool e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
-    if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
-    return e;
-}
 
 // Work-list rounds (full tiles). Round 0 tests every cell of the tile against one snapshot
 // and queues the local minima; every later round fires the queued cells and re-tests ONLY
@@ -1061,9 +1154,11 @@ __device__ __forceinline__ void halo_coords(int h, int& lx, int& ly, int& lz) {
     }
 }
 
-template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG, bool EARLY = false, bool WL = false>
+template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG, bool EARLY = false, bool WL = false,
+          int HW = 1>
 __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
-    constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
+    static_assert(HW == 1 || (HW == 2 && NDIM == 2 && !EARLY && !WL && !REG && !DB), "2-wide halo: 2-D V0 only");
+    constexpr int SX = TX + 4, SY = TY + 2 * HW, SZ = (NDIM == 3) ? TZ + 2 * HW : 1;
     constexpr int SXY = SX * SY;
     constexpr int NSLOT = SXY * SZ;
     constexpr int NSLOTP = (NSLOT + 15) & ~15;          // keep each buffer 128-B aligned
@@ -1084,7 +1179,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     unsigned long long* red = thm + 112;                            // NW
     unsigned long long* bar = red + NW;                             // 2
     unsigned short* Q = (unsigned short*)(bar + 2);                 // fire queue(s), see tma_smem_bytes
-    unsigned int* claim = (unsigned int*)(Q + ((tma_queue_entries(NCELL, NT, WL, EARLY || REG) + 7) & ~(size_t)7));
+    unsigned int* claim = (unsigned int*)(Q + ((tma_queue_entries(NCELL, NT, WL, EARLY || REG, HW) + 7) & ~(size_t)7));
     unsigned int* qcnt = claim + 2 * (NCELL / 32);                  // WL: 4 queue counters
 
     const Geo& g = P.g;
@@ -1095,7 +1190,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
     __syncthreads();
 
-    auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3)) * SXY + (ly + 1) * SX + lx + 2; };
+    auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3 ? HW : 0)) * SXY + (ly + HW) * SX + lx + 2; };
     const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
     // work items: every tile (phase < 0), or the tiles of one checkerboard colour: item k is
     // column pair j = k % hx of tile row k / hx, tx = 2j + ((row parity + phase) & 1)
@@ -1151,19 +1246,29 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
         }
         if (!valid) continue;   // odd tiles_x: the last column pair has one tile
         if (fast) {
-            for (int h = tid; h < NHALO; h += NT) {
-                int lx, ly, lz;
-                halo_coords<NDIM, TX, TY, TZ>(h, lx, ly, lz);
-                S[slot(lx, ly, lz)] = ld_word_t<true>(P, x0 + lx, y0 + ly, z0 + lz);
+            if constexpr (HW == 1) {
+                for (int h = tid; h < NHALO; h += NT) {
+                    int lx, ly, lz;
+                    halo_coords<NDIM, TX, TY, TZ>(h, lx, ly, lz);
+                    S[slot(lx, ly, lz)] = ld_word_t<true>(P, x0 + lx, y0 + ly, z0 + lz);
+                }
+            } else {   // 2-wide halo: rows -2, -1, TY, TY+1 (full width), then columns -2, -1, TX, TX+1
+                constexpr int RW = TX + 4, NH2 = 4 * RW + 4 * TY;
+                for (int h = tid; h < NH2; h += NT) {
+                    int lx, ly;
+                    if (h < 4 * RW) { const int r = h / RW; ly = r < 2 ? r - 2 : TY + r - 2; lx = h % RW - 2; }
+                    else { const int h2 = h - 4 * RW, c = h2 / TY; lx = c < 2 ? c - 2 : TX + c - 2; ly = h2 % TY; }
+                    S[slot(lx, ly, 0)] = ld_word_t<true>(P, x0 + lx, y0 + ly, 0);
+                }
             }
             mbar_wait(&bar[b], (ph >> b) & 1u);
             ph ^= 1u << b;
         } else {
             for (int i = tid; i < NSLOT; i += NT) {
-                const int lx = i % SX - 2, ly = (i / SX) % SY - 1, lz = (NDIM == 3) ? i / SXY - 1 : 0;
-                if (lx < -1 || lx > TX) continue;
+                const int lx = i % SX - 2, ly = (i / SX) % SY - HW, lz = (NDIM == 3) ? i / SXY - HW : 0;
+                if (lx < -HW || lx >= TX + HW) continue;
                 const int out = (lx < 0 || lx >= TX) + (ly < 0 || ly >= TY) + ((NDIM == 3) && (lz < 0 || lz >= TZ));
-                if (out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
+                if (HW == 2 || out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
             }
         }
         __syncthreads();
@@ -1182,8 +1287,8 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
             }
         }
         if (!done_reg) {
-            rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true, EARLY>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st)
-                          : tile_rounds<NDIM, TX, TY, TZ, NT, false, EARLY>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st);
+            rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true, EARLY, HW>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st)
+                          : tile_rounds<NDIM, TX, TY, TZ, NT, false, EARLY, HW>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st);
         }
         rounds_max = rounds > rounds_max ? rounds : rounds_max;
         __syncthreads();

@@ -132,10 +132,11 @@ def test_tiled_2d_ragged(aca, oracle_mod, tile):
     assert_same(g, o)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
 def test_kernel_variants(aca, oracle_mod, variant):
     """Persistent TMA kernel (0), uncompacted per-tile kernel (1), double-buffered TMA
-    kernel (2), register-resident synchronous rounds (3), work-list rounds (4): identical
+    kernel (2), register-resident synchronous rounds (3), work-list rounds (4), 2-wide redundant
+    halo (5): identical
     trajectories, 2-D (full + ragged tiles, odd width) and 3-D."""
     for dims, tile, T in (((256, 192), (64, 64), 5.0), ((200, 150), (64, 32), 4.0), ((130, 70), (32, 32), 4.0),
                           ((64, 48, 40), (32, 16, 8), 3.0), ((40, 24, 20), (16, 16, 16), 3.0)):
@@ -318,3 +319,26 @@ def test_class_histogram(aca, oracle_mod, dims):
     thr = oracle_mod.flip_table(nd, 1.0, 1.0, 0.1, 1)
     rate = sum(int(c) * t / 2 ** 32 for c, t in zip(want, thr))
     assert abs(st["nfold_rate"] - rate) < 1e-6 * max(1.0, rate)
+
+
+@pytest.mark.parametrize("case", ["tiny", "shards", "ties", "metro_field", "law2", "rounds"])
+def test_two_wide_halo(aca, oracle_mod, case):
+    """Variant 5 (2-wide halo, inner ring simulated redundantly): lattices smaller than a tile
+    (the box is a periodic unrolling with repeated cells), virtual shards (rows outside the
+    shard stay frozen), forced ties, Metropolis with field, the r^(1/8) law, many rounds."""
+    kw = dict(dims=(200, 150), Ts=[3.0, 6.0], seed=53, whole_lattice=-1, variant=5)
+    if case == "tiny":
+        kw.update(dims=(20, 12))
+    elif case == "shards":
+        kw.update(dims=(128, 256), shards=4)
+    elif case == "ties":
+        kw.update(tie_bits=30)
+    elif case == "metro_field":
+        kw.update(rule=1, h=0.1, beta=0.6)
+    elif case == "law2":
+        kw.update(law=2)
+    elif case == "rounds":
+        kw.update(rounds_per_launch=24)
+    dims, Ts = kw.pop("dims"), kw.pop("Ts")
+    g, o = run_pair(aca, oracle_mod, dims, Ts, **kw)
+    assert_same(g, o)
