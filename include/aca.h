@@ -171,6 +171,27 @@ int64_t aca_num_cells(const aca_sim* s);
  * before the time already simulated), ACA_ERANGE (frame times overflow), run_until errors. */
 int aca_run_frames(aca_sim* s, double dt, int64_t K0, int64_t count, int B, uint8_t* out);
 
+/* ---- Aggregated Poisson stream (fig:amcpoi; docs/PRIMITIVES.md P8) ----
+ * The 2-D periodic lattice (dims[0] x dims[1], multiples of m) is partitioned into m x m
+ * subarrays (m = 1, 2, 4, 8). Each subarray carries one Poisson stream of rate lambda m^2; at
+ * each arrival one of its cells, chosen uniformly at random, is updated (heat-bath or
+ * Metropolis, P4), after waiting for the subarrays that hold the cell's outside neighbours.
+ * One GPU thread per subarray, conservative launches until every T(C) >= T. The trajectory
+ * depends on m; for m = 1 it is the main path's trajectory exactly.
+ * Outputs (host, caller-owned, each may be NULL): spins_out[N] (int8 row-major), T_out[ntiles]
+ * (Q32 next arrival per subarray), n_out[ntiles] (arrivals per subarray), st. budget: arrivals
+ * per subarray per launch (<= 0: 64). Device memory is allocated and freed inside the call.
+ * Errors: ACA_EINVAL (arguments), ACA_ENOMEM, ACA_ENODEV, ACA_ECUDA, ACA_ESTATE. */
+typedef struct {
+    uint64_t arrivals, flips, event_hash;   /* event hash: P7 with the cell choice l mixed in */
+    int64_t bond_sum, magnetisation;        /* from spins_out (0 if it is NULL) */
+    uint64_t launches;
+    double gpu_seconds;                     /* device time of the simulation launches */
+} aca_agg_stats;
+int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule, uint64_t seed,
+                double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
+                aca_agg_stats* st, int device);
+
 /* ---- Time-only efficiency model ----
  * Synchronous iterations of fig:s1c1pe on the local times only (valid because next_t does
  * not depend on the states for the Ising model): each iteration every

@@ -651,3 +651,116 @@ int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda,
     free(t); free(fire);
     return 0;
 }
+
+/* ---------------------------------------------------------------- aggregated Poisson stream
+ * fig:amcpoi: the 2-D torus is partitioned into m x m subarrays C (m a power
+ * of two dividing both sides; C = Y (nx/m) + X). Each C carries ONE Poisson stream of rate
+ * lambda m^2 (the sum of its cells' streams); at each arrival a cell of C is
+ * chosen uniformly at random (Step 2) and updated (Step 4), and T(C) advances by
+ * -ln r / (lambda m^2) (Step 5). docs/PRIMITIVES.md P8: the k-th arrival of C uses Philox ctr
+ * (k, C_lo, C_hi, tag_e): w0 = flip uniform (P4), (w1, w2) = the increment NLOG-2((w1 << 32) |
+ * w2) at INV = floor(2^32 / (lambda m^2) + 0.5), at least 1, w3 = the cell choice
+ * l = w3 >> (32 - log2 m^2) (l = 0 for m = 1; local index l = j m + i). T0(C) comes from ctr
+ * (0, C_lo, C_hi, tag_i) the same way. Tags: (tag_e, tag_i) = (3, 4), except (0, 1) for m = 1,
+ * where C = c and the algorithm IS fig:a1c1pe with the per-cell streams of P1 (the special
+ * case pins this code to the main oracle bit for bit). Spins start from P5. The serial
+ * definition: process arrivals in increasing (T(C), C) order while T(C) < T (a heap over
+ * subarrays). The trajectory depends on m and is unique for a given m.
+ * Event hash: P7 with ^ (l << 1) added (l = 0 for m = 1). Test infrastructure only.
+ * Returns 0, -1 on bad arguments. */
+typedef struct { uint64_t T; int64_t C; } agg_key;
+
+static int agg_less(const uint64_t* T, int64_t a, int64_t b) { return T[a] < T[b] || (T[a] == T[b] && a < b); }
+
+static void agg_sift(uint32_t* H, int64_t n, const uint64_t* T, int64_t i) {
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < n && agg_less(T, H[l], H[m])) m = l;
+        if (r < n && agg_less(T, H[r], H[m])) m = r;
+        if (m == i) return;
+        uint32_t tmp = H[i]; H[i] = H[m]; H[m] = tmp;
+        i = m;
+    }
+}
+
+static uint64_t agg_delta(uint32_t w1, uint32_t w2, uint64_t inv) {
+    uint64_t q = oracle_nlog_q32(((uint64_t)w1 << 32) | w2);
+    uint64_t d = (uint64_t)(((unsigned __int128)q * inv) >> 32);
+    return d < 1 ? 1 : d;
+}
+
+int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule,
+                   uint64_t seed, double init_q, uint64_t T_q32, int8_t* spins_out, uint64_t* T_out,
+                   uint32_t* n_out, oracle_stats* st) {
+    int64_t nx = dims[0], ny = dims[1];
+    if (m < 1 || (m & (m - 1)) || m > 8 || nx % m || ny % m || nx < 2 || ny < 2) return -1;
+    if (!(lambda > 0) || !(beta >= 0) || (rule != 0 && rule != 1)) return -1;
+    int lg = 0;
+    while ((1 << lg) < m * m) lg++;
+    const uint32_t tag_e = m == 1 ? 0u : 3u, tag_i = m == 1 ? 1u : 4u;
+    int64_t mx = nx / m, my = ny / m, NC = mx * my, N = nx * ny;
+    uint64_t thr[14];
+    oracle_flip_table(2, beta, J, h, rule, thr);
+    uint64_t inv = (uint64_t)floor(4294967296.0 / (lambda * (double)(m * m)) + 0.5);
+    uint64_t thr_init = (uint64_t)floor(init_q * 4294967296.0);
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    int8_t* s = (int8_t*)malloc((size_t)N);
+    uint64_t* T = (uint64_t*)malloc((size_t)NC * 8);
+    uint32_t* n = (uint32_t*)calloc((size_t)NC, 4);
+    uint32_t* H = (uint32_t*)malloc((size_t)NC * 4);
+    if (!s || !T || !n || !H) { free(s); free(T); free(n); free(H); return -1; }
+    for (int64_t c = 0; c < N; c++) {                       /* P5 spins */
+        uint32_t ctr[4] = {0, (uint32_t)((uint64_t)c & 0xffffffffu), (uint32_t)((uint64_t)c >> 32), 1u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        s[c] = ((uint64_t)w[0] < thr_init) ? -1 : 1;
+    }
+    for (int64_t C = 0; C < NC; C++) {
+        uint32_t ctr[4] = {0, (uint32_t)((uint64_t)C & 0xffffffffu), (uint32_t)((uint64_t)C >> 32), tag_i}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        T[C] = agg_delta(w[1], w[2], inv);
+        H[C] = (uint32_t)C;
+    }
+    for (int64_t i = NC / 2 - 1; i >= 0; i--) agg_sift(H, NC, T, i);
+    uint64_t arrivals = 0, flips = 0, hash = 0;
+    while (NC > 0) {
+        int64_t C = H[0];
+        if (T[C] >= T_q32) break;
+        uint32_t k = n[C];
+        uint32_t ctr[4] = {k, (uint32_t)((uint64_t)C & 0xffffffffu), (uint32_t)((uint64_t)C >> 32), tag_e}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        int64_t l = lg == 0 ? 0 : (int64_t)(w[3] >> (32 - lg));   /* Step 2: uniform cell of C */
+        int64_t X = C % mx, Y = C / mx;
+        int64_t x = X * m + l % m, y = Y * m + l / m;
+        int64_t c = y * nx + x;
+        int sigma = s[y * nx + (x + nx - 1) % nx] + s[y * nx + (x + 1) % nx] + s[((y + ny - 1) % ny) * nx + x] +
+                    s[((y + 1) % ny) * nx + x];
+        int sc = s[c];
+        int idx = (sigma + 4) / 2 + 5 * (sc + 1) / 2;
+        int ns = sc;
+        if ((uint64_t)w[0] < thr[idx]) { ns = -sc; flips++; }   /* Step 4 */
+        s[c] = (int8_t)ns;
+        hash += oracle_mix64(T[C] ^ rotl64((uint64_t)C, 20) ^ rotl64((uint64_t)k, 44) ^ ((uint64_t)l << 1) ^
+                             (uint64_t)(ns > 0 ? 1 : 0));
+        T[C] += agg_delta(w[1], w[2], inv);                   /* Step 5 */
+        n[C] = k + 1;
+        arrivals++;
+        agg_sift(H, NC, T, 0);
+    }
+    if (spins_out) memcpy(spins_out, s, (size_t)N);
+    if (T_out) memcpy(T_out, T, (size_t)NC * 8);
+    if (n_out) memcpy(n_out, n, (size_t)NC * 4);
+    if (st) {
+        memset(st, 0, sizeof *st);
+        st->arrivals = arrivals; st->flips = flips; st->event_hash = hash;
+        int64_t B = 0, M = 0;
+        for (int64_t y = 0; y < ny; y++)
+            for (int64_t x = 0; x < nx; x++) {
+                int v = s[y * nx + x];
+                M += v;
+                B += v * (s[y * nx + (x + 1) % nx] + s[((y + 1) % ny) * nx + x]);
+            }
+        st->bond_sum = B; st->magnetisation = M;
+    }
+    free(s); free(T); free(n); free(H);
+    return 0;
+}

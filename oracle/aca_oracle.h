@@ -102,6 +102,13 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
 int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                           uint64_t* fired_per_round, uint64_t* t_out);
 
+/* Aggregated Poisson stream (fig:amcpoi; docs/PRIMITIVES.md P8): 2-D torus
+ * in m x m subarrays, one cumulative stream per subarray, serial (T(C), C) order. Outputs may
+ * be NULL: spins[N], T[ntiles], n[ntiles]; st gets arrivals, flips, event_hash, B, M. */
+int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule,
+                   uint64_t seed, double init_q, uint64_t T_q32, int8_t* spins_out, uint64_t* T_out,
+                   uint32_t* n_out, oracle_stats* st);
+
 #ifdef __cplusplus
 }
 #endif

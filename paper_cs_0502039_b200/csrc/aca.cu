@@ -18,6 +18,7 @@
 #include "../../include/aca.h"
 #include "aca_kernels.cuh"
 #include "aca_eff.cuh"
+#include "aca_agg.cuh"
 #include "nlog_tables.cuh"
 
 using namespace aca;
@@ -1297,6 +1298,127 @@ int aca_run_frames(aca_sim* S, double dt, int64_t K0, int64_t count, int B, uint
     }
     S->fr = FrameParams{};
     drop_graph(S);
+    return rc;
+}
+
+// ---------------------------------------------------------------- aggregated Poisson stream
+int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule, uint64_t seed,
+                double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
+                aca_agg_stats* st, int device) {
+    if (!dims) return fail(ACA_EINVAL, "null dims");
+    if (m != 1 && m != 2 && m != 4 && m != 8) return fail(ACA_EINVAL, "m must be 1, 2, 4 or 8");
+    const int64_t nx = dims[0], ny = dims[1];
+    if (nx < 2 || ny < 2 || nx % m || ny % m || nx * ny > ((int64_t)1 << 32) || nx > (1 << 30) || ny > (1 << 30))
+        return fail(ACA_EINVAL, "dims must be >= 2, multiples of m, N <= 2^32");
+    if (!(lambda > 0) || !std::isfinite(lambda) || !(beta >= 0) || !std::isfinite(beta) || !std::isfinite(J) ||
+        !std::isfinite(h))
+        return fail(ACA_EINVAL, "bad lambda / beta / J / h");
+    if (rule != ACA_HEATBATH && rule != ACA_METROPOLIS) return fail(ACA_EINVAL, "rule must be 0 or 1");
+    if (!(init_q >= 0 && init_q <= 1)) return fail(ACA_EINVAL, "init_q must be in [0, 1]");
+    if (!(T >= 0) || !std::isfinite(T) || T * 4294967296.0 > 1.8e19) return fail(ACA_EINVAL, "bad T");
+    if (budget < 1) budget = 64;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
+    if (device >= 0) CK(cudaSetDevice(device));
+    AggParams A{};
+    A.nx = (int)nx; A.ny = (int)ny; A.m = m;
+    A.lg = 0;
+    while ((1 << A.lg) < m * m) ++A.lg;
+    A.mx = (int)(nx / m); A.my = (int)(ny / m);
+    philox_round_keys((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), A.rk);
+    A.inv = (unsigned long long)std::floor(4294967296.0 / (lambda * (double)(m * m)) + 0.5);
+    A.Tend = (unsigned long long)std::floor(T * 4294967296.0 + 0.5);
+    A.tag_e = m == 1 ? 0u : 3u;
+    A.tag_i = m == 1 ? 1u : 4u;
+    A.budget = budget;
+    A.do_hash = 1;
+    unsigned long long thr[14];
+    flip_table(2, beta, J, h, rule, thr);
+    for (int i = 0; i < 10; ++i) A.thr[i] = thr[i];
+    A.thr_init = (unsigned long long)std::floor(init_q * 4294967296.0);
+    const int64_t NC = (int64_t)A.mx * A.my;
+    unsigned long long* dlr = nullptr;
+    AggAcc* dacc = nullptr;
+    int8_t* dsp = nullptr;
+    cudaStream_t str = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto cleanup = [&]() {
+        if (str) cudaStreamSynchronize(str);
+        cudaFree(A.mask); cudaFree(A.T); cudaFree(A.n); cudaFree(dlr); cudaFree(dacc); cudaFree(dsp);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (str) cudaStreamDestroy(str);
+    };
+    if (cudaMalloc(&A.mask, NC * 8) != cudaSuccess || cudaMalloc(&A.T, NC * 8) != cudaSuccess ||
+        cudaMalloc(&A.n, NC * 4) != cudaSuccess || cudaMalloc(&dlr, sizeof(ACA_NLOG_LR)) != cudaSuccess ||
+        cudaMalloc(&dacc, sizeof(AggAcc)) != cudaSuccess) {
+        cleanup();
+        return fail(ACA_ENOMEM, "device allocation failed");
+    }
+    int rc = ACA_OK;
+    AggAcc hacc{};
+    uint64_t launches = 0;
+    do {
+        if (cudaStreamCreateWithFlags(&str, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(ACA_ECUDA, "stream"); break; }
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaMemcpyAsync(dlr, ACA_NLOG_LR, sizeof(ACA_NLOG_LR), cudaMemcpyHostToDevice, str);
+        cudaMemsetAsync(dacc, 0, sizeof(AggAcc), str);
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device >= 0 ? device : 0);
+        const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((NC + 255) / 256, (long long)nsm * 8));
+        agg_init_kernel<<<grid, 256, 0, str>>>(A, dlr);
+        cudaEventRecord(e0, str);
+        for (int batch = 0;; ++batch) {
+            for (int kk = 0; kk < 8; ++kk) {
+                if (kk == 7) cudaMemsetAsync(&dacc->active, 0, 16, str);   // active + blocked of the last launch
+                agg_round_kernel<<<grid, 256, 0, str>>>(A, dlr, dacc);
+                ++launches;
+            }
+            if (cudaMemcpyAsync(&hacc, dacc, sizeof(AggAcc), cudaMemcpyDeviceToHost, str) != cudaSuccess ||
+                cudaStreamSynchronize(str) != cudaSuccess) {
+                rc = fail(ACA_ECUDA, "aggregated kernels failed: %s", cudaGetErrorString(cudaGetLastError()));
+                break;
+            }
+            if (hacc.active == 0) break;
+            if (batch > (1 << 24)) { rc = fail(ACA_ESTATE, "no termination"); break; }
+        }
+        if (rc) break;
+        cudaEventRecord(e1, str);
+        cudaStreamSynchronize(str);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (spins_out) {
+            if (cudaMalloc(&dsp, (size_t)nx * ny) != cudaSuccess) { rc = fail(ACA_ENOMEM, "spins"); break; }
+            agg_unpack_kernel<<<grid, 256, 0, str>>>(A, dsp);
+            if (cudaMemcpyAsync(spins_out, dsp, (size_t)nx * ny, cudaMemcpyDeviceToHost, str) != cudaSuccess) {
+                rc = fail(ACA_ECUDA, "copy spins");
+                break;
+            }
+        }
+        if (T_out && cudaMemcpyAsync(T_out, A.T, NC * 8, cudaMemcpyDeviceToHost, str) != cudaSuccess) { rc = fail(ACA_ECUDA, "copy T"); break; }
+        if (n_out && cudaMemcpyAsync(n_out, A.n, NC * 4, cudaMemcpyDeviceToHost, str) != cudaSuccess) { rc = fail(ACA_ECUDA, "copy n"); break; }
+        cudaStreamSynchronize(str);
+        if (st) {
+            memset(st, 0, sizeof *st);
+            st->arrivals = hacc.arrivals;
+            st->flips = hacc.flips;
+            st->event_hash = hacc.hash;
+            st->launches = launches;
+            st->gpu_seconds = ms * 1e-3;
+            if (spins_out) {
+                long long B = 0, M = 0;
+                for (int64_t y = 0; y < ny; ++y)
+                    for (int64_t x = 0; x < nx; ++x) {
+                        const int v = spins_out[y * nx + x];
+                        M += v;
+                        B += v * (spins_out[y * nx + (x + 1) % nx] + spins_out[((y + 1) % ny) * nx + x]);
+                    }
+                st->bond_sum = B;
+                st->magnetisation = M;
+            }
+        }
+    } while (0);
+    cleanup();
     return rc;
 }
 }  // extern "C"
