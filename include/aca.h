@@ -192,6 +192,17 @@ int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J
                 double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
                 aca_agg_stats* st, int device);
 
+/* ---- Modified BKL (docs/PRIMITIVES.md P9) ----
+ * Same partition, arguments and outputs as aca_agg_run (m = 2, 4, 8; lambda >= 1e-6). In
+ * every subarray the boundary layer Gamma_0 (fixed class, weight |Gamma_0|) follows the
+ * standard model and waits for the neighbouring subarrays; the (m-2) x (m-2) kernel runs the
+ * BKL n-fold way (classes by flip probability, the selected kernel cell always flips), so no
+ * state or class change ever crosses a subarray boundary and nothing rolls back. The event
+ * counters n(C) count iterations (kernel rejections are skipped); st->flips counts changes. */
+int aca_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule, uint64_t seed,
+                double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
+                aca_agg_stats* st, int device);
+
 /* ---- Time-only efficiency model ----
  * Synchronous iterations of fig:s1c1pe on the local times only (valid because next_t does
  * not depend on the states for the Ising model): each iteration every

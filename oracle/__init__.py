@@ -112,6 +112,7 @@ def lib():
                                      ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_uint64, ctypes.c_double,
                                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.POINTER(Stats)]
+        L.oracle_bkl_run.argtypes = L.oracle_agg_run.argtypes
         L.oracle_efficiency_run.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
                                             ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                                             ctypes.c_void_p]
@@ -284,16 +285,18 @@ def efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False)
     return (fired, t) if want_times else fired
 
 
-def agg_run(dims, m, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1, init_q=0.5):
-    """Aggregated Poisson stream (fig:amcpoi): spins[ny, nx], T[ntiles], n[ntiles], stats."""
+def agg_run(dims, m, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1, init_q=0.5, bkl=False):
+    """Aggregated Poisson stream (fig:amcpoi), or with bkl=True the modified BKL of
+    PAPER.md:1126-1191: spins[ny, nx], T[ntiles], n[ntiles], stats."""
     nx, ny = int(dims[0]), int(dims[1])
     nt = (nx // m) * (ny // m)
     sp = np.zeros(nx * ny, np.int8)
     Tt = np.zeros(nt, np.uint64)
     nn = np.zeros(nt, np.uint32)
     st = Stats()
-    rc = lib().oracle_agg_run(_dims(dims), m, lam, beta, J, h, rule, seed, init_q, to_q32(T), sp.ctypes.data,
-                              Tt.ctypes.data, nn.ctypes.data, ctypes.byref(st))
+    fn = lib().oracle_bkl_run if bkl else lib().oracle_agg_run
+    rc = fn(_dims(dims), m, lam, beta, J, h, rule, seed, init_q, to_q32(T), sp.ctypes.data,
+            Tt.ctypes.data, nn.ctypes.data, ctypes.byref(st))
     if rc != 0:
         raise ValueError("oracle_agg_run rejected the arguments")
     return sp.reshape(ny, nx), Tt, nn, st.as_dict()

@@ -764,3 +764,142 @@ int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, doubl
     free(s); free(T); free(n); free(H);
     return 0;
 }
+
+/* ---------------------------------------------------------------- modified BKL (P9)
+ * every m x m subarray (m in {2, 4, 8}) of the 2-D torus runs the BKL
+ * n-fold way on its kernel (the (m-2) x (m-2) interior) and the standard procedure on its
+ * boundary layer Gamma_0 (fixed class, weight |Gamma_0|, may or may not change; waits for the
+ * neighbouring subarrays like fig:amcpoi). Kernel classes Gamma_k are the P4 table indices
+ * k = idx(s, Sigma) with integer weights W_k = |Gamma_k| thr_k (thr_k = 2^32 p_k); W_0 =
+ * |Gamma_0| 2^32; W = W_0 + sum W_k. Iteration n of C: (w0..w3) = Philox ctr (n, C, 0, 5);
+ * u = floor(((w0 << 32) | w1) W / 2^64). u < W_0: boundary cell number u >> 32 (increasing local
+ * index l), flip iff (u & 0xffffffff) < thr[idx]. Otherwise o = u - W_0 selects class k (in
+ * order 0..9) and its cell number o / thr_k (increasing l); that cell flips. The next event
+ * time: T(C) += max(1, (NLOG-2((w2 << 32) | w3) INV) >> 32), INV = floor(2^64 / (lambda W') +
+ * 0.5) in IEEE double, W' = the total weight AFTER the event (the new configuration holds until
+ * the next event: the waiting time uses its rates). T0(C) uses ctr (0, C, 0, 6) and the initial
+ * W. Spins start from P5. Serial definition: events in increasing (T(C), C) order while
+ * T(C) < T. Event hash as P8 (l mixed in). Test infrastructure only. 0, or -1 on bad args. */
+static uint64_t bkl_weights(const int8_t* s, int64_t nx, int64_t ny, int64_t X, int64_t Y, int m,
+                            const uint64_t* thr, int* cls /* [m*m], -1 for the boundary layer */) {
+    uint64_t W = 0;
+    for (int l = 0; l < m * m; l++) {
+        int i = l % m, j = l / m;
+        if (i == 0 || j == 0 || i == m - 1 || j == m - 1) { cls[l] = -1; W += 1ULL << 32; continue; }
+        int64_t x = X * m + i, y = Y * m + j;
+        int sig = s[y * nx + x - 1] + s[y * nx + x + 1] + s[(y - 1) * nx + x] + s[(y + 1) * nx + x];
+        int sc = s[y * nx + x];
+        int k = (sig + 4) / 2 + 5 * (sc + 1) / 2;
+        cls[l] = k;
+        W += thr[k];
+    }
+    (void)ny;
+    return W;
+}
+
+static uint64_t bkl_delta(uint32_t w2, uint32_t w3, double lambda, uint64_t W) {
+    uint64_t q = oracle_nlog_q32(((uint64_t)w2 << 32) | w3);
+    uint64_t inv = (uint64_t)floor(18446744073709551616.0 / (lambda * (double)W) + 0.5);
+    uint64_t d = (uint64_t)(((unsigned __int128)q * inv) >> 32);
+    return d < 1 ? 1 : d;
+}
+
+int oracle_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule,
+                   uint64_t seed, double init_q, uint64_t T_q32, int8_t* spins_out, uint64_t* T_out,
+                   uint32_t* n_out, oracle_stats* st) {
+    int64_t nx = dims[0], ny = dims[1];
+    if ((m != 2 && m != 4 && m != 8) || nx % m || ny % m || nx < 2 || ny < 2) return -1;
+    if (!(lambda > 0) || !(beta >= 0) || (rule != 0 && rule != 1)) return -1;
+    int64_t mx = nx / m, my = ny / m, NC = mx * my, N = nx * ny;
+    uint64_t thr[14];
+    oracle_flip_table(2, beta, J, h, rule, thr);
+    uint64_t thr_init = (uint64_t)floor(init_q * 4294967296.0);
+    uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    int8_t* s = (int8_t*)malloc((size_t)N);
+    uint64_t* T = (uint64_t*)malloc((size_t)NC * 8);
+    uint32_t* n = (uint32_t*)calloc((size_t)NC, 4);
+    uint32_t* H = (uint32_t*)malloc((size_t)NC * 4);
+    int cls[64];
+    if (!s || !T || !n || !H) { free(s); free(T); free(n); free(H); return -1; }
+    for (int64_t c = 0; c < N; c++) {
+        uint32_t ctr[4] = {0, (uint32_t)((uint64_t)c & 0xffffffffu), (uint32_t)((uint64_t)c >> 32), 1u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        s[c] = ((uint64_t)w[0] < thr_init) ? -1 : 1;
+    }
+    for (int64_t C = 0; C < NC; C++) {
+        uint32_t ctr[4] = {0, (uint32_t)((uint64_t)C & 0xffffffffu), (uint32_t)((uint64_t)C >> 32), 6u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        uint64_t W = bkl_weights(s, nx, ny, C % mx, C / mx, m, thr, cls);
+        T[C] = bkl_delta(w[2], w[3], lambda, W);
+        H[C] = (uint32_t)C;
+    }
+    for (int64_t i = NC / 2 - 1; i >= 0; i--) agg_sift(H, NC, T, i);
+    uint64_t arrivals = 0, flips = 0, hash = 0;
+    while (NC > 0) {
+        int64_t C = H[0];
+        if (T[C] >= T_q32) break;
+        int64_t X = C % mx, Y = C / mx;
+        uint32_t k = n[C];
+        uint32_t ctr[4] = {k, (uint32_t)((uint64_t)C & 0xffffffffu), (uint32_t)((uint64_t)C >> 32), 5u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        uint64_t W = bkl_weights(s, nx, ny, X, Y, m, thr, cls);
+        uint64_t Xr = ((uint64_t)w[0] << 32) | w[1];
+        uint64_t u = (uint64_t)(((unsigned __int128)Xr * W) >> 64);
+        uint64_t W0 = (uint64_t)(4 * m - 4) << 32;
+        int l = -1, ns = 0;
+        if (u < W0) {                                   /* boundary layer: the standard model */
+            uint64_t b = u >> 32, rem = u & 0xffffffffULL, cnt = 0;
+            for (int q = 0; q < m * m; q++)
+                if (cls[q] < 0 && cnt++ == b) { l = q; break; }
+            int64_t x = X * m + l % m, y = Y * m + l / m;
+            int sig = s[y * nx + (x + nx - 1) % nx] + s[y * nx + (x + 1) % nx] + s[((y + ny - 1) % ny) * nx + x] +
+                      s[((y + 1) % ny) * nx + x];
+            int sc = s[y * nx + x];
+            int idx = (sig + 4) / 2 + 5 * (sc + 1) / 2;
+            ns = sc;
+            if (rem < thr[idx]) { ns = -sc; flips++; }
+            s[y * nx + x] = (int8_t)ns;
+        } else {                                        /* kernel: BKL, the selected cell flips */
+            uint64_t o = u - W0;
+            int kc = 0;
+            for (; kc < 10; kc++) {
+                uint64_t cntk = 0;
+                for (int q = 0; q < m * m; q++) cntk += (cls[q] == kc);
+                uint64_t Wk = cntk * thr[kc];
+                if (o < Wk) break;
+                o -= Wk;
+            }
+            uint64_t r = o / thr[kc], cnt = 0;
+            for (int q = 0; q < m * m; q++)
+                if (cls[q] == kc && cnt++ == r) { l = q; break; }
+            int64_t x = X * m + l % m, y = Y * m + l / m;
+            ns = -s[y * nx + x];
+            s[y * nx + x] = (int8_t)ns;
+            flips++;
+        }
+        hash += oracle_mix64(T[C] ^ rotl64((uint64_t)C, 20) ^ rotl64((uint64_t)k, 44) ^ ((uint64_t)l << 1) ^
+                             (uint64_t)(ns > 0 ? 1 : 0));
+        uint64_t W2 = bkl_weights(s, nx, ny, X, Y, m, thr, cls);
+        T[C] += bkl_delta(w[2], w[3], lambda, W2);
+        n[C] = k + 1;
+        arrivals++;
+        agg_sift(H, NC, T, 0);
+    }
+    if (spins_out) memcpy(spins_out, s, (size_t)N);
+    if (T_out) memcpy(T_out, T, (size_t)NC * 8);
+    if (n_out) memcpy(n_out, n, (size_t)NC * 4);
+    if (st) {
+        memset(st, 0, sizeof *st);
+        st->arrivals = arrivals; st->flips = flips; st->event_hash = hash;
+        int64_t B = 0, M = 0;
+        for (int64_t y = 0; y < ny; y++)
+            for (int64_t x = 0; x < nx; x++) {
+                int v = s[y * nx + x];
+                M += v;
+                B += v * (s[y * nx + (x + 1) % nx] + s[((y + 1) % ny) * nx + x]);
+            }
+        st->bond_sum = B; st->magnetisation = M;
+    }
+    free(s); free(T); free(n); free(H);
+    return 0;
+}

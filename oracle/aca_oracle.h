@@ -109,6 +109,13 @@ int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, doubl
                    uint64_t seed, double init_q, uint64_t T_q32, int8_t* spins_out, uint64_t* T_out,
                    uint32_t* n_out, oracle_stats* st);
 
+/* Modified BKL (docs/PRIMITIVES.md P9): per m x m subarray (m = 2, 4, 8)
+ * the n-fold way on the kernel, the standard model on the boundary layer; same outputs as
+ * oracle_agg_run. */
+int oracle_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule,
+                   uint64_t seed, double init_q, uint64_t T_q32, int8_t* spins_out, uint64_t* T_out,
+                   uint32_t* n_out, oracle_stats* st);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: 
 EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
-           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run"]
+           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run"]
 POISSON, UNIFORM, ROOT8 = 0, 1, 2   # asynchrony laws (aca_options.law)
 
 
@@ -102,6 +102,7 @@ def lib():
     L.aca_agg_run.argtypes = [vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                               ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, vp,
                               ctypes.POINTER(aca_agg_stats), ctypes.c_int]
+    L.aca_bkl_run.argtypes = L.aca_agg_run.argtypes
     L.aca_run_frames.argtypes = [vp, ctypes.c_double, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]
     L.aca_efficiency_run.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
                                      ctypes.c_int64, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
@@ -269,9 +270,10 @@ class aca_agg_stats(ctypes.Structure):
 
 
 def aca_agg_run(dims, m, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=ACA_HEATBATH, seed=1, init_q=0.5, budget=64,
-                want_state=True, device=-1):
-    """Aggregated Poisson stream (fig:amcpoi) on the GPU: (spins[ny, nx], T[ntiles], n[ntiles],
-    stats) — the state arrays are None when want_state is False."""
+                want_state=True, device=-1, bkl=False):
+    """Aggregated Poisson stream (fig:amcpoi) on the GPU, or with bkl=True the modified BKL of
+    PAPER.md:1126-1191: (spins[ny, nx], T[ntiles], n[ntiles], stats) — the state arrays are
+    None when want_state is False."""
     nx, ny = int(dims[0]), int(dims[1])
     nt = (nx // m) * (ny // m) if nx % m == 0 and ny % m == 0 else 1
     d = (ctypes.c_int64 * 2)(nx, ny)
@@ -279,7 +281,8 @@ def aca_agg_run(dims, m, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=ACA_HEATBATH, 
     Tt = np.zeros(nt, np.uint64) if want_state else None
     nn = np.zeros(nt, np.uint32) if want_state else None
     st = aca_agg_stats()
-    _check(lib().aca_agg_run(ctypes.cast(d, ctypes.c_void_p), int(m), float(lam), float(beta), float(J), float(h),
+    fn = lib().aca_bkl_run if bkl else lib().aca_agg_run
+    _check(fn(ctypes.cast(d, ctypes.c_void_p), int(m), float(lam), float(beta), float(J), float(h),
                              int(rule), int(seed), float(init_q), float(T), int(budget),
                              _ptr(sp) if want_state else None, _ptr(Tt) if want_state else None,
                              _ptr(nn) if want_state else None, ctypes.byref(st), int(device)))

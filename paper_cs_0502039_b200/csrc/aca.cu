@@ -1302,11 +1302,13 @@ int aca_run_frames(aca_sim* S, double dt, int64_t K0, int64_t count, int B, uint
 }
 
 // ---------------------------------------------------------------- aggregated Poisson stream
-int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule, uint64_t seed,
-                double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
-                aca_agg_stats* st, int device) {
+static int agg_run_impl(bool bkl, const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule,
+                        uint64_t seed, double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out,
+                        uint32_t* n_out, aca_agg_stats* st, int device) {
     if (!dims) return fail(ACA_EINVAL, "null dims");
     if (m != 1 && m != 2 && m != 4 && m != 8) return fail(ACA_EINVAL, "m must be 1, 2, 4 or 8");
+    if (bkl && m == 1) return fail(ACA_EINVAL, "modified BKL needs m = 2, 4 or 8");
+    if (bkl && !(lambda >= 1e-6)) return fail(ACA_EINVAL, "modified BKL needs lambda >= 1e-6");
     const int64_t nx = dims[0], ny = dims[1];
     if (nx < 2 || ny < 2 || nx % m || ny % m || nx * ny > ((int64_t)1 << 32) || nx > (1 << 30) || ny > (1 << 30))
         return fail(ACA_EINVAL, "dims must be >= 2, multiples of m, N <= 2^32");
@@ -1336,6 +1338,14 @@ int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J
     flip_table(2, beta, J, h, rule, thr);
     for (int i = 0; i < 10; ++i) A.thr[i] = thr[i];
     A.thr_init = (unsigned long long)std::floor(init_q * 4294967296.0);
+    BklExtra E{};
+    E.lambda = lambda;
+    for (int l = 0; l < m * m; ++l) {
+        const int i = l % m, j = l / m;
+        if (i == 0 || j == 0 || i == m - 1 || j == m - 1) E.B |= 1ull << l;
+        else E.K |= 1ull << l;
+    }
+    E.W0 = (unsigned long long)__builtin_popcountll(E.B) << 32;
     const int64_t NC = (int64_t)A.mx * A.my;
     unsigned long long* dlr = nullptr;
     AggAcc* dacc = nullptr;
@@ -1366,12 +1376,14 @@ int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J
         int nsm = 148;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device >= 0 ? device : 0);
         const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((NC + 255) / 256, (long long)nsm * 8));
-        agg_init_kernel<<<grid, 256, 0, str>>>(A, dlr);
+        if (bkl) bkl_init_kernel<<<grid, 256, 0, str>>>(A, E, dlr);
+        else agg_init_kernel<<<grid, 256, 0, str>>>(A, dlr);
         cudaEventRecord(e0, str);
         for (int batch = 0;; ++batch) {
             for (int kk = 0; kk < 8; ++kk) {
                 if (kk == 7) cudaMemsetAsync(&dacc->active, 0, 16, str);   // active + blocked of the last launch
-                agg_round_kernel<<<grid, 256, 0, str>>>(A, dlr, dacc);
+                if (bkl) bkl_round_kernel<<<grid, 256, 0, str>>>(A, E, dlr, dacc);
+                else agg_round_kernel<<<grid, 256, 0, str>>>(A, dlr, dacc);
                 ++launches;
             }
             if (cudaMemcpyAsync(&hacc, dacc, sizeof(AggAcc), cudaMemcpyDeviceToHost, str) != cudaSuccess ||
@@ -1420,5 +1432,19 @@ int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J
     } while (0);
     cleanup();
     return rc;
+}
+
+int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule, uint64_t seed,
+                double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
+                aca_agg_stats* st, int device) {
+    return agg_run_impl(false, dims, m, lambda, beta, J, h, rule, seed, init_q, T, budget, spins_out, T_out, n_out, st,
+                        device);
+}
+
+int aca_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J, double h, int rule, uint64_t seed,
+                double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
+                aca_agg_stats* st, int device) {
+    return agg_run_impl(true, dims, m, lambda, beta, J, h, rule, seed, init_q, T, budget, spins_out, T_out, n_out, st,
+                        device);
 }
 }  // extern "C"

@@ -48,3 +48,21 @@ def test_agg_rejects_bad_arguments(aca):
     for dims, m in (((10, 8), 4), ((8, 8), 3), ((8, 8), 16)):
         with pytest.raises(aca.AcaError):
             aca.aca_agg_run(dims, m, 1.0)
+
+
+@pytest.mark.parametrize("dims,m", [((64, 64), 8), ((64, 48), 4), ((40, 24), 2), ((8, 8), 8), ((16, 8), 8),
+                                    ((256, 128), 8), ((4, 4), 4)])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_bkl_bit_identical(aca, oracle_mod, dims, m, rule):
+    """Modified BKL: bit-identical to its serial oracle for the partition."""
+    kw = dict(beta=0.44 if rule == 0 else 0.9, h=0.0 if rule == 0 else 0.1, rule=rule, seed=11 + m)
+    g = aca.aca_agg_run(dims, m, 6.0, budget=16, bkl=True, **kw)
+    o = oracle_mod.agg_run(dims, m, 6.0, bkl=True, **kw)
+    _same(g, o)
+
+
+@pytest.mark.parametrize("budget", [1, 1000])
+def test_bkl_budget_invariance(aca, oracle_mod, budget):
+    g = aca.aca_agg_run((96, 64), 8, 5.0, beta=0.6, rule=1, h=0.1, seed=78, budget=budget, bkl=True)
+    o = oracle_mod.agg_run((96, 64), 8, 5.0, beta=0.6, rule=1, h=0.1, seed=78, bkl=True)
+    _same(g, o)
