@@ -125,6 +125,24 @@ def ncu_traffic(kernel_tag):
         return None
 
 
+def issue_roofline(kernel_tag):
+    """Secondary roofline of the tile kernel, which is issue/ALU-bound: warp instructions issued
+    per second in the committed ncu --set full capture against the issue limit of the chip
+    (4 SMSPs x 1 warp-instruction/cycle per SM, B300_MICROARCH.md 'Per-warp issue scheduler';
+    148 SMs at the captured SM clock)."""
+    p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        d = json.load(open(p)).get(kernel_tag, {})
+        inst, ms, clk = d["warp_inst_per_launch"], d["launch_ms"], d["sm_clock_hz"]
+        ach = inst / (ms * 1e-3)
+        peak = 148 * 4 * clk
+        return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s", "frac": ach / peak,
+                "alu_pipe_frac": d.get("alu_pipe_pct", 0) / 100.0, "source": d.get("source"),
+                "note": "measured under ncu (cold cache, serialised), not in this run"}
+    except Exception:
+        return None
+
+
 def algorithmic_bytes_per_cell(ndim, tile):
     """Per launch (in place, 1-cell halo): read each cell's packed word (t, rank, n, s: 8 B)
     and write it back (8 B), plus the halo words of the tile faces. DESIGN.md 'Roofline'."""
@@ -301,6 +319,7 @@ def main():
                        "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
                        "event_hash": not args.no_hash},
             "roofline": roof,
+            "roofline_issue": issue_roofline(tag),
             "firing_fraction": fired / tested if tested else None,
             "arrivals_per_cell_per_sweep": (fired / launches / n_local) if launches else None,
             "gpu_launches": int(kl + 2 * args.steps),

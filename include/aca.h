@@ -216,6 +216,11 @@ int aca_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J
  * Errors: ACA_EINVAL (arguments), ACA_ENOMEM, ACA_ENODEV, ACA_ECUDA. */
 int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                        uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds);
+/* The same with the q-th degree neighbourhood neighbors^q (Eq. neiq: all
+ * cells within Manhattan distance q, |neighbors^q| - 1 = 2q(q+1) on the square array), q in
+ * [1, 8]; aca_efficiency_run is q = 1. */
+int aca_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds, int q,
+                         uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds);
 
 /* ---- Self-test hooks (device primitives through the ABI; host buffers, n elements) ----
  * P1: out[4n] = our Philox(ctr[4i..], key[2i..]); ref[4n] = cuRAND's device

@@ -113,6 +113,9 @@ def lib():
                                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.POINTER(Stats)]
         L.oracle_bkl_run.argtypes = L.oracle_agg_run.argtypes
+        L.oracle_efficiency_run_q.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
+                                              ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int,
+                                              ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_efficiency_run.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
                                             ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p,
                                             ctypes.c_void_p]
@@ -274,13 +277,14 @@ def window_cell(dims, center, T, radius, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=H
     return so.value, to.value, no.value, bool(ex.value)
 
 
-def efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False):
-    """Time-only model of PAPER.md:1355-1442: N0 per synchronous iteration (and final times)."""
+def efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False, q=1):
+    """Time-only model of PAPER.md:1355-1442 (q-th degree neighbourhood, Eq. neiq): N0 per
+    synchronous iteration (and final times)."""
     n = int(np.prod(dims))
     fired = np.zeros(rounds, np.uint64)
     t = np.zeros(n, np.uint64) if want_times else None
-    rc = lib().oracle_efficiency_run(len(dims), _dims(dims), law, lam, seed, rounds, fired.ctypes.data,
-                                     t.ctypes.data if want_times else None)
+    rc = lib().oracle_efficiency_run_q(len(dims), _dims(dims), law, lam, seed, rounds, q, fired.ctypes.data,
+                                       t.ctypes.data if want_times else None)
     assert rc == 0
     return (fired, t) if want_times else fired
 

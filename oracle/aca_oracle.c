@@ -608,6 +608,15 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
  * infrastructure only. Returns 0, or -1 on bad arguments. */
 int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                           uint64_t* fired_per_round, uint64_t* t_out) {
+    return oracle_efficiency_run_q(ndim, dims, law, lambda, seed, rounds, 1, fired_per_round, t_out);
+}
+
+/* q-th degree neighbourhood (Eq. neiq): neighbors^q(c) =
+ * neighbors(neighbors^(q-1)(c)), i.e. every cell within Manhattan distance q; a cell passes the
+ * test when its (t, c) is below all of them. q = 1 is the model above. */
+int oracle_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
+                            int q, uint64_t* fired_per_round, uint64_t* t_out) {
+    if (q < 1 || q > 8) return -1;
     if (ndim < 1 || ndim > 3 || law < 0 || law > 2 || !(lambda > 0) || rounds < 0) return -1;
     int64_t d[3] = {1, 1, 1}, N = 1;
     for (int a = 0; a < ndim; a++) { if (dims[a] < 2) return -1; d[a] = dims[a]; N *= dims[a]; }
@@ -626,16 +635,18 @@ int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda,
         for (int64_t c = 0; c < N; c++) {          /* test: all against the same times */
             int64_t x = c % d[0], y = (c / d[0]) % d[1], z = c / (d[0] * d[1]);
             int ok = 1;
-            for (int a = 0; a < ndim && ok; a++) {
-                for (int s = -1; s <= 1 && ok; s += 2) {
-                    int64_t xx = x, yy = y, zz = z;
-                    if (a == 0) xx = (x + s + d[0]) % d[0];
-                    if (a == 1) yy = (y + s + d[1]) % d[1];
-                    if (a == 2) zz = (z + s + d[2]) % d[2];
-                    int64_t nb = (zz * d[1] + yy) * d[0] + xx;
-                    if (!(t[c] < t[nb] || (t[c] == t[nb] && c < nb))) ok = 0;
-                }
-            }
+            int qy = ndim >= 2 ? q : 0, qz = ndim >= 3 ? q : 0;
+            for (int dz = -qz; dz <= qz && ok; dz++)
+                for (int dy = -qy; dy <= qy && ok; dy++)
+                    for (int dx = -q; dx <= q && ok; dx++) {
+                        int dist = (dx < 0 ? -dx : dx) + (dy < 0 ? -dy : dy) + (dz < 0 ? -dz : dz);
+                        if (dist == 0 || dist > q) continue;
+                        int64_t xx = ((x + dx) % d[0] + d[0]) % d[0];
+                        int64_t yy = ((y + dy) % d[1] + d[1]) % d[1];
+                        int64_t zz = ((z + dz) % d[2] + d[2]) % d[2];
+                        int64_t nb = (zz * d[1] + yy) * d[0] + xx;
+                        if (nb != c && !(t[c] < t[nb] || (t[c] == t[nb] && c < nb))) ok = 0;
+                    }
             fire[c] = (unsigned char)ok;
             n0 += (uint64_t)ok;
         }

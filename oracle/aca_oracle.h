@@ -101,6 +101,9 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
  * ndim 1..3, law P3L. fired_per_round[rounds] (N0 per iteration) and t_out[N] may be NULL. */
 int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                           uint64_t* fired_per_round, uint64_t* t_out);
+/* The same with the q-th degree neighbourhood (Eq. neiq: all cells within Manhattan distance q). */
+int oracle_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
+                            int q, uint64_t* fired_per_round, uint64_t* t_out);
 
 /* Aggregated Poisson stream (fig:amcpoi; docs/PRIMITIVES.md P8): 2-D torus
  * in m x m subarrays, one cumulative stream per subarray, serial (T(C), C) order. Outputs may

@@ -23,7 +23,7 @@ ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: 
 EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
-           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run"]
+           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q"]
 POISSON, UNIFORM, ROOT8 = 0, 1, 2   # asynchrony laws (aca_options.law)
 
 
@@ -103,6 +103,8 @@ def lib():
                               ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, vp,
                               ctypes.POINTER(aca_agg_stats), ctypes.c_int]
     L.aca_bkl_run.argtypes = L.aca_agg_run.argtypes
+    L.aca_efficiency_run_q.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
+                                       ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     L.aca_run_frames.argtypes = [vp, ctypes.c_double, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]
     L.aca_efficiency_run.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
                                      ctypes.c_int64, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
@@ -300,7 +302,7 @@ def aca_run_frames(p, dt, K0, count, B=4):
     return np.where(pm > 0, 1, -1).astype(np.int8)
 
 
-def aca_efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False, device=-1):
+def aca_efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False, device=-1, q=1):
     """Time-only efficiency model on the GPU: N0 per synchronous
     iteration (uint64[rounds]), the final times if asked, and the device seconds."""
     d = (ctypes.c_int64 * len(dims))(*[int(v) for v in dims])
@@ -308,9 +310,9 @@ def aca_efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=Fa
     n = int(np.prod(dims))
     t = np.zeros(n, np.uint64) if want_times else None
     sec = ctypes.c_double(0.0)
-    _check(lib().aca_efficiency_run(len(dims), ctypes.cast(d, ctypes.c_void_p), int(law), float(lam), int(seed),
-                                    int(rounds), _ptr(fired), _ptr(t) if want_times else None, int(device),
-                                    ctypes.byref(sec)))
+    _check(lib().aca_efficiency_run_q(len(dims), ctypes.cast(d, ctypes.c_void_p), int(law), float(lam), int(seed),
+                                      int(rounds), int(q), _ptr(fired), _ptr(t) if want_times else None, int(device),
+                                      ctypes.byref(sec)))
     return (fired, t, sec.value) if want_times else (fired, sec.value)
 
 

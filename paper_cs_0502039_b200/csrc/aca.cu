@@ -1158,7 +1158,13 @@ int aca_selftest_nlog(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* delt
 // ---------------------------------------------------------------- time-only efficiency model
 int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                        uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds) {
+    return aca_efficiency_run_q(ndim, dims, law, lambda, seed, rounds, 1, fired_per_round, t_out, device, gpu_seconds);
+}
+
+int aca_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds, int q,
+                         uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds) {
     if (ndim < 1 || ndim > 3 || !dims) return fail(ACA_EINVAL, "ndim must be 1, 2 or 3");
+    if (q < 1 || q > 8) return fail(ACA_EINVAL, "q must be in [1, 8]");
     if (law < 0 || law > 2) return fail(ACA_EINVAL, "law must be 0, 1 or 2");
     if (!(lambda > 0) || !std::isfinite(lambda)) return fail(ACA_EINVAL, "lambda must be > 0");
     if (rounds < 0 || rounds > (int64_t)1 << 31) return fail(ACA_EINVAL, "rounds out of range");
@@ -1178,7 +1184,8 @@ int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, ui
     philox_round_keys((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), P.rk);
     P.inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
     P.law = law;
-    const bool small = N < ((int64_t)1 << 32);   // 32-bit indices: Lemire division, compacted kernel
+    P.q = q;
+    const bool small = N < ((int64_t)1 << 32) && q == 1;   // 32-bit indices: Lemire division, compacted kernel
     auto recip = [](unsigned long long d) { return (unsigned long long)(~0ull / d) + 1ull; };   // ceil(2^64/d), d >= 2
     P.mx = recip((unsigned long long)P.nx);
     P.my = recip((unsigned long long)P.ny < 2 ? 2ull : (unsigned long long)P.ny);

@@ -23,6 +23,7 @@ struct EffParams {
     uint32_t rk[20];
     unsigned long long inv_lambda;
     int law;
+    int q;                               // neighbourhood degree (Eq. neiq): Manhattan radius
 };
 
 __global__ void __launch_bounds__(256) eff_init_kernel(unsigned long long* __restrict__ t, const EffParams P,
@@ -54,21 +55,21 @@ __global__ void __launch_bounds__(256) eff_round_kernel(const unsigned long long
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < P.N; c += (long long)gridDim.x * blockDim.x) {
         const unsigned long long t = tin[c];
         const long long x = c % P.nx;
-        const long long row = c - x;
-        const long long xm = row + (x == 0 ? P.nx - 1 : x - 1), xp = row + (x == P.nx - 1 ? 0 : x + 1);
-        bool ok = lex_below(t, c, __ldg(tin + xm), xm) && lex_below(t, c, __ldg(tin + xp), xp);
-        if (NDIM >= 2) {
-            const long long y = (c / P.nx) % P.ny;
-            const long long ym = c + ((y == 0 ? P.ny - 1 : y - 1) - y) * P.nx;
-            const long long yp = c + ((y == P.ny - 1 ? 0 : y + 1) - y) * P.nx;
-            ok = ok && lex_below(t, c, __ldg(tin + ym), ym) && lex_below(t, c, __ldg(tin + yp), yp);
-        }
-        if (NDIM == 3) {
-            const long long z = c / nxy;
-            const long long zm = c + ((z == 0 ? P.nz - 1 : z - 1) - z) * nxy;
-            const long long zp = c + ((z == P.nz - 1 ? 0 : z + 1) - z) * nxy;
-            ok = ok && lex_below(t, c, __ldg(tin + zm), zm) && lex_below(t, c, __ldg(tin + zp), zp);
-        }
+        const long long y = NDIM >= 2 ? (c / P.nx) % P.ny : 0;
+        const long long z = NDIM == 3 ? c / nxy : 0;
+        bool ok = true;
+        const int q = P.q, qy = NDIM >= 2 ? q : 0, qz = NDIM == 3 ? q : 0;
+        for (int dz = -qz; dz <= qz && ok; ++dz)
+            for (int dy = -qy; dy <= qy && ok; ++dy)
+                for (int dx = -q; dx <= q && ok; ++dx) {
+                    const int dist = abs(dx) + abs(dy) + abs(dz);
+                    if (dist == 0 || dist > q) continue;
+                    const long long xx = ((x + dx) % P.nx + P.nx) % P.nx;
+                    const long long yy = NDIM >= 2 ? ((y + dy) % P.ny + P.ny) % P.ny : 0;
+                    const long long zz = NDIM == 3 ? ((z + dz) % P.nz + P.nz) % P.nz : 0;
+                    const long long nb = (zz * P.ny + yy) * P.nx + xx;
+                    if (nb != c) ok = lex_below(t, c, __ldg(tin + nb), nb);
+                }
         unsigned long long tn = t;
         if (ok) {
             const u32x4 r = philox4x32_10_rk(round, (uint32_t)c, (uint32_t)((unsigned long long)c >> 32), 2u, P.rk);

@@ -60,7 +60,8 @@ def full(path):
 def num(s):
     v, u = s.split(" ", 1)
     v = float(v.replace(",", ""))
-    mult = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}.get(u.strip(), 1.0)
+    mult = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12, "Ghz": 1e9, "Mhz": 1e6,
+            "hz": 1.0}.get(u.strip(), 1.0)
     return v * mult
 
 
@@ -89,8 +90,17 @@ def main():
         wb = sum(num(c["dram__bytes_write.sum"]) for c in F) / len(F)
         summ = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
         cur = json.load(open(summ)) if os.path.exists(summ) else {}
+        def avg(key):
+            vals = [num(c[key]) for c in F if key in c]
+            return sum(vals) / len(vals) if vals else None
+        dur = avg("gpu__time_duration.sum")   # in the unit ncu printed (ms)
         cur[ktag] = {"dram_bytes_per_launch": rb + wb, "dram_read": rb, "dram_write": wb,
                      "launches_per_sweep": per_sweep, "dram_bytes_per_sweep": (rb + wb) * per_sweep,
+                     "warp_inst_per_launch": avg("smsp__inst_executed.sum"),
+                     "launch_ms": dur,
+                     "issue_active_pct": avg("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                     "alu_pipe_pct": avg("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                     "sm_clock_hz": avg("sm__cycles_elapsed.avg.per_second"),
                      "source": "profiles/%s" % tag}
         json.dump(cur, open(summ, "w"), indent=1)
     print("wrote", d)

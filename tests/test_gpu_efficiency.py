@@ -43,3 +43,12 @@ def test_efficiency_rejects_bad_arguments(aca):
     for dims, law in (((1,), 0), ((4, 4), 3)):
         with pytest.raises(aca.AcaError):
             aca.aca_efficiency_run(dims, 5, law=law)
+
+
+@pytest.mark.parametrize("dims", [(9,), (1000,), (40, 30), (13, 7), (10, 8, 6)])
+@pytest.mark.parametrize("q", [2, 3])
+def test_efficiency_q_bit_identical(aca, oracle_mod, dims, q):
+    """q-th degree neighbourhood (Eq. neiq): every N0 and final time."""
+    f_g, t_g, _ = aca.aca_efficiency_run(dims, 80, law=0, seed=41, want_times=True, q=q)
+    f_o, t_o = oracle_mod.efficiency_run(dims, 80, law=0, seed=41, want_times=True, q=q)
+    assert np.array_equal(f_g, f_o) and np.array_equal(t_g, t_o)

@@ -55,3 +55,39 @@ def test_efficiency_rate_invariance(oracle_mod):
     a = oracle_mod.efficiency_run((32, 32), 100, law=1, lam=1.0, seed=9)
     b = oracle_mod.efficiency_run((32, 32), 100, law=1, lam=0.5, seed=9)
     assert np.array_equal(a, b)
+
+
+def _neighbors_q(q, L=31):
+    """Eq. neiq taken literally on an L x L torus: neighbors^1(c) = c and
+    its 4 neighbours; neighbors^q = neighbors(neighbors^(q-1))."""
+    def nb(c):
+        x, y = c
+        return {c, ((x - 1) % L, y), ((x + 1) % L, y), (x, (y - 1) % L), (x, (y + 1) % L)}
+    S = {(0, 0)}
+    for _ in range(q):
+        S = set().union(*(nb(c) for c in S))
+    return S
+
+
+@pytest.mark.parametrize("q", [1, 2, 3, 4])
+def test_neighbourhood_q_definition(q):
+    """|neighbors^q(c)| - 1 = 2q(q+1), and the set is exactly the cells
+    within Manhattan distance q — the set the oracle's test loops over."""
+    S = _neighbors_q(q)
+    assert len(S) - 1 == 2 * q * (q + 1)
+    L = 31
+    diamond = {((dx) % L, (dy) % L) for dx in range(-q, q + 1) for dy in range(-q, q + 1) if abs(dx) + abs(dy) <= q}
+    assert S == diamond
+
+
+def test_efficiency_q_special_cases(oracle_mod):
+    """q = 1 is the plain model; an n-circle with q >= (n-1)/2 is one neighbourhood, so exactly
+    the global minimum fires each iteration; efficiency falls with q ("low efficiency",
+    PAPER.md:1011-1020)."""
+    a = oracle_mod.efficiency_run((40, 30), 120, seed=4)
+    b = oracle_mod.efficiency_run((40, 30), 120, seed=4, q=1)
+    assert np.array_equal(a, b)
+    for n, q in ((9, 4), (10, 5), (5, 2)):
+        assert set(oracle_mod.efficiency_run((n,), 80, seed=2, q=q).tolist()) == {1}
+    effs = [oracle_mod.efficiency_run((96, 96), 300, seed=6, q=q)[100:].mean() / 96 ** 2 for q in (1, 2, 3)]
+    assert effs[0] > effs[1] > effs[2] > 0
