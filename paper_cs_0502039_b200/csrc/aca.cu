@@ -1186,6 +1186,8 @@ int aca_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, 
     P.law = law;
     P.q = q;
     const bool small = N < ((int64_t)1 << 32) && q == 1;   // 32-bit indices: Lemire division, compacted kernel
+    bool stream2d = true;                                   // 2-D row-streaming kernel (ACA_EFF_STREAM=0: off)
+    if (const char* e = getenv("ACA_EFF_STREAM")) stream2d = atoi(e) != 0;
     auto recip = [](unsigned long long d) { return (unsigned long long)(~0ull / d) + 1ull; };   // ceil(2^64/d), d >= 2
     P.mx = recip((unsigned long long)P.nx);
     P.my = recip((unsigned long long)P.ny < 2 ? 2ull : (unsigned long long)P.ny);
@@ -1220,7 +1222,10 @@ int aca_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, 
         for (int64_t r = 0; r < rounds; ++r) {
             const unsigned long long* tin = (r & 1) ? b : a;
             unsigned long long* tout = (r & 1) ? a : b;
-            if (small) {
+            if (small && ndim == 2 && stream2d) {
+                const dim3 g2((unsigned)((P.nx + EFF_W - 1) / EFF_W), (unsigned)((P.ny + EFF_H - 1) / EFF_H));
+                eff_round_kernel_2d<<<g2, EFF_W, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
+            } else if (small) {
                 if (ndim == 1) eff_round_kernel_c<1><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
                 else if (ndim == 2) eff_round_kernel_c<2><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);
                 else eff_round_kernel_c<3><<<grid, 256, 0, st>>>(tin, tout, P, dlr, (uint32_t)r, fired);

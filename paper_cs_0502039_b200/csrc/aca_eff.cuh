@@ -185,4 +185,117 @@ __global__ void __launch_bounds__(256) eff_round_kernel_c(const unsigned long lo
     }
 }
 
+// Row-streaming iteration for 2-D tori (N < 2^32, q = 1): a CTA of EFF_W threads owns a strip
+// of EFF_W columns and a band of EFF_H rows; each thread owns one column and keeps the times
+// of rows y-1, y, y+1 in registers, so every time is read from HBM once per iteration (plus
+// two halo rows per band and two halo columns per row); the x-neighbours come from a
+// double-buffered shared row (one barrier per row). Firing cells are queued per warp and drawn
+// together every EFF_G rows by all warps at once (full lanes; a per-warp schedule would make
+// every row's barrier wait for some warp's draws). Same results as eff_round_kernel_c.
+constexpr int EFF_W = 256, EFF_H = 64, EFF_G = 8;
+
+__global__ void __launch_bounds__(EFF_W) eff_round_kernel_2d(const unsigned long long* __restrict__ tin,
+                                                              unsigned long long* __restrict__ tout, const EffParams P,
+                                                              const unsigned long long* __restrict__ lr_g,
+                                                              uint32_t round, unsigned long long* __restrict__ fired) {
+    __shared__ unsigned long long lr[512];
+    __shared__ unsigned long long row[2][EFF_W + 2];           // [0] left halo, [1..W] strip, [W+1] right halo
+    __shared__ uint32_t qc[EFF_W / 32][32 * EFF_G];
+    __shared__ unsigned long long qt[EFF_W / 32][32 * EFF_G];
+    __shared__ unsigned int red[EFF_W / 32];
+    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nx = (uint32_t)P.nx, ny = (uint32_t)P.ny;
+    const uint32_t x0 = blockIdx.x * EFF_W, yb = blockIdx.y * EFF_H;
+    const uint32_t x = x0 + threadIdx.x;
+    const bool inx = x < nx;
+    const uint32_t ye = min(yb + EFF_H, ny);
+    const uint32_t xl = x == 0 ? nx - 1 : x - 1, xr = x + 1 == nx ? 0 : x + 1;
+    // the strip's neighbour columns: in the shared row when they fall inside the strip
+    const bool l_in = inx && xl >= x0 && xl < x0 + EFF_W, r_in = inx && xr >= x0 && xr < x0 + EFF_W;
+    const int l_slot = l_in ? (int)(xl - x0) + 1 : 0, r_slot = r_in ? (int)(xr - x0) + 1 : EFF_W + 1;
+    // halo columns: the only outside neighbours a strip's threads can have
+    const uint32_t xhl = x0 == 0 ? nx - 1 : x0 - 1;
+    const uint32_t xhr = x0 + EFF_W < nx ? x0 + EFF_W : 0;
+    auto row_of = [&](uint32_t yy) { return yy >= ny ? yy - ny : yy; };
+    // registers: rows y-1, y, y+1 of the thread's column, and a prefetch ring of the next rows
+    // (memory-level parallelism); the edge threads also prefetch their halo column
+    constexpr int PF = 4;
+    unsigned long long tu = 0, tm = 0, td = 0, pf[PF];
+    if (inx) {
+        const uint32_t yu = yb == 0 ? ny - 1 : yb - 1;
+        tu = tin[(size_t)yu * nx + x];
+        tm = tin[(size_t)yb * nx + x];
+#pragma unroll
+        for (int k = 0; k < PF; ++k) pf[k] = tin[(size_t)row_of(yb + 1 + k) * nx + x];
+    }
+    const bool hthr = threadIdx.x == 0 || threadIdx.x == EFF_W - 1;
+    const uint32_t xh = threadIdx.x == 0 ? xhl : xhr;
+    unsigned long long ph[PF + 1];
+    if (hthr) {
+#pragma unroll
+        for (int k = 0; k <= PF; ++k) ph[k] = tin[(size_t)row_of(yb + k) * nx + xh];
+    }
+    unsigned int n0 = 0;
+    int qn = 0;                                                      // warp queue length (uniform)
+    int buf = 0;
+    for (uint32_t y = yb; y < ye; ++y) {
+        const uint32_t ydn = y + 1 == ny ? 0 : y + 1;
+        const uint32_t yup = y == 0 ? ny - 1 : y - 1;
+        if (inx) {
+            td = pf[0];
+#pragma unroll
+            for (int k = 0; k < PF - 1; ++k) pf[k] = pf[k + 1];
+            if (y + 1 + PF < ye + 1) pf[PF - 1] = tin[(size_t)row_of(y + 1 + PF) * nx + x];
+        }
+        row[buf][threadIdx.x + 1] = tm;
+        if (hthr) {
+            row[buf][threadIdx.x == 0 ? 0 : EFF_W + 1] = ph[0];
+#pragma unroll
+            for (int k = 0; k < PF; ++k) ph[k] = ph[k + 1];
+            if (y + 1 + PF < ye) ph[PF] = tin[(size_t)row_of(y + 1 + PF) * nx + xh];
+        }
+        __syncthreads();
+        bool ok = false;
+        const uint32_t c = y * nx + x;
+        if (inx) {
+            const unsigned long long tl = row[buf][l_slot], tr = row[buf][r_slot];
+            const uint32_t cl = y * nx + xl, cr = y * nx + xr, cu = yup * nx + x, cd = ydn * nx + x;
+            ok = lex_below(tm, c, tl, cl) && lex_below(tm, c, tr, cr) && lex_below(tm, c, tu, cu) &&
+                 lex_below(tm, c, td, cd);
+            if (!ok) tout[c] = tm;
+        }
+        // queue the firing cells of this row (warp ballot)
+        const unsigned int bm = __ballot_sync(0xffffffffu, ok);
+        if (ok) {
+            const int pos = qn + __popc(bm & ((1u << lane) - 1u));
+            qc[warp][pos] = c;
+            qt[warp][pos] = tm;
+        }
+        qn += __popc(bm);
+        if ((y - yb) % EFF_G == EFF_G - 1 || y + 1 == ye) {          // all warps draw together (same row)
+            __syncwarp();
+            for (int i = lane; i < qn; i += 32) {
+                const uint32_t cc = qc[warp][i];
+                const u32x4 r = philox4x32_10_rk(round, cc, 0u, 2u, P.rk);
+                tout[cc] = qt[warp][i] + delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, 0, P.law);
+            }
+            n0 += lane == 0 ? (unsigned int)qn : 0u;
+            qn = 0;
+            __syncwarp();
+        }
+        tu = tm;
+        tm = td;
+        buf ^= 1;
+    }
+    for (int o = 16; o > 0; o >>= 1) n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+    if (lane == 0) red[warp] = n0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long sacc = 0;
+        for (int w = 0; w < EFF_W / 32; ++w) sacc += red[w];
+        atomicAdd(fired + round, sacc);
+    }
+}
+
 }  // namespace aca

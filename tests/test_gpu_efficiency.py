@@ -52,3 +52,12 @@ def test_efficiency_q_bit_identical(aca, oracle_mod, dims, q):
     f_g, t_g, _ = aca.aca_efficiency_run(dims, 80, law=0, seed=41, want_times=True, q=q)
     f_o, t_o = oracle_mod.efficiency_run(dims, 80, law=0, seed=41, want_times=True, q=q)
     assert np.array_equal(f_g, f_o) and np.array_equal(t_g, t_o)
+
+
+@pytest.mark.parametrize("dims", [(700, 300), (256, 64), (257, 65), (33, 130)])
+def test_efficiency_2d_streaming_kernel(aca, oracle_mod, dims):
+    """The 2-D row-streaming kernel (strips of 256 columns, bands of 64 rows, partial strips and
+    bands, halo columns across strips and the periodic wrap) equals the oracle."""
+    f_g, t_g, _ = aca.aca_efficiency_run(dims, 60, law=1, seed=43, want_times=True)
+    f_o, t_o = oracle_mod.efficiency_run(dims, 60, law=1, seed=43, want_times=True)
+    assert np.array_equal(f_g, f_o) and np.array_equal(t_g, t_o)
