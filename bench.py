@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--launches-per-check", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0, help="tile kernel variant (ablation; 0 = default)")
     ap.add_argument("--early-reject", type=int, default=-1, help="a10 early rejection (-1 = config default)")
+    ap.add_argument("--checkerboard", type=int, default=0, help="1/0 = checkerboard sweeps (default), -1 = off")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true", help="skip the P7 event hash (diagnostics only)")
@@ -242,6 +243,8 @@ def main():
         opts["launches_per_check"] = args.launches_per_check
     if args.variant:
         opts["variant"] = args.variant
+    if args.checkerboard:
+        opts["checkerboard"] = args.checkerboard
     stream = torch.cuda.Stream()            # non-default stream: the library captures CUDA graphs on it
     torch.cuda.set_stream(stream)
     opts["stream"] = stream.cuda_stream
@@ -313,7 +316,8 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
                        "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
-                       "tile": list(tile), "rounds_per_tile_visit": args.rounds or 4, "variant": args.variant,
+                       "tile": list(tile), "rounds_per_tile_visit": args.rounds or cfg.get("opts", {}).get("rounds_per_launch", 4),
+                       "variant": args.variant,
                        "sweep": "checkerboard: 2 kernel launches per outer round (tile colours 0, 1)",
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
                        "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
