@@ -35,7 +35,10 @@ extern "C" {
 
 typedef struct aca_sim aca_sim; /* opaque, library-owned */
 
-enum { ACA_HEATBATH = 0, ACA_METROPOLIS = 1 };
+/* next_state rules: Glauber heat-bath and Metropolis Ising (P4), and rule 2, the asynchronous
+ * Game of Life (P10): Conway's B3/S23 rule on the Moore neighbourhood, a
+ * deterministic next_state (2-D only; the Philox draw then only gives the increment). */
+enum { ACA_HEATBATH = 0, ACA_METROPOLIS = 1, ACA_LIFE = 2 };
 
 enum {
     ACA_OK = 0,

@@ -82,6 +82,7 @@ def lib():
         L.oracle_run_until_sync_naive_leq.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
         L.oracle_run_until_sync_naive_leq.restype = ctypes.c_int64
         L.oracle_get_spins.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+        L.oracle_set_spins.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_get_times.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_get_counters.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_get_stats.argtypes = [ctypes.c_void_p, ctypes.POINTER(Stats)]
@@ -225,6 +226,11 @@ class OracleSim:
         if rc != 0:
             raise ValueError("T decreased")
         return rc
+
+    def set_spins(self, spins):
+        a = np.ascontiguousarray(np.asarray(spins, np.int8).ravel())
+        assert a.size == self.N
+        lib().oracle_set_spins(self._p, a.ctypes.data)
 
     def spins(self):
         a = np.empty(self.N, np.int8)

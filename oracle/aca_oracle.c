@@ -141,7 +141,9 @@ struct oracle_sim {
 
 int64_t oracle_num_cells(const oracle_sim* s) { return s->N; }
 
-/* neighbours of c with multiplicity, order -x,+x,-y,+y[,-z,+z]; periodic. */
+/* neighbours of c with multiplicity, order -x,+x,-y,+y[,-z,+z]; periodic.
+ * rule 2 (asynchronous Game of Life, P10): the 8 Moore neighbours, the same four first, then
+ * (-x,-y), (+x,-y), (-x,+y), (+x,+y). */
 static int neighbours(const oracle_sim* S, int64_t c, int64_t* nb) {
     int64_t nx = S->dims[0], ny = S->dims[1];
     int64_t x = c % nx, y = (c / nx) % ny, zz = (S->ndim == 3) ? c / (nx * ny) : 0;
@@ -155,6 +157,10 @@ static int neighbours(const oracle_sim* S, int64_t c, int64_t* nb) {
         int64_t nz = S->dims[2];
         nb[4] = ((zz + nz - 1) % nz) * nx * ny + y * nx + x;
         nb[5] = ((zz + 1) % nz) * nx * ny + y * nx + x;
+    }
+    if (S->rule == 2) {
+        int64_t xm = (x + nx - 1) % nx, xp = (x + 1) % nx, ym = (y + ny - 1) % ny, yp = (y + 1) % ny;
+        nb[4] = ym * nx + xm; nb[5] = ym * nx + xp; nb[6] = yp * nx + xm; nb[7] = yp * nx + xp;
     }
     return S->zc;
 }
@@ -174,14 +180,14 @@ oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, doub
     if (ndim != 2 && ndim != 3) return NULL;
     if (law < 0 || law > 2) return NULL;
     if (!(lambda > 0) || !isfinite(lambda) || !(beta >= 0) || !isfinite(beta)) return NULL;
-    if (rule != 0 && rule != 1) return NULL;
+    if (rule != 0 && rule != 1 && !(rule == 2 && ndim == 2)) return NULL;
     if (!(init_q >= 0 && init_q <= 1)) return NULL;
     if (tie_bits < 0 || tie_bits > 40) return NULL;
     int64_t N = 1;
     for (int a = 0; a < ndim; a++) { if (dims[a] < 2) return NULL; N *= dims[a]; }
     if (N >= (1LL << 32)) return NULL;
     oracle_sim* S = (oracle_sim*)calloc(1, sizeof(oracle_sim));
-    S->ndim = ndim; S->zc = 2 * ndim; S->N = N;
+    S->ndim = ndim; S->zc = rule == 2 ? 8 : 2 * ndim; S->N = N;
     for (int a = 0; a < 3; a++) S->dims[a] = a < ndim ? dims[a] : 1;
     S->lambda = lambda; S->beta = beta; S->J = J; S->h = h; S->rule = rule;
     S->seed = seed; S->init_q = init_q; S->tie_bits = tie_bits; S->law = law;
@@ -217,17 +223,23 @@ void oracle_destroy(oracle_sim* S) {
  * flip iff w0 < thr[idx], then t += Delta, n += 1. new_s / new_t are returned so the
  * synchronous variant can commit them later. */
 static void arrival(oracle_sim* S, int64_t c, int8_t* new_s, uint64_t* new_t) {
-    int64_t nb[6];
+    int64_t nb[8];
     int z = neighbours(S, c, nb);
     int sigma = 0;
     for (int j = 0; j < z; j++) sigma += S->s[nb[j]];
     int sc = S->s[c];
-    int idx = (sigma + z) / 2 + (z + 1) * (sc + 1) / 2;
     uint32_t k = S->n[c];
     uint32_t w[4];
     draw(S, k, c, 0u, w);
     int ns = sc;
-    if ((uint64_t)w[0] < S->thr[idx]) { ns = -sc; S->flips++; }
+    if (S->rule == 2) {   /* P10: Conway's rule on the Moore neighbourhood, deterministic */
+        int live = (sigma + z) / 2;
+        ns = (live == 3 || (sc > 0 && live == 2)) ? 1 : -1;
+        if (ns != sc) S->flips++;
+    } else {
+        int idx = (sigma + z) / 2 + (z + 1) * (sc + 1) / 2;
+        if ((uint64_t)w[0] < S->thr[idx]) { ns = -sc; S->flips++; }
+    }
     uint64_t tev = S->t[c];
     S->event_hash += oracle_mix64(tev ^ rotl64((uint64_t)c, 20) ^ rotl64((uint64_t)k, 44) ^
                                   (uint64_t)(ns > 0 ? 1 : 0));
@@ -282,7 +294,7 @@ int oracle_run_until_q32(oracle_sim* S, uint64_t T) {
  * fig:s1c1pe without a tie-break, which lets tied neighbours fire in the same round. */
 static int eligible_rule(const oracle_sim* S, int64_t c, uint64_t T, int naive_leq) {
     if (S->t[c] >= T) return 0;
-    int64_t nb[6];
+    int64_t nb[8];
     int z = neighbours(S, c, nb);
     for (int j = 0; j < z; j++) {
         if (naive_leq ? !(S->t[c] <= S->t[nb[j]]) : !lex_less(S, c, nb[j])) return 0;
@@ -313,7 +325,7 @@ int oracle_run_until_random_order(oracle_sim* S, uint64_t T, uint64_t choice_see
         int8_t ns; uint64_t nt;
         arrival(S, c, &ns, &nt);
         S->s[c] = ns; S->t[c] = nt; S->n[c] += 1;
-        int64_t touch[7];
+        int64_t touch[9];
         touch[0] = c;
         int z = neighbours(S, c, touch + 1);
         for (int j = 0; j <= z; j++) {
@@ -375,7 +387,7 @@ void oracle_get_counters(const oracle_sim* S, uint32_t* out) { memcpy(out, S->n,
  * (PAPER.md:1680): B counts each bond once along +e_a, periodic. */
 void oracle_get_stats(const oracle_sim* S, oracle_stats* o) {
     memset(o, 0, sizeof(*o));
-    int64_t nb[6];
+    int64_t nb[8];
     uint64_t tmin = ~0ULL, tmax = 0, arr = 0;
     int64_t B = 0, M = 0;
     for (int64_t c = 0; c < S->N; c++) {
@@ -492,6 +504,7 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
                        uint64_t seed, double init_q, int tie_bits, uint64_t T, const int64_t* center,
                        int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
                        int* exact_out, int law) {
+    if (rule == 2) return -1;   /* the window oracle covers the Ising rules only */
     int64_t D[3] = {1, 1, 1}, W[3] = {1, 1, 1}, lo[3] = {0, 0, 0};
     int fullax[3] = {1, 1, 1};
     int64_t NW = 1;
@@ -913,4 +926,9 @@ int oracle_bkl_run(const int64_t* dims, int m, double lambda, double beta, doubl
     }
     free(s); free(T); free(n); free(H);
     return 0;
+}
+
+/* Replace the spins (user-supplied initial configuration); times and counters unchanged. */
+void oracle_set_spins(oracle_sim* S, const int8_t* spins) {
+    for (int64_t c = 0; c < S->N; c++) S->s[c] = spins[c] > 0 ? 1 : -1;
 }

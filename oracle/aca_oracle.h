@@ -64,6 +64,7 @@ int64_t oracle_run_until_sync(oracle_sim* s, uint64_t T_q32, uint64_t* fired_per
 int64_t oracle_run_until_sync_naive_leq(oracle_sim* s, uint64_t T_q32);
 
 void oracle_get_spins(const oracle_sim* s, int8_t* out);
+void oracle_set_spins(oracle_sim* s, const int8_t* spins);
 void oracle_get_times(const oracle_sim* s, uint64_t* out);
 void oracle_get_counters(const oracle_sim* s, uint32_t* out);
 void oracle_get_stats(const oracle_sim* s, oracle_stats* out);

@@ -15,7 +15,7 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_PKG, "libaca.so")
 
-ACA_HEATBATH, ACA_METROPOLIS = 0, 1
+ACA_HEATBATH, ACA_METROPOLIS, ACA_LIFE = 0, 1, 2
 ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: "ACA_ENCCL",
           -5: "ACA_ESTATE", -6: "ACA_ERANGE", -7: "ACA_ENODEV"}
 

@@ -248,6 +248,7 @@ struct TileKey {
     int ndim, tx, ty, tz, nt;
     void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1];
     void* fn_early;   // variant 0 with the a10 early-rejection path compiled in
+    void* fn_life;    // variant 0 with the Moore neighbourhood (rule 2, 2-D only; nullptr in 3-D)
 };
 
 #define TK(ND, TX, TY, TZ, NT, MB, MBD, MBR, MBW)                                                         \
@@ -262,7 +263,8 @@ struct TileKey {
       tma_smem(ND, TX, TY, TZ, NT, 1, false, true), tma_smem(ND, TX, TY, TZ, NT, 1, true),              \
       tma_smem(ND, TX, TY, TZ, NT, 1, false, false, ND == 2 ? 2 : 1), tile_smem(ND, TX, TY, TZ, NT)},  \
      {true, false, true, true, true, true, false},                                                   \
-     (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>}
+     (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>,                            \
+     (ND == 2 ? (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, false, false, 1, (ND == 2)> : nullptr)}
 
 const TileKey kTiles[] = {
     TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 64, 1, 256, 4, 2, 3, 4),
@@ -309,6 +311,7 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.tiles_z = sh.tiles_z;
     P.phase = -1;
     P.fr = S->fr;
+    P.life = S->rule == ACA_LIFE ? 1 : 0;
     P.fast = (S->opt.law == 0 && S->inv_lambda == (1ull << 32) && S->opt.tie_bits == 0 && S->fr.nb == 0 &&
               S->N < ((int64_t)1 << 32)) ? 1 : 0;
     {   // parity of the shard's first tile row in global tile coordinates (colouring only)
@@ -560,7 +563,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         return fail(ACA_EINVAL, "lambda outside [2^-31, 2^32]");
     if (!(beta >= 0) || !std::isfinite(beta)) return fail(ACA_EINVAL, "beta must be >= 0 and finite");
     if (!std::isfinite(J) || !std::isfinite(h)) return fail(ACA_EINVAL, "J and h must be finite");
-    if (rule != ACA_HEATBATH && rule != ACA_METROPOLIS) return fail(ACA_EINVAL, "rule must be 0 or 1");
+    if (rule != ACA_HEATBATH && rule != ACA_METROPOLIS && !(rule == ACA_LIFE && ndim == 2))
+        return fail(ACA_EINVAL, "rule must be 0 (heat-bath), 1 (Metropolis) or 2 (Game of Life, 2-D)");
     aca_options opt;
     aca_default_options(&opt);
     if (opt_in) {
@@ -571,6 +575,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (!(opt.init_q >= 0 && opt.init_q <= 1)) return fail(ACA_EINVAL, "init_q must be in [0, 1]");
     if (opt.tie_bits < 0 || opt.tie_bits > 40) return fail(ACA_EINVAL, "tie_bits must be in [0, 40]");
     if (opt.law < 0 || opt.law > 2) return fail(ACA_EINVAL, "law must be 0 (Poisson), 1 (uniform) or 2 (r^1/8)");
+    if (rule == ACA_LIFE && (opt.early_reject || opt.sync_rounds))
+        return fail(ACA_EINVAL, "the Game of Life rule has no early rejection / sync-round kernel");
     if (opt.shards < 1) opt.shards = 1;
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(ACA_EINVAL, "bad rank/world");
     if ((opt.world > 1 || opt.nccl_id) && opt.shards != 1)
@@ -628,7 +634,10 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->thr_init = (unsigned long long)std::floor(opt.init_q * 4294967296.0);
     uint64_t max_rank = 0;
     for (int a = 0; a < ndim; ++a) max_rank += (uint64_t)(dims[a] - 1);
-    S->RB = bits_for(max_rank);
+    // rule 2 (Moore neighbourhood): the rank x + y cannot order diagonal neighbours across the
+    // periodic boundary, so it is left out of the word (RB = 0) and the kernels break time ties
+    // by comparing cell ids explicitly
+    S->RB = rule == ACA_LIFE ? 0 : bits_for(max_rank);
     {
         // largest unscaled increment of the law: NLOG-2(1) for Poisson, < 2^32 otherwise
         const unsigned long long umax = opt.law == 0 ? 190530846196ull : (1ull << 32);
@@ -692,11 +701,12 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         const int v = S->sync ? NVARIANT : opt.variant;
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
         S->kern = ((v == 0 || v == 5) && opt.early_reject) ? sel->fn_early : sel->fn[v];
+        if (rule == ACA_LIFE) S->kern = sel->fn_life;   // V0 with the Moore neighbourhood (any variant)
         S->nthreads = sel->nt;
-        S->smem = sel->smem[v];
+        S->smem = rule == ACA_LIFE ? sel->smem[0] : sel->smem[v];
         if ((v == 0 || v == 5) && opt.early_reject)   // a10 candidates need a full per-warp queue
             S->smem = tma_smem(ndim, tx, ty, tz, sel->nt, 1, false, true);
-        if (sel->persistent[v]) {   // persistent: as many CTAs as fit on the device at once
+        if (rule == ACA_LIFE ? true : sel->persistent[v]) {   // persistent: as many CTAs as fit on the device
             if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
                 return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
             int nsm = 0, occ = 0;

@@ -109,6 +109,7 @@ struct KParams {
     unsigned long long thm[98];          // a10 table, see commit_loop (2 (Z+1)^2 entries)
     FrameParams fr;                      // output frames (off unless aca_run_frames)
     int fast;                            // fire_fast applies (law 0, lambda 1, no ties, no frames, N < 2^32)
+    int life;                            // rule 2: asynchronous Game of Life (Moore neighbourhood, P10)
 };
 
 __device__ __forceinline__ int wrapi(int v, int n) {
@@ -200,7 +201,9 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
     const uint32_t sb = (uint32_t)(w & 1ull);
     const uint32_t idx = ones + (uint32_t)(z + 1) * sb;          // (Sigma+z)/2 + (z+1)(s+1)/2
     const u32x4 r = philox4x32_10_rk(k, (uint32_t)c, (uint32_t)(c >> 32), 0u, rk);
-    const uint32_t flip = (unsigned long long)r.x < thr[idx] ? 1u : 0u;
+    // z = 8: asynchronous Game of Life (P10), Conway's rule on the Moore neighbourhood
+    const uint32_t flip = z == 8 ? ((ones == 3u || (sb && ones == 2u)) ? 1u : 0u) ^ sb
+                                 : ((unsigned long long)r.x < thr[idx] ? 1u : 0u);
     const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
     o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;   // t += d, n += 1, s ^= flip
     o.flip = flip;
@@ -256,6 +259,14 @@ __device__ __forceinline__ unsigned long long cell_id(const Geo& g, int gx, int 
                        : ((unsigned long long)(gz + g.z0) * g.NY + gy) * g.nx + gx;
 }
 
+// Global row-major id of the cell at shard-local coordinates (gx, gy) of a 2-D shard, wrapped
+// periodically (the explicit (t, c) tie-break of the Moore neighbourhood, where the packed
+// rank cannot order diagonal neighbours across the periodic boundary).
+__device__ __forceinline__ long long id2(const Geo& g, int gx, int gy) {
+    const int x = wrapi(gx, g.nx), y = wrapi(gy + g.y0, g.NY);
+    return (long long)y * g.nx + x;
+}
+
 // 32-bit cell id (N < 2^32; the Philox counter word c_hi is then 0)
 __device__ __forceinline__ uint32_t cell_id32(const Geo& g, int gx, int gy, int gz) {
     return g.ndim == 2 ? (uint32_t)(gy + g.y0) * (uint32_t)g.nx + (uint32_t)gx
@@ -274,7 +285,8 @@ __device__ __forceinline__ FireOut fire_fast(unsigned long long w, uint32_t ones
     const uint32_t sb = (uint32_t)(w & 1ull);
     const uint32_t idx = ones + (uint32_t)(z + 1) * sb;
     const u32x4 r = philox4x32_10_rk(k, c, 0u, 0u, rk);
-    const uint32_t flip = (unsigned long long)r.x < thr[idx] ? 1u : 0u;
+    const uint32_t flip = z == 8 ? ((ones == 3u || (sb && ones == 2u)) ? 1u : 0u) ^ sb
+                                 : ((unsigned long long)r.x < thr[idx] ? 1u : 0u);
     uint64_t d = nlog_q32(((uint64_t)r.y << 32) | r.z, lr, ACA_LN2_Q48);
     d = d < 1ull ? 1ull : d;
     o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;
@@ -536,19 +548,20 @@ __device__ __forceinline__ void ring_coords(int ri, int& lx, int& ly) {
     else { const int r2 = ri - 2 * (TX + 2); lx = r2 < TY ? -1 : TX; ly = r2 % TY; }
 }
 
-template <int NDIM, int TX, int TY, int TZ, int NT, bool FULL, bool EARLY, int HW = 1>
+template <int NDIM, int TX, int TY, int TZ, int NT, bool FULL, bool EARLY, int HW = 1, bool MOORE = false>
 __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned long long* S, unsigned short* Q,
                                                     const unsigned long long* thr, const unsigned long long* thm,
                                                     const unsigned long long* lr, int x0, int y0, int z0,
                                                     unsigned long long wlim, TileStats& st) {
     static_assert(HW == 1 || (HW == 2 && NDIM == 2 && !EARLY), "2-wide halo: 2-D, no a10");
+    static_assert(!MOORE || (NDIM == 2 && HW == 1 && !EARLY), "Moore neighbourhood: 2-D V0 only");
     constexpr int SX = TX + 4, SY = TY + 2 * HW;
     constexpr int SXY = SX * SY;
     constexpr int NCELL = TX * TY * TZ;
     constexpr int NW = NT / 32;
     constexpr int CPW = NCELL / NW;
     constexpr int JPL = CPW / 32;
-    constexpr int Z = 2 * NDIM;
+    constexpr int Z = MOORE ? 8 : 2 * NDIM;
     constexpr bool FASTMAP = (TX % 32 == 0) && (CPW % TX == 0) && (TY % (CPW / TX == 0 ? 1 : CPW / TX) == 0);
     constexpr int LPR = TX / 32 > 0 ? TX / 32 : 1;
     const Geo& g = P.g;
@@ -634,6 +647,9 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                     unsigned int m = min(min(VH[2 * (s - 1) + 1], VH[2 * (s + 1) + 1]),
                                          min(VH[2 * (s - SX) + 1], VH[2 * (s + SX) + 1]));
                     if (NDIM == 3) m = min(m, min(VH[2 * (s - SXY) + 1], VH[2 * (s + SXY) + 1]));
+                    if (MOORE)
+                        m = min(min(m, min(VH[2 * (s - SX - 1) + 1], VH[2 * (s - SX + 1) + 1])),
+                                min(VH[2 * (s + SX - 1) + 1], VH[2 * (s + SX + 1) + 1]));
                     mv[k] = m;
                 }
 #pragma unroll
@@ -650,8 +666,25 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 tmask &= tmask - 1u;
                 const int s = cell_slot(j);
                 const unsigned long long w = VS[s];
-                bool e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
-                if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+                bool e;
+                if (MOORE) {   // rank bits are 0: compare the times, then the cell ids
+                    const int o = wbase + lane + 32 * j;
+                    const int lx = o % TX, ly = (o / TX) % TY;
+                    const unsigned long long t = w >> g.TSH;
+                    const long long cs = id2(g, x0 + lx, y0 + ly);
+                    e = true;
+#pragma unroll
+                    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            if (dx == 0 && dy == 0) continue;
+                            const unsigned long long tn = VS[s + dy * SX + dx] >> g.TSH;
+                            e = e && (t < tn || (t == tn && cs < id2(g, x0 + lx + dx, y0 + ly + dy)));
+                        }
+                } else {
+                    e = w < VS[s - 1] && w < VS[s + 1] && w < VS[s - SX] && w < VS[s + SX];
+                    if (NDIM == 3) e = e && w < VS[s - SXY] && w < VS[s + SXY];
+                }
                 emask |= (uint32_t)e << j;
             }
             if constexpr (HW == 2) {   // the lane's ring cells take mask bits JPL, JPL + 1
@@ -757,6 +790,9 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             uint32_t ones = (VH[2 * (s - 1)] & 1u) + (VH[2 * (s + 1)] & 1u) + (VH[2 * (s - SX)] & 1u) +
                             (VH[2 * (s + SX)] & 1u);
             if (NDIM == 3) ones += (VH[2 * (s - SXY)] & 1u) + (VH[2 * (s + SXY)] & 1u);
+            if (MOORE)
+                ones += (VH[2 * (s - SX - 1)] & 1u) + (VH[2 * (s - SX + 1)] & 1u) + (VH[2 * (s + SX - 1)] & 1u) +
+                        (VH[2 * (s + SX + 1)] & 1u);
             if (P.fast) {   // uniform: Poisson law, lambda = 1, no tie stress, no frames, N < 2^32
                 const FireOut f = fire_fast(w, ones, Z, cell_id32(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
                                             P.do_hash);
@@ -1155,7 +1191,7 @@ __device__ __forceinline__ void halo_coords(int h, int& lx, int& ly, int& lz) {
 }
 
 template <int NDIM, int TX, int TY, int TZ, int NT, int MINB, bool DB, bool REG, bool EARLY = false, bool WL = false,
-          int HW = 1>
+          int HW = 1, bool MOORE = false>
 __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     static_assert(HW == 1 || (HW == 2 && NDIM == 2 && !EARLY && !WL && !REG && !DB), "2-wide halo: 2-D V0 only");
     constexpr int SX = TX + 4, SY = TY + 2 * HW, SZ = (NDIM == 3) ? TZ + 2 * HW : 1;
@@ -1166,7 +1202,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     constexpr int NCELL = TX * TY * TZ;
     constexpr int NROWS = TY * TZ;
     constexpr int NW = NT / 32;
-    constexpr int NHALO = NDIM == 2 ? 2 * (TX + TY) : 2 * (TX * TY + TX * TZ + TY * TZ);
+    constexpr int NHALO = (NDIM == 2 ? 2 * (TX + TY) : 2 * (TX * TY + TX * TZ + TY * TZ)) + (MOORE ? 4 : 0);
     static_assert(NCELL % NT == 0 && (NCELL / NW) % 32 == 0 && TX % 4 == 0, "tile/block mismatch");
 
     if (*(volatile unsigned int*)&P.ctl->done) return;
@@ -1249,7 +1285,12 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
             if constexpr (HW == 1) {
                 for (int h = tid; h < NHALO; h += NT) {
                     int lx, ly, lz;
-                    halo_coords<NDIM, TX, TY, TZ>(h, lx, ly, lz);
+                    if (MOORE && h >= NHALO - 4) {   // the four corner cells (diagonal neighbours)
+                        const int q = h - (NHALO - 4);
+                        lx = (q & 1) ? TX : -1; ly = (q & 2) ? TY : -1; lz = 0;
+                    } else {
+                        halo_coords<NDIM, TX, TY, TZ>(h, lx, ly, lz);
+                    }
                     S[slot(lx, ly, lz)] = ld_word_t<true>(P, x0 + lx, y0 + ly, z0 + lz);
                 }
             } else {   // 2-wide halo: rows -2, -1, TY, TY+1 (full width), then columns -2, -1, TX, TX+1
@@ -1268,7 +1309,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
                 const int lx = i % SX - 2, ly = (i / SX) % SY - HW, lz = (NDIM == 3) ? i / SXY - HW : 0;
                 if (lx < -HW || lx >= TX + HW) continue;
                 const int out = (lx < 0 || lx >= TX) + (ly < 0 || ly >= TY) + ((NDIM == 3) && (lz < 0 || lz >= TZ));
-                if (HW == 2 || out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
+                if (HW == 2 || MOORE || out <= 1) S[i] = ld_word(P, x0 + lx, y0 + ly, z0 + lz);
             }
         }
         __syncthreads();
@@ -1287,8 +1328,10 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
             }
         }
         if (!done_reg) {
-            rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true, EARLY, HW>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st)
-                          : tile_rounds<NDIM, TX, TY, TZ, NT, false, EARLY, HW>(P, S, Q, thr, thm, lr, x0, y0, z0, wlim, st);
+            rounds = full ? tile_rounds<NDIM, TX, TY, TZ, NT, true, EARLY, HW, MOORE>(P, S, Q, thr, thm, lr, x0, y0, z0,
+                                                                                      wlim, st)
+                          : tile_rounds<NDIM, TX, TY, TZ, NT, false, EARLY, HW, MOORE>(P, S, Q, thr, thm, lr, x0, y0, z0,
+                                                                                       wlim, st);
         }
         rounds_max = rounds > rounds_max ? rounds : rounds_max;
         __syncthreads();
@@ -1368,6 +1411,21 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
             const unsigned long long a = VS[xm], b = VS[xp], c2 = VS[ym], d2 = VS[yp];
             bool ok = w < a && w < b && w < c2 && w < d2;
             uint32_t ones = (uint32_t)(a & 1ull) + (uint32_t)(b & 1ull) + (uint32_t)(c2 & 1ull) + (uint32_t)(d2 & 1ull);
+            if (P.life) {   // Moore neighbourhood, explicit (t, c) order (rank bits are 0)
+                const int xmm = x == 0 ? g.nx - 1 : x - 1, xpp = x == g.nx - 1 ? 0 : x + 1;
+                const int ymm = y == 0 ? g.ny - 1 : y - 1, ypp = y == g.ny - 1 ? 0 : y + 1;
+                const int nbs[8] = {xm, xp, ym, yp, ymm * g.nx + xmm, ymm * g.nx + xpp, ypp * g.nx + xmm,
+                                    ypp * g.nx + xpp};
+                const unsigned long long t = w >> g.TSH;
+                ok = true;
+                ones = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const unsigned long long wn = VS[nbs[q]], tn = wn >> g.TSH;
+                    ok = ok && (t < tn || (t == tn && i < nbs[q]));
+                    ones += (uint32_t)(wn & 1ull);
+                }
+            }
             if (g.ndim == 3) {
                 const int zm = i + ((z == 0 ? g.nz - 1 : z - 1) - z) * pl;
                 const int zp = i + ((z == g.nz - 1 ? 0 : z + 1) - z) * pl;
@@ -1376,7 +1434,7 @@ __global__ void __launch_bounds__(NT) whole_kernel(const KParams P) {
                 ones += (uint32_t)(e & 1ull) + (uint32_t)(f & 1ull);
             }
             if (!ok) continue;
-            const FireOut o = fire(w, ones, Z, (unsigned long long)i, g, thr, lr, P.rk, P.inv_lambda,
+            const FireOut o = fire(w, ones, P.life ? 8 : Z, (unsigned long long)i, g, thr, lr, P.rk, P.inv_lambda,
                                    P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
             if (!o.ok) continue;
             hacc += o.h;
@@ -1438,7 +1496,7 @@ __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const
         const u32x4 r = philox4x32_10(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, key0, key1);
         const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
         const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
-        words[i] = w_pack(t0, rank, 0ull, sb, g);
+        words[i] = w_pack(t0, g.RB ? rank : 0ull, 0ull, sb, g);
     }
 }
 
@@ -1491,7 +1549,7 @@ __global__ void pack_kernel(unsigned long long* __restrict__ words, const int8_t
         const unsigned long long t = times ? times[i] : w_time(w, g);
         const unsigned long long k = counters ? counters[i] : w_count(w, g);
         const unsigned long long sb = spins ? (spins[i] > 0 ? 1ull : 0ull) : (w & 1ull);
-        words[i] = w_pack(t, rank, k, sb, g);
+        words[i] = w_pack(t, g.RB ? rank : 0ull, k, sb, g);
     }
 }
 
@@ -1500,7 +1558,7 @@ __global__ void repack_kernel(unsigned long long* __restrict__ words, Geo a, Geo
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const unsigned long long w = words[i];
-        const unsigned long long rank = (w >> (a.NB + 1)) & ((1ull << a.RB) - 1ull);
+        const unsigned long long rank = a.RB ? (w >> (a.NB + 1)) & ((1ull << a.RB) - 1ull) : 0ull;
         words[i] = w_pack(w_time(w, a), rank, w_count(w, a), w & 1ull, b);
     }
 }

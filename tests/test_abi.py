@@ -66,7 +66,8 @@ def test_no_cpu_fallback_without_gpu(libaca):
 
 def test_invalid_arguments_are_rejected_before_the_device(libaca):
     bad = [dict(dims=(1, 8)), dict(dims=(8,)), dict(dims=(8, 8), periodic=0), dict(dims=(8, 8), lam=0.0),
-           dict(dims=(8, 8), beta=-1.0), dict(dims=(8, 8), rule=2), dict(dims=(8, 8), lam=float("nan"))]
+           dict(dims=(8, 8), beta=-1.0), dict(dims=(8, 8), rule=3), dict(dims=(4, 4, 4), rule=2),
+           dict(dims=(8, 8), lam=float("nan"))]
     for kw in bad:
         dims = kw.pop("dims")
         with pytest.raises(libaca.AcaError) as ei:

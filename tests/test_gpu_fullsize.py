@@ -117,3 +117,30 @@ def test_full_size_sampled_parity(aca, oracle_mod, name, n_random, radii):
     mu = N * cfg["lam"] * T
     assert abs(tot - mu) < 5 * math.sqrt(mu)
     assert st["t_min"] >= oracle_mod.to_q32(T)
+
+
+def _onsager_u(beta):
+    import mpmath
+    mpmath.mp.dps = 50
+    b = mpmath.mpf(beta)
+    k = 2 * mpmath.sinh(2 * b) / mpmath.cosh(2 * b) ** 2
+    return float(-mpmath.coth(2 * b) * (1 + 2 / mpmath.pi * (2 * mpmath.tanh(2 * b) ** 2 - 1) * mpmath.ellipk(k ** 2)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("beta,rule", [(0.35, 1), (0.30, 0), (0.60, 0)])
+def test_energy_matches_onsager_at_scale(aca, beta, rule):
+    """Physics of the GPU path at scale, independent of the oracle: on a 1024^2 torus the energy
+    per spin E/N = -B/N, averaged over T = 40..80 after a burn-in, equals Onsager's exact value
+    (textbook closed form) within 0.004 (finite-size and sampling error are far smaller away
+    from beta_c; closer to beta_c, e.g. 0.40, relaxation from a random start takes longer).
+    beta = 0.6 starts ordered (init_q = 0) to avoid slow domain coarsening."""
+    import numpy as np
+    g = aca.Sim((1024, 1024), beta=beta, rule=rule, seed=99, init_q=0.0 if beta > 0.5 else 0.5)
+    es = []
+    for T in range(20, 81, 2):
+        g.run_until(float(T))
+        if T >= 40:
+            es.append(-g.stats()["bond_sum"] / 1024 ** 2)
+    u = _onsager_u(beta)
+    assert abs(np.mean(es) - u) < 0.004, (np.mean(es), u)

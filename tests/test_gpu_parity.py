@@ -342,3 +342,51 @@ def test_two_wide_halo(aca, oracle_mod, case):
     dims, Ts = kw.pop("dims"), kw.pop("Ts")
     g, o = run_pair(aca, oracle_mod, dims, Ts, **kw)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("case", ["whole", "tiny", "tiled", "t32", "t64x32", "t128", "shards", "ties", "law2",
+                                  "block", "frames"])
+def test_game_of_life(aca, oracle_mod, case):
+    """Rule 2 (asynchronous Game of Life, P10): Moore neighbourhood, Conway's
+    rule, explicit (t, c) tie-break (no rank bits): bit-identical trajectories on the
+    whole-lattice kernel, tiled with ragged tiles (corner halo cells), virtual shards, forced
+    ties, another law, a user-set still life, and frames."""
+    kw = dict(dims=(200, 150), Ts=[3.0, 6.0], seed=61, rule=2, init_q=0.6, whole_lattice=-1)
+    if case == "whole":
+        kw.update(dims=(24, 20), whole_lattice=1)
+    elif case == "tiny":
+        kw.update(dims=(3, 5), whole_lattice=0)
+    elif case == "t32":
+        kw.update(tile=(32, 32))
+    elif case == "t64x32":
+        kw.update(tile=(64, 32))
+    elif case == "t128":
+        kw.update(tile=(128, 64))
+    elif case == "shards":
+        kw.update(dims=(128, 96), shards=4)
+    elif case == "ties":
+        kw.update(tie_bits=30)
+    elif case == "law2":
+        kw.update(law=2)
+    if case == "block":
+        dims = (96, 64)
+        s = -np.ones((64, 96), np.int8)
+        s[10:12, 20:22] = 1
+        g = aca.Sim(dims, rule=2, seed=5, whole_lattice=-1)
+        g.set_spins(s)
+        g.run_until(10.0)
+        assert np.array_equal(g.spins(), s) and g.stats()["flips"] == 0
+        return
+    if case == "frames":
+        dims = (130, 70)
+        g = aca.Sim(dims, rule=2, seed=7, init_q=0.6, whole_lattice=-1)
+        o = oracle_mod.OracleSim(dims, rule=2, seed=7, init_q=0.6)
+        got = g.frames(0.5, 1, 6, B=3)
+        dq = int(np.floor(0.5 * 4294967296.0 + 0.5))
+        for k in range(6):
+            o.run_until_q32((1 + k) * dq + 1)
+            assert np.array_equal(got[k], o.spins())
+        return
+    dims, Ts = kw.pop("dims"), kw.pop("Ts")
+    g, o = run_pair(aca, oracle_mod, dims, Ts, **kw)
+    assert_same(g, o)
