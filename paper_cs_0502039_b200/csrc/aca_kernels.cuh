@@ -435,8 +435,9 @@ __global__ void __launch_bounds__(NT) tile_kernel(const KParams P) {
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds);
 }
 
-// Shared-memory layout of tile_tma_kernel (host and device): words (NB_ buffers), the P3 table,
-// P4/a10 tables, reduction scratch, 2 mbarriers, then the fire queue(s): per-warp queues of
+// Shared-memory layout of tile_tma_kernel (host and device): words (NB_ buffers), the P4/a10
+// tables, reduction scratch, 2 mbarriers, then the fire queue(s) (the P3 table is read from
+// global memory through L1): per-warp queues of
 // CPW/2 + 16 entries (the eligible cells of a warp form an independent set: at most one per
 // two cells of each row segment), CPW with a10 candidates, or the work-list's two CTA queues
 // plus claim bitmaps and counters.
@@ -452,7 +453,7 @@ __host__ __device__ constexpr size_t tma_queue_entries(int ncell, int nt, bool w
 }
 __host__ __device__ constexpr size_t tma_smem_bytes(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl,
                                                     bool early, int hw = 1) {
-    return (tma_words(ndim, tx, ty, tz, hw) * nbuf + 512 + 16 + 112 + nt / 32 + 2) * 8 +
+    return (tma_words(ndim, tx, ty, tz, hw) * nbuf + 16 + 112 + nt / 32 + 2) * 8 +
            ((tma_queue_entries(tx * ty * tz, nt, wl, early, hw) * 2 + 15) & ~(size_t)15) +
            (wl ? (size_t)tx * ty * tz / 32 * 8 + 16 : 0);
 }
@@ -1209,8 +1210,10 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
 
     extern __shared__ __align__(128) unsigned long long smem[];
     unsigned long long* Sb = smem;                                  // NB_ x NSLOTP words
-    unsigned long long* lr = Sb + NB_ * NSLOTP;                     // 512
-    unsigned long long* thr = lr + 512;                             // 16
+    // The NLOG-2 table (4 KB) is read through L1 from global memory (it stays resident): keeping it
+    // out of shared memory lets 5 CTAs of a 64x64 tile share an SM instead of 4.
+    const unsigned long long* lr = P.lr;
+    unsigned long long* thr = Sb + NB_ * NSLOTP;                    // 16
     unsigned long long* thm = thr + 16;                             // 112 (a10 table)
     unsigned long long* red = thm + 112;                            // NW
     unsigned long long* bar = red + NW;                             // 2
@@ -1220,7 +1223,6 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
 
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
     for (int i = tid; i < 112; i += NT) thm[i] = i < 98 ? P.thm[i] : ~0ull;
     if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
