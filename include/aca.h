@@ -85,7 +85,9 @@ typedef struct {
                                    0 (default) Poisson, next_t = t - ln(r)/lambda (Eq. newt1i,
                                    PAPER.md:485-488); 1 uniform, next_t - t = r/lambda
                                    (PAPER.md:1389-1393); 2 next_t - t = r^(1/8)/lambda
-                                   (PAPER.md:1425-1430). r from the arrival's Philox draw. */
+                                   (PAPER.md:1425-1430); 3 Gaussian period of mean 1/lambda
+                                   and sd 1/(4 lambda) (Irwin-Hall(12), negative periods
+                                   clamped). r from the arrival's draw. */
 } aca_options;
 
 typedef struct {

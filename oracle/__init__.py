@@ -148,7 +148,7 @@ def nlog_batch(X):
     return q
 
 
-POISSON, UNIFORM, ROOT8 = 0, 1, 2   # P3L asynchrony laws
+POISSON, UNIFORM, ROOT8, GAUSS = 0, 1, 2, 3   # P3L asynchrony laws
 
 
 def cell_time_counter(seed, c, T, lam=1.0, tie_bits=0, law=POISSON):

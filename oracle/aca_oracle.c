@@ -60,6 +60,17 @@ uint64_t oracle_inv_lambda(double lambda) { return (uint64_t)floor(4294967296.0 
  *          r = (w1 + 0.5) * 2^-32 in IEEE double (sqrt is correctly rounded). */
 uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law) {
     if (law == 1) return (uint64_t)w1;
+    if (law == 3) {   /* Gaussian period: Irwin-Hall(12), mean 1, sd 1/4 (P3L) */
+        const uint32_t kg[2] = {0x243F6A88u, 0x85A308D3u};
+        uint64_t S = 0;
+        for (uint32_t j = 0; j < 3; j++) {
+            uint32_t ctr[4] = {w1, w2, j, 9u}, o[4];
+            oracle_philox4x32_10(ctr, kg, o);
+            S += (uint64_t)o[0] + o[1] + o[2] + o[3];
+        }
+        int64_t U = (int64_t)(S >> 2) - (int64_t)(1ULL << 31);
+        return U < 1 ? 1 : (uint64_t)U;
+    }
     if (law == 2) {
         double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
         return (uint64_t)floor(sqrt(sqrt(sqrt(r))) * 4294967296.0);
@@ -178,7 +189,7 @@ oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double b
 oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, double beta, double J,
                               double h, int rule, uint64_t seed, double init_q, int tie_bits, int law) {
     if (ndim != 2 && ndim != 3) return NULL;
-    if (law < 0 || law > 2) return NULL;
+    if (law < 0 || law > 3) return NULL;
     if (!(lambda > 0) || !isfinite(lambda) || !(beta >= 0) || !isfinite(beta)) return NULL;
     if (rule != 0 && rule != 1 && !(rule == 2 && ndim == 2)) return NULL;
     if (!(init_q >= 0 && init_q <= 1)) return NULL;
@@ -630,7 +641,7 @@ int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda,
 int oracle_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                             int q, uint64_t* fired_per_round, uint64_t* t_out) {
     if (q < 1 || q > 8) return -1;
-    if (ndim < 1 || ndim > 3 || law < 0 || law > 2 || !(lambda > 0) || rounds < 0) return -1;
+    if (ndim < 1 || ndim > 3 || law < 0 || law > 3 || !(lambda > 0) || rounds < 0) return -1;
     int64_t d[3] = {1, 1, 1}, N = 1;
     for (int a = 0; a < ndim; a++) { if (dims[a] < 2) return -1; d[a] = dims[a]; N *= dims[a]; }
     uint64_t inv = oracle_inv_lambda(lambda);

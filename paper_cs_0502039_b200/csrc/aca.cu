@@ -574,7 +574,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     }
     if (!(opt.init_q >= 0 && opt.init_q <= 1)) return fail(ACA_EINVAL, "init_q must be in [0, 1]");
     if (opt.tie_bits < 0 || opt.tie_bits > 40) return fail(ACA_EINVAL, "tie_bits must be in [0, 40]");
-    if (opt.law < 0 || opt.law > 2) return fail(ACA_EINVAL, "law must be 0 (Poisson), 1 (uniform) or 2 (r^1/8)");
+    if (opt.law < 0 || opt.law > 3)
+        return fail(ACA_EINVAL, "law must be 0 (Poisson), 1 (uniform), 2 (r^1/8) or 3 (Gaussian period)");
     if (rule == ACA_LIFE && (opt.early_reject || opt.sync_rounds))
         return fail(ACA_EINVAL, "the Game of Life rule has no early rejection / sync-round kernel");
     if (opt.shards < 1) opt.shards = 1;
@@ -640,7 +641,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->RB = rule == ACA_LIFE ? 0 : bits_for(max_rank);
     {
         // largest unscaled increment of the law: NLOG-2(1) for Poisson, < 2^32 otherwise
-        const unsigned long long umax = opt.law == 0 ? 190530846196ull : (1ull << 32);
+        const unsigned long long umax = opt.law == 0 ? 190530846196ull : opt.law == 3 ? (3ull << 32) : (1ull << 32);
         const unsigned __int128 p = (unsigned __int128)umax * S->inv_lambda;
         S->max_delta = (unsigned long long)(p >> 32) + 1 + (opt.tie_bits ? (1ull << opt.tie_bits) : 0ull);
         const int tb = bits_for(S->max_delta);
@@ -1114,7 +1115,7 @@ extern "C" {
 int aca_selftest_law(uint64_t n, const uint64_t* X, int law, uint64_t inv_lambda, int tie_bits, uint64_t* u,
                      uint64_t* delta) {
     if (!X || !u || !delta) return fail(ACA_EINVAL, "null buffer");
-    if (law < 0 || law > 2) return fail(ACA_EINVAL, "bad law");
+    if (law < 0 || law > 3) return fail(ACA_EINVAL, "bad law");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
     uint64_t *dx = nullptr, *du = nullptr, *dd = nullptr;
@@ -1175,7 +1176,7 @@ int aca_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, 
                          uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds) {
     if (ndim < 1 || ndim > 3 || !dims) return fail(ACA_EINVAL, "ndim must be 1, 2 or 3");
     if (q < 1 || q > 8) return fail(ACA_EINVAL, "q must be in [1, 8]");
-    if (law < 0 || law > 2) return fail(ACA_EINVAL, "law must be 0, 1 or 2");
+    if (law < 0 || law > 3) return fail(ACA_EINVAL, "law must be 0, 1, 2 or 3");
     if (!(lambda > 0) || !std::isfinite(lambda)) return fail(ACA_EINVAL, "lambda must be > 0");
     if (rounds < 0 || rounds > (int64_t)1 << 31) return fail(ACA_EINVAL, "rounds out of range");
     if (rounds > 0 && !fired_per_round) return fail(ACA_EINVAL, "null fired_per_round");

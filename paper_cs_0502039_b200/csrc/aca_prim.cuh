@@ -91,9 +91,21 @@ __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long lon
 //   1 uniform on (0,1):    U = w1
 //   2 r^(1/8):             U = floor(sqrt(sqrt(sqrt(r))) * 2^32), r = (w1 + 0.5) 2^-32
 //     (IEEE double; sqrt is correctly rounded on the device as on the host)
+//   3 Gaussian period:        S = sum of the 12 words of Philox (w1, w2, j, 9) under the
+//     fixed key (0x243F6A88, 0x85A308D3), j = 0..2; U = max(1, (S >> 2) - 2^31): mean 1, sd 1/4
 __device__ __forceinline__ uint64_t law_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr,
                                             uint64_t ln2_q48, int law) {
     if (law == 1) return (uint64_t)w1;
+    if (law == 3) {   // Gaussian period: Irwin-Hall(12) of three sub-draws
+        uint64_t S = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 3; ++j) {
+            const u32x4 o = philox4x32_10(w1, w2, j, 9u, 0x243F6A88u, 0x85A308D3u);
+            S += (uint64_t)o.x + o.y + o.z + o.w;
+        }
+        const long long U = (long long)(S >> 2) - (1ll << 31);
+        return U < 1 ? 1ull : (uint64_t)U;
+    }
     if (law == 2) {
         const double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
         return (uint64_t)(__dsqrt_rn(__dsqrt_rn(__dsqrt_rn(r))) * 4294967296.0);

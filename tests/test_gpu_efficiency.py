@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("dims", [(2,), (37,), (1000,), (2, 2), (13, 7), (64, 48), (2, 2, 2), (12, 10, 8)])
-@pytest.mark.parametrize("law", [0, 1, 2])
+@pytest.mark.parametrize("law", [0, 1, 2, 3])
 def test_efficiency_bit_identical(aca, oracle_mod, dims, law):
     rounds = 150
     f_g, t_g, _ = aca.aca_efficiency_run(dims, rounds, law=law, seed=31, want_times=True)
@@ -40,7 +40,7 @@ def test_efficiency_large_arrays_match_paper(aca, ndim, law, value, tol):
 
 
 def test_efficiency_rejects_bad_arguments(aca):
-    for dims, law in (((1,), 0), ((4, 4), 3)):
+    for dims, law in (((1,), 0), ((4, 4), 4)):
         with pytest.raises(aca.AcaError):
             aca.aca_efficiency_run(dims, 5, law=law)
 

@@ -75,7 +75,7 @@ def test_nlog_bit_identical_to_oracle(aca, oracle_mod):
         assert list(d) == want
 
 
-@pytest.mark.parametrize("law", [0, 1, 2])
+@pytest.mark.parametrize("law", [0, 1, 2, 3])
 def test_law_bit_identical_to_oracle(aca, oracle_mod, law):
     """P3L asynchrony laws: the device's unscaled increment and
     Delta equal the oracle's on random and edge inputs, for several lambda / tie settings."""
@@ -91,7 +91,7 @@ def test_law_bit_identical_to_oracle(aca, oracle_mod, law):
         assert list(d) == want_d
 
 
-@pytest.mark.parametrize("law", [1, 2])
+@pytest.mark.parametrize("law", [1, 2, 3])
 def test_law_trajectories(aca, oracle_mod, law):
     """Whole trajectories under the uniform and r^(1/8) laws: whole-lattice, tiled 2-D with
     ragged tiles, 3-D tiles, with field and both rules."""

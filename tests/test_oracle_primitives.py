@@ -239,7 +239,7 @@ def test_law_root8_distribution(oracle_mod):
     assert abs(v.mean() - 8 / 9) < 4 * math.sqrt(8 / 10 - (8 / 9) ** 2) / math.sqrt(len(v))
 
 
-@pytest.mark.parametrize("law", [1, 2])
+@pytest.mark.parametrize("law", [1, 2, 3])
 def test_law_closed_form_times(oracle_mod, law):
     """Arrival times are state-independent under every law: the oracle's
     final (t, n) equal each cell's own partial sums."""
@@ -249,3 +249,40 @@ def test_law_closed_form_times(oracle_mod, law):
     for c in range(120):
         tc, nc = oracle_mod.cell_time_counter(5, c, 7.0, law=law)
         assert (int(t.flat[c]), int(n.flat[c])) == (tc, nc)
+
+
+def _irwin_hall_cdf(x, n=12):
+    """Exact Irwin-Hall CDF, using the symmetry F(x) = 1 - F(n - x) to keep the alternating sum
+    well conditioned."""
+    x = np.asarray(x, float)
+    lo = np.minimum(x, n - x)
+    f = np.zeros_like(lo)
+    for k in range(n + 1):
+        term = (-1) ** k * math.comb(n, k) * np.clip(lo - k, 0, None) ** n
+        f += term
+    f /= math.factorial(n)
+    return np.where(x <= n / 2, f, 1 - f)
+
+
+def test_law_gauss_distribution(oracle_mod):
+    """Law 3 (Gaussian period): U/2^32 = S/4 - 1/2 with S ~ Irwin-Hall(12):
+    mean 1 and sd 1/4 exactly in distribution; KS against the exact Irwin-Hall CDF."""
+    from scipy import stats
+    v = []
+    for c in range(20000):
+        w = oracle_mod.philox((0, c, 0, 0), (77, 1))
+        v.append(oracle_mod.law_q32(w[1], w[2], 3) / 2.0 ** 32)
+    v = np.array(v)
+    assert abs(v.mean() - 1.0) < 4 * 0.25 / math.sqrt(len(v))
+    assert abs(v.std() - 0.25) < 0.01
+    ks = stats.kstest(4 * (v + 0.5), lambda x: _irwin_hall_cdf(x))
+    assert ks.pvalue > 1e-4, ks
+    assert v.min() > 0
+
+
+def test_law_gauss_is_a_function_of_the_draw(oracle_mod):
+    """The sub-draws are keyed by (w1, w2) only: the same arrival draw gives the same period, a
+    different one (almost surely) a different period."""
+    a = oracle_mod.law_q32(123, 456, 3)
+    assert a == oracle_mod.law_q32(123, 456, 3) and a != oracle_mod.law_q32(124, 456, 3)
+    assert oracle_mod.delta(123, 456, 2.0, 0, 3) in (a // 2, a // 2 + 1, max(1, a // 2))
