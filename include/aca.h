@@ -88,6 +88,11 @@ typedef struct {
                                    (PAPER.md:1425-1430); 3 Gaussian period of mean 1/lambda
                                    and sd 1/(4 lambda) (Irwin-Hall(12), negative periods
                                    clamped). r from the arrival's draw. */
+    int32_t halo_mode;          /* sharded handles: 0 (default) = push, the tile kernel stores its
+                                   boundary rows into the neighbour shard's halo as it writes them
+                                   back (no exchange step; exact because words only grow and are
+                                   never torn); 1 = exchange the halo rows before every launch
+                                   (device copies / NCCL send-recv). Same results. */
 } aca_options;
 
 typedef struct {

@@ -102,6 +102,8 @@ struct Shard {
     unsigned long long* words = nullptr;
     unsigned long long* halo_lo = nullptr;  // 1 row (2-D) / plane (3-D)
     unsigned long long* halo_hi = nullptr;
+    unsigned long long* push_lo = nullptr;  // push mode: the lower neighbour's halo_hi
+    unsigned long long* push_hi = nullptr;  // ... and the upper neighbour's halo_lo
     Ctl* ctl = nullptr;
     size_t n = 0;          // owned cells
     size_t face = 0;       // cells of one row / plane of the sharded axis
@@ -143,6 +145,7 @@ struct aca_sim {
     bool whole = false;
     bool sync = false;
     bool phased = false;           // checkerboard sweeps (two launches per outer round)
+    bool push = false;             // sharded: boundary rows pushed into the neighbours' halos by the kernel
     size_t smem = 0;
     int persistent_ctas = 0;       // > 0: grid size of the persistent tile kernel
     void* kern = nullptr;          // selected tile/whole kernel
@@ -291,6 +294,8 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.words = sh.words;
     P.halo_lo = sh.halo_lo;
     P.halo_hi = sh.halo_hi;
+    P.push_lo = sh.push_lo;
+    P.push_hi = sh.push_hi;
     P.ctl = sh.ctl;
     P.lr = S->d_lr;
     P.key0 = (uint32_t)(S->seed & 0xffffffffu);
@@ -357,8 +362,10 @@ int exchange(aca_sim* S) {
 // colour 1, with a halo exchange before each.
 int launch_round(aca_sim* S) {
     for (int ph = S->phased ? 0 : -1; ph < (S->phased ? 2 : 0); ++ph) {
-        int rc = exchange(S);
-        if (rc) return rc;
+        if (!S->push) {   // push mode: the kernels store boundary rows into the neighbours' halos
+            int rc = exchange(S);
+            if (rc) return rc;
+        }
         for (auto& sh : S->shards) {
             KParams P = make_params(S, sh);
             P.phase = ph;
@@ -750,6 +757,15 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         }
     }
     set_geo_layout(S);
+    // push mode for virtual shards on this device (the persistent tile kernels store their
+    // boundary rows into the neighbour shard's halo; multi-process handles use halo exchange)
+    if (S->G > 1 && !S->use_nccl && S->persistent_ctas > 0 && opt.halo_mode == 0) {
+        S->push = true;
+        for (int s2 = 0; s2 < S->G; ++s2) {
+            S->shards[s2].push_lo = S->shards[(s2 + S->G - 1) % S->G].halo_hi;
+            S->shards[s2].push_hi = S->shards[(s2 + 1) % S->G].halo_lo;
+        }
+    }
     if (int r = init_state(S)) return bail(r);
     if (cudaMallocHost(&S->h_ctl, 2 * sizeof(Ctl) * S->shards.size()) != cudaSuccess)
         return bail(fail(ACA_ENOMEM, "pinned ctl"));
@@ -781,6 +797,10 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         CK(cudaMemcpyAsync(&S->shards[i].ctl->wlim, &S->h_ctl[i].wlim, sizeof(unsigned long long),
                            cudaMemcpyHostToDevice, S->stream));
         CK(cudaMemsetAsync(&S->shards[i].ctl->done, 0, sizeof(unsigned int), S->stream));
+    }
+    if (S->push) {   // push mode: fill the halos once; the kernels keep them current
+        rc = exchange(S);
+        if (rc) return rc;
     }
     rc = build_graph(S);
     if (rc) return rc;

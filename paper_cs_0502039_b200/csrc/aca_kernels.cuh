@@ -89,6 +89,11 @@ struct KParams {
     unsigned long long* words;
     const unsigned long long* halo_lo;   // sharded axis: row/plane just below the shard
     const unsigned long long* halo_hi;   // ... and just above
+    // push mode (sharded): where this shard's first / last row (plane) goes — the lower
+    // neighbour's halo_hi and the upper neighbour's halo_lo (same device, or a peer GPU's memory
+    // mapped over NVLink). nullptr: halos are exchanged between launches instead.
+    unsigned long long* push_lo;
+    unsigned long long* push_hi;
     Ctl* ctl;
     const unsigned long long* lr;        // device copy of ACA_NLOG_LR (512 entries)
     uint32_t key0, key1;
@@ -137,6 +142,20 @@ __device__ __forceinline__ unsigned long long ld_word_t(const KParams& P, int gx
 }
 __device__ __forceinline__ unsigned long long ld_word(const KParams& P, int gx, int gy, int gz) {
     return ld_word_t<false>(P, gx, gy, gz);
+}
+
+// Write-back of one owned word; in push mode a word of the shard's first / last row (plane) is
+// also stored into the neighbour shard's halo. Any interleaving with the neighbour's reads is
+// exact: an aligned 8-byte word is never torn, every stored value is a state the cell really
+// held and words only grow (stale-read argument of fig:amcgen), so the
+// neighbour needs no synchronisation with this store — it sees an older or a newer state.
+__device__ __forceinline__ void push_word(const KParams& P, int gx, int gy, int gz, unsigned long long w) {
+    const Geo& g = P.g;
+    if (!P.push_lo) return;
+    const int a = g.ndim == 2 ? gy : gz, n = g.ndim == 2 ? g.ny : g.nz;
+    const size_t f = g.ndim == 2 ? (size_t)gx : (size_t)gy * g.nx + gx;
+    if (a == 0) P.push_lo[f] = w;
+    if (a == n - 1) P.push_hi[f] = w;
 }
 
 // ---------------------------------------------------------------- TMA bulk-copy helpers
@@ -837,8 +856,10 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             int lx, ly;
             ring_coords<TX, TY>(tid + k * NT, lx, ly);
             const int gy = y0 + ly;
-            const size_t gi = (size_t)(g.sharded ? gy : wrapi(gy, g.ny)) * g.nx + wrapi(x0 + lx, g.nx);
+            const int gyy = g.sharded ? gy : wrapi(gy, g.ny), gxx = wrapi(x0 + lx, g.nx);
+            const size_t gi = (size_t)gyy * g.nx + gxx;
             P.words[gi] = VS[rs[k]];
+            push_word(P, gxx, gyy, 0, VS[rs[k]]);
         }
     }
     return rounds;
@@ -1347,6 +1368,14 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
                 const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&S[slot(m2, ly, lz)]);
                 *reinterpret_cast<ulonglong2*>(P.words + gi + m2) = v;
                 active += (v.x < wlim) + (v.y < wlim);
+                if (P.push_lo) {
+                    const int a = NDIM == 2 ? y0 + ly : z0 + lz, n = NDIM == 2 ? g.ny : g.nz;
+                    if (a == 0 || a == n - 1) {
+                        const size_t f = NDIM == 2 ? (size_t)(x0 + m2) : (size_t)(y0 + ly) * g.nx + x0 + m2;
+                        *reinterpret_cast<ulonglong2*>((a == 0 ? P.push_lo : P.push_hi) + f) = v;
+                        if (a == 0 && n == 1) *reinterpret_cast<ulonglong2*>(P.push_hi + f) = v;
+                    }
+                }
             }
         } else {
             for (int o = tid; o < NCELL; o += NT) {
@@ -1356,6 +1385,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
                     const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
                     const unsigned long long w = S[slot(lx, ly, lz)];
                     P.words[gi] = w;
+                    push_word(P, gx, gy, gz, w);
                     active += w < wlim;
                 }
             }

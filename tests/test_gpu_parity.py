@@ -189,14 +189,20 @@ def test_forced_ties(aca, oracle_mod, tie_bits):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("halo_mode", [0, 1])
 @pytest.mark.parametrize("shards", [2, 4, 8])
-def test_virtual_shards(aca, oracle_mod, shards):
-    """G row strips (2-D) / z slabs (3-D) on one device with halo exchange each outer round:
-    the multi-GPU partition and halo logic with the transport replaced by device copies."""
-    g, o = run_pair(aca, oracle_mod, (128, 64 * shards // 2), [4.0], seed=19, shards=shards)
+def test_virtual_shards(aca, oracle_mod, shards, halo_mode):
+    """G row strips (2-D) / z slabs (3-D) on one device: the multi-GPU partition and halo logic.
+    halo_mode 0: the tile kernels push their boundary rows into the neighbour shard's halo as
+    they write back (no exchange step); 1: halo rows copied before every launch. Also an odd
+    width (unvectorised write-back path) and ragged tiles."""
+    g, o = run_pair(aca, oracle_mod, (128, 64 * shards // 2), [4.0], seed=19, shards=shards, halo_mode=halo_mode)
     assert_same(g, o)
     g, o = run_pair(aca, oracle_mod, (32, 16, 8 * shards), [3.0], beta=0.22, seed=19, shards=shards,
-                    tile=(16, 16, 16))
+                    tile=(16, 16, 16), halo_mode=halo_mode)
+    assert_same(g, o)
+    g, o = run_pair(aca, oracle_mod, (77, 12 * shards), [3.0], rule=1, h=0.1, seed=29, shards=shards,
+                    tile=(32, 32), halo_mode=halo_mode)
     assert_same(g, o)
 
 
