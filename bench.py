@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--variant", type=int, default=0, help="tile kernel variant (ablation; 0 = default)")
     ap.add_argument("--early-reject", type=int, default=-1, help="a10 early rejection (-1 = config default)")
     ap.add_argument("--checkerboard", type=int, default=0, help="1/0 = checkerboard sweeps (default), -1 = off")
+    ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
+                    help="N>1 halo transport: kernel stores into CUDA-IPC-mapped neighbour halos (push "
+                         "mode, default) or NCCL send/recv between launches")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true", help="skip the P7 event hash (diagnostics only)")
@@ -250,10 +253,14 @@ def main():
     opts["stream"] = stream.cuda_stream
     if world > 1:
         adist.partition(dims, world)
-        uid = aca.aca_nccl_unique_id() if rank == 0 else bytes(128)
-        opts.update(world=world, rank=rank, nccl_id=adist.broadcast_bytes(uid))
+        opts.update(world=world, rank=rank)
+        if args.transport == "nccl":
+            uid = aca.aca_nccl_unique_id() if rank == 0 else bytes(128)
+            opts.update(nccl_id=adist.broadcast_bytes(uid), halo_mode=1)
     sim = aca.Sim(dims, lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
                   seed=args.seed, **opts)
+    if world > 1 and args.transport == "ipc":
+        adist.ipc_connect(sim.handle)
     n_local = aca.aca_num_cells(sim.handle)
 
     def step(seed):

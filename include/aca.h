@@ -62,7 +62,9 @@ typedef struct {
     int32_t device;             /* CUDA device ordinal; -1 = current device */
     int32_t shards;             /* virtual row/plane shards on this device (default 1) */
     int32_t rank, world;        /* multi-process strips: this rank of `world` (default 0, 1) */
-    const void* nccl_id;        /* world > 1: 128-byte ncclUniqueId shared by all ranks */
+    const void* nccl_id;        /* world > 1 with halo_mode 1: 128-byte ncclUniqueId shared by
+                                   all ranks (halo rows by NCCL send/recv). world 1: a ring of
+                                   one through NCCL (transport test). Unused in push mode. */
     void* stream;               /* cudaStream_t to run on; NULL = library-owned stream */
     int32_t event_hash;         /* 1 (default): accumulate the P7 event hash */
     int32_t whole_lattice;      /* 1: one CTA holds the whole lattice with periodic
@@ -92,7 +94,9 @@ typedef struct {
                                    boundary rows into the neighbour shard's halo as it writes them
                                    back (no exchange step; exact because words only grow and are
                                    never torn); 1 = exchange the halo rows before every launch
-                                   (device copies / NCCL send-recv). Same results. */
+                                   (device copies / NCCL send-recv). Same results. world > 1
+                                   with 0: the neighbours' halos are mapped by CUDA IPC
+                                   (aca_ipc_export / aca_ipc_import below). */
 } aca_options;
 
 typedef struct {
@@ -166,6 +170,25 @@ int aca_nccl_unique_id(void* out128);
 
 /* Number of cells of the handle (rank-local for multi-process handles). */
 int64_t aca_num_cells(const aca_sim* s);
+
+/* ---- Multi-process push mode (CUDA IPC; world > 1, halo_mode 0) ----
+ * One process per GPU owns a strip (2-D) / slab (3-D). Instead of exchanging halos between
+ * launches, every rank's tile kernel stores its boundary rows straight into its ring
+ * neighbours' halo buffers (over NVLink when they are on other GPUs) as it writes tiles back;
+ * a rank never waits for another inside a run (any interleaving is exact: words only grow and
+ * are never torn). A run starts with an epoch barrier and ends when every rank reports no
+ * active cell, both through small {epoch, active} slots mapped into every process.
+ * aca_ipc_export writes this rank's blob (ACA_IPC_BLOB_BYTES: IPC handles of its two halo
+ * buffers and its slot); the caller gathers all ranks' blobs in rank order and passes them to
+ * aca_ipc_import (world x ACA_IPC_BLOB_BYTES bytes), once, before the first run_until.
+ * Errors: ACA_ESTATE (not a push-mode handle / imported twice / run before import), ACA_EINVAL,
+ * ACA_ECUDA. Stats, frames and getters are rank-local as for the NCCL mode; the boundary
+ * bond term of aca_get_stats reads the halo copy of the neighbour's row, so take stats before
+ * any neighbour resets or sets its state (a barrier between runs and resets keeps it exact).
+ * Needs the persistent tile kernel (variant 0, 4 or 5; ACA_EINVAL at create otherwise). */
+#define ACA_IPC_BLOB_BYTES 192
+int aca_ipc_export(const aca_sim* s, void* out, size_t size);
+int aca_ipc_import(aca_sim* s, const void* blobs, size_t size);
 
 /* ---- Output frames (fig:genout) ----
  * Continue the simulation and capture the state of every cell at the frame times

@@ -23,7 +23,8 @@ ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: 
 EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
-           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q"]
+           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q", "aca_ipc_export", "aca_ipc_import"]
+ACA_IPC_BLOB_BYTES = 192
 POISSON, UNIFORM, ROOT8, GAUSS = 0, 1, 2, 3   # asynchrony laws (aca_options.law)
 
 
@@ -103,6 +104,8 @@ def lib():
                               ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, vp,
                               ctypes.POINTER(aca_agg_stats), ctypes.c_int]
     L.aca_bkl_run.argtypes = L.aca_agg_run.argtypes
+    L.aca_ipc_export.argtypes = [vp, vp, ctypes.c_size_t]
+    L.aca_ipc_import.argtypes = [vp, vp, ctypes.c_size_t]
     L.aca_efficiency_run_q.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
                                        ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     L.aca_run_frames.argtypes = [vp, ctypes.c_double, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]
@@ -269,6 +272,19 @@ class aca_agg_stats(ctypes.Structure):
     _fields_ = [("arrivals", ctypes.c_uint64), ("flips", ctypes.c_uint64), ("event_hash", ctypes.c_uint64),
                 ("bond_sum", ctypes.c_int64), ("magnetisation", ctypes.c_int64), ("launches", ctypes.c_uint64),
                 ("gpu_seconds", ctypes.c_double)]
+
+
+def aca_ipc_export(p):
+    """This rank's IPC blob (multi-process push mode)."""
+    buf = (ctypes.c_uint8 * ACA_IPC_BLOB_BYTES)()
+    _check(lib().aca_ipc_export(p, ctypes.cast(buf, ctypes.c_void_p), ACA_IPC_BLOB_BYTES))
+    return bytes(buf)
+
+
+def aca_ipc_import(p, blobs):
+    """All ranks' blobs, in rank order (bytes of world x ACA_IPC_BLOB_BYTES)."""
+    b = (ctypes.c_uint8 * len(blobs)).from_buffer_copy(blobs)
+    _check(lib().aca_ipc_import(p, ctypes.cast(b, ctypes.c_void_p), len(blobs)))
 
 
 def aca_agg_run(dims, m, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=ACA_HEATBATH, seed=1, init_q=0.5, budget=64,

@@ -14,6 +14,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <thread>
+#include <chrono>
 
 #include "../../include/aca.h"
 #include "aca_kernels.cuh"
@@ -146,6 +148,12 @@ struct aca_sim {
     bool sync = false;
     bool phased = false;           // checkerboard sweeps (two launches per outer round)
     bool push = false;             // sharded: boundary rows pushed into the neighbours' halos by the kernel
+    bool ipc = false;              // multi-process push mode: halos of the neighbour ranks mapped by CUDA IPC
+    bool ipc_ready = false;        // aca_ipc_import done
+    unsigned long long* d_slot = nullptr;              // this rank's {epoch, active} (exported)
+    std::vector<unsigned long long*> peer_slot;        // every rank's slot (own = d_slot)
+    std::vector<void*> ipc_opened;                     // mappings to close in aca_destroy
+    uint64_t epoch = 0;
     size_t smem = 0;
     int persistent_ctas = 0;       // > 0: grid size of the persistent tile kernel
     void* kern = nullptr;          // selected tile/whole kernel
@@ -541,6 +549,8 @@ void aca_destroy(aca_sim* S) {
         cudaFree(sh.ctl);
     }
     if (S->comm && nccl().ok) nccl().destroy(S->comm);
+    for (void* p : S->ipc_opened) cudaIpcCloseMemHandle(p);
+    cudaFree(S->d_slot);
     cudaFree(S->d_lr);
     cudaFree(S->scratch);
     cudaFree(S->d_stat);
@@ -589,7 +599,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) return fail(ACA_EINVAL, "bad rank/world");
     if ((opt.world > 1 || opt.nccl_id) && opt.shards != 1)
         return fail(ACA_EINVAL, "NCCL (multi-process) handles use shards = 1");
-    if (opt.world > 1 && !opt.nccl_id) return fail(ACA_EINVAL, "world > 1 needs nccl_id");
+    if (opt.world > 1 && !opt.nccl_id && opt.halo_mode != 0)
+        return fail(ACA_EINVAL, "world > 1 with halo_mode 1 (exchange) needs nccl_id");
     if (opt.rounds_per_launch < 0 || opt.launches_per_check < 0) return fail(ACA_EINVAL, "negative counts");
     if (opt.variant < 0 || opt.variant >= NVARIANT) return fail(ACA_EINVAL, "variant must be in [0, %d)", NVARIANT);
 
@@ -624,7 +635,10 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (cudaSetDevice(S->device) != cudaSuccess) { delete S; return fail(ACA_ECUDA, "cudaSetDevice(%d)", S->device); }
     S->rank = opt.world > 1 ? opt.rank : 0;
     S->world = opt.world;
-    S->use_nccl = opt.nccl_id != nullptr;   // world 1 + nccl_id: the ring of one (self-exchange)
+    // world > 1, halo_mode 0: push over CUDA IPC mappings of the neighbours' halos (no NCCL);
+    // otherwise an nccl_id selects NCCL send/recv exchange (world 1 + nccl_id: the ring of one)
+    S->ipc = opt.world > 1 && opt.halo_mode == 0;
+    S->use_nccl = !S->ipc && opt.nccl_id != nullptr;
     S->G = opt.world > 1 ? 1 : opt.shards;
     S->sync = opt.sync_rounds != 0;
     S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 4;   // measured knee with checkerboard sweeps
@@ -770,6 +784,13 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (cudaMallocHost(&S->h_ctl, 2 * sizeof(Ctl) * S->shards.size()) != cudaSuccess)
         return bail(fail(ACA_ENOMEM, "pinned ctl"));
 
+    if (S->ipc && !(S->persistent_ctas > 0 && !S->whole))
+        return bail(fail(ACA_EINVAL, "multi-process push mode needs the persistent tile kernel (variant 0/4/5)"));
+    if (S->ipc) {   // this rank's {epoch, active} slot, read by every rank through CUDA IPC
+        if (cudaMalloc(&S->d_slot, 16) != cudaSuccess) return bail(fail(ACA_ENOMEM, "ipc slot"));
+        if (cudaMemset(S->d_slot, 0, 16) != cudaSuccess) return bail(fail(ACA_ECUDA, "ipc slot"));
+        S->push = true;   // push pointers are set by aca_ipc_import
+    }
     if (S->use_nccl) {
         NcclApi& api = nccl();
         if (!api.ok) return bail(fail(ACA_ENCCL, "NCCL symbols not found in the process (load torch.distributed nccl first)"));
@@ -798,7 +819,28 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
                            cudaMemcpyHostToDevice, S->stream));
         CK(cudaMemsetAsync(&S->shards[i].ctl->done, 0, sizeof(unsigned int), S->stream));
     }
-    if (S->push) {   // push mode: fill the halos once; the kernels keep them current
+    if (S->ipc) {
+        // multi-process push mode: write this rank's boundary rows into the neighbours' halos,
+        // then wait until every rank has done so for this run (epoch barrier on the mapped
+        // slots); from then on no rank waits for another until termination
+        if (!S->ipc_ready) return fail(ACA_ESTATE, "multi-process push mode: call aca_ipc_import first");
+        Shard& sh = S->shards[0];
+        CK(cudaMemcpyAsync(sh.push_lo, sh.words, sh.face * 8, cudaMemcpyDeviceToDevice, S->stream));
+        CK(cudaMemcpyAsync(sh.push_hi, sh.words + (sh.n - sh.face), sh.face * 8, cudaMemcpyDeviceToDevice, S->stream));
+        CK(cudaStreamSynchronize(S->stream));
+        S->epoch += 1;
+        const unsigned long long mine[2] = {S->epoch, 1ull};
+        CK(cudaMemcpy(S->d_slot, mine, 16, cudaMemcpyHostToDevice));
+        for (int r = 0; r < S->world; ++r) {
+            for (long spins = 0;; ++spins) {
+                unsigned long long v[2];
+                CK(cudaMemcpy(v, S->peer_slot[r], 16, cudaMemcpyDeviceToHost));
+                if (v[0] >= S->epoch) break;
+                if (spins > 20000000) return fail(ACA_ESTATE, "rank %d never reached run %llu", r, (unsigned long long)S->epoch);
+                std::this_thread::sleep_for(std::chrono::microseconds(20));
+            }
+        }
+    } else if (S->push) {   // push mode: fill the halos once; the kernels keep them current
         rc = exchange(S);
         if (rc) return rc;
     }
@@ -853,6 +895,30 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         bool done = false;
         rc = retire(pipelined ? prev : 0, &done);
         if (rc) return rc;
+        if (S->ipc && done) {
+            // this rank has no cell below T any more (monotone: halos only grow); publish that
+            // and wait, without issuing more batches, until every rank has. A rank whose epoch is
+            // already ahead has seen all ranks done for this run.
+            if (outstanding >= 0) {
+                bool dummy;
+                rc = retire(outstanding, &dummy);
+                if (rc) return rc;
+                outstanding = -1;
+            }
+            const unsigned long long act = 0ull;
+            CK(cudaMemcpy(S->d_slot + 1, &act, 8, cudaMemcpyHostToDevice));
+            for (long spins = 0;; ++spins) {
+                bool all = true;
+                for (int r = 0; r < S->world && all; ++r) {
+                    unsigned long long v[2];
+                    CK(cudaMemcpy(v, S->peer_slot[r], 16, cudaMemcpyDeviceToHost));
+                    all = v[0] > S->epoch || (v[0] == S->epoch && v[1] == 0ull);
+                }
+                if (all) break;
+                if (spins > 50000000) return fail(ACA_ESTATE, "peers never finished run %llu", (unsigned long long)S->epoch);
+                std::this_thread::sleep_for(std::chrono::microseconds(20));
+            }
+        }
         if (S->use_nccl) {
             // every rank must agree: all-reduce of the local "still active" flag
             NcclApi& api = nccl();
@@ -1489,5 +1555,55 @@ int aca_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J
                 aca_agg_stats* st, int device) {
     return agg_run_impl(true, dims, m, lambda, beta, J, h, rule, seed, init_q, T, budget, spins_out, T_out, n_out, st,
                         device);
+}
+
+// ---------------------------------------------------------------- multi-process push (CUDA IPC)
+int aca_ipc_export(const aca_sim* S, void* out, size_t size) {
+    if (!S || !out) return fail(ACA_EINVAL, "null argument");
+    if (!S->ipc) return fail(ACA_ESTATE, "not a multi-process push-mode handle (world > 1, halo_mode 0)");
+    if (size != ACA_IPC_BLOB_BYTES) return fail(ACA_EINVAL, "blob size must be %d", ACA_IPC_BLOB_BYTES);
+    CK(cudaSetDevice(S->device));
+    cudaIpcMemHandle_t h[3];
+    CK(cudaIpcGetMemHandle(&h[0], S->shards[0].halo_lo));
+    CK(cudaIpcGetMemHandle(&h[1], S->shards[0].halo_hi));
+    CK(cudaIpcGetMemHandle(&h[2], S->d_slot));
+    memcpy(out, h, sizeof h);
+    return ACA_OK;
+}
+
+int aca_ipc_import(aca_sim* S, const void* blobs, size_t size) {
+    if (!S || !blobs) return fail(ACA_EINVAL, "null argument");
+    if (!S->ipc) return fail(ACA_ESTATE, "not a multi-process push-mode handle (world > 1, halo_mode 0)");
+    if (size != (size_t)S->world * ACA_IPC_BLOB_BYTES) return fail(ACA_EINVAL, "expected world x %d bytes", ACA_IPC_BLOB_BYTES);
+    if (S->ipc_ready) return fail(ACA_ESTATE, "already imported");
+    CK(cudaSetDevice(S->device));
+    const cudaIpcMemHandle_t* H = (const cudaIpcMemHandle_t*)blobs;   // [rank][3]
+    auto open = [&](int r, int which, void** p) -> int {
+        if (r == S->rank) {   // own buffers (world 1 never gets here)
+            *p = which == 0 ? (void*)S->shards[0].halo_lo : which == 1 ? (void*)S->shards[0].halo_hi : (void*)S->d_slot;
+            return ACA_OK;
+        }
+        cudaError_t e = cudaIpcOpenMemHandle(p, H[3 * r + which], cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return fail(ACA_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+        S->ipc_opened.push_back(*p);
+        return ACA_OK;
+    };
+    const int lo = (S->rank + S->world - 1) % S->world, hi = (S->rank + 1) % S->world;
+    void* p = nullptr;
+    int rc = open(lo, 1, &p);   // the lower neighbour's halo_hi receives my first row
+    if (rc) return rc;
+    S->shards[0].push_lo = (unsigned long long*)p;
+    rc = open(hi, 0, &p);        // the upper neighbour's halo_lo receives my last row
+    if (rc) return rc;
+    S->shards[0].push_hi = (unsigned long long*)p;
+    S->peer_slot.assign(S->world, nullptr);
+    for (int r = 0; r < S->world; ++r) {
+        rc = open(r, 2, &p);
+        if (rc) return rc;
+        S->peer_slot[r] = (unsigned long long*)p;
+    }
+    S->ipc_ready = true;
+    drop_graph(S);   // kernel parameters (push pointers) changed
+    return ACA_OK;
 }
 }  // extern "C"

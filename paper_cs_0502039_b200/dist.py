@@ -1,7 +1,8 @@
 """Host-side multi-process plumbing (torch.distributed): partition of the sharded axis,
 ncclUniqueId distribution, max/sum reductions of timings and counters, gathering of
-rank-local shards. No arithmetic of the method lives here; the halo exchange itself runs
-inside libaca.so (NCCL send/recv between ring neighbours).
+rank-local shards, and the CUDA-IPC handle exchange of the multi-process push mode. No
+arithmetic of the method lives here; the halo traffic itself runs inside libaca.so (kernel
+stores into the neighbours' mapped halos, or NCCL send/recv).
 Works with the gloo backend on CPU tensors (tests) and with nccl on GPUs (bench)."""
 import numpy as np
 import torch
@@ -37,6 +38,22 @@ def broadcast_bytes(payload, src=0, nbytes=128):
         t.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
     dist.broadcast(t, src)
     return bytes(t.cpu().numpy().tobytes())
+
+
+def all_gather_bytes(payload):
+    """Every rank's bytes (equal lengths), concatenated in rank order."""
+    b = bytes(payload)
+    t = torch.frombuffer(bytearray(b), dtype=torch.uint8).to(_device())
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return b"".join(bytes(o.cpu().numpy().tobytes()) for o in out)
+
+
+def ipc_connect(handle):
+    """Multi-process push mode: exchange the CUDA-IPC blobs (aca_ipc_export) of all ranks and
+    map the neighbours' halos and every rank's slot into this process (aca_ipc_import)."""
+    import paper_cs_0502039_b200 as aca
+    aca.aca_ipc_import(handle, all_gather_bytes(aca.aca_ipc_export(handle)))
 
 
 def reduce_max(x):

@@ -35,7 +35,9 @@ def _worker(rank, world, port, q):
         full = np.arange(16 * 8, dtype=np.int64).reshape(8, 16)
         local = full[y0:y1].ravel().astype(np.uint64)
         g = adist.gather_shards(local, dims)
-        q.put((rank, parts, uid == bytes(range(128)), tmax, tot, bool(np.array_equal(g, full.astype(np.uint64)))))
+        blobs = adist.all_gather_bytes(bytes([rank + 1]) * 192)   # IPC blob exchange (push mode)
+        q.put((rank, parts, uid == bytes(range(128)) and blobs == b"\x01" * 192 + b"\x02" * 192, tmax, tot,
+               bool(np.array_equal(g, full.astype(np.uint64)))))
     finally:
         dist.destroy_process_group()
 
