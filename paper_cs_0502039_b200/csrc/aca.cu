@@ -128,7 +128,7 @@ struct aca_sim {
     unsigned long long thr[14] = {};
     unsigned long long thm[98] = {};   // a10 early-rejection table (see commit_loop)
     int bulk = 1;
-    int defer_tail = 0;            // ablation only: deferring costs arrivals per sweep
+    int defer_tail = 0;            // ablation (ACA_DEFER_TAIL=1): carry the partial fire chunk; costs arrivals per sweep
     unsigned long long thr_init = 0;
     unsigned long long max_delta = 0;
     uint64_t T_last = 0;

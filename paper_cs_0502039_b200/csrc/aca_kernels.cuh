@@ -160,6 +160,12 @@ __device__ __forceinline__ void push_word(const KParams& P, int gx, int gy, int 
 
 // ---------------------------------------------------------------- TMA bulk-copy helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// one 16-B aligned pair of shared words, read as a volatile (each 8-B word single-copy atomic)
+__device__ __forceinline__ ulonglong2 lds128v(const volatile unsigned long long* p) {
+    ulonglong2 v;
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(smem_u32((const void*)p)) : "memory");
+    return v;
+}
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -168,13 +174,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                  ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+#ifndef MBAR_SUSPEND_NS
+#define MBAR_SUSPEND_NS 20000   // try_wait suspend-time hint: waiting warps sleep instead of spinning
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}"
-        ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+        ::"r"(smem_u32(bar)), "r"(parity), "r"(MBAR_SUSPEND_NS) : "memory");
 }
 // global -> shared bulk copy (size % 16 == 0, both addresses 16-B aligned), completes on bar
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
@@ -317,6 +326,31 @@ __device__ __forceinline__ FireOut fire_fast(unsigned long long w, uint32_t ones
                     (unsigned long long)(sb ^ flip));
     }
     return o;
+}
+
+// The high-half test of two horizontally adjacent cells (PAIRMAP): cell k (k = 0, 1) is active
+// iff ah_k < wh and a candidate iff also ah_k <= m_k (bit `bit0 << k` of em); any equality
+// (ah_k == m_k or ah_k == wh) clears `tie`, sending the lane to the exact full-word pass.
+// Written with explicit predicates so each decision is one compare and one predicated op.
+__device__ __forceinline__ void pair_test(unsigned int ah0, unsigned int ah1, unsigned int m0, unsigned int m1,
+                                          unsigned int wh, uint32_t bit0, uint32_t& em, int& nt,
+                                          unsigned int& tie) {
+    asm("{\n\t.reg .pred pa, pb, pl, pm, pt;\n\t"
+        "setp.lt.u32 pa, %3, %7;\n\t"
+        "setp.lt.u32 pb, %4, %7;\n\t"
+        "setp.le.and.u32 pl, %3, %5, pa;\n\t"
+        "setp.le.and.u32 pm, %4, %6, pb;\n\t"
+        "@pl or.b32 %0, %0, %8;\n\t"
+        "@pm or.b32 %0, %0, %9;\n\t"
+        "@pa add.s32 %1, %1, 1;\n\t"
+        "@pb add.s32 %1, %1, 1;\n\t"
+        "setp.eq.u32 pt, %3, %5;\n\t"
+        "setp.eq.or.u32 pt, %4, %6, pt;\n\t"
+        "setp.eq.or.u32 pt, %3, %7, pt;\n\t"
+        "setp.eq.or.u32 pt, %4, %7, pt;\n\t"
+        "@pt mov.u32 %2, 0;\n\t}"
+        : "+r"(em), "+r"(nt), "+r"(tie)
+        : "r"(ah0), "r"(ah1), "r"(m0), "r"(m1), "r"(wh), "r"(bit0), "r"(bit0 << 1));
 }
 
 // ------------------------------------------------------------------------ uncompacted tile kernel
@@ -472,7 +506,7 @@ __host__ __device__ constexpr size_t tma_queue_entries(int ncell, int nt, bool w
 }
 __host__ __device__ constexpr size_t tma_smem_bytes(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl,
                                                     bool early, int hw = 1) {
-    return (tma_words(ndim, tx, ty, tz, hw) * nbuf + 16 + 112 + nt / 32 + 2) * 8 +
+    return (tma_words(ndim, tx, ty, tz, hw) * nbuf + 16 + 112 + 512 + nt / 32 + 2) * 8 +
            ((tma_queue_entries(tx * ty * tz, nt, wl, early, hw) * 2 + 15) & ~(size_t)15) +
            (wl ? (size_t)tx * ty * tz / 32 * 8 + 16 : 0);
 }
@@ -628,26 +662,49 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
         }
     }
+    // PAIRMAP (2-D, 64-wide tiles): lane `lane` owns the column pair (2 lane, 2 lane + 1) of the
+    // warp's CPW / TX rows; cell j is row j / 2, column 2 lane + j % 2. The test then reads each
+    // row pair with one 128-bit load and reuses every loaded row as the neighbour row of the
+    // next: 1.5 loads per cell instead of 5. Otherwise lane `lane` owns columns lane + 32 k.
+    constexpr int RPW = CPW / TX;
+    constexpr bool PAIRMAP = NDIM == 2 && TX == 64 && HW == 1 && !MOORE && !EARLY && CPW % TX == 0 &&
+                             RPW % 2 == 0 && JPL == 2 * RPW;
     int s0 = 0;
-    if (FASTMAP) {
+    if (PAIRMAP) {
+        s0 = slot(2 * lane, warp * RPW, 0);
+    } else if (FASTMAP) {
         const int row0 = warp * (CPW / TX);
         s0 = slot(lane, row0 % TY, row0 / TY);
     }
     unsigned int rounds = 0;
+    auto cell_o = [&](int j) {   // tile-local cell index of the lane's j-th cell
+        if (PAIRMAP) return wbase + (j >> 1) * TX + 2 * lane + (j & 1);
+        return wbase + lane + 32 * j;
+    };
     auto cell_slot = [&](int j) {
+        if (PAIRMAP) return s0 + (j >> 1) * SX + (j & 1);
         if (FASTMAP) return s0 + (j / LPR) * SX + 32 * (j % LPR);
-        const int o = wbase + lane + 32 * j;
+        const int o = cell_o(j);
         return slot(o % TX, (o / TX) % TY, o / (TX * TY));
     };
     auto cell_valid = [&](int j) {
         if (FULL) return true;
-        const int o = wbase + lane + 32 * j;
+        const int o = cell_o(j);
         const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
         return x0 + lx < g.nx && y0 + ly < g.ny && (NDIM == 2 || z0 + lz < g.nz);
     };
     uint32_t fl32 = 0, fi32 = 0;   // fast-path flips / fires (folded into st at the end)
+    // Carried fire chunk (P.defer_tail, 1-cell halo): a round fires whole 32-lane chunks only;
+    // its partial last chunk moves to the front of the warp's queue and fires first in the next
+    // round (or in the last round, which fires everything). A carried cell stays a local minimum
+    // (its neighbours cannot pass it before it fires), so it is exact; its owner lane keeps it
+    // in `pend` so it is not queued twice.
+    const bool carry_on = HW == 1 && P.defer_tail;
+    uint32_t pend = 0;
+    int carry = 0;
     for (int r = 0; r < P.rounds; ++r) {
         uint32_t emask = 0, amask = 0;
+        int ntest = 0;   // PAIRMAP counts tested cells directly
         if constexpr (!EARLY) {
             // Branch-free test in batches of TB cells: every load of the batch is issued before
             // any compare (the lane's cells are independent), the 32-bit high halves decide
@@ -655,6 +712,54 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             constexpr int TB = 4;
             static_assert(JPL % TB == 0, "cells per lane must be a multiple of the test batch");
             uint32_t tmask = 0;
+            if constexpr (PAIRMAP) {
+                const unsigned int wh = (unsigned int)(wlim >> 32);
+                unsigned int tiec = ~0u;
+                // rows of the lane's column pair, top to bottom; `a` holds row rr, `b` row rr + 1
+                const ulonglong2 up = lds128v(&VS[s0 - SX]);
+                unsigned int uh0 = (unsigned int)(up.x >> 32), uh1 = (unsigned int)(up.y >> 32);
+                ulonglong2 a = lds128v(&VS[s0]);
+#pragma unroll
+                for (int rr = 0; rr < RPW; ++rr) {
+                    const int sr = s0 + rr * SX;
+                    const ulonglong2 b = lds128v(&VS[sr + SX]);   // row rr + 1 (halo row for the last)
+                    const unsigned int lh = VH[2 * (sr - 1) + 1], rh = VH[2 * (sr + 2) + 1];
+                    const unsigned int ah0 = (unsigned int)(a.x >> 32), ah1 = (unsigned int)(a.y >> 32);
+                    const unsigned int m0 = min(min(lh, ah1), min(uh0, (unsigned int)(b.x >> 32)));
+                    const unsigned int m1 = min(min(ah0, rh), min(uh1, (unsigned int)(b.y >> 32)));
+                    const int j = 2 * rr;
+                    // Decided on the 32-bit high halves: active iff high(w) < high(wlim), eligible
+                    // iff high(w) <= the neighbours' minimum. A lane that sees any equality (with a
+                    // neighbour, or with the T bucket) redoes its cells on the full words below.
+                    if constexpr (FULL) {
+                        pair_test(ah0, ah1, m0, m1, wh, 1u << j, emask, ntest, tiec);
+                    } else {
+                        if (cell_valid(j) && ah0 < wh) {
+                            ++ntest;
+                            if (ah0 <= m0) emask |= 1u << j;
+                        }
+                        if (cell_valid(j + 1) && ah1 < wh) {
+                            ++ntest;
+                            if (ah1 <= m1) emask |= 2u << j;
+                        }
+                        if (ah0 == m0 || ah0 == wh || ah1 == m1 || ah1 == wh) tiec = 0u;
+                    }
+                    uh0 = ah0; uh1 = ah1;
+                    a = b;
+                }
+                if (tiec == 0u) {   // rare: exact test of the lane's cells on the full words
+                    emask = 0;
+                    ntest = 0;
+#pragma unroll 1
+                    for (int j = 0; j < JPL; ++j) {
+                        const int sj = cell_slot(j);
+                        const unsigned long long w = VS[sj];
+                        if (!cell_valid(j) || w >= wlim) continue;
+                        ++ntest;
+                        if (w < VS[sj - 1] && w < VS[sj + 1] && w < VS[sj - SX] && w < VS[sj + SX]) emask |= 1u << j;
+                    }
+                }
+            } else
 #pragma unroll
             for (int j0 = 0; j0 < JPL; j0 += TB) {
                 unsigned long long wv[TB];
@@ -688,7 +793,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 const unsigned long long w = VS[s];
                 bool e;
                 if (MOORE) {   // rank bits are 0: compare the times, then the cell ids
-                    const int o = wbase + lane + 32 * j;
+                    const int o = cell_o(j);
                     const int lx = o % TX, ly = (o / TX) % TY;
                     const unsigned long long t = w >> g.TSH;
                     const long long cs = id2(g, x0 + lx, y0 + ly);
@@ -760,7 +865,8 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
             amask |= (uint32_t)act << j;
         }
-        st.tested += __popc(amask);
+        st.tested += __popc(amask) + ntest;
+        emask &= ~pend;   // carried cells are queued already
         const int mine = __popc(emask);
         int incl = mine;
 #pragma unroll
@@ -768,18 +874,34 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             const int v = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += v;
         }
-        const int cnt = __shfl_sync(0xffffffffu, incl, 31);
-        int pos = incl - mine;
-        while (emask) {
-            const int j = __ffs(emask) - 1;
-            emask &= emask - 1u;
-            q[pos++] = (unsigned short)(j < JPL ? wbase + lane + 32 * j : NCELL + tid + (j - JPL) * NT);
+        const int cnt = carry + __shfl_sync(0xffffffffu, incl, 31);
+        int pos = carry + incl - mine;
+        const int nfire = (carry_on && r < P.rounds - 1 && cnt > 32) ? (cnt & ~31) : cnt;
+        pend = 0;
+        if (carry_on) {
+            while (emask) {
+                const int j = __ffs(emask) - 1;
+                emask &= emask - 1u;
+                if (pos >= nfire) pend |= 1u << j;
+                q[pos++] = (unsigned short)cell_o(j);
+            }
+        } else if constexpr (PAIRMAP) {
+            // entry of cell j = base + (j / 2) TX + j % 2
+            unsigned short* qp = q + pos;
+            const int base = wbase + 2 * lane;
+            while (emask) {
+                const int j = __ffs(emask) - 1;
+                emask &= emask - 1u;
+                *qp++ = (unsigned short)(base + (j >> 1) * TX + (j & 1));
+            }
+        } else {
+            while (emask) {
+                const int j = __ffs(emask) - 1;
+                emask &= emask - 1u;
+                q[pos++] = (unsigned short)((HW == 1 || j < JPL) ? cell_o(j) : NCELL + tid + (j - JPL) * NT);
+            }
         }
         __syncwarp();
-        // Fire whole 32-lane chunks only; the partial tail chunk waits for the next round (its
-        // cells stay local minima, and every active cell is re-tested each round anyway). The
-        // last round, and rounds with a single (partial) chunk, fire everything.
-        const int nfire = (P.defer_tail && r < P.rounds - 1 && cnt > 32) ? (cnt & ~31) : cnt;
         for (int i = lane; i < nfire; i += 32) {
             const int o = q[i];
             if (HW == 2 && o >= NCELL) {   // ring cell of an idle neighbour tile: a real arrival
@@ -835,6 +957,14 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         // a queued cell is still a local minimum until its word is written, and lanes of a warp
         // are not guaranteed to reconverge after the divergent fire loop.
         __syncwarp();
+        if (cnt > nfire) {   // move the partial chunk (< 32 entries) to the queue front
+            const int nc = cnt - nfire;
+            const unsigned short e = lane < nc ? q[nfire + lane] : (unsigned short)0;
+            __syncwarp();
+            if (lane < nc) q[lane] = e;
+            __syncwarp();
+        }
+        carry = cnt - nfire;
         ++rounds;
         if (P.round_mode == 0) {
             if (__syncthreads_count(cnt > 0) == 0) break;   // CTA-wide stall detection
@@ -1231,12 +1361,10 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
 
     extern __shared__ __align__(128) unsigned long long smem[];
     unsigned long long* Sb = smem;                                  // NB_ x NSLOTP words
-    // The NLOG-2 table (4 KB) is read through L1 from global memory (it stays resident): keeping it
-    // out of shared memory lets 5 CTAs of a 64x64 tile share an SM instead of 4.
-    const unsigned long long* lr = P.lr;
     unsigned long long* thr = Sb + NB_ * NSLOTP;                    // 16
     unsigned long long* thm = thr + 16;                             // 112 (a10 table)
-    unsigned long long* red = thm + 112;                            // NW
+    unsigned long long* lr = thm + 112;                             // 512 (NLOG-2 table, 4 KB)
+    unsigned long long* red = lr + 512;                             // NW
     unsigned long long* bar = red + NW;                             // 2
     unsigned short* Q = (unsigned short*)(bar + 2);                 // fire queue(s), see tma_smem_bytes
     unsigned int* claim = (unsigned int*)(Q + ((tma_queue_entries(NCELL, NT, WL, EARLY || REG, HW) + 7) & ~(size_t)7));
@@ -1246,6 +1374,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
     for (int i = tid; i < 112; i += NT) thm[i] = i < 98 ? P.thm[i] : ~0ull;
+    for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
     if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); }
     __syncthreads();
 
