@@ -1454,7 +1454,9 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
                     S[slot(lx, ly, 0)] = ld_word_t<true>(P, x0 + lx, y0 + ly, 0);
                 }
             }
-            mbar_wait(&bar[b], (ph >> b) & 1u);
+            // one warp waits for the TMA rows (the others block in the barrier below without
+            // taking issue slots); the barrier then orders the rows before every thread's reads
+            if (warp == 0) mbar_wait(&bar[b], (ph >> b) & 1u);
             ph ^= 1u << b;
         } else {
             for (int i = tid; i < NSLOT; i += NT) {
@@ -1486,6 +1488,34 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
                                                                                        wlim, st);
         }
         rounds_max = rounds > rounds_max ? rounds : rounds_max;
+        // Per-warp write-back: with the per-warp fire queues a warp's own cells (the tile-linear
+        // range [warp CPW, (warp + 1) CPW)) are final once its round loop ends, so each warp
+        // stores its rows while the others are still firing; one barrier (below) then guards
+        // the buffer against the next staging.
+        constexpr bool WARP_WB = HW == 1 && !WL && !REG && !DB;
+        constexpr int CPW = NCELL / NW;
+        if (WARP_WB && fast) {
+            const int wb0 = warp * CPW;
+            for (int idx = lane; idx < CPW / 2; idx += 32) {
+                const int o = wb0 + 2 * idx;
+                const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0 + lx
+                                            : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0 + lx;
+                const ulonglong2 v = lds128v(&S[slot(lx, ly, lz)]);
+                *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
+                active += (v.x < wlim) + (v.y < wlim);
+                if (P.push_lo) {
+                    const int a = NDIM == 2 ? y0 + ly : z0 + lz, n = NDIM == 2 ? g.ny : g.nz;
+                    if (a == 0 || a == n - 1) {
+                        const size_t f = NDIM == 2 ? (size_t)(x0 + lx) : (size_t)(y0 + ly) * g.nx + x0 + lx;
+                        *reinterpret_cast<ulonglong2*>((a == 0 ? P.push_lo : P.push_hi) + f) = v;
+                        if (a == 0 && n == 1) *reinterpret_cast<ulonglong2*>(P.push_hi + f) = v;
+                    }
+                }
+            }
+            __syncthreads();   // the buffer is rewritten by a later staging
+            continue;
+        }
         __syncthreads();
 
         if (fast) {
