@@ -55,7 +55,7 @@ typedef struct {
     uint32_t struct_size;       /* = sizeof(aca_options); checked */
     double init_q;              /* P5: probability that s0(c) = -1 (default 0.5) */
     int32_t tile[3];            /* CTA tile (x, y, z); 0 = default (64x64, 32x16x8) */
-    int32_t rounds_per_launch;  /* R_max in-tile rounds per tile visit (0 = default 4) */
+    int32_t rounds_per_launch;  /* R_max in-tile rounds per tile visit (0 = default 5) */
     int32_t launches_per_check; /* K launches between host checks of termination (0 = 16) */
     int32_t tie_bits;           /* P3b tie-stress quantisation (0 = off) */
     int32_t sync_rounds;        /* 1: exact fig:s1c1pe two-phase rounds */

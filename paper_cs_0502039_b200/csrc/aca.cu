@@ -641,7 +641,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->use_nccl = !S->ipc && opt.nccl_id != nullptr;
     S->G = opt.world > 1 ? 1 : opt.shards;
     S->sync = opt.sync_rounds != 0;
-    S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 4;   // measured knee with checkerboard sweeps
+    S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 5;   // measured best (c3, c4, c5) with checkerboard sweeps
     S->K = opt.launches_per_check > 0 ? opt.launches_per_check : 16;
     if (const char* e = getenv("ACA_ROUND_MODE")) S->round_mode = atoi(e);
 
