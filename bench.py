@@ -323,7 +323,7 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
                        "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
-                       "tile": list(tile), "rounds_per_tile_visit": args.rounds or cfg.get("opts", {}).get("rounds_per_launch", 4),
+                       "tile": list(tile), "rounds_per_tile_visit": args.rounds or cfg.get("opts", {}).get("rounds_per_launch", aca.DEFAULT_ROUNDS),
                        "variant": args.variant,
                        "sweep": "checkerboard: 2 kernel launches per outer round (tile colours 0, 1)",
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,

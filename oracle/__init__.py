@@ -65,8 +65,8 @@ def lib():
         L.oracle_inv_lambda.restype = ctypes.c_uint64
         L.oracle_flip_table.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                         ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
-        L.oracle_mix64.argtypes = [ctypes.c_uint64]
-        L.oracle_mix64.restype = ctypes.c_uint64
+        L.oracle_ev_hash.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int]
+        L.oracle_ev_hash.restype = ctypes.c_uint64
         L.oracle_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_double,
                                     ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
                                     ctypes.c_uint64, ctypes.c_double, ctypes.c_int]
@@ -175,8 +175,9 @@ def flip_table(ndim, beta, J=1.0, h=0.0, rule=HEATBATH):
     return [int(v) for v in out]
 
 
-def mix64(z):
-    return lib().oracle_mix64(z)
+def ev_hash(w3, t, l, new_spin):
+    """P7 event hash term of one arrival."""
+    return lib().oracle_ev_hash(w3, t, l, new_spin)
 
 
 def _dims(dims):

@@ -124,13 +124,13 @@ void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint
 }
 
 /* ---------------------------------------------------------------- P7 */
-uint64_t oracle_mix64(uint64_t z) {
-    z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ULL;
-    z ^= z >> 27; z *= 0x94d049bb133111ebULL;
-    z ^= z >> 31;
-    return z;
+/* P7 event hash term (docs/PRIMITIVES.md): h = (w3 | 1) * (t ^ (l << 1) ^ s') mod 2^64, with w3
+ * the fourth Philox word of the arrival's draw, t the arrival time, l the cell within the
+ * subarray (0 for one-cell engines) and s' = 1 iff the new spin is +1. A checksum of our own
+ * design, not arithmetic of the paper's method. */
+uint64_t oracle_ev_hash(uint32_t w3, uint64_t t, uint64_t l, int new_spin) {
+    return (uint64_t)(w3 | 1u) * (t ^ (l << 1) ^ (uint64_t)(new_spin > 0 ? 1 : 0));
 }
-static uint64_t rotl64(uint64_t v, int r) { return (v << r) | (v >> (64 - r)); }
 
 /* ---------------------------------------------------------------- simulation state */
 struct oracle_sim {
@@ -252,8 +252,7 @@ static void arrival(oracle_sim* S, int64_t c, int8_t* new_s, uint64_t* new_t) {
         if ((uint64_t)w[0] < S->thr[idx]) { ns = -sc; S->flips++; }
     }
     uint64_t tev = S->t[c];
-    S->event_hash += oracle_mix64(tev ^ rotl64((uint64_t)c, 20) ^ rotl64((uint64_t)k, 44) ^
-                                  (uint64_t)(ns > 0 ? 1 : 0));
+    S->event_hash += oracle_ev_hash(w[3], tev, 0, ns);
     *new_s = (int8_t)ns;
     *new_t = tev + oracle_delta_law(w[1], w[2], S->inv_lambda, S->tie_bits, S->law);
 }
@@ -774,8 +773,7 @@ int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, doubl
         int ns = sc;
         if ((uint64_t)w[0] < thr[idx]) { ns = -sc; flips++; }   /* Step 4 */
         s[c] = (int8_t)ns;
-        hash += oracle_mix64(T[C] ^ rotl64((uint64_t)C, 20) ^ rotl64((uint64_t)k, 44) ^ ((uint64_t)l << 1) ^
-                             (uint64_t)(ns > 0 ? 1 : 0));
+        hash += oracle_ev_hash(w[3], T[C], (uint64_t)l, ns);
         T[C] += agg_delta(w[1], w[2], inv);                   /* Step 5 */
         n[C] = k + 1;
         arrivals++;
@@ -912,8 +910,7 @@ int oracle_bkl_run(const int64_t* dims, int m, double lambda, double beta, doubl
             s[y * nx + x] = (int8_t)ns;
             flips++;
         }
-        hash += oracle_mix64(T[C] ^ rotl64((uint64_t)C, 20) ^ rotl64((uint64_t)k, 44) ^ ((uint64_t)l << 1) ^
-                             (uint64_t)(ns > 0 ? 1 : 0));
+        hash += oracle_ev_hash(w[3], T[C], (uint64_t)l, ns);
         uint64_t W2 = bkl_weights(s, nx, ny, X, Y, m, thr, cls);
         T[C] += bkl_delta(w[2], w[3], lambda, W2);
         n[C] = k + 1;

@@ -40,8 +40,8 @@ uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law);
 uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits, int law);
 /* P4: thresholds, 2*(2*ndim+1) entries written to out. */
 void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint64_t* out);
-/* P7 */
-uint64_t oracle_mix64(uint64_t z);
+/* P7 event hash term: (w3 | 1) * (t ^ (l << 1) ^ [new_spin > 0]) mod 2^64 */
+uint64_t oracle_ev_hash(uint32_t w3, uint64_t t, uint64_t l, int new_spin);
 
 /* Returns NULL on invalid arguments. ndim in {2,3}, every dim >= 2, N < 2^32. */
 oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double beta, double J,

@@ -109,8 +109,7 @@ __global__ void __launch_bounds__(256) agg_round_kernel(const AggParams A, const
             q = (__umul64hi(q, A.inv) << 32) | ((q * A.inv) >> 32);
             q = q < 1 ? 1 : q;
             if (A.do_hash)
-                hsh += mix64(T ^ rotl64((unsigned long long)C, 20) ^ rotl64((unsigned long long)k, 44) ^
-                             ((unsigned long long)l << 1) ^ (unsigned long long)(sb ^ flip));
+                hsh += ev_hash(r.w, T, ((unsigned long long)l << 1) ^ (unsigned long long)(sb ^ flip));
             msk ^= (unsigned long long)flip << l;
             flips += flip;
             ++arr;
@@ -270,8 +269,7 @@ __global__ void __launch_bounds__(256) bkl_round_kernel(const AggParams A, const
                 flip = 1u;
             }
             if (A.do_hash)
-                hsh += mix64(T ^ rotl64((unsigned long long)C, 20) ^ rotl64((unsigned long long)k, 44) ^
-                             ((unsigned long long)l << 1) ^ (unsigned long long)(sb ^ flip));
+                hsh += ev_hash(r.w, T, ((unsigned long long)l << 1) ^ (unsigned long long)(sb ^ flip));
             msk ^= (unsigned long long)flip << l;
             flips += flip;
             ++arr;

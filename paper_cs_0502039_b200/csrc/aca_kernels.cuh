@@ -247,10 +247,7 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
     }
     o.h = 0;
     o.ok = true;
-    if (do_hash) {
-        const unsigned long long t = w >> g.TSH;
-        o.h = mix64(t ^ rotl64(c, 20) ^ rotl64((unsigned long long)k, 44) ^ (unsigned long long)(sb ^ flip));
-    }
+    if (do_hash) o.h = ev_hash(r.w, w >> g.TSH, (unsigned long long)(sb ^ flip));
     return o;
 }
 
@@ -306,6 +303,11 @@ __device__ __forceinline__ uint32_t cell_id32(const Geo& g, int gx, int gy, int 
     return g.ndim == 2 ? (uint32_t)(gy + g.y0) * (uint32_t)g.nx + (uint32_t)gx
                        : ((uint32_t)(gz + g.z0) * (uint32_t)g.NY + (uint32_t)gy) * (uint32_t)g.nx + (uint32_t)gx;
 }
+template <int NDIM>
+__device__ __forceinline__ uint32_t cell_id32t(const Geo& g, int gx, int gy, int gz) {
+    return NDIM == 2 ? (uint32_t)(gy + g.y0) * (uint32_t)g.nx + (uint32_t)gx
+                     : ((uint32_t)(gz + g.z0) * (uint32_t)g.NY + (uint32_t)gy) * (uint32_t)g.nx + (uint32_t)gx;
+}
 
 // fire() for the common configuration (Poisson law, lambda = 1, tie_bits = 0, no output frames,
 // N < 2^32): the same integers with the general branches compiled out. The caller raises the
@@ -326,11 +328,7 @@ __device__ __forceinline__ FireOut fire_fast(unsigned long long w, uint32_t ones
     o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;
     o.flip = flip;
     o.h = 0;
-    if (do_hash) {
-        const unsigned long long t = w >> g.TSH;
-        o.h = mix64(t ^ rotl64((unsigned long long)c, 20) ^ rotl64((unsigned long long)k, 44) ^
-                    (unsigned long long)(sb ^ flip));
-    }
+    if (do_hash) o.h = ev_hash(r.w, w >> g.TSH, (unsigned long long)(sb ^ flip));
     return o;
 }
 
@@ -571,10 +569,7 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
         if (u == 0) flip = (unsigned long long)r.x < thr[k + (uint32_t)(Z + 1) * sb] ? 1u : 0u;
         else if ((unsigned long long)r.x < tm) break;     // a flip is possible in some world: wait
         const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, P.tie_bits, P.law);
-        if (P.do_hash) {
-            const unsigned long long t = w >> g.TSH;
-            st.hacc += mix64(t ^ rotl64(cid, 20) ^ rotl64((unsigned long long)n, 44) ^ (unsigned long long)(sb ^ flip));
-        }
+        if (P.do_hash) st.hacc += ev_hash(r.w, w >> g.TSH, (unsigned long long)(sb ^ flip));
         if (P.fr.nb) {
             const unsigned long long tp = w >> g.TSH;
             frame_write(P.fr, tp, tp + d, cid, sb ^ flip);
@@ -942,7 +937,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 ones += (VH[2 * (s - SX - 1)] & 1u) + (VH[2 * (s - SX + 1)] & 1u) + (VH[2 * (s + SX - 1)] & 1u) +
                         (VH[2 * (s + SX + 1)] & 1u);
             if (P.fast) {   // uniform: Poisson law, lambda = 1, no tie stress, no frames, N < 2^32
-                const FireOut f = fire_fast(w, ones, Z, cell_id32(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
+                const FireOut f = fire_fast(w, ones, Z, cell_id32t<NDIM>(g, x0 + lx, y0 + ly, z0 + lz), g, thr, lr, P.rk,
                                             P.do_hash);
                 if (!f.ok) { atomicOr(&P.ctl->overflow, 1u); continue; }
                 VS[s] = f.wnew;

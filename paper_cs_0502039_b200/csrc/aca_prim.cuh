@@ -133,12 +133,11 @@ __device__ __forceinline__ uint64_t delta_q32(uint32_t w1, uint32_t w2, const un
 }
 
 // ---------------------------------------------------------------- P7 event hash
-__device__ __forceinline__ uint64_t mix64(uint64_t z) {
-    z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ull;
-    z ^= z >> 27; z *= 0x94d049bb133111ebull;
-    z ^= z >> 31;
-    return z;
+// P7 event hash term (docs/PRIMITIVES.md): h = (w3 | 1) * (t ^ (l << 1) ^ s') mod 2^64, w3 the
+// fourth Philox word of the arrival's draw, t its time before the increment, l the cell within
+// the subarray (0 for the per-cell engines), s' = 1 iff the new spin is +1.
+__device__ __forceinline__ uint64_t ev_hash(uint32_t w3, uint64_t t, uint64_t lsb) {
+    return (uint64_t)(w3 | 1u) * (t ^ lsb);
 }
-__device__ __forceinline__ uint64_t rotl64(uint64_t v, int r) { return (v << r) | (v >> (64 - r)); }
 
 }  // namespace aca

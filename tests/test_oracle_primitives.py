@@ -180,24 +180,34 @@ def test_flip_table_appendix_values(oracle_mod):
     assert set(oracle_mod.flip_table(3, 0.0, 1.0, 0.3, 1)) == {2 ** 32}
 
 
-def test_mix64_is_splitmix_finaliser(oracle_mod):
-    """P7 finaliser against a direct big-int evaluation of its definition and a bijection
-    spot check (the finaliser is invertible, so distinct inputs give distinct outputs)."""
+def test_event_hash_term(oracle_mod):
+    """P7 term h = (w3 | 1) (t ^ (l << 1) ^ s') mod 2^64 (docs/PRIMITIVES.md; a checksum of
+    our own design): the C implementation against big-int arithmetic on extreme and random
+    words, and injectivity in t for a fixed draw (odd multiplier), so two arrivals of one draw
+    at different times never cancel."""
     M = (1 << 64) - 1
-    r = random.Random(1)
-    seen = set()
-    for _ in range(2000):
-        z0 = r.getrandbits(64)
-        z = z0
-        z ^= z >> 30
-        z = (z * 0xBF58476D1CE4E5B9) & M
-        z ^= z >> 27
-        z = (z * 0x94D049BB133111EB) & M
-        z ^= z >> 31
-        v = oracle_mod.mix64(z0)
-        assert v == z
-        seen.add(v)
-    assert len(seen) == 2000
+    r = random.Random(7)
+    cases = [(0, 0, 0, -1), (0xFFFFFFFF, M, 0, 1), (1, 1 << 63, 63, 1), (0xFFFFFFFE, 12345, 0, -1)]
+    cases += [(r.getrandbits(32), r.getrandbits(64), r.randrange(64), r.choice((-1, 1))) for _ in range(2000)]
+    for w3, t, l, s in cases:
+        assert oracle_mod.ev_hash(w3, t, l, s) == ((w3 | 1) * (t ^ (l << 1) ^ (1 if s > 0 else 0))) & M
+    w3 = r.getrandbits(32)
+    ts = [r.getrandbits(40) for _ in range(3000)]
+    assert len({oracle_mod.ev_hash(w3, t, 0, 1) for t in ts}) == len(set(ts))
+
+
+def test_event_hash_of_the_first_arrival(oracle_mod):
+    """The oracle's event_hash after exactly one arrival equals the P7 term built from that
+    arrival's own P1 draw (w3 of Philox(seed; ctr = (0, c, 0, 0))), its time and new spin."""
+    dims, seed = (6, 5), 0x1234_5678_9ABC
+    o = oracle_mod.OracleSim(dims, beta=0.44, seed=seed)
+    t0 = o.times().ravel()
+    c = int(np.lexsort((np.arange(t0.size), t0))[0])     # smallest (t, c)
+    o.run_until_q32(int(t0[c]) + 1)
+    st = o.stats()
+    assert st["arrivals"] == 1
+    w = oracle_mod.philox((0, c, 0, 0), (seed & 0xFFFFFFFF, seed >> 32))
+    assert st["event_hash"] == oracle_mod.ev_hash(w[3], int(t0[c]), 0, int(o.spins().ravel()[c]))
 
 
 # ---------------------------------------------------------------- P3L asynchrony laws
