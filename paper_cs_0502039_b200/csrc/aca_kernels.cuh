@@ -903,6 +903,32 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
         }
         __syncwarp();
+        if (PAIRMAP && P.fast) {
+            // The common case (2-D, 64-wide tiles, Poisson, lambda = 1, no frames): the queue and
+            // the words are addressed with 32-bit shared-window offsets held in registers.
+            const uint32_t qa = smem_u32(q), sa = smem_u32(S);
+            const uint32_t cb = (uint32_t)(y0 + g.y0) * (uint32_t)g.nx + (uint32_t)x0;
+            for (int i = lane; i < nfire; i += 32) {
+                uint32_t o;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(o) : "r"(qa + 2u * (uint32_t)i) : "memory");
+                const uint32_t lx = o & (TX - 1), ly = o / TX;
+                const uint32_t a = sa + 8u * (o + 4u * ly + (uint32_t)(SX + 2));   // slot(lx, ly, 0)
+                unsigned long long w;
+                uint32_t b0, b1, b2, b3;
+                asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(a) : "memory");
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b0) : "r"(a - 8u) : "memory");
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b1) : "r"(a + 8u) : "memory");
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b2) : "r"(a - 8u * SX) : "memory");
+                asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b3) : "r"(a + 8u * SX) : "memory");
+                const uint32_t ones = (b0 & 1u) + (b1 & 1u) + (b2 & 1u) + (b3 & 1u);
+                const FireOut f = fire_fast(w, ones, Z, cb + ly * (uint32_t)g.nx + lx, g, thr, lr, P.rk, P.do_hash);
+                if (!f.ok) { atomicOr(&P.ctl->overflow, 1u); continue; }
+                asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(a), "l"(f.wnew) : "memory");
+                st.hacc += f.h;
+                fl32 += f.flip;
+                ++fi32;
+            }
+        } else
         for (int i = lane; i < nfire; i += 32) {
             const int o = q[i];
             if (HW == 2 && o >= NCELL) {   // ring cell of an idle neighbour tile: a real arrival
