@@ -887,13 +887,18 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 q[pos++] = (unsigned short)cell_o(j);
             }
         } else if constexpr (PAIRMAP) {
-            // entry of cell j = base + (j / 2) TX + j % 2
-            unsigned short* qp = q + pos;
-            const int base = wbase + 2 * lane;
+            // entry of cell j = base + (j / 2) TX + j % 2 = base | ((j << 5) & 0x1c0) | (j & 1)
+            // (base = warp CPW + 2 lane has no bits in 0x1c1); highest bit first
+            static_assert(TX == 64 && RPW <= 8, "PAIRMAP entry packing");
+            uint32_t qp = smem_u32(q) + 2u * (uint32_t)pos;
+            const uint32_t base = (uint32_t)(wbase + 2 * lane);
             while (emask) {
-                const int j = __ffs(emask) - 1;
-                emask &= emask - 1u;
-                *qp++ = (unsigned short)(base + (j >> 1) * TX + (j & 1));
+                uint32_t j;
+                asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(emask));
+                emask ^= 1u << j;
+                const uint32_t e = base | ((j << 5) & 0x1c0u) | (j & 1u);
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(qp), "h"((unsigned short)e) : "memory");
+                qp += 2u;
             }
         } else {
             while (emask) {
