@@ -67,9 +67,19 @@ __host__ __device__ inline void philox_round_keys(uint32_t k0, uint32_t k1, uint
 __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long long* __restrict__ lr,
                                              uint64_t ln2_q48) {
     const uint64_t x = X | 1ull;
-    const int z = __clzll((long long)x);
-    const uint64_t m = (x << z) << 1;
-    const uint32_t mh = (uint32_t)(m >> 32), ml = (uint32_t)m;
+    const uint32_t xh = (uint32_t)(x >> 32), xl = (uint32_t)x;
+    int z;
+    uint32_t mh, ml;   // m = x << (z + 1) mod 2^64, the mantissa bits below the leading one
+    if (xh != 0u) {    // all but 2^-32 of the draws: 32-bit leading-zero count and funnel shifts
+        z = __clz((int)xh);
+        mh = __funnelshift_lc(xl, xh, z + 1);
+        ml = __funnelshift_lc(0u, xl, z + 1);
+    } else {
+        z = __clzll((long long)x);
+        const uint64_t m = (x << z) << 1;
+        mh = (uint32_t)(m >> 32);
+        ml = (uint32_t)m;
+    }
     const uint32_t i = mh >> 24;
     const uint32_t g = __funnelshift_r(ml, mh, 24);          // bits 24..55 of m
     const uint64_t Li = lr[2 * i];

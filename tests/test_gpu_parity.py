@@ -64,6 +64,8 @@ def test_nlog_bit_identical_to_oracle(aca, oracle_mod):
     rng = np.random.default_rng(2)
     X = rng.integers(0, 2 ** 63, size=1 << 20, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, 1 << 20).astype(np.uint64)
     edges = [0, 1, 2, 3, 2 ** 63, 2 ** 63 + 1, 2 ** 64 - 1, 2 ** 64 - 2] + [2 ** k for k in range(64)]
+    edges += [2 ** 32 - 1, 2 ** 32 + 1, 2 ** 33 - 1, 2 ** 31 + 12345, (2 ** 32 - 1) << 32, (2 ** 32 + 7) << 30]
+    edges += [(2 ** k) - 1 for k in range(2, 64)] + [(2 ** k) + 1 for k in range(1, 64)]
     for i in range(256):
         edges += [((1 << 63) | (i << 55)) >> s for s in (0, 5, 33, 62)]
     X = np.concatenate([np.array(edges, np.uint64), X])
