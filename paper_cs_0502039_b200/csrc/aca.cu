@@ -278,7 +278,8 @@ struct TileKey {
      (ND == 2 ? (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, false, false, 1, (ND == 2)> : nullptr)}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 64, 1, 256, 4, 2, 3, 4),
+    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 32, 1, 128, 8, 6, 8, 8),
+    TK(2, 64, 64, 1, 256, 4, 2, 3, 4),
     TK(2, 128, 64, 1, 512, 1, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8, 8), TK(3, 16, 16, 16, 256, 2, 1, 2, 2),
     TK(3, 32, 16, 8, 256, 2, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
 };
@@ -717,8 +718,12 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         }
         if (ndim == 2) tz = 1;
         const TileKey* sel = nullptr;
+        const char* nt_env = getenv("ACA_TILE_NT");   // ablation: pick the block size of a tile shape
+        const int want_nt = nt_env ? atoi(nt_env) : 0;
         for (const auto& k : kTiles)
-            if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz) sel = &k;
+            if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz && (want_nt == 0 || k.nt == want_nt) &&
+                !sel)
+                sel = &k;
         if (!sel) return bail(fail(ACA_EINVAL, "unsupported tile %dx%dx%d for ndim %d", tx, ty, tz, ndim));
         const int v = S->sync ? NVARIANT : opt.variant;
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;

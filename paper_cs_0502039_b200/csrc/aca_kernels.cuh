@@ -336,6 +336,20 @@ __device__ __forceinline__ FireOut fire_fast(unsigned long long w, uint32_t ones
 // iff ah_k < wh and a candidate iff also ah_k <= m_k (bit `bit0 << k` of em); any equality
 // (ah_k == m_k or ah_k == wh) clears `tie`, sending the lane to the exact full-word pass.
 // Written with explicit predicates so each decision is one compare and one predicated op.
+// The same for one cell (COLMAP).
+__device__ __forceinline__ void one_test(unsigned int ah, unsigned int m, unsigned int wh, uint32_t bit, uint32_t& em,
+                                         int& nt, unsigned int& tie) {
+    asm("{\n\t.reg .pred pa, pl, pt;\n\t"
+        "setp.lt.u32 pa, %3, %5;\n\t"
+        "setp.le.and.u32 pl, %3, %4, pa;\n\t"
+        "@pl or.b32 %0, %0, %6;\n\t"
+        "@pa add.s32 %1, %1, 1;\n\t"
+        "setp.eq.u32 pt, %3, %4;\n\t"
+        "setp.eq.or.u32 pt, %3, %5, pt;\n\t"
+        "@pt mov.u32 %2, 0;\n\t}"
+        : "+r"(em), "+r"(nt), "+r"(tie)
+        : "r"(ah), "r"(m), "r"(wh), "r"(bit));
+}
 __device__ __forceinline__ void pair_test(unsigned int ah0, unsigned int ah1, unsigned int m0, unsigned int m1,
                                           unsigned int wh, uint32_t bit0, uint32_t& em, int& nt,
                                           unsigned int& tie) {
@@ -670,6 +684,10 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
     constexpr int RPW = CPW / TX;
     constexpr bool PAIRMAP = NDIM == 2 && TX == 64 && HW == 1 && !MOORE && !EARLY && CPW % TX == 0 &&
                              RPW % 2 == 0 && JPL == 2 * RPW;
+    // COLMAP (3-D, 32-wide tiles, one z-plane per warp): lane `lane` owns column `lane` of the
+    // warp's plane and walks its rows, reusing each row as the y-neighbour of the next (5 loads
+    // per cell instead of 7).
+    constexpr bool COLMAP = NDIM == 3 && TX == 32 && HW == 1 && !MOORE && !EARLY && CPW == TX * TY && JPL == TY;
     int s0 = 0;
     if (PAIRMAP) {
         s0 = slot(2 * lane, warp * RPW, 0);
@@ -758,6 +776,45 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                         if (!cell_valid(j) || w >= wlim) continue;
                         ++ntest;
                         if (w < VS[sj - 1] && w < VS[sj + 1] && w < VS[sj - SX] && w < VS[sj + SX]) emask |= 1u << j;
+                    }
+                }
+            } else if constexpr (COLMAP) {
+                const unsigned int wh = (unsigned int)(wlim >> 32);
+                unsigned int tiec = ~0u;
+                unsigned int uh = VH[2 * (s0 - SX) + 1];
+                unsigned long long a = VS[s0];
+#pragma unroll
+                for (int rr = 0; rr < TY; ++rr) {
+                    const int sr = s0 + rr * SX;
+                    const unsigned long long b = VS[sr + SX];   // row rr + 1 (halo row for the last)
+                    const unsigned int ah = (unsigned int)(a >> 32);
+                    const unsigned int m = min(min(min(VH[2 * (sr - 1) + 1], VH[2 * (sr + 1) + 1]),
+                                                   min(VH[2 * (sr - SXY) + 1], VH[2 * (sr + SXY) + 1])),
+                                               min(uh, (unsigned int)(b >> 32)));
+                    if constexpr (FULL) {
+                        one_test(ah, m, wh, 1u << rr, emask, ntest, tiec);
+                    } else {
+                        if (cell_valid(rr) && ah < wh) {
+                            ++ntest;
+                            if (ah <= m) emask |= 1u << rr;
+                        }
+                        if (ah == m || ah == wh) tiec = 0u;
+                    }
+                    uh = ah;
+                    a = b;
+                }
+                if (tiec == 0u) {   // rare: exact test of the lane's cells on the full words
+                    emask = 0;
+                    ntest = 0;
+#pragma unroll 1
+                    for (int j = 0; j < JPL; ++j) {
+                        const int sj = cell_slot(j);
+                        const unsigned long long w = VS[sj];
+                        if (!cell_valid(j) || w >= wlim) continue;
+                        ++ntest;
+                        if (w < VS[sj - 1] && w < VS[sj + 1] && w < VS[sj - SX] && w < VS[sj + SX] &&
+                            w < VS[sj - SXY] && w < VS[sj + SXY])
+                            emask |= 1u << j;
                     }
                 }
             } else
@@ -908,25 +965,31 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
         }
         __syncwarp();
-        if (PAIRMAP && P.fast) {
-            // The common case (2-D, 64-wide tiles, Poisson, lambda = 1, no frames): the queue and
-            // the words are addressed with 32-bit shared-window offsets held in registers.
+        if ((PAIRMAP || COLMAP) && P.fast) {
+            // The common case (64-wide 2-D / 32-wide 3-D tiles, Poisson, lambda = 1, no frames):
+            // the queue and the words are addressed with 32-bit shared-window offsets.
             const uint32_t qa = smem_u32(q), sa = smem_u32(S);
             const uint32_t cb = (uint32_t)(y0 + g.y0) * (uint32_t)g.nx + (uint32_t)x0;
             for (int i = lane; i < nfire; i += 32) {
                 uint32_t o;
                 asm volatile("ld.shared.u16 %0, [%1];" : "=r"(o) : "r"(qa + 2u * (uint32_t)i) : "memory");
-                const uint32_t lx = o & (TX - 1), ly = o / TX;
-                const uint32_t a = sa + 8u * (o + 4u * ly + (uint32_t)(SX + 2));   // slot(lx, ly, 0)
+                const uint32_t lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                const uint32_t a = sa + 8u * (uint32_t)slot((int)lx, (int)ly, (int)lz);
                 unsigned long long w;
-                uint32_t b0, b1, b2, b3;
+                uint32_t b0, b1, b2, b3, b4 = 0, b5 = 0;
                 asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(a) : "memory");
                 asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b0) : "r"(a - 8u) : "memory");
                 asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b1) : "r"(a + 8u) : "memory");
                 asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b2) : "r"(a - 8u * SX) : "memory");
                 asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b3) : "r"(a + 8u * SX) : "memory");
-                const uint32_t ones = (b0 & 1u) + (b1 & 1u) + (b2 & 1u) + (b3 & 1u);
-                const FireOut f = fire_fast(w, ones, Z, cb + ly * (uint32_t)g.nx + lx, g, thr, lr, P.rk, P.do_hash);
+                if constexpr (NDIM == 3) {
+                    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b4) : "r"(a - 8u * SXY) : "memory");
+                    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(b5) : "r"(a + 8u * SXY) : "memory");
+                }
+                const uint32_t ones = (b0 & 1u) + (b1 & 1u) + (b2 & 1u) + (b3 & 1u) + (b4 & 1u) + (b5 & 1u);
+                const uint32_t cid = NDIM == 2 ? cb + ly * (uint32_t)g.nx + lx
+                                               : cell_id32t<NDIM>(g, x0 + (int)lx, y0 + (int)ly, z0 + (int)lz);
+                const FireOut f = fire_fast(w, ones, Z, cid, g, thr, lr, P.rk, P.do_hash);
                 if (!f.ok) { atomicOr(&P.ctl->overflow, 1u); continue; }
                 asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(a), "l"(f.wnew) : "memory");
                 st.hacc += f.h;
