@@ -281,7 +281,7 @@ const TileKey kTiles[] = {
     TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 32, 1, 128, 8, 6, 8, 8),
     TK(2, 64, 64, 1, 256, 4, 2, 3, 4),
     TK(2, 128, 64, 1, 512, 1, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8, 8), TK(3, 16, 16, 16, 256, 2, 1, 2, 2),
-    TK(3, 32, 16, 8, 256, 2, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
+    TK(3, 32, 16, 8, 256, 3, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
 };
 
 constexpr int WHOLE_NT = 1024;
