@@ -554,7 +554,7 @@ struct TileStats {
 //    before the arrival, fig:amcgen stale-read argument PAPER.md:833-871). This is the exact
 //    use of the BKL observation that most attempts are rejections.
 // thm[(s*(Z+1) + u)*(Z+1) + k] (k = known +1 neighbours) > 2^32 means "wait".
-template <int NDIM, int SX, int SXY>
+template <int NDIM, int SX, int SXY, bool FASTP = false>
 __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned long long* VS, int s,
                                             unsigned long long cid, const unsigned long long* thr,
                                             const unsigned long long* thm, const unsigned long long* lr,
@@ -578,13 +578,21 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
         if (tm > (1ull << 32)) break;                     // must wait for the u neighbours
         const uint32_t n = w_count(w, g);
         if (n == (uint32_t)((1ull << g.NB) - 1ull)) { atomicOr(&P.ctl->overflow, 1u); break; }
-        const u32x4 r = philox4x32_10_rk(n, (uint32_t)cid, (uint32_t)(cid >> 32), 0u, P.rk);
+        // FASTP (P.fast: Poisson, lambda = 1, no tie stress, no frames, N < 2^32): the same
+        // integers with the general branches compiled out
+        const u32x4 r = philox4x32_10_rk(n, (uint32_t)cid, FASTP ? 0u : (uint32_t)(cid >> 32), 0u, P.rk);
         uint32_t flip = 0;
         if (u == 0) flip = (unsigned long long)r.x < thr[k + (uint32_t)(Z + 1) * sb] ? 1u : 0u;
         else if ((unsigned long long)r.x < tm) break;     // a flip is possible in some world: wait
-        const unsigned long long d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, P.tie_bits, P.law);
+        unsigned long long d;
+        if constexpr (FASTP) {
+            d = nlog_q32(((uint64_t)r.y << 32) | r.z, lr, ACA_LN2_Q48);
+            d = d < 1ull ? 1ull : d;
+        } else {
+            d = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, P.inv_lambda, P.tie_bits, P.law);
+        }
         if (P.do_hash) st.hacc += ev_hash(r.w, w >> g.TSH, (unsigned long long)(sb ^ flip));
-        if (P.fr.nb) {
+        if (!FASTP && P.fr.nb) {
             const unsigned long long tp = w >> g.TSH;
             frame_write(P.fr, tp, tp + d, cid, sb ^ flip);
         }
@@ -1020,7 +1028,11 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             const int lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
             const int s = slot(lx, ly, lz);
             if (EARLY) {
-                commit_loop<NDIM, SX, SXY>(P, VS, s, cell_id(g, x0 + lx, y0 + ly, z0 + lz), thr, thm, lr, wlim, st);
+                if (P.fast)
+                    commit_loop<NDIM, SX, SXY, true>(P, VS, s, cell_id32t<NDIM>(g, x0 + lx, y0 + ly, z0 + lz), thr, thm,
+                                                     lr, wlim, st);
+                else
+                    commit_loop<NDIM, SX, SXY>(P, VS, s, cell_id(g, x0 + lx, y0 + ly, z0 + lz), thr, thm, lr, wlim, st);
                 continue;
             }
             const unsigned long long w = VS[s];
