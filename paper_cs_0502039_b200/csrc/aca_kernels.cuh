@@ -1906,42 +1906,74 @@ struct StatAcc {
     unsigned long long hist[14];
 };
 
+// a9 statistics of one shard: B, M, sum n, max n, t range and the (s, Sigma) class histogram.
+// Each warp walks whole rows (x fastest) in a grid-stride loop over the shard's rows, so the
+// neighbour rows are plain pointers (periodic wrap, or the halo rows of a sharded axis) and
+// no per-cell division is needed; the histogram is counted with warp ballots (lane b holds
+// bin b) instead of shared-memory atomics.
 template <int NT>
 __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out, unsigned long long n_local) {
     const Geo& g = P.g;
-    __shared__ unsigned int hs[14];
-    if (threadIdx.x < 14) hs[threadIdx.x] = 0;
-    __syncthreads();
-    long long bond = 0, mag = 0;
-    unsigned long long arr = 0, tmin = ~0ull, tmax = 0, nmax = 0;
-    const unsigned long long plane = (unsigned long long)g.nx * g.ny;
+    const int lane = threadIdx.x & 31;
+    const int nwarps = gridDim.x * (NT / 32);
+    const int gw = blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+    const int nx = g.nx, ny = g.ny, nz = g.ndim == 3 ? g.nz : 1;
     const int Z = 2 * g.ndim;
-    for (unsigned long long i = blockIdx.x * (unsigned long long)NT + threadIdx.x; i < n_local;
-         i += (unsigned long long)gridDim.x * NT) {
-        const unsigned long long w = P.words[i];
-        const int s = (w & 1ull) ? 1 : -1;
-        const int x = (int)(i % g.nx);
-        int y, z;
-        if (g.ndim == 2) { y = (int)(i / g.nx); z = 0; }
-        else { y = (int)((i / g.nx) % g.ny); z = (int)(i / plane); }
-        const int ux = (int)(ld_word(P, x + 1, y, z) & 1ull), uy = (int)(ld_word(P, x, y + 1, z) & 1ull);
-        const int dx = (int)(ld_word(P, x - 1, y, z) & 1ull), dy = (int)(ld_word(P, x, y - 1, z) & 1ull);
-        int ones = ux + uy + dx + dy;
-        int plus = 2 * (ux + uy) - 2;
-        if (g.ndim == 3) {
-            const int uz = (int)(ld_word(P, x, y, z + 1) & 1ull), dz = (int)(ld_word(P, x, y, z - 1) & 1ull);
-            plus += 2 * uz - 1;
-            ones += uz + dz;
+    const size_t plane = (size_t)nx * ny;
+    long long bond = 0, mag = 0;
+    unsigned long long arr = 0, tmin = ~0ull, tmax = 0, nmax = 0, hcount = 0;
+    constexpr int SEG = 256;   // cells of a row per work item
+    const int nseg = (nx + SEG - 1) / SEG;
+    for (long long item = gw; item < (long long)ny * nz * nseg; item += nwarps) {
+        const int r = (int)(item / nseg), sg = (int)(item % nseg);
+        const int y = r % ny, z = r / ny;
+        const unsigned long long* cur = P.words + (size_t)r * nx;
+        const unsigned long long *yu, *yd, *zu = nullptr, *zd = nullptr;
+        if (g.ndim == 2) {
+            yu = y + 1 < ny ? cur + nx : (g.sharded ? P.halo_hi : P.words);
+            yd = y > 0 ? cur - nx : (g.sharded ? P.halo_lo : P.words + (size_t)(ny - 1) * nx);
+        } else {
+            yu = y + 1 < ny ? cur + nx : cur - (size_t)(ny - 1) * nx;
+            yd = y > 0 ? cur - nx : cur + (size_t)(ny - 1) * nx;
+            zu = z + 1 < nz ? cur + plane : (g.sharded ? P.halo_hi + (size_t)y * nx : P.words + (size_t)y * nx);
+            zd = z > 0 ? cur - plane
+                       : (g.sharded ? P.halo_lo + (size_t)y * nx : P.words + ((size_t)(nz - 1) * ny + y) * nx);
         }
-        atomicAdd(&hs[ones + (Z + 1) * (s > 0 ? 1 : 0)], 1u);
-        bond += s * plus;
-        mag += s;
-        const unsigned long long k = w_count(w, g);
-        arr += k;
-        nmax = k > nmax ? k : nmax;
-        const unsigned long long t = w_time(w, g);
-        tmin = t < tmin ? t : tmin;
-        tmax = t > tmax ? t : tmax;
+        const int xend = min(nx, (sg + 1) * SEG);
+        for (int x0 = sg * SEG; x0 < xend; x0 += 32) {
+            const int x = x0 + lane;
+            const bool valid = x < xend;
+            int idx = 31;   // histogram bin (31 = no cell)
+            if (valid) {
+                const unsigned long long w = cur[x];
+                const int sp = (int)(w & 1ull);
+                const int xr = x + 1 < nx ? x + 1 : 0, xl = x > 0 ? x - 1 : nx - 1;
+                const int ux = (int)(cur[xr] & 1ull), dx = (int)(cur[xl] & 1ull);
+                const int uy = (int)(yu[x] & 1ull), dy = (int)(yd[x] & 1ull);
+                int ones = ux + dx + uy + dy;
+                int plus = 2 * (ux + uy) - 2;
+                if (g.ndim == 3) {
+                    const int uz = (int)(zu[x] & 1ull), dz = (int)(zd[x] & 1ull);
+                    ones += uz + dz;
+                    plus += 2 * uz - 1;
+                }
+                idx = ones + (Z + 1) * sp;
+                const int sv = 2 * sp - 1;
+                bond += sv * plus;
+                mag += sv;
+                const unsigned long long k = w_count(w, g);
+                arr += k;
+                nmax = k > nmax ? k : nmax;
+                const unsigned long long t = w_time(w, g);
+                tmin = t < tmin ? t : tmin;
+                tmax = t > tmax ? t : tmax;
+            }
+#pragma unroll
+            for (int b = 0; b < 14; ++b) {
+                const unsigned int m = __ballot_sync(0xffffffffu, idx == b);
+                if (lane == b) hcount += __popc(m);
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1955,7 +1987,7 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         tmax = b > tmax ? b : tmax;
         nmax = c > nmax ? c : nmax;
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         atomicAdd((unsigned long long*)&out->bond, (unsigned long long)bond);
         atomicAdd((unsigned long long*)&out->mag, (unsigned long long)mag);
         atomicAdd(&out->arrivals, arr);
@@ -1963,8 +1995,8 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         atomicMax(&out->tmax, tmax);
         atomicMax(&out->nmax, nmax);
     }
-    __syncthreads();
-    if (threadIdx.x < 14 && hs[threadIdx.x]) atomicAdd(&out->hist[threadIdx.x], (unsigned long long)hs[threadIdx.x]);
+    if (lane < 14 && hcount) atomicAdd(&out->hist[lane], hcount);
+    (void)n_local;
 }
 
 }  // namespace aca
