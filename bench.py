@@ -228,10 +228,19 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    # ACA_BENCH_SHARED_GPU=1 (plumbing check only): every rank on cuda:0 with a gloo process
+    # group, so the N > 1 path (partition, IPC push transport, reductions) runs on one GPU.
+    # Its numbers are time-sliced and meaningless; the driver never sets it.
+    shared = os.environ.get("ACA_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = workloads.config(args.config)
     dims = tuple(cfg["dims"])
     ndim = len(dims)
