@@ -690,7 +690,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
     // row pair with one 128-bit load and reuses every loaded row as the neighbour row of the
     // next: 1.5 loads per cell instead of 5. Otherwise lane `lane` owns columns lane + 32 k.
     constexpr int RPW = CPW / TX;
-    constexpr bool PAIRMAP = NDIM == 2 && TX == 64 && HW == 1 && !MOORE && !EARLY && CPW % TX == 0 &&
+    constexpr bool PAIRMAP = NDIM == 2 && TX == 64 && HW == 1 && !MOORE && CPW % TX == 0 &&
                              RPW % 2 == 0 && JPL == 2 * RPW;
     // COLMAP (3-D, 32-wide tiles, one z-plane per warp): lane `lane` owns column `lane` of the
     // warp's plane and walks its rows, reusing each row as the y-neighbour of the next (5 loads
@@ -887,6 +887,34 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                     if (act && is_local_min<NDIM, SX, SXY>(VS, VH, rs[k], w)) emask |= 1u << (JPL + k);
                 }
             }
+        } else if constexpr (PAIRMAP) {
+            // a10 with the column-pair walk: the four neighbours' full words are in registers,
+            // so u (neighbours below) and k (+1 spins among the others) come from one pass;
+            // u = 0 is the local minimum (words are distinct), else the a10 table decides
+            const ulonglong2 up = lds128v(&VS[s0 - SX]);
+            unsigned long long u0 = up.x, u1 = up.y;
+            ulonglong2 a = lds128v(&VS[s0]);
+            auto early_cell = [&](unsigned long long w, unsigned long long n0, unsigned long long n1,
+                                  unsigned long long n2, unsigned long long n3, int j) {
+                if (!cell_valid(j) || w >= wlim) return;
+                ++ntest;
+                const uint32_t b0 = n0 < w, b1 = n1 < w, b2 = n2 < w, b3 = n3 < w;
+                const uint32_t u = b0 + b1 + b2 + b3;
+                const uint32_t k = (b0 ? 0u : (uint32_t)(n0 & 1ull)) + (b1 ? 0u : (uint32_t)(n1 & 1ull)) +
+                                   (b2 ? 0u : (uint32_t)(n2 & 1ull)) + (b3 ? 0u : (uint32_t)(n3 & 1ull));
+                const bool e = u == 0u || thm[((uint32_t)(w & 1ull) * (Z + 1) + u) * (Z + 1) + k] <= (1ull << 32);
+                emask |= (uint32_t)e << j;
+            };
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) {
+                const int sr = s0 + rr * SX;
+                const ulonglong2 b = lds128v(&VS[sr + SX]);
+                const unsigned long long lw = VS[sr - 1], rw = VS[sr + 2];
+                early_cell(a.x, lw, a.y, u0, b.x, 2 * rr);
+                early_cell(a.y, a.x, rw, u1, b.y, 2 * rr + 1);
+                u0 = a.x; u1 = a.y;
+                a = b;
+            }
         } else
 #pragma unroll
         for (int j = 0; j < JPL; ++j) {
@@ -973,7 +1001,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
         }
         __syncwarp();
-        if ((PAIRMAP || COLMAP) && P.fast) {
+        if ((PAIRMAP || COLMAP) && !EARLY && P.fast) {
             // The common case (64-wide 2-D / 32-wide 3-D tiles, Poisson, lambda = 1, no frames):
             // the queue and the words are addressed with 32-bit shared-window offsets.
             const uint32_t qa = smem_u32(q), sa = smem_u32(S);
