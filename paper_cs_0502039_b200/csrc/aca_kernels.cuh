@@ -1828,15 +1828,28 @@ __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const
     __shared__ unsigned long long lr[512];
     for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
     __syncthreads();
-    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n_local;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        unsigned long long c, rank;
-        cell_coords(g, i, c, rank);
-        const u32x4 r = philox4x32_10(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, key0, key1);
-        const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
-        const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
-        words[i] = w_pack(t0, g.RB ? rank : 0ull, 0ull, sb, g);
+    // work items = row segments of 256 cells (x fastest): coordinates without per-cell division
+    constexpr int SEG = 256;
+    const int nx = g.nx, ny = g.ny, nz = g.ndim == 3 ? g.nz : 1;
+    const int nseg = (nx + SEG - 1) / SEG;
+    const long long nitems = (long long)ny * nz * nseg;
+    for (long long item = blockIdx.x * (long long)(blockDim.x / 32) + (threadIdx.x >> 5); item < nitems;
+         item += (long long)gridDim.x * (blockDim.x / 32)) {
+        const int row = (int)(item / nseg), sg = (int)(item % nseg);
+        const int y = row % ny, z = row / ny;
+        const unsigned long long gy = g.ndim == 2 ? (unsigned long long)(y + g.y0) : (unsigned long long)y;
+        const unsigned long long gz = g.ndim == 2 ? 0ull : (unsigned long long)(z + g.z0);
+        const unsigned long long cbase = g.ndim == 2 ? gy * nx : (gz * g.NY + gy) * nx;
+        const int xend = min(nx, (sg + 1) * SEG);
+        for (int x = sg * SEG + (threadIdx.x & 31); x < xend; x += 32) {
+            const unsigned long long c = cbase + x, rank = (unsigned long long)x + gy + gz;
+            const u32x4 r = philox4x32_10(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, key0, key1);
+            const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
+            const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
+            words[(size_t)row * nx + x] = w_pack(t0, g.RB ? rank : 0ull, 0ull, sb, g);
+        }
     }
+    (void)n_local;
 }
 
 // Frame pre-fill at the start of a frame chunk: every arrival before the chunk is at most the
