@@ -471,7 +471,7 @@ int device_stats(aca_sim* S) {
     if (rc) return rc;
     for (auto& sh : S->shards) {
         KParams P = make_params(S, sh);
-        stats_kernel<256><<<592, 256, 0, S->stream>>>(P, S->d_stat, (unsigned long long)sh.n);
+        stats_kernel<256><<<1184, 256, 0, S->stream>>>(P, S->d_stat, (unsigned long long)sh.n);
         CK(cudaGetLastError());
     }
     CK(cudaMemcpyAsync(S->h_stat, S->d_stat, sizeof(StatAcc), cudaMemcpyDeviceToHost, S->stream));

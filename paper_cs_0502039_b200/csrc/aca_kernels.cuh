@@ -1962,11 +1962,16 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
     const int Z = 2 * g.ndim;
     const size_t plane = (size_t)nx * ny;
     long long bond = 0, mag = 0;
-    unsigned long long arr = 0, tmin = ~0ull, tmax = 0, nmax = 0, hcount = 0;
-    constexpr int SEG = 256;   // cells of a row per work item
+    unsigned long long arr = 0, wmin = ~0ull, wmax = 0;
+    unsigned int nmax = 0;
+    unsigned int hc[14];
+#pragma unroll
+    for (int b = 0; b < 14; ++b) hc[b] = 0;
+    constexpr int SEG = 256;   // cells of a row per work item (8 per lane)
     const int nseg = (nx + SEG - 1) / SEG;
-    for (long long item = gw; item < (long long)ny * nz * nseg; item += nwarps) {
-        const int r = (int)(item / nseg), sg = (int)(item % nseg);
+    const int nitems = ny * nz * nseg;
+    for (int item = gw; item < nitems; item += nwarps) {
+        const int r = item / nseg, sg = item - r * nseg;
         const int y = r % ny, z = r / ny;
         const unsigned long long* cur = P.words + (size_t)r * nx;
         const unsigned long long *yu, *yd, *zu = nullptr, *zd = nullptr;
@@ -1980,42 +1985,43 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
             zd = z > 0 ? cur - plane
                        : (g.sharded ? P.halo_lo + (size_t)y * nx : P.words + ((size_t)(nz - 1) * ny + y) * nx);
         }
+        // per item: 32-bit partial sums, and the histogram as 14 nibble counters (<= 8 cells)
+        int ib = 0, im = 0;
+        unsigned int ia = 0;
+        unsigned long long nib = 0;
         const int xend = min(nx, (sg + 1) * SEG);
-        for (int x0 = sg * SEG; x0 < xend; x0 += 32) {
-            const int x = x0 + lane;
-            const bool valid = x < xend;
-            int idx = 31;   // histogram bin (31 = no cell)
-            if (valid) {
-                const unsigned long long w = cur[x];
-                const int sp = (int)(w & 1ull);
-                const int xr = x + 1 < nx ? x + 1 : 0, xl = x > 0 ? x - 1 : nx - 1;
-                const int ux = (int)(cur[xr] & 1ull), dx = (int)(cur[xl] & 1ull);
-                const int uy = (int)(yu[x] & 1ull), dy = (int)(yd[x] & 1ull);
-                int ones = ux + dx + uy + dy;
-                int plus = 2 * (ux + uy) - 2;
-                if (g.ndim == 3) {
-                    const int uz = (int)(zu[x] & 1ull), dz = (int)(zd[x] & 1ull);
-                    ones += uz + dz;
-                    plus += 2 * uz - 1;
-                }
-                idx = ones + (Z + 1) * sp;
-                const int sv = 2 * sp - 1;
-                bond += sv * plus;
-                mag += sv;
-                const unsigned long long k = w_count(w, g);
-                arr += k;
-                nmax = k > nmax ? k : nmax;
-                const unsigned long long t = w_time(w, g);
-                tmin = t < tmin ? t : tmin;
-                tmax = t > tmax ? t : tmax;
+#pragma unroll 4
+        for (int x = sg * SEG + lane; x < xend; x += 32) {
+            const unsigned long long w = cur[x];
+            const int sp = (int)(w & 1ull);
+            const int xr = x + 1 < nx ? x + 1 : 0, xl = x > 0 ? x - 1 : nx - 1;
+            const int ux = (int)(cur[xr] & 1ull), dx = (int)(cur[xl] & 1ull);
+            const int uy = (int)(yu[x] & 1ull), dy = (int)(yd[x] & 1ull);
+            int ones = ux + dx + uy + dy;
+            int plus = 2 * (ux + uy) - 2;
+            if (g.ndim == 3) {
+                const int uz = (int)(zu[x] & 1ull), dz = (int)(zd[x] & 1ull);
+                ones += uz + dz;
+                plus += 2 * uz - 1;
             }
-#pragma unroll
-            for (int b = 0; b < 14; ++b) {
-                const unsigned int m = __ballot_sync(0xffffffffu, idx == b);
-                if (lane == b) hcount += __popc(m);
-            }
+            nib += 1ull << (4 * (ones + (Z + 1) * sp));
+            const int sv = 2 * sp - 1;
+            ib += sv * plus;
+            im += sv;
+            const unsigned int k = w_count(w, g);
+            ia += k;
+            nmax = k > nmax ? k : nmax;
+            wmin = w < wmin ? w : wmin;   // the time is monotone in the word
+            wmax = w > wmax ? w : wmax;
         }
+        bond += ib;
+        mag += im;
+        arr += ia;
+#pragma unroll
+        for (int b = 0; b < 14; ++b) hc[b] += (unsigned int)(nib >> (4 * b)) & 15u;
     }
+    unsigned long long tmin = wmin == ~0ull ? ~0ull : w_time(wmin, g), tmax = w_time(wmax, g);
+    unsigned long long nmx = nmax;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         bond += __shfl_xor_sync(0xffffffffu, bond, o);
@@ -2023,10 +2029,12 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         arr += __shfl_xor_sync(0xffffffffu, arr, o);
         const unsigned long long a = __shfl_xor_sync(0xffffffffu, tmin, o);
         const unsigned long long b = __shfl_xor_sync(0xffffffffu, tmax, o);
-        const unsigned long long c = __shfl_xor_sync(0xffffffffu, nmax, o);
+        const unsigned long long c = __shfl_xor_sync(0xffffffffu, nmx, o);
         tmin = a < tmin ? a : tmin;
         tmax = b > tmax ? b : tmax;
-        nmax = c > nmax ? c : nmax;
+        nmx = c > nmx ? c : nmx;
+#pragma unroll
+        for (int b2 = 0; b2 < 14; ++b2) hc[b2] += __shfl_xor_sync(0xffffffffu, hc[b2], o);
     }
     if (lane == 0) {
         atomicAdd((unsigned long long*)&out->bond, (unsigned long long)bond);
@@ -2034,9 +2042,11 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
         atomicAdd(&out->arrivals, arr);
         atomicMin(&out->tmin, tmin);
         atomicMax(&out->tmax, tmax);
-        atomicMax(&out->nmax, nmax);
+        atomicMax(&out->nmax, nmx);
+#pragma unroll
+        for (int b = 0; b < 14; ++b)
+            if (hc[b]) atomicAdd(&out->hist[b], (unsigned long long)hc[b]);
     }
-    if (lane < 14 && hcount) atomicAdd(&out->hist[lane], hcount);
     (void)n_local;
 }
 
