@@ -540,8 +540,18 @@ __host__ __device__ constexpr size_t tma_smem_bytes(int ndim, int tx, int ty, in
 // tie), (ii) compacts the eligible cells with a warp scan, (iii) fires them with all lanes
 // busy. A queued cell's neighbourhood is frozen until it fires (no neighbour can pass its
 // own test while the cell's lower word is unchanged), so compaction preserves exactness.
+// Per-lane counters of one tile visit (32-bit: at most NCELL x R x bulk per visit); the tile
+// kernels fold them into 64-bit totals after every visit (TileTotals).
 struct TileStats {
-    unsigned long long fired = 0, flips = 0, tested = 0, hacc = 0;
+    unsigned int fired = 0, flips = 0, tested = 0;
+    unsigned long long hacc = 0;
+};
+struct TileTotals {
+    unsigned long long fired = 0, flips = 0, tested = 0;
+    __device__ __forceinline__ void fold(TileStats& st) {
+        fired += st.fired; flips += st.flips; tested += st.tested;
+        st.fired = st.flips = st.tested = 0;
+    }
 };
 
 // Commit the pending arrivals of the cell in slot s for as long as that is exact (a10):
@@ -1522,6 +1532,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     const bool vec_ok = (g.nx % 2) == 0;
     const bool reverse = P.phase < 0 && ((*(volatile unsigned long long*)&P.ctl->launches) & 1ull);
     TileStats st;
+    TileTotals tot;
     unsigned long long active = 0;
     unsigned int rounds_max = 0;
     uint32_t ph = 0;   // bit b: parity of bar[b]
@@ -1636,6 +1647,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
                                                                                        wlim, st);
         }
         rounds_max = rounds > rounds_max ? rounds : rounds_max;
+        tot.fold(st);
         // Per-warp write-back: with the per-warp fire queues a warp's own cells (the tile-linear
         // range [warp CPW, (warp + 1) CPW)) are final once its round loop ends, so each warp
         // stores its rows while the others are still firing; one barrier (below) then guards
@@ -1700,9 +1712,10 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
         __syncthreads();   // the buffer is rewritten by a later staging
     }
     const unsigned long long s_act = block_sum<NT>(active, red);
-    const unsigned long long s_fir = block_sum<NT>(st.fired, red);
-    const unsigned long long s_flp = block_sum<NT>(st.flips, red);
-    const unsigned long long s_tst = block_sum<NT>(st.tested, red);
+    tot.fold(st);
+    const unsigned long long s_fir = block_sum<NT>(tot.fired, red);
+    const unsigned long long s_flp = block_sum<NT>(tot.flips, red);
+    const unsigned long long s_tst = block_sum<NT>(tot.tested, red);
     const unsigned long long s_hsh = block_sum<NT>(st.hacc, red);
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase);
 }
