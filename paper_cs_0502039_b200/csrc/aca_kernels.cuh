@@ -1533,7 +1533,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     const bool reverse = P.phase < 0 && ((*(volatile unsigned long long*)&P.ctl->launches) & 1ull);
     TileStats st;
     TileTotals tot;
-    unsigned long long active = 0;
+    unsigned int active = 0;   // cells of this CTA still below T (< 2^32: N < 2^32)
     unsigned int rounds_max = 0;
     uint32_t ph = 0;   // bit b: parity of bar[b]
 
@@ -1711,7 +1711,7 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
         }
         __syncthreads();   // the buffer is rewritten by a later staging
     }
-    const unsigned long long s_act = block_sum<NT>(active, red);
+    const unsigned long long s_act = block_sum<NT>((unsigned long long)active, red);
     tot.fold(st);
     const unsigned long long s_fir = block_sum<NT>(tot.fired, red);
     const unsigned long long s_flp = block_sum<NT>(tot.flips, red);
