@@ -75,21 +75,21 @@ def test_config2_full_digest(aca, oracle_mod):
         assert st[k] == v, k
 
 
+@pytest.mark.parametrize("seed", workloads.PARITY_SEEDS)
 @pytest.mark.parametrize("name,n_random,radii", [
     ("c3", 40, (8, 16, 32, 64)),
     ("c4", 24, (4, 8, 12, 16)),
     ("c5", 24, (8, 16, 32, 64, 96)),
 ])
-def test_full_size_sampled_parity(aca, oracle_mod, name, n_random, radii):
+def test_full_size_sampled_parity(aca, oracle_mod, name, n_random, radii, seed):
     cfg = workloads.config(name)
     dims, T = tuple(cfg["dims"]), cfg["T"]
     kw = dict(lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"])
-    seed = workloads.PARITY_SEEDS[0]
     g = aca.Sim(dims, seed=seed, init_q=cfg["init_q"], tile=cfg["tile"], **cfg.get("opts", {}), **kw)
     g.run_until(T)
     st = g.stats()
 
-    pts = sample_cells(dims, cfg["tile"], n_random, seed=7)
+    pts = sample_cells(dims, cfg["tile"], n_random, seed=7 + seed)
     idx = np.array([flat(c, dims) for c in pts], np.int64)
     s_g, t_g, n_g = g.cells(idx)
     unverified = 0
