@@ -140,6 +140,24 @@ __device__ __forceinline__ unsigned long long ld_word_t(const KParams& P, int gx
     if (gz >= g.nz) return P.halo_hi[(size_t)y * g.nx + x];
     return P.words[((size_t)gz * g.ny + y) * g.nx + x];
 }
+// Address of the word at (gx, gy, gz) with the same wrap / halo rules (the start of a halo row
+// for the face TMA copies).
+template <bool ONE>
+__device__ __forceinline__ const unsigned long long* word_ptr_t(const KParams& P, int gx, int gy, int gz) {
+    const Geo& g = P.g;
+    const int x = ONE ? wrap1(gx, g.nx) : wrapi(gx, g.nx);
+    if (g.ndim == 2) {
+        if (!g.sharded) return P.words + (size_t)(ONE ? wrap1(gy, g.ny) : wrapi(gy, g.ny)) * g.nx + x;
+        if (gy < 0) return P.halo_lo + x;
+        if (gy >= g.ny) return P.halo_hi + x;
+        return P.words + (size_t)gy * g.nx + x;
+    }
+    const int y = ONE ? wrap1(gy, g.ny) : wrapi(gy, g.ny);
+    if (!g.sharded) return P.words + ((size_t)(ONE ? wrap1(gz, g.nz) : wrapi(gz, g.nz)) * g.ny + y) * g.nx + x;
+    if (gz < 0) return P.halo_lo + (size_t)y * g.nx + x;
+    if (gz >= g.nz) return P.halo_hi + (size_t)y * g.nx + x;
+    return P.words + ((size_t)gz * g.ny + y) * g.nx + x;
+}
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -1552,18 +1570,32 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
         fast = full && vec_ok;
         return tx < P.tiles_x;
     };
+    // FACE_TMA: the halo rows of the y faces (and the z faces in 3-D) are contiguous in x like
+    // the tile's own rows, so they arrive by TMA as well (from the wrapped rows or the shard's
+    // halo buffers); only the x-face columns are loaded by threads.
+    constexpr bool FACE_TMA = HW == 1 && !MOORE;
+    constexpr int NFACE = FACE_TMA ? (NDIM == 2 ? 2 : 2 * TY + 2 * TZ) : 0;
     auto issue = [&](int it, int b) {   // warp 0: TMA of the tile's own rows into buffer b
         int x0, y0, z0; bool fast, full;
         if (!origin(it, x0, y0, z0, fast, full) || !fast) return;
-        if (lane == 0) mbar_arrive_expect_tx(&bar[b], (uint32_t)NROWS * TX * 8u);
+        if (lane == 0) mbar_arrive_expect_tx(&bar[b], (uint32_t)(NROWS + NFACE) * TX * 8u);
         __syncwarp();
         fence_proxy_async();
         unsigned long long* S = Sb + b * NSLOTP;
-        for (int row = lane; row < NROWS; row += 32) {
-            const int ly = row % TY, lz = row / TY;
-            const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
-                                        : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
-            bulk_g2s(&S[slot(0, ly, lz)], P.words + gi, TX * 8, &bar[b]);
+        for (int row = lane; row < NROWS + NFACE; row += 32) {
+            if (row < NROWS) {
+                const int ly = row % TY, lz = row / TY;
+                const size_t gi = NDIM == 2 ? (size_t)(y0 + ly) * g.nx + x0
+                                            : ((size_t)(z0 + lz) * g.ny + (y0 + ly)) * g.nx + x0;
+                bulk_g2s(&S[slot(0, ly, lz)], P.words + gi, TX * 8, &bar[b]);
+            } else {
+                const int k = row - NROWS;
+                int ly, lz;
+                if (NDIM == 2) { ly = k == 0 ? -1 : TY; lz = 0; }
+                else if (k < 2 * TY) { lz = k < TY ? -1 : TZ; ly = k % TY; }      // z faces
+                else { const int k2 = k - 2 * TY; ly = k2 < TZ ? -1 : TY; lz = k2 % TZ; }   // y faces
+                bulk_g2s(&S[slot(0, ly, lz)], word_ptr_t<true>(P, x0, y0 + ly, z0 + lz), TX * 8, &bar[b]);
+            }
         }
     };
 
@@ -1580,7 +1612,12 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
         }
         if (!valid) continue;   // odd tiles_x: the last column pair has one tile
         if (fast) {
-            if constexpr (HW == 1) {
+            if constexpr (FACE_TMA) {   // x-face columns only: left and right of every own row
+                for (int h = tid; h < 2 * NROWS; h += NT) {
+                    const int row = h >> 1, lx = (h & 1) ? TX : -1, ly = row % TY, lz = row / TY;
+                    S[slot(lx, ly, lz)] = ld_word_t<true>(P, x0 + lx, y0 + ly, z0 + lz);
+                }
+            } else if constexpr (HW == 1) {
                 for (int h = tid; h < NHALO; h += NT) {
                     int lx, ly, lz;
                     if (MOORE && h >= NHALO - 4) {   // the four corner cells (diagonal neighbours)
