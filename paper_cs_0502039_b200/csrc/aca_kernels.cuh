@@ -158,9 +158,6 @@ __device__ __forceinline__ const unsigned long long* word_ptr_t(const KParams& P
     if (gz >= g.nz) return P.halo_hi + (size_t)y * g.nx + x;
     return P.words + ((size_t)gz * g.ny + y) * g.nx + x;
 }
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_word(const KParams& P, int gx, int gy, int gz) {
     return ld_word_t<false>(P, gx, gy, gz);
 }
@@ -195,9 +192,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                  ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-#ifndef ACA_PF_NEXT
-#define ACA_PF_NEXT 0   // 1: L2 prefetch of the next tile's rows (ablation: slower)
-#endif
 #ifndef MBAR_SUSPEND_NS
 #define MBAR_SUSPEND_NS 20000   // try_wait suspend-time hint: waiting warps sleep instead of spinning
 #endif
@@ -1650,19 +1644,6 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
             }
         }
         __syncthreads();
-
-        // L2 prefetch of the rows of this CTA's next tile while this one runs its rounds
-        if (ACA_PF_NEXT && HW == 1 && !DB && warp == 0 && it + (int)gridDim.x < ntiles) {
-            int nx0, ny0, nz0; bool nfast, nfull;
-            if (origin(it + gridDim.x, nx0, ny0, nz0, nfast, nfull) && nfast) {
-                for (int row = lane; row < NROWS; row += 32) {
-                    const int ly = row % TY, lz = row / TY;
-                    const size_t gi = NDIM == 2 ? (size_t)(ny0 + ly) * g.nx + nx0
-                                                : ((size_t)(nz0 + lz) * g.ny + (ny0 + ly)) * g.nx + nx0;
-                    bulk_prefetch_l2(P.words + gi, TX * 8);
-                }
-            }
-        }
 
         unsigned int rounds = 0;
         bool done_reg = false;
