@@ -345,23 +345,29 @@ def main():
             "gpu_launches": int(kl + 2 * args.steps),
             "clocks": clk}
 
-    # end-to-end through the public API with host buffers: H2D of the initial spins,
-    # run, stats, D2H of the final spins, every step
+    # end-to-end through the public API with host buffers: every step copies its initial spins
+    # host -> device and its final spins device -> host (pinned buffers). The copies are
+    # pipelined with the simulation through the asynchronous spin I/O calls: step k+1's input
+    # is staged while step k runs, and step k's output drains while step k+1 runs.
     if not args.no_e2e:
         import torch as _t
-        host_in = _t.from_numpy(workloads.host_spins((n_local,), seed=7)).pin_memory()
-        host_out = _t.empty(n_local, dtype=_t.int8).pin_memory()
+        host_in = [_t.from_numpy(workloads.host_spins((n_local,), seed=7 + j)).pin_memory() for j in range(2)]
+        host_out = [_t.empty(n_local, dtype=_t.int8).pin_memory() for _ in range(2)]
         e_arr = 0
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        aca.aca_stage_spins(sim.handle, host_in[0], 0)
         for k in range(args.steps):
             sim.reset(args.seed + k)
-            aca.aca_set_spins(sim.handle, host_in)
+            aca.aca_set_spins_staged(sim.handle, k % 2)
+            if k + 1 < args.steps:
+                aca.aca_stage_spins(sim.handle, host_in[(k + 1) % 2], (k + 1) % 2)
             sim.run_until(cfg["T"])
             e_arr += sim.stats()["arrivals"]
-            aca.aca_get_spins(sim.handle, host_out)
+            aca.aca_get_spins_async(sim.handle, host_out[k % 2])
+        aca.aca_sync(sim.handle)
         torch.cuda.synchronize()
         et = time.perf_counter() - t0
         if world > 1:

@@ -171,6 +171,24 @@ int aca_nccl_unique_id(void* out128);
 /* Number of cells of the handle (rank-local for multi-process handles). */
 int64_t aca_num_cells(const aca_sim* s);
 
+/* ---- Asynchronous spin I/O (pipelining the per-step host copies with the simulation) ----
+ * aca_stage_spins: enqueue the host-to-device copy of `count` (= aca_num_cells) spins (+-1, int8,
+ *   x fastest) into staging slot `slot` (0 or 1) on the handle's copy stream, and return. The host
+ *   buffer must stay valid until the copy is done (aca_sync); pinned memory makes it a DMA.
+ * aca_set_spins_staged: the handle's stream waits for that copy, then sets the spins from the
+ *   slot (as aca_set_spins: times, counters and ranks unchanged). Returns without waiting.
+ * aca_get_spins_async: enqueue the unpacking of the current spins on the handle's stream and
+ *   their device-to-host copy into `out` on the copy stream (two output slots alternate);
+ *   returns at once. `out` holds the spins of the state at the call after aca_sync.
+ * aca_sync: wait for all work enqueued on both streams.
+ * Work on the handle's stream stays in call order (reset, set, run_until, getters), so these
+ * calls compose with the synchronous API. Staging uses 4 bytes per cell of device memory.
+ * Errors: ACA_EINVAL (count, slot, null), ACA_ESTATE (set before any stage), ACA_ENOMEM, ACA_ECUDA. */
+int aca_stage_spins(aca_sim* s, const int8_t* spins, size_t count, int slot);
+int aca_set_spins_staged(aca_sim* s, int slot);
+int aca_get_spins_async(aca_sim* s, int8_t* out, size_t count);
+int aca_sync(aca_sim* s);
+
 /* ---- Multi-process push mode (CUDA IPC; world > 1, halo_mode 0) ----
  * One process per GPU owns a strip (2-D) / slab (3-D). Instead of exchanging halos between
  * launches, every rank's tile kernel stores its boundary rows straight into its ring

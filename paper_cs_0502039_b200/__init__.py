@@ -23,7 +23,8 @@ ERRORS = {0: "ACA_OK", -1: "ACA_EINVAL", -2: "ACA_ENOMEM", -3: "ACA_ECUDA", -4: 
 EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_q32", "aca_get_spins",
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
-           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q", "aca_ipc_export", "aca_ipc_import"]
+           "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q", "aca_ipc_export", "aca_ipc_import",
+           "aca_stage_spins", "aca_set_spins_staged", "aca_get_spins_async", "aca_sync"]
 ACA_IPC_BLOB_BYTES = 192
 DEFAULT_ROUNDS = 5   # in-tile rounds per tile visit when aca_options.rounds_per_launch = 0 (aca.cu)
 POISSON, UNIFORM, ROOT8, GAUSS = 0, 1, 2, 3   # asynchrony laws (aca_options.law)
@@ -106,6 +107,10 @@ def lib():
                               ctypes.POINTER(aca_agg_stats), ctypes.c_int]
     L.aca_bkl_run.argtypes = L.aca_agg_run.argtypes
     L.aca_ipc_export.argtypes = [vp, vp, ctypes.c_size_t]
+    L.aca_stage_spins.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_int]
+    L.aca_set_spins_staged.argtypes = [vp, ctypes.c_int]
+    L.aca_get_spins_async.argtypes = [vp, vp, ctypes.c_size_t]
+    L.aca_sync.argtypes = [vp]
     L.aca_ipc_import.argtypes = [vp, vp, ctypes.c_size_t]
     L.aca_efficiency_run_q.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
                                        ctypes.c_int64, ctypes.c_int, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
@@ -224,6 +229,35 @@ def aca_set_spins(p, spins):
     else:
         n = spins.numel()
     _check(lib().aca_set_spins(p, _ptr(spins), n))
+
+
+def _host_spins(spins):
+    if not hasattr(spins, "data_ptr"):
+        spins = np.ascontiguousarray(spins, np.int8).ravel()
+        return spins, spins.size
+    return spins, spins.numel()
+
+
+def aca_stage_spins(p, spins, slot):
+    """Enqueue the host-to-device copy of the spins into staging slot 0/1 (returns at once; keep
+    `spins` alive, ideally pinned, until aca_sync)."""
+    spins, n = _host_spins(spins)
+    _check(lib().aca_stage_spins(p, _ptr(spins), n, int(slot)))
+    return spins
+
+
+def aca_set_spins_staged(p, slot):
+    _check(lib().aca_set_spins_staged(p, int(slot)))
+
+
+def aca_get_spins_async(p, out):
+    """Enqueue unpacking + device-to-host copy of the spins into `out` (valid after aca_sync)."""
+    n = out.numel() if hasattr(out, "data_ptr") else out.size
+    _check(lib().aca_get_spins_async(p, _ptr(out), n))
+
+
+def aca_sync(p):
+    _check(lib().aca_sync(p))
 
 
 def aca_reset(p, seed):

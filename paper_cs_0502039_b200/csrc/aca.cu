@@ -134,6 +134,13 @@ struct aca_sim {
     uint64_t T_last = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    // asynchronous spin I/O (aca_stage_spins / aca_set_spins_staged / aca_get_spins_async)
+    cudaStream_t cstream = nullptr;           // copy stream
+    int8_t* stage_in[2] = {nullptr, nullptr};
+    int8_t* stage_out[2] = {nullptr, nullptr};
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_pack[2] = {nullptr, nullptr};
+    cudaEvent_t ev_unp[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+    int out_slot = 0;
     unsigned long long* d_lr = nullptr;
     std::vector<Shard> shards;
     int G = 1;                     // shards on this device
@@ -565,6 +572,14 @@ void aca_destroy(aca_sim* S) {
             if (S->evb[a][b]) cudaEventDestroy(S->evb[a][b]);
     cudaFree(S->d_flag);
     if (S->h_flag) cudaFreeHost(S->h_flag);
+    if (S->cstream) cudaStreamSynchronize(S->cstream);
+    for (int a = 0; a < 2; ++a) {
+        cudaFree(S->stage_in[a]);
+        cudaFree(S->stage_out[a]);
+        for (cudaEvent_t e : {S->ev_h2d[a], S->ev_pack[a], S->ev_unp[a], S->ev_d2h[a]})
+            if (e) cudaEventDestroy(e);
+    }
+    if (S->cstream) cudaStreamDestroy(S->cstream);
     if (S->own_stream && S->stream) cudaStreamDestroy(S->stream);
     delete S;
 }
@@ -1156,6 +1171,84 @@ int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
         off += sh.n;
     }
     CK(cudaStreamSynchronize(S->stream));
+    return ACA_OK;
+}
+
+// ---------------------------------------------------------------- asynchronous spin I/O
+static int ensure_async_io(aca_sim* S) {
+    if (S->cstream) return ACA_OK;
+    size_t n = 0;
+    for (auto& sh : S->shards) n += sh.n;
+    CK(cudaStreamCreateWithFlags(&S->cstream, cudaStreamNonBlocking));
+    for (int a = 0; a < 2; ++a) {
+        if (cudaMalloc(&S->stage_in[a], n) != cudaSuccess || cudaMalloc(&S->stage_out[a], n) != cudaSuccess)
+            return fail(ACA_ENOMEM, "staging buffers (%zu cells)", n);
+        for (cudaEvent_t* e : {&S->ev_h2d[a], &S->ev_pack[a], &S->ev_unp[a], &S->ev_d2h[a]})
+            CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        // initial state: nothing pending on any slot
+        CK(cudaEventRecord(S->ev_pack[a], S->stream));
+        CK(cudaEventRecord(S->ev_d2h[a], S->cstream));
+    }
+    return ACA_OK;
+}
+
+int aca_stage_spins(aca_sim* S, const int8_t* spins, size_t count, int slot) {
+    int rc = check_count(S, count, spins);
+    if (rc) return rc;
+    if (slot < 0 || slot > 1) return fail(ACA_EINVAL, "slot must be 0 or 1");
+    CK(cudaSetDevice(S->device));
+    rc = ensure_async_io(S);
+    if (rc) return rc;
+    CK(cudaStreamWaitEvent(S->cstream, S->ev_pack[slot], 0));   // the slot's previous pack has read it
+    CK(cudaMemcpyAsync(S->stage_in[slot], spins, count, cudaMemcpyHostToDevice, S->cstream));
+    CK(cudaEventRecord(S->ev_h2d[slot], S->cstream));
+    return ACA_OK;
+}
+
+int aca_set_spins_staged(aca_sim* S, int slot) {
+    if (!S) return fail(ACA_EINVAL, "null handle");
+    if (slot < 0 || slot > 1) return fail(ACA_EINVAL, "slot must be 0 or 1");
+    if (!S->cstream) return fail(ACA_ESTATE, "nothing staged (call aca_stage_spins first)");
+    CK(cudaSetDevice(S->device));
+    CK(cudaStreamWaitEvent(S->stream, S->ev_h2d[slot], 0));
+    size_t off = 0;
+    for (auto& sh : S->shards) {
+        pack_kernel<<<1184, 256, 0, S->stream>>>(sh.words, S->stage_in[slot] + off, nullptr, nullptr, sh.g,
+                                                 (unsigned long long)sh.n, 0ull);
+        CK(cudaGetLastError());
+        off += sh.n;
+    }
+    CK(cudaEventRecord(S->ev_pack[slot], S->stream));
+    return ACA_OK;
+}
+
+int aca_get_spins_async(aca_sim* S, int8_t* out, size_t count) {
+    int rc = check_count(S, count, out);
+    if (rc) return rc;
+    CK(cudaSetDevice(S->device));
+    rc = ensure_async_io(S);
+    if (rc) return rc;
+    const int k = S->out_slot;
+    S->out_slot ^= 1;
+    CK(cudaStreamWaitEvent(S->stream, S->ev_d2h[k], 0));       // the slot's previous copy has drained
+    size_t off = 0;
+    for (auto& sh : S->shards) {
+        unpack_kernel<<<1184, 256, 0, S->stream>>>(sh.words, S->stage_out[k] + off, nullptr, nullptr, sh.g, sh.n);
+        CK(cudaGetLastError());
+        off += sh.n;
+    }
+    CK(cudaEventRecord(S->ev_unp[k], S->stream));
+    CK(cudaStreamWaitEvent(S->cstream, S->ev_unp[k], 0));
+    CK(cudaMemcpyAsync(out, S->stage_out[k], count, cudaMemcpyDeviceToHost, S->cstream));
+    CK(cudaEventRecord(S->ev_d2h[k], S->cstream));
+    return ACA_OK;
+}
+
+int aca_sync(aca_sim* S) {
+    if (!S) return fail(ACA_EINVAL, "null handle");
+    CK(cudaSetDevice(S->device));
+    CK(cudaStreamSynchronize(S->stream));
+    if (S->cstream) CK(cudaStreamSynchronize(S->cstream));
     return ACA_OK;
 }
 

@@ -1924,6 +1924,12 @@ __global__ void frame_prefill_kernel(const unsigned long long* __restrict__ word
 __global__ void pack_kernel(unsigned long long* __restrict__ words, const int8_t* __restrict__ spins,
                             const unsigned long long* __restrict__ times, const unsigned int* __restrict__ counters,
                             Geo g, unsigned long long n, unsigned long long base) {
+    if (spins && !times && !counters) {   // spins only: the (t, rank, n) fields are unchanged
+        for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+             i += (unsigned long long)gridDim.x * blockDim.x)
+            words[i] = (words[i] & ~1ull) | (spins[i] > 0 ? 1ull : 0ull);
+        return;
+    }
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         unsigned long long c, rank;
