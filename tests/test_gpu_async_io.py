@@ -11,13 +11,14 @@ import workloads
 pytestmark = pytest.mark.gpu
 
 
-def test_pipelined_steps_equal_synchronous_and_oracle(aca, oracle_mod):
-    dims, T, beta = (200, 136), 3.0, 0.4406868
-    n = dims[0] * dims[1]
+@pytest.mark.parametrize("dims,opts", [((200, 136), {}), ((256, 192), {"shards": 2}), ((40, 36, 24), {})])
+def test_pipelined_steps_equal_synchronous_and_oracle(aca, oracle_mod, dims, opts):
+    T, beta = 3.0, (0.4406868 if len(dims) == 2 else 0.2216544)
+    n = int(np.prod(dims))
     inputs = [torch.from_numpy(workloads.host_spins((n,), seed=11 + k)).pin_memory() for k in range(3)]
     outs = [torch.empty(n, dtype=torch.int8).pin_memory() for _ in range(3)]
 
-    a = aca.Sim(dims, beta=beta, seed=5)
+    a = aca.Sim(dims, beta=beta, seed=5, **opts)
     aca.aca_stage_spins(a.handle, inputs[0], 0)
     for k in range(3):
         a.reset(5 + k)
@@ -28,7 +29,7 @@ def test_pipelined_steps_equal_synchronous_and_oracle(aca, oracle_mod):
         aca.aca_get_spins_async(a.handle, outs[k])
     aca.aca_sync(a.handle)
 
-    b = aca.Sim(dims, beta=beta, seed=5)
+    b = aca.Sim(dims, beta=beta, seed=5, **opts)
     for k in range(3):
         b.reset(5 + k)
         aca.aca_set_spins(b.handle, inputs[k])
