@@ -1031,7 +1031,9 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             for (int i = lane; i < nfire; i += 32) {
                 uint32_t o;
                 asm volatile("ld.shared.u16 %0, [%1];" : "=r"(o) : "r"(qa + 2u * (uint32_t)i) : "memory");
-                const uint32_t lx = o % TX, ly = (o / TX) % TY, lz = o / (TX * TY);
+                // o < NCELL: in 2-D the row is o / TX and there is no plane index
+                const uint32_t lx = o % TX, ly = NDIM == 3 ? (o / TX) % TY : o / TX,
+                               lz = NDIM == 3 ? o / (TX * TY) : 0u;
                 const uint32_t a = sa + 8u * (uint32_t)slot((int)lx, (int)ly, (int)lz);
                 unsigned long long w;
                 uint32_t b0, b1, b2, b3, b4 = 0, b5 = 0;
