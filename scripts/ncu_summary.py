@@ -93,7 +93,12 @@ def main():
         def avg(key):
             vals = [num(c[key]) for c in F if key in c]
             return sum(vals) / len(vals) if vals else None
-        dur = avg("gpu__time_duration.sum")   # in the unit ncu printed (ms)
+        def ms_of(v):   # duration in milliseconds whatever unit ncu printed
+            val, u = v.split(" ", 1)
+            return float(val.replace(",", "")) * {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3,
+                                                  "second": 1e3}.get(u.strip(), 1.0)
+        durs = [ms_of(c["gpu__time_duration.sum"]) for c in F if "gpu__time_duration.sum" in c]
+        dur = sum(durs) / len(durs) if durs else None
         cur[ktag] = {"dram_bytes_per_launch": rb + wb, "dram_read": rb, "dram_write": wb,
                      "launches_per_sweep": per_sweep, "dram_bytes_per_sweep": (rb + wb) * per_sweep,
                      "warp_inst_per_launch": avg("smsp__inst_executed.sum"),
