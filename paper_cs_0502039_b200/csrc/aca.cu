@@ -758,6 +758,24 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
             S->persistent_ctas = nsm * occ;
             S->phased = opt.checkerboard >= 0;
         }
+        // barrier-free tile pipeline (ACA_ASYNC_TILES=1, experiment): 2-D 64x64 tiles covering the
+        // shard exactly with an even number of tiles per row, per-warp round exit
+        const char* as_env = getenv("ACA_ASYNC_TILES");
+        const int64_t local_rows = dims[saxis] / parts;
+        if (as_env && atoi(as_env) == 1 && ndim == 2 && tx == 64 && ty == 64 && sel->nt == 256 && v == 0 &&
+            rule != ACA_LIFE && !S->sync && dims[0] % 128 == 0 && local_rows % 64 == 0 && S->round_mode == 2) {
+            S->kern = opt.early_reject ? (void*)tile_as_kernel<64, 64, 256, 2, true>
+                                       : (void*)tile_as_kernel<64, 64, 256, 2, false>;
+            S->smem = tma_smem(2, 64, 64, 1, 256, 2, false, opt.early_reject != 0);
+            if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
+                return bail(fail(ACA_ECUDA, "smem attribute (async tiles)"));
+            int nsm = 0, occ = 0;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, 256, S->smem) != cudaSuccess || occ < 1)
+                return bail(fail(ACA_ECUDA, "occupancy query failed"));
+            S->persistent_ctas = nsm * occ;
+            S->phased = opt.checkerboard >= 0;
+        }
     }
     if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
         return bail(fail(ACA_ECUDA, "smem attribute"));

@@ -1740,6 +1740,129 @@ __global__ void __launch_bounds__(NT, MINB) tile_tma_kernel(const KParams P) {
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase);
 }
 
+// ------------------------------------------------------------ barrier-free tile pipeline (2-D)
+// Variant "async tiles" (ACA_ASYNC_TILES=1; lattices whose shard is a whole number of 64-wide
+// tiles with an even tile count per row): two TMA buffers per CTA; each warp waits only for the
+// TMA of its tile (mbarrier), loads the x-halo cells of its own rows, runs its rounds and writes
+// its own rows back; the last warp to leave a buffer issues the TMA of the CTA's tile after next
+// into it. No CTA barrier inside the tile loop: a warp may already work on the next tile while
+// its neighbours finish this one (their rows are only read; a warp's cells are fired by that
+// warp alone).
+template <int TX, int TY, int NT, int MINB, bool EARLY>
+__global__ void __launch_bounds__(NT, MINB) tile_as_kernel(const KParams P) {
+    constexpr int NDIM = 2, TZ = 1, HW = 1;
+    constexpr int SX = TX + 4, SY = TY + 2, SXY = SX * SY;
+    constexpr int NSLOTP = (SXY + 15) & ~15;
+    constexpr int NCELL = TX * TY, NW = NT / 32, CPW = NCELL / NW, RPW = CPW / TX;
+    static_assert(CPW % TX == 0 && 2 * RPW <= 32, "rows per warp");
+    if (*(volatile unsigned int*)&P.ctl->done) return;
+    extern __shared__ __align__(128) unsigned long long smem[];
+    unsigned long long* Sb = smem;                        // 2 x NSLOTP
+    unsigned long long* thr = Sb + 2 * NSLOTP;            // 16
+    unsigned long long* thm = thr + 16;                   // 112 (entries 98.. are pad)
+    unsigned long long* lr = thm + 112;                   // 512
+    unsigned long long* red = lr + 512;                   // NW
+    unsigned long long* bar = red + NW;                   // 2 full barriers
+    unsigned short* Q = (unsigned short*)(bar + 2);
+    unsigned int* cnt = (unsigned int*)(thm + 100);       // 2 buffer-release counters (thm pad)
+    const Geo& g = P.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
+    for (int i = tid; i < 112; i += NT) thm[i] = i < 98 ? P.thm[i] : ~0ull;
+    for (int i = tid; i < 512; i += NT) lr[i] = P.lr[i];
+    __syncthreads();
+    if (tid == 0) { mbar_init(&bar[0], 1); mbar_init(&bar[1], 1); cnt[0] = 0u; cnt[1] = 0u; }
+    __syncthreads();
+    auto slot = [](int lx, int ly) { return (ly + 1) * SX + lx + 2; };
+    const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
+    const int hx = P.tiles_x >> 1;
+    const int ntiles = P.phase < 0 ? P.tiles_x * P.tiles_y : hx * P.tiles_y;
+    const bool reverse = P.phase < 0 && ((*(volatile unsigned long long*)&P.ctl->launches) & 1ull);
+    auto origin = [&](int it, int& x0, int& y0) {
+        int tx, ty;
+        if (P.phase < 0) {
+            const int tile = reverse ? ntiles - 1 - it : it;
+            tx = tile % P.tiles_x; ty = tile / P.tiles_x;
+        } else {
+            ty = it / hx;
+            tx = 2 * (it % hx) + ((ty + P.row_par0 + P.phase) & 1);
+        }
+        x0 = tx * TX; y0 = ty * TY;
+    };
+    auto issue = [&](int it, int b) {   // one warp: TMA of the tile's rows and y-face halo rows
+        int x0, y0;
+        origin(it, x0, y0);
+        if (lane == 0) mbar_arrive_expect_tx(&bar[b], (uint32_t)(TY + 2) * TX * 8u);
+        __syncwarp();
+        fence_proxy_async();
+        unsigned long long* S = Sb + b * NSLOTP;
+        for (int row = lane; row < TY + 2; row += 32) {
+            const int ly = row < TY ? row : (row == TY ? -1 : TY);
+            bulk_g2s(&S[slot(0, ly)], word_ptr_t<true>(P, x0, y0 + ly, 0), TX * 8, &bar[b]);
+        }
+    };
+    if (warp == 0) {
+        if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+        if ((int)(blockIdx.x + gridDim.x) < ntiles) issue(blockIdx.x + gridDim.x, 1);
+    }
+    TileStats st;
+    TileTotals tot;
+    unsigned int active = 0, rounds_max = 0;
+    int k = 0;
+    for (int it = blockIdx.x; it < ntiles; it += gridDim.x, ++k) {
+        const int b = k & 1;
+        unsigned long long* S = Sb + b * NSLOTP;
+        int x0, y0;
+        origin(it, x0, y0);
+        mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
+        if (lane < 2 * RPW) {   // the x-halo cells of this warp's rows
+            const int row = warp * RPW + (lane >> 1), lx = (lane & 1) ? TX : -1;
+            S[slot(lx, row)] = ld_word_t<true>(P, x0 + lx, y0 + row, 0);
+        }
+        __syncwarp();
+        const unsigned int rounds = tile_rounds<NDIM, TX, TY, TZ, NT, true, EARLY, HW, false>(
+            P, S, Q, thr, thm, lr, x0, y0, 0, wlim, st);
+        rounds_max = rounds > rounds_max ? rounds : rounds_max;
+        tot.fold(st);
+        for (int idx = lane; idx < CPW / 2; idx += 32) {   // write back this warp's rows
+            const int o = warp * CPW + 2 * idx;
+            const int lx = o % TX, ly = o / TX;
+            const size_t gi = (size_t)(y0 + ly) * g.nx + x0 + lx;
+            const ulonglong2 v = lds128v(&S[slot(lx, ly)]);
+            *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
+            active += (v.x < wlim) + (v.y < wlim);
+            if (P.push_lo) {
+                const int a = y0 + ly;
+                if (a == 0 || a == g.ny - 1) {
+                    *reinterpret_cast<ulonglong2*>((a == 0 ? P.push_lo : P.push_hi) + x0 + lx) = v;
+                    if (a == 0 && g.ny == 1) *reinterpret_cast<ulonglong2*>(P.push_hi + x0 + lx) = v;
+                }
+            }
+        }
+        __syncwarp();
+        // release the buffer; the last warp out refills it with the tile after next
+        unsigned int ticket = 0;
+        if (lane == 0) {
+            __threadfence_block();
+            ticket = atomicAdd(&cnt[b], 1u);
+        }
+        ticket = __shfl_sync(0xffffffffu, ticket, 0);
+        if (ticket == NW - 1) {
+            __threadfence_block();
+            if (lane == 0) cnt[b] = 0u;
+            if (it + 2 * (int)gridDim.x < ntiles) issue(it + 2 * gridDim.x, b);
+        }
+    }
+    __syncthreads();
+    tot.fold(st);
+    const unsigned long long s_act = block_sum<NT>((unsigned long long)active, red);
+    const unsigned long long s_fir = block_sum<NT>(tot.fired, red);
+    const unsigned long long s_flp = block_sum<NT>(tot.flips, red);
+    const unsigned long long s_tst = block_sum<NT>(tot.tested, red);
+    const unsigned long long s_hsh = block_sum<NT>(st.hacc, red);
+    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase);
+}
+
 // ------------------------------------------------------------ whole-lattice kernel
 // One CTA holds the entire (small) lattice in shared memory with true periodic addressing
 // and runs rounds until no cell has t < T: the whole run_until in one launch. This is the

@@ -409,3 +409,15 @@ def test_ablation_switches_stay_exact(aca, oracle_mod, env, tile, dims, monkeypa
     monkeypatch.setenv(*env)
     g, o = run_pair(aca, oracle_mod, dims, [3.0, 6.0], beta=0.4406868, seed=71, tile=tile)
     assert_same(g, o)
+
+
+@pytest.mark.parametrize("dims,kw", [((256, 192), dict(beta=0.4406868)),
+                                     ((256, 256), dict(beta=0.4406868, shards=2)),
+                                     ((256, 128), dict(beta=0.4406868, checkerboard=-1)),
+                                     ((256, 128), dict(beta=1.0, h=0.1, rule=1, init_q=0.05, early_reject=1))])
+def test_async_tile_pipeline_exact(aca, oracle_mod, dims, kw, monkeypatch):
+    """The barrier-free tile pipeline (ACA_ASYNC_TILES=1: two TMA buffers, per-warp waits and
+    write-back, the last warp out refills the buffer) reaches the oracle's trajectory."""
+    monkeypatch.setenv("ACA_ASYNC_TILES", "1")
+    g, o = run_pair(aca, oracle_mod, dims, [2.0, 5.0], seed=83, tile=(64, 64), **kw)
+    assert_same(g, o)
