@@ -458,10 +458,11 @@ constexpr size_t CHUNK = (size_t)1 << 25;   // cells per getter chunk (256 MB of
 
 // P5 initial state on the device + zeroed control blocks.
 int init_state(aca_sim* S) {
-    const uint32_t k0 = (uint32_t)(S->seed & 0xffffffffu), k1 = (uint32_t)(S->seed >> 32);
+    RoundKeys K;
+    philox_round_keys((uint32_t)(S->seed & 0xffffffffu), (uint32_t)(S->seed >> 32), K.rk);
     for (auto& sh : S->shards) {
         CK(cudaMemsetAsync(sh.ctl, 0, sizeof(Ctl), S->stream));
-        init_kernel<<<1184, 256, 0, S->stream>>>(sh.words, sh.g, S->d_lr, k0, k1, S->thr_init, S->inv_lambda,
+        init_kernel<<<1184, 256, 0, S->stream>>>(sh.words, sh.g, S->d_lr, K, S->thr_init, S->inv_lambda,
                                                   S->opt.tie_bits, (unsigned long long)sh.n, S->opt.law);
         CK(cudaGetLastError());
     }

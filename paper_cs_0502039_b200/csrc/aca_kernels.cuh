@@ -1978,8 +1978,10 @@ __device__ __forceinline__ void cell_coords(const Geo& g, unsigned long long li,
     }
 }
 
+struct RoundKeys { uint32_t rk[20]; };   // Philox round keys of the seed (philox_round_keys)
+
 __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const unsigned long long* __restrict__ lr_g,
-                            uint32_t key0, uint32_t key1, unsigned long long thr_init, unsigned long long inv_lambda,
+                            const RoundKeys K, unsigned long long thr_init, unsigned long long inv_lambda,
                             int tie_bits, unsigned long long n_local, int law) {
     __shared__ unsigned long long lr[512];
     for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
@@ -1999,7 +2001,7 @@ __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const
         const int xend = min(nx, (sg + 1) * SEG);
         for (int x = sg * SEG + (threadIdx.x & 31); x < xend; x += 32) {
             const unsigned long long c = cbase + x, rank = (unsigned long long)x + gy + gz;
-            const u32x4 r = philox4x32_10(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, key0, key1);
+            const u32x4 r = philox4x32_10_rk(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, K.rk);
             const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
             const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
             words[(size_t)row * nx + x] = w_pack(t0, g.RB ? rank : 0ull, 0ull, sb, g);
