@@ -286,7 +286,7 @@ struct TileKey {
 
 const TileKey kTiles[] = {
     TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 32, 1, 128, 8, 6, 8, 8),
-    TK(2, 64, 64, 1, 256, 4, 2, 3, 4),
+    TK(2, 64, 64, 1, 256, 4, 2, 3, 4), TK(2, 64, 64, 1, 512, 2, 1, 1, 1),
     TK(2, 128, 64, 1, 512, 1, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8, 8), TK(3, 16, 16, 16, 256, 2, 1, 2, 2),
     TK(3, 32, 16, 8, 256, 3, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
 };
@@ -735,7 +735,17 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         if (ndim == 2) tz = 1;
         const TileKey* sel = nullptr;
         const char* nt_env = getenv("ACA_TILE_NT");   // ablation: pick the block size of a tile shape
-        const int want_nt = nt_env ? atoi(nt_env) : 0;
+        int want_nt = nt_env ? atoi(nt_env) : 0;
+        if (!nt_env && ndim == 2 && tx == 64 && ty == 64) {
+            // few tiles per launch (config 2: 128 per colour on 148 SMs): 512 threads per 64x64
+            // tile halve each round's latency; with many tiles the 256-thread kernel (4 CTAs/SM)
+            // is faster (measured: c2 +7 %, c3 -28 % for 512)
+            int nsm = 148;
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
+            const int64_t rows = dims[1] / parts;
+            const int64_t tiles = ((dims[0] + 63) / 64) * ((rows + 63) / 64);
+            if ((int64_t)dims[0] * rows >= ((int64_t)1 << 20) && tiles / 2 < 2 * (int64_t)nsm) want_nt = 512;
+        }
         for (const auto& k : kTiles)
             if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz && (want_nt == 0 || k.nt == want_nt) &&
                 !sel)

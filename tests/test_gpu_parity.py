@@ -402,7 +402,8 @@ def test_game_of_life(aca, oracle_mod, case):
 
 @pytest.mark.parametrize("env,tile,dims", [(("ACA_DEFER_TAIL", "1"), (64, 64), (320, 200)),
                                            (("ACA_TILE_NT", "128"), (64, 32), (320, 200)),
-                                           (("ACA_TILE_NT", "256"), (64, 32), (200, 136))])
+                                           (("ACA_TILE_NT", "256"), (64, 32), (200, 136)),
+                                           (("ACA_TILE_NT", "512"), (64, 64), (320, 200))])
 def test_ablation_switches_stay_exact(aca, oracle_mod, env, tile, dims, monkeypatch):
     """Ablation switches read at aca_create: the carried partial fire chunk (ACA_DEFER_TAIL=1)
     and the block size of a tile shape (ACA_TILE_NT) change the schedule, never the result."""
