@@ -269,7 +269,19 @@ def main():
     sim = aca.Sim(dims, lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
                   seed=args.seed, **opts)
     if world > 1 and args.transport == "ipc":
-        adist.ipc_connect(sim.handle)
+        failed = 0
+        try:
+            adist.ipc_connect(sim.handle)
+        except aca.AcaError as e:   # e.g. no peer mapping between these GPUs
+            failed = 1
+            print("rank %d: CUDA-IPC push transport unavailable (%s)" % (rank, e), file=sys.stderr)
+        if adist.reduce_sum_int(failed) > 0:   # every rank switches to the NCCL exchange together
+            sim.close()
+            uid = aca.aca_nccl_unique_id() if rank == 0 else bytes(128)
+            opts.update(nccl_id=adist.broadcast_bytes(uid), halo_mode=1)
+            args.transport = "nccl"
+            sim = aca.Sim(dims, lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
+                          seed=args.seed, **opts)
     n_local = aca.aca_num_cells(sim.handle)
 
     def step(seed):
@@ -336,6 +348,8 @@ def main():
                        "variant": args.variant,
                        "sweep": "checkerboard: 2 kernel launches per outer round (tile colours 0, 1)",
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
+                       "halo_transport": (("cuda-ipc push" if args.transport == "ipc" else "nccl exchange")
+                                          if world > 1 else "none (one shard)"),
                        "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
                        "event_hash": not args.no_hash},
             "roofline": roof,
