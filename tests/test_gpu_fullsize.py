@@ -53,18 +53,20 @@ def bond_sum(spins, ndim):
     return int(sum((s * np.roll(s, -1, axis=ax)).sum() for ax in range(ndim)))
 
 
-def test_config2_full_digest(aca, oracle_mod):
+@pytest.mark.parametrize("seed", workloads.PARITY_SEEDS)
+def test_config2_full_digest(aca, oracle_mod, seed):
     """Config 2 in full (1024^2, Metropolis beta 0.40, T = 100, ~1.05e8 arrivals) against the
-    digests of a full oracle run (tests/golden/c2_seed1.json, written by
-    scripts/make_golden.py from oracle/ only): every spin, time and counter, bit for bit."""
+    digests of a full oracle run (tests/golden/c2_seed<k>.json, written by
+    scripts/make_golden.py from oracle/ only): every spin, time and counter, bit for bit, in the
+    bench configuration (R = 6, 512-thread tiles) for all three parity seeds."""
     import hashlib
     import json
     import os
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c2_seed1.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c2_seed%d.json" % seed)
     gold = json.load(open(path))
     cfg = workloads.config("c2")
     g = aca.Sim(cfg["dims"], lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
-                seed=gold["seed"], init_q=cfg["init_q"], tile=cfg["tile"])
+                seed=gold["seed"], init_q=cfg["init_q"], tile=cfg["tile"], **cfg.get("opts", {}))
     g.run_until(cfg["T"])
     dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
     assert dig(g.spins()) == gold["sha256_spins_int8"]
