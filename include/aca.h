@@ -74,7 +74,13 @@ typedef struct {
                                    TMA-staged, per-warp compacted firing (default); 1 = one CTA
                                    per tile, uncompacted; 2 = 0 with double-buffered TMA; 3 =
                                    register-resident synchronous rounds; 4 = work-list rounds
-                                   (re-test only cells whose neighbourhood changed). */
+                                   (re-test only cells whose neighbourhood changed); 5 = 0 with
+                                   a 2-wide halo whose inner ring is advanced redundantly (2-D).
+                                   The block size of a tile shape is chosen by the library
+                                   (512 threads for 64x64 tiles when a launch has fewer than two
+                                   tiles per SM). Environment switches for ablations only:
+                                   ACA_TILE_NT, ACA_DEFER_TAIL, ACA_ASYNC_TILES, ACA_BULK,
+                                   ACA_ROUND_MODE, ACA_EFF_STREAM. */
     int32_t early_reject;       /* 1: a cell may also commit arrivals that are rejected for
                                    every possible state of the neighbours it still waits for
                                    (exact; pays off at low temperature, config 5). 0 = off */
