@@ -1,7 +1,9 @@
 """Write tests/golden/<config>_seed<k>.json: SHA-256 digests of the final spins, times and
 counters plus the integer statistics of a FULL oracle run of a BASELINE config.
 Calls only oracle/ (the serial PQ oracle); nothing here touches the CUDA path.
-usage: python scripts/make_golden.py c2 [seed]"""
+usage: python scripts/make_golden.py c2 [seed] [T']
+With T' (< the config's T) the run stops at T' and the file is <config>_seed<k>_T<T'>.json: an
+interim full-lattice digest for configs whose full-T oracle run takes hours."""
 import hashlib
 import json
 import os
@@ -25,6 +27,9 @@ def main():
     name = sys.argv[1]
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else workloads.PARITY_SEEDS[0]
     cfg = workloads.config(name)
+    interim = len(sys.argv) > 3
+    if interim:
+        cfg["T"] = float(sys.argv[3])
     t0 = time.time()
     o = oracle.OracleSim(cfg["dims"], lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
                          seed=seed, init_q=cfg["init_q"])
@@ -35,7 +40,8 @@ def main():
            "generated_by": "scripts/make_golden.py (oracle/ only)", "oracle_seconds": round(time.time() - t0, 1),
            "sha256_spins_int8": digest(o.spins()), "sha256_times_u64": digest(o.times()),
            "sha256_counters_u32": digest(o.counters()), "stats": {k: int(v) for k, v in st.items()}}
-    path = os.path.join(ROOT, "tests", "golden", "%s_seed%d.json" % (name, seed))
+    stem = "%s_seed%d" % (name, seed) + ("_T%g" % cfg["T"] if interim else "")
+    path = os.path.join(ROOT, "tests", "golden", stem + ".json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print(path, out["oracle_seconds"], "s")
