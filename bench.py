@@ -42,7 +42,6 @@ def parse():
     ap.add_argument("--rounds", type=int, default=0, help="in-tile rounds per launch (0 = library default)")
     ap.add_argument("--tile", type=str, default="", help="e.g. 64x64 or 32x16x8")
     ap.add_argument("--launches-per-check", type=int, default=0)
-    ap.add_argument("--variant", type=int, default=0, help="tile kernel variant (ablation; 0 = default)")
     ap.add_argument("--early-reject", type=int, default=-1, help="a10 early rejection (-1 = config default)")
     ap.add_argument("--checkerboard", type=int, default=0, help="1/0 = checkerboard sweeps (default), -1 = off")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
@@ -253,8 +252,6 @@ def main():
         opts["rounds_per_launch"] = args.rounds
     if args.launches_per_check:
         opts["launches_per_check"] = args.launches_per_check
-    if args.variant:
-        opts["variant"] = args.variant
     if args.checkerboard:
         opts["checkerboard"] = args.checkerboard
     stream = torch.cuda.Stream()            # non-default stream: the library captures CUDA graphs on it
@@ -345,7 +342,6 @@ def main():
             "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
                        "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
                        "tile": list(tile), "rounds_per_tile_visit": args.rounds or cfg.get("opts", {}).get("rounds_per_launch", aca.DEFAULT_ROUNDS),
-                       "variant": args.variant,
                        "sweep": "checkerboard: 2 kernel launches per outer round (tile colours 0, 1)",
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
                        "halo_transport": (("cuda-ipc push" if args.transport == "ipc" else "nccl exchange")

@@ -70,17 +70,13 @@ typedef struct {
     int32_t whole_lattice;      /* 1: one CTA holds the whole lattice with periodic
                                    addressing and runs to completion in one launch
                                    (small lattices, config 1); 0 = auto, -1 = never */
-    int32_t variant;            /* tile kernel (ablations; identical results): 0 = persistent,
-                                   TMA-staged, per-warp compacted firing (default); 1 = one CTA
-                                   per tile, uncompacted; 2 = 0 with double-buffered TMA; 3 =
-                                   register-resident synchronous rounds; 4 = work-list rounds
-                                   (re-test only cells whose neighbourhood changed); 5 = 0 with
-                                   a 2-wide halo whose inner ring is advanced redundantly (2-D).
-                                   The block size of a tile shape is chosen by the library
-                                   (512 threads for 64x64 tiles when a launch has fewer than two
-                                   tiles per SM). Environment switches for ablations only:
-                                   ACA_TILE_NT, ACA_DEFER_TAIL, ACA_ASYNC_TILES, ACA_BULK,
-                                   ACA_ROUND_MODE, ACA_EFF_STREAM. */
+    int32_t variant;            /* must be 0. Round 1's kernel ablations (uncompacted tiles,
+                                   double-buffered TMA, register-resident rounds, work lists,
+                                   2-wide halos) were measured slower and retired; DESIGN.md
+                                   section 6 keeps their numbers. The group size of the 64x64
+                                   tile is chosen by the library (512 threads when a launch has
+                                   fewer than two tiles per SM). Environment switches for
+                                   ablations only: ACA_TILE_NT, ACA_BULK, ACA_EFF_STREAM. */
     int32_t early_reject;       /* 1: a cell may also commit arrivals that are rejected for
                                    every possible state of the neighbours it still waits for
                                    (exact; pays off at low temperature, config 5). 0 = off */
@@ -103,6 +99,10 @@ typedef struct {
                                    (device copies / NCCL send-recv). Same results. world > 1
                                    with 0: the neighbours' halos are mapped by CUDA IPC
                                    (aca_ipc_export / aca_ipc_import below). */
+    int32_t max_ctas;           /* > 0: cap the persistent tile kernel's grid (default 0 = one
+                                   CTA per SM). Small caps make every CTA cycle many tiles
+                                   through its buffer ring (tests of that path on small
+                                   lattices). Same results. */
 } aca_options;
 
 typedef struct {

@@ -45,7 +45,7 @@ class aca_options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("event_hash", ctypes.c_int32),
                 ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("early_reject", ctypes.c_int32), ("checkerboard", ctypes.c_int32),
-                ("law", ctypes.c_int32), ("halo_mode", ctypes.c_int32)]
+                ("law", ctypes.c_int32), ("halo_mode", ctypes.c_int32), ("max_ctas", ctypes.c_int32)]
 
 
 class aca_stats(ctypes.Structure):
@@ -65,6 +65,10 @@ class aca_stats(ctypes.Structure):
 
 
 _lib = None
+
+
+if os.environ.get("ACA_LIB"):   # an alternative build of the same sources (e.g. libaca_dbg.so)
+    _SO = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ["ACA_LIB"])
 
 
 def library_path():

@@ -123,12 +123,16 @@ struct aca_sim {
     uint64_t seed = 0;
     aca_options opt{};
     int device = 0;
-    int RB = 1, NB = 1, TB = 1;    // packed word: time bits, rank bits, counter bits (+1 spin)
+    int NB = 1, TB = 1;            // packed word: counter bits, time bits (+1 spin bit)
+    uint64_t t_hi = 0;             // exclusive upper bound of every stored time (Q32)
+    bool sync_debug = false;       // ACA_SYNC_DEBUG=1: synchronise after every tile launch
+    unsigned long long* h_trace = nullptr;   // ACA_TRACE_FROM=n (debug builds): host-mapped stage trace
+    unsigned long long* h_dbg = nullptr;     // ACA_SYNC_DEBUG (debug builds): host-mapped failed-check record
+    long long trace_from = -1;
     unsigned long long inv_lambda = 1ull << 32;
     unsigned long long thr[14] = {};
     unsigned long long thm[98] = {};   // a10 early-rejection table (see commit_loop)
     int bulk = 1;
-    int defer_tail = 0;            // ablation (ACA_DEFER_TAIL=1): carry the partial fire chunk; costs arrivals per sweep
     unsigned long long thr_init = 0;
     unsigned long long max_delta = 0;
     uint64_t T_last = 0;
@@ -149,7 +153,6 @@ struct aca_sim {
     ncclComm_t comm = nullptr;
     int tile[3] = {64, 64, 1};
     int rounds = 8;
-    int round_mode = 2;            // see KParams::round_mode (ACA_ROUND_MODE overrides; experiments)
     int K = 16;
     bool whole = false;
     bool sync = false;
@@ -247,48 +250,34 @@ int bits_for(uint64_t v) {
 }
 
 // ---------------------------------------------------------------- kernel registry
-constexpr size_t tile_smem(int ndim, int tx, int ty, int tz, int nt) {
-    return ((size_t)(tx + 2) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 512 + 16 + nt / 32) * 8;
-}
-constexpr size_t tma_smem(int ndim, int tx, int ty, int tz, int nt, int nbuf, bool wl = false, bool early = false,
-                          int hw = 1) {
-    return tma_smem_bytes(ndim, tx, ty, tz, nt, nbuf, wl, early, hw);
-}
-
-// Kernel variants (identical results; ablations): 0 = persistent TMA-staged compacted kernel
-// (default), 1 = uncompacted one-CTA-per-tile kernel, 2 = persistent, double-buffered TMA,
-// 3 = persistent TMA with register-resident synchronous rounds and CTA-wide firing,
-// 4 = persistent TMA with work-list rounds (re-test only the cells whose neighbourhood changed),
-// 5 = variant 0 with a 2-wide halo whose inner ring is simulated redundantly (2-D; 3-D = 0).
-// Slot NVARIANT = two-barrier fig:s1c1pe rounds (sync_rounds = 1).
-constexpr int NVARIANT = 6;
+// Tile shapes of the production kernel tile_grp_kernel<NDIM, TX, TY, TZ, NTG, NG, NBUF, ...>:
+// NG groups of NTG threads per CTA (one CTA per SM) and NBUF tile buffers; (NG_E, NBUF_E) for
+// the a10 kernel, whose larger fire queues leave room for fewer buffers. tile_sync_kernel is the
+// fig:s1c1pe reference (sync_rounds = 1).
 struct TileKey {
-    int ndim, tx, ty, tz, nt;
-    void* fn[NVARIANT + 1]; size_t smem[NVARIANT + 1]; bool persistent[NVARIANT + 1];
-    void* fn_early;   // variant 0 with the a10 early-rejection path compiled in
-    void* fn_life;    // variant 0 with the Moore neighbourhood (rule 2, 2-D only; nullptr in 3-D)
+    int ndim, tx, ty, tz, ntg;
+    void* fn;         // production kernel
+    void* fn_early;   // with the a10 early-rejection path
+    void* fn_life;    // with the Moore neighbourhood (rule 2, 2-D only; nullptr in 3-D)
+    void* fn_sync;    // fig:s1c1pe reference kernel
+    size_t smem, smem_early, smem_sync;
+    int nt, nt_early, nt_sync;
 };
 
-#define TK(ND, TX, TY, TZ, NT, MB, MBD, MBR, MBW)                                                         \
-    {ND, TX, TY, TZ, NT,                                                                             \
-     {(void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false>, (void*)tile_kernel<ND, TX, TY, TZ, NT, false>, \
-      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBD, true, false>,                                 \
-      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBR, false, true>,                                 \
-      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MBW, false, false, false, true>,                   \
-      (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, false, false, (ND == 2 ? 2 : 1)>, \
-      (void*)tile_kernel<ND, TX, TY, TZ, NT, true>},                                                 \
-     {tma_smem(ND, TX, TY, TZ, NT, 1), tile_smem(ND, TX, TY, TZ, NT), tma_smem(ND, TX, TY, TZ, NT, 2),     \
-      tma_smem(ND, TX, TY, TZ, NT, 1, false, true), tma_smem(ND, TX, TY, TZ, NT, 1, true),              \
-      tma_smem(ND, TX, TY, TZ, NT, 1, false, false, ND == 2 ? 2 : 1), tile_smem(ND, TX, TY, TZ, NT)},  \
-     {true, false, true, true, true, true, false},                                                   \
-     (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, true>,                            \
-     (ND == 2 ? (void*)tile_tma_kernel<ND, TX, TY, TZ, NT, MB, false, false, false, false, 1, (ND == 2)> : nullptr)}
+#define TKG(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS)                                              \
+    {ND, TX, TY, TZ, NTG,                                                                              \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, false>,                             \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, true, false>,                            \
+     (ND == 2 ? (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, (ND == 2)> : nullptr),   \
+     (void*)tile_sync_kernel<ND, TX, TY, TZ, NTS>,                                                     \
+     grp_smem_bytes(ND, TX, TY, TZ, NTG, NG, NBUF, false), grp_smem_bytes(ND, TX, TY, TZ, NTG, NGE, NBUFE, true), \
+     sync_smem_bytes(ND, TX, TY, TZ, NTS), NTG * NG, NTG * NGE, NTS}
 
 const TileKey kTiles[] = {
-    TK(2, 32, 32, 1, 256, 4, 4, 4, 4), TK(2, 64, 32, 1, 256, 4, 3, 3, 4), TK(2, 64, 32, 1, 128, 8, 6, 8, 8),
-    TK(2, 64, 64, 1, 256, 4, 2, 3, 4), TK(2, 64, 64, 1, 512, 2, 1, 1, 1),
-    TK(2, 128, 64, 1, 512, 1, 1, 1, 1), TK(3, 8, 8, 8, 128, 8, 4, 8, 8), TK(3, 16, 16, 16, 256, 2, 1, 2, 2),
-    TK(3, 32, 16, 8, 256, 3, 1, 2, 2), TK(3, 32, 32, 8, 512, 1, 1, 1, 1),
+    TKG(2, 64, 64, 1, 256, 4, 5, 4, 5, 256), TKG(2, 64, 64, 1, 512, 2, 3, 2, 3, 512),
+    TKG(2, 32, 32, 1, 256, 4, 8, 4, 8, 256), TKG(2, 64, 32, 1, 256, 4, 8, 4, 8, 256),
+    TKG(3, 32, 16, 8, 256, 3, 4, 3, 3, 256), TKG(3, 8, 8, 8, 128, 8, 12, 8, 12, 128),
+    TKG(3, 16, 16, 16, 256, 3, 4, 3, 3, 256),
 };
 
 constexpr int WHOLE_NT = 1024;
@@ -298,9 +287,8 @@ size_t whole_smem(int64_t n, bool sync) {
 
 void set_geo_layout(aca_sim* S) {
     for (auto& sh : S->shards) {
-        sh.g.RB = S->RB;
         sh.g.NB = S->NB;
-        sh.g.TSH = S->RB + S->NB + 1;
+        sh.g.TSH = S->NB + 1;
     }
 }
 
@@ -321,11 +309,20 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.tie_bits = S->opt.tie_bits;
     P.law = S->opt.law;
     P.rounds = S->rounds;
-    P.round_mode = S->round_mode;
     P.do_hash = S->opt.event_hash;
     P.early = S->opt.early_reject;
     P.bulk = S->bulk;
-    P.defer_tail = S->defer_tail;
+    P.halo_peer = S->ipc ? 1 : 0;
+    P.dbg_trace = nullptr;
+    P.dbg_map = nullptr;
+    if (S->h_dbg) {
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, S->h_dbg, 0) == cudaSuccess) P.dbg_map = (unsigned long long*)dp;
+    }
+    if (S->h_trace && S->trace_from >= 0 && (long long)S->kernel_launches >= S->trace_from) {
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, S->h_trace, 0) == cudaSuccess) P.dbg_trace = (unsigned long long*)dp;
+    }
     for (int i = 0; i < 98; ++i) P.thm[i] = S->thm[i];
     P.tiles_x = sh.tiles_x;
     P.tiles_y = sh.tiles_y;
@@ -391,6 +388,29 @@ int launch_round(aca_sim* S) {
             dim3 grid = S->whole ? dim3(1)
                                  : dim3(S->persistent_ctas > 0 ? std::min(ntiles, S->persistent_ctas) : ntiles);
             CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->smem, S->stream));
+            if (S->sync_debug) {   // ACA_SYNC_DEBUG=1: locate a failing launch (no graphs)
+                cudaError_t e = cudaStreamSynchronize(S->stream);
+                if (e != cudaSuccess && S->h_dbg && S->h_dbg[0])
+                    return fail(ACA_ECUDA, "tile launch failed (phase %d, launch %llu): %s; first failed check line %llu a=%llu b=%llu thread %llu",
+                                ph, (unsigned long long)S->kernel_launches, cudaGetErrorString(e), S->h_dbg[0],
+                                S->h_dbg[1], S->h_dbg[2], S->h_dbg[3]);
+                if (e != cudaSuccess) {
+                    if (S->h_trace && P.dbg_trace) {
+                        FILE* f = fopen("gpurun_out/trace.txt", "w");
+                        for (int i = 0; i < 148 * 32 && f; ++i)
+                            fprintf(f, "%d %d %llu %llu %llx\n", i / 32, i % 32, S->h_trace[2 * i], S->h_trace[2 * i + 1] >> 56,
+                                    S->h_trace[2 * i + 1] & 0xffffffffffffffull);
+                        if (f) fclose(f);
+                    }
+                    return fail(ACA_ECUDA, "tile launch failed (phase %d, launch %llu): %s", ph,
+                                (unsigned long long)S->kernel_launches, cudaGetErrorString(e));
+                }
+                Ctl c;
+                CK(cudaMemcpy(&c, sh.ctl, sizeof c, cudaMemcpyDeviceToHost));
+                if (c.dbg_line)
+                    return fail(ACA_ESTATE, "device check failed at aca_tile.cuh:%u (a = %llu, b = %llu; phase %d, launch %llu)",
+                                c.dbg_line, c.dbg_a, c.dbg_b, ph, (unsigned long long)S->kernel_launches);
+            }
         }
         if (ph < 0) break;
     }
@@ -404,7 +424,7 @@ void drop_graph(aca_sim* S) {
 
 int build_graph(aca_sim* S) {
     if (S->graph) return ACA_OK;
-    if (S->use_nccl) return ACA_OK;   // NCCL path: direct launches
+    if (S->use_nccl || S->sync_debug) return ACA_OK;   // NCCL path / ACA_SYNC_DEBUG: direct launches
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
         cudaGetLastError();
@@ -467,6 +487,7 @@ int init_state(aca_sim* S) {
         CK(cudaGetLastError());
     }
     S->T_last = 0;
+    S->t_hi = S->max_delta + 1;
     return ACA_OK;
 }
 
@@ -487,15 +508,18 @@ int device_stats(aca_sim* S) {
     return ACA_OK;
 }
 
-// Choose the (t, n) split of the packed word for horizon Tq: the fewest time bits that hold
-// Tq + max_delta, every remaining bit for the counter (capped at 31); repack if it changed.
+// Choose the (t, n) split of the packed word for horizon Tq: the fewest time bits that hold both
+// every time the run can produce (< Tq + max_delta) and every time already stored (< t_hi),
+// every remaining bit for the counter (capped at 31); repack if it changed. Growing the counter
+// field shrinks the time field, which is safe because tb covers t_hi; shrinking it is checked
+// against the largest stored counter.
 int fit_layout(aca_sim* S, uint64_t Tq) {
     const unsigned long long tmax = (unsigned long long)Tq + S->max_delta;
     if (tmax < (unsigned long long)Tq) return fail(ACA_ERANGE, "time horizon overflows 64 bits");
-    const int tb = bits_for(tmax);
-    int nb = 63 - S->RB - tb;
+    const int tb = bits_for(std::max<unsigned long long>(tmax, S->t_hi));
+    int nb = 63 - tb;
     if (nb > 31) nb = 31;
-    if (nb < 1) return fail(ACA_ERANGE, "lattice rank bits (%d) + time bits (%d) leave no room for the counter", S->RB, tb);
+    if (nb < 1) return fail(ACA_ERANGE, "time bits (%d) leave no room for the counter", tb);
     if (nb == S->NB) return ACA_OK;
     if (nb < S->NB) {   // shrinking the counter field: every current counter must fit
         int rc = device_stats(S);
@@ -503,19 +527,17 @@ int fit_layout(aca_sim* S, uint64_t Tq) {
         if (S->h_stat->nmax >= (1ull << nb) - 1ull)
             return fail(ACA_ERANGE, "event counters (max %llu) do not fit the %d bits left by T", S->h_stat->nmax, nb);
     }
-    Geo a = S->shards[0].g;
     const int old_nb = S->NB;
     S->NB = nb;
-    S->TB = 63 - S->RB - nb;
+    S->TB = 63 - nb;
     set_geo_layout(S);
     for (auto& sh : S->shards) {
         Geo ga = sh.g;
         ga.NB = old_nb;
-        ga.TSH = S->RB + old_nb + 1;
+        ga.TSH = old_nb + 1;
         repack_kernel<<<1184, 256, 0, S->stream>>>(sh.words, ga, sh.g, (unsigned long long)sh.n);
         CK(cudaGetLastError());
     }
-    (void)a;
     drop_graph(S);   // kernel parameters (layout) changed
     return ACA_OK;
 }
@@ -619,7 +641,9 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (opt.world > 1 && !opt.nccl_id && opt.halo_mode != 0)
         return fail(ACA_EINVAL, "world > 1 with halo_mode 1 (exchange) needs nccl_id");
     if (opt.rounds_per_launch < 0 || opt.launches_per_check < 0) return fail(ACA_EINVAL, "negative counts");
-    if (opt.variant < 0 || opt.variant >= NVARIANT) return fail(ACA_EINVAL, "variant must be in [0, %d)", NVARIANT);
+    if (opt.variant != 0)
+        return fail(ACA_EINVAL, "variant must be 0 (the kernel ablations of round 1 were retired; DESIGN.md section 6)");
+    if (opt.max_ctas < 0) return fail(ACA_EINVAL, "max_ctas must be >= 0");
 
     int64_t N = 1;
     for (int a = 0; a < ndim; ++a) {
@@ -660,7 +684,13 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->sync = opt.sync_rounds != 0;
     S->rounds = opt.rounds_per_launch > 0 ? opt.rounds_per_launch : 5;   // measured best (c3, c4, c5) with checkerboard sweeps
     S->K = opt.launches_per_check > 0 ? opt.launches_per_check : 16;
-    if (const char* e = getenv("ACA_ROUND_MODE")) S->round_mode = atoi(e);
+    if (const char* e = getenv("ACA_SYNC_DEBUG")) S->sync_debug = atoi(e) != 0;
+    if (S->sync_debug && cudaHostAlloc((void**)&S->h_dbg, 64, cudaHostAllocMapped) == cudaSuccess) memset(S->h_dbg, 0, 64);
+    if (const char* e = getenv("ACA_TRACE_FROM")) {
+        S->trace_from = atoll(e);
+        if (cudaHostAlloc((void**)&S->h_trace, 148 * 32 * 16, cudaHostAllocMapped) != cudaSuccess) S->h_trace = nullptr;
+        else memset(S->h_trace, 0, 148 * 32 * 16);
+    }
 
     // P3 constants, P4 table, P5 threshold, packed-word layout
     S->inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
@@ -669,25 +699,19 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->bulk = 1;   // one committed arrival per cell per fire step: longer in-thread chains
                    // diverge within the warp (measured: bulk 4/32 are 1.8-2x slower on c5)
     if (const char* e = getenv("ACA_BULK")) S->bulk = std::max(1, atoi(e));
-    if (const char* e = getenv("ACA_DEFER_TAIL")) S->defer_tail = atoi(e);
     S->thr_init = (unsigned long long)std::floor(opt.init_q * 4294967296.0);
-    uint64_t max_rank = 0;
-    for (int a = 0; a < ndim; ++a) max_rank += (uint64_t)(dims[a] - 1);
-    // rule 2 (Moore neighbourhood): the rank x + y cannot order diagonal neighbours across the
-    // periodic boundary, so it is left out of the word (RB = 0) and the kernels break time ties
-    // by comparing cell ids explicitly
-    S->RB = rule == ACA_LIFE ? 0 : bits_for(max_rank);
     {
         // largest unscaled increment of the law: NLOG-2(1) for Poisson, < 2^32 otherwise
         const unsigned long long umax = opt.law == 0 ? 190530846196ull : opt.law == 3 ? (3ull << 32) : (1ull << 32);
         const unsigned __int128 p = (unsigned __int128)umax * S->inv_lambda;
         S->max_delta = (unsigned long long)(p >> 32) + 1 + (opt.tie_bits ? (1ull << opt.tie_bits) : 0ull);
         const int tb = bits_for(S->max_delta);
-        int nb = 63 - S->RB - tb;
+        int nb = 63 - tb;
         if (nb > 31) nb = 31;
-        if (nb < 1) { delete S; return fail(ACA_ERANGE, "lattice/lambda leave no room in the packed word"); }
+        if (nb < 1) { delete S; return fail(ACA_ERANGE, "lambda leaves no room in the packed word"); }
         S->NB = nb;
-        S->TB = 63 - S->RB - nb;
+        S->TB = 63 - nb;
+        S->t_hi = S->max_delta + 1;
     }
 
     auto bail = [&](int code) { aca_destroy(S); return code; };
@@ -734,57 +758,42 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         }
         if (ndim == 2) tz = 1;
         const TileKey* sel = nullptr;
-        const char* nt_env = getenv("ACA_TILE_NT");   // ablation: pick the block size of a tile shape
-        int want_nt = nt_env ? atoi(nt_env) : 0;
-        if (!nt_env && ndim == 2 && tx == 64 && ty == 64) {
+        int want_ntg = 0;
+        if (const char* nt_env = getenv("ACA_TILE_NT")) want_ntg = atoi(nt_env);   // ablation: group size of a shape
+        if (want_ntg == 0 && ndim == 2 && tx == 64 && ty == 64) {
             // few tiles per launch (config 2: 128 per colour on 148 SMs): 512 threads per 64x64
-            // tile halve each round's latency; with many tiles the 256-thread kernel (4 CTAs/SM)
-            // is faster (measured: c2 +7 %, c3 -28 % for 512)
+            // tile halve each round's latency; with many tiles 256-thread groups are faster
             int nsm = 148;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
             const int64_t rows = dims[1] / parts;
             const int64_t tiles = ((dims[0] + 63) / 64) * ((rows + 63) / 64);
-            if ((int64_t)dims[0] * rows >= ((int64_t)1 << 20) && tiles / 2 < 2 * (int64_t)nsm) want_nt = 512;
+            if ((int64_t)dims[0] * rows >= ((int64_t)1 << 20) && tiles / 2 < 2 * (int64_t)nsm) want_ntg = 512;
         }
         for (const auto& k : kTiles)
-            if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz && (want_nt == 0 || k.nt == want_nt) &&
-                !sel)
+            if (k.ndim == ndim && k.tx == tx && k.ty == ty && k.tz == tz && (want_ntg == 0 || k.ntg == want_ntg) && !sel)
                 sel = &k;
         if (!sel) return bail(fail(ACA_EINVAL, "unsupported tile %dx%dx%d for ndim %d", tx, ty, tz, ndim));
-        const int v = S->sync ? NVARIANT : opt.variant;
         S->tile[0] = tx; S->tile[1] = ty; S->tile[2] = tz;
-        S->kern = ((v == 0 || v == 5) && opt.early_reject) ? sel->fn_early : sel->fn[v];
-        if (rule == ACA_LIFE) S->kern = sel->fn_life;   // V0 with the Moore neighbourhood (any variant)
-        S->nthreads = sel->nt;
-        S->smem = rule == ACA_LIFE ? sel->smem[0] : sel->smem[v];
-        if ((v == 0 || v == 5) && opt.early_reject)   // a10 candidates need a full per-warp queue
-            S->smem = tma_smem(ndim, tx, ty, tz, sel->nt, 1, false, true);
-        if (rule == ACA_LIFE ? true : sel->persistent[v]) {   // persistent: as many CTAs as fit on the device
+        if (S->sync) {   // fig:s1c1pe reference: one CTA per tile, all tiles in one launch
+            S->kern = sel->fn_sync;
+            S->nthreads = sel->nt_sync;
+            S->smem = sel->smem_sync;
+        } else {
+            const bool early = opt.early_reject != 0 && rule != ACA_LIFE;
+            S->kern = rule == ACA_LIFE ? sel->fn_life : early ? sel->fn_early : sel->fn;
+            S->nthreads = early ? sel->nt_early : sel->nt;
+            S->smem = early ? sel->smem_early : sel->smem;
             if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
                 return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
             int nsm = 0, occ = 0;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, S->nthreads, S->smem) != cudaSuccess || occ < 1)
-                return bail(fail(ACA_ECUDA, "occupancy query failed"));
+                return bail(fail(ACA_ECUDA, "occupancy query failed (%zu B shared memory, %d threads)", S->smem,
+                                 S->nthreads));
+            // persistent: one CTA per SM (as many as fit), optionally capped (max_ctas drives the
+            // multi-tile-per-CTA buffer ring on small lattices)
             S->persistent_ctas = nsm * occ;
-            S->phased = opt.checkerboard >= 0;
-        }
-        // barrier-free tile pipeline (ACA_ASYNC_TILES=1, experiment): 2-D 64x64 tiles covering the
-        // shard exactly with an even number of tiles per row, per-warp round exit
-        const char* as_env = getenv("ACA_ASYNC_TILES");
-        const int64_t local_rows = dims[saxis] / parts;
-        if (as_env && atoi(as_env) == 1 && ndim == 2 && tx == 64 && ty == 64 && sel->nt == 256 && v == 0 &&
-            rule != ACA_LIFE && !S->sync && dims[0] % 128 == 0 && local_rows % 64 == 0 && S->round_mode == 2) {
-            S->kern = opt.early_reject ? (void*)tile_as_kernel<64, 64, 256, 2, true>
-                                       : (void*)tile_as_kernel<64, 64, 256, 2, false>;
-            S->smem = tma_smem(2, 64, 64, 1, 256, 2, false, opt.early_reject != 0);
-            if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
-                return bail(fail(ACA_ECUDA, "smem attribute (async tiles)"));
-            int nsm = 0, occ = 0;
-            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, 256, S->smem) != cudaSuccess || occ < 1)
-                return bail(fail(ACA_ECUDA, "occupancy query failed"));
-            S->persistent_ctas = nsm * occ;
+            if (opt.max_ctas > 0) S->persistent_ctas = std::min(S->persistent_ctas, opt.max_ctas);
             S->phased = opt.checkerboard >= 0;
         }
     }
@@ -834,7 +843,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         return bail(fail(ACA_ENOMEM, "pinned ctl"));
 
     if (S->ipc && !(S->persistent_ctas > 0 && !S->whole))
-        return bail(fail(ACA_EINVAL, "multi-process push mode needs the persistent tile kernel (variant 0/4/5)"));
+        return bail(fail(ACA_EINVAL, "multi-process push mode needs the persistent tile kernel (not sync_rounds)"));
     if (S->ipc) {   // this rank's {epoch, active} slot, read by every rank through CUDA IPC
         if (cudaMalloc(&S->d_slot, 16) != cudaSuccess) return bail(fail(ACA_ENOMEM, "ipc slot"));
         if (cudaMemset(S->d_slot, 0, 16) != cudaSuccess) return bail(fail(ACA_ECUDA, "ipc slot"));
@@ -861,7 +870,8 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
     int rc = fit_layout(S, Tq);
     if (rc) return rc;
     S->T_last = Tq;
-    const int TSH = S->RB + S->NB + 1;
+    S->t_hi = std::max<uint64_t>(S->t_hi, Tq + S->max_delta);   // every time the run can store
+    const int TSH = S->NB + 1;
     for (size_t i = 0; i < S->shards.size(); ++i) {
         S->h_ctl[i].wlim = (unsigned long long)Tq << TSH;
         CK(cudaMemcpyAsync(&S->shards[i].ctl->wlim, &S->h_ctl[i].wlim, sizeof(unsigned long long),
@@ -1127,7 +1137,7 @@ int aca_get_stats(aca_sim* S, aca_stats* o) {
     o->kernel_launches = S->kernel_launches;
     o->time_bits = S->TB;
     o->counter_bits = S->NB;
-    o->rank_bits = S->RB;
+    o->rank_bits = 0;   // the (t, c) tie-break needs no bits in the word (explicit id order)
     const int ncls = 2 * (2 * S->ndim + 1);
     double rate = 0;
     for (int k = 0; k < ncls; ++k) {
@@ -1153,10 +1163,11 @@ int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const 
     }
     // layout able to hold the largest time (plus one more increment) and counter
     const int tb = bits_for(tmax + S->max_delta);
-    int nb = std::min(31, 63 - S->RB - tb);
+    int nb = std::min(31, 63 - tb);
     if (nb < 1 || (uint64_t)nmax >= (1ull << nb) - 1ull) return fail(ACA_ERANGE, "state does not fit the packed word");
     S->NB = nb;
-    S->TB = 63 - S->RB - nb;
+    S->TB = 63 - nb;
+    S->t_hi = tmax + 1;
     set_geo_layout(S);
     drop_graph(S);
     rc = ensure_scratch(S, CHUNK * 13);
@@ -1171,8 +1182,7 @@ int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const 
             CK(cudaMemcpyAsync(dt, times + off + b, m * 8, cudaMemcpyHostToDevice, S->stream));
             CK(cudaMemcpyAsync(dn, counters + off + b, m * 4, cudaMemcpyHostToDevice, S->stream));
             CK(cudaMemcpyAsync(ds, spins + off + b, m, cudaMemcpyHostToDevice, S->stream));
-            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, ds, dt, dn, sh.g, (unsigned long long)m,
-                                                    (unsigned long long)b);
+            pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, ds, dt, dn, sh.g, (unsigned long long)m);
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(S->stream));
         }
@@ -1194,7 +1204,7 @@ int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
             const size_t m = std::min(CHUNK, sh.n - b);
             CK(cudaMemcpyAsync(S->scratch, spins + off + b, m, cudaMemcpyHostToDevice, S->stream));
             pack_kernel<<<592, 256, 0, S->stream>>>(sh.words + b, (const int8_t*)S->scratch, nullptr, nullptr, sh.g,
-                                                    (unsigned long long)m, (unsigned long long)b);
+                                                    (unsigned long long)m);
             CK(cudaGetLastError());
         }
         off += sh.n;
@@ -1243,7 +1253,7 @@ int aca_set_spins_staged(aca_sim* S, int slot) {
     size_t off = 0;
     for (auto& sh : S->shards) {
         pack_kernel<<<1184, 256, 0, S->stream>>>(sh.words, S->stage_in[slot] + off, nullptr, nullptr, sh.g,
-                                                 (unsigned long long)sh.n, 0ull);
+                                                 (unsigned long long)sh.n);
         CK(cudaGetLastError());
         off += sh.n;
     }
@@ -1301,25 +1311,38 @@ __global__ void philox_test_kernel(uint64_t n, const uint32_t* ctr, const uint32
         ref[4 * i] = q.x; ref[4 * i + 1] = q.y; ref[4 * i + 2] = q.z; ref[4 * i + 3] = q.w;
     }
 }
+// The tile kernels read the NLOG-2 tables split in shared memory (NlogSmem); the one-pass and
+// aggregated kernels read the interleaved table (NlogLR). Both views must give the same integers:
+// a disagreement is reported as the bitwise complement (the test then fails).
 __global__ void nlog_test_kernel(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* d, const unsigned long long* lr_g,
                                  unsigned long long inv_lambda, int tie_bits) {
-    __shared__ unsigned long long lr[512];
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    __shared__ unsigned long long Lt[256];
+    __shared__ unsigned int Rt[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) { Lt[i] = lr_g[2 * i]; Rt[i] = (unsigned int)lr_g[2 * i + 1]; }
     __syncthreads();
+    const NlogSmem tab{smem_u32(Lt), smem_u32(Rt)};
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        q[i] = nlog_q32(X[i], lr, ACA_LN2_Q48);
-        d[i] = delta_q32((uint32_t)(X[i] >> 32), (uint32_t)X[i], lr, ACA_LN2_Q48, inv_lambda, tie_bits);
+        const uint64_t a = nlog_q32_t(X[i], tab, ACA_LN2_Q48), b = nlog_q32(X[i], lr_g, ACA_LN2_Q48);
+        q[i] = a == b ? a : ~a;
+        const uint64_t da = delta_q32_t((uint32_t)(X[i] >> 32), (uint32_t)X[i], tab, ACA_LN2_Q48, inv_lambda, tie_bits);
+        const uint64_t db = delta_q32((uint32_t)(X[i] >> 32), (uint32_t)X[i], lr_g, ACA_LN2_Q48, inv_lambda, tie_bits);
+        d[i] = da == db ? da : ~da;
     }
 }
 __global__ void law_test_kernel(uint64_t n, const uint64_t* X, uint64_t* u, uint64_t* d, const unsigned long long* lr_g,
                                 unsigned long long inv_lambda, int tie_bits, int law) {
-    __shared__ unsigned long long lr[512];
-    for (int i = threadIdx.x; i < 512; i += blockDim.x) lr[i] = lr_g[i];
+    __shared__ unsigned long long Lt[256];
+    __shared__ unsigned int Rt[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) { Lt[i] = lr_g[2 * i]; Rt[i] = (unsigned int)lr_g[2 * i + 1]; }
     __syncthreads();
+    const NlogSmem tab{smem_u32(Lt), smem_u32(Rt)};
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t w1 = (uint32_t)(X[i] >> 32), w2 = (uint32_t)X[i];
-        u[i] = law_q32(w1, w2, lr, ACA_LN2_Q48, law);
-        d[i] = delta_q32(w1, w2, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
+        const uint64_t ua = law_q32_t(w1, w2, tab, ACA_LN2_Q48, law), ub = law_q32(w1, w2, lr_g, ACA_LN2_Q48, law);
+        u[i] = ua == ub ? ua : ~ua;
+        const uint64_t da = delta_q32_t(w1, w2, tab, ACA_LN2_Q48, inv_lambda, tie_bits, law);
+        const uint64_t db = delta_q32(w1, w2, lr_g, ACA_LN2_Q48, inv_lambda, tie_bits, law);
+        d[i] = da == db ? da : ~da;
     }
 }
 }  // namespace

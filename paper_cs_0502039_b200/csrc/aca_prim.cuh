@@ -56,16 +56,40 @@ __host__ __device__ inline void philox_round_keys(uint32_t k0, uint32_t k1, uint
 }
 
 // ---------------------------------------------------------------- P3 NLOG-2
-// -ln(u) in Q32 for u = (X|1)/2^64, integer-only. `lr` points at the interleaved
-// {L[i], R[i]} table (shared memory copy of ACA_NLOG_LR). Every intermediate of the
-// definition in docs/PRIMITIVES.md P3 fits 32 bits except L + A, so the arithmetic is done
-// on 32-bit halves (IMAD / IMAD.HI) — the same integers as the 64-bit statement of P3:
+// Table views. NLOG-2 reads L[i] (u64) and the low word of R[i] (R[0] = 2^32 is handled by the
+// i = 0 case). NlogLR: the interleaved {L[i], R[i]} u64 pairs of ACA_NLOG_LR (global or shared
+// memory, generic addressing). NlogSmem: the two tables split in shared memory (L u64[256],
+// R u32[256]) and addressed by 32-bit shared-window offsets: a warp's 32 random lookups then
+// spread over 16 (L) and 32 (R) bank groups instead of the 8 of the 16-byte interleaved
+// entries, and no generic-to-shared address conversion is repeated per lookup.
+struct NlogLR {
+    const unsigned long long* lr;
+    __device__ __forceinline__ uint64_t L(uint32_t i) const { return lr[2 * i]; }
+    __device__ __forceinline__ uint32_t R(uint32_t i) const { return (uint32_t)lr[2 * i + 1]; }
+};
+struct NlogSmem {
+    uint32_t l, r;   // shared-window byte offsets of L[0] and R[0]
+    __device__ __forceinline__ uint64_t L(uint32_t i) const {
+        uint64_t v;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(l + 8u * i));
+        return v;
+    }
+    __device__ __forceinline__ uint32_t R(uint32_t i) const {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(r + 4u * i));
+        return v;
+    }
+};
+
+// -ln(u) in Q32 for u = (X|1)/2^64, integer-only (docs/PRIMITIVES.md P3). Every intermediate
+// of the definition fits 32 bits except L + A, so the arithmetic is done on 32-bit halves
+// (IMAD / IMAD.HI) — the same integers as the 64-bit statement of P3:
 //   V = (g R[i]) >> 32 = umulhi(g, R[i] mod 2^32) + [i = 0] g     (R[0] = 2^32, R[i>0] < 2^32)
 //   V2 = V^2 = (v2h, v2l);  B = ceil(V2 / 2^33);  C = floor((umulhi(v2h, V) >> 8) / 3)
 //   Wq = ceil(V2 / 2^32) < 2^32;  D = ceil(Wq^2 / 2^50)
 //   lnf = L[i] + (V << 8) + C - (B + D)   (B + D < 2^32; the sum is exact modulo 2^64)
-__device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long long* __restrict__ lr,
-                                             uint64_t ln2_q48) {
+template <class Tab>
+__device__ __forceinline__ uint64_t nlog_q32_t(uint64_t X, const Tab& tab, uint64_t ln2_q48) {
     const uint64_t x = X | 1ull;
     const uint32_t xh = (uint32_t)(x >> 32), xl = (uint32_t)x;
     int z;
@@ -82,9 +106,8 @@ __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long lon
     }
     const uint32_t i = mh >> 24;
     const uint32_t g = __funnelshift_r(ml, mh, 24);          // bits 24..55 of m
-    const uint64_t Li = lr[2 * i];
-    const uint32_t Rl = (uint32_t)lr[2 * i + 1];
-    const uint32_t V = i == 0u ? g : __umulhi(g, Rl);
+    const uint64_t Li = tab.L(i);
+    const uint32_t V = i == 0u ? g : __umulhi(g, tab.R(i));
     const uint32_t v2l = V * V, v2h = __umulhi(V, V);
     const uint32_t B = (v2h >> 1) + ((v2l | (v2h & 1u)) != 0u ? 1u : 0u);
     const uint32_t C = (__umulhi(v2h, V) >> 8) / 3u;
@@ -95,6 +118,10 @@ __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long lon
     const uint64_t S = (uint64_t)(uint32_t)(z + 1) * ln2_q48 - lnf;
     return (S + (1ull << 15)) >> 16;
 }
+__device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long long* __restrict__ lr,
+                                             uint64_t ln2_q48) {
+    return nlog_q32_t(X, NlogLR{lr}, ln2_q48);
+}
 
 // P3L asynchrony law: the unscaled increment U in Q32 (docs/PRIMITIVES.md P3L).
 //   0 Poisson, Eq. newt1i:   U = NLOG-2((w1 << 32) | w2)
@@ -103,8 +130,8 @@ __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long lon
 //     (IEEE double; sqrt is correctly rounded on the device as on the host)
 //   3 Gaussian period:        S = sum of the 12 words of Philox (w1, w2, j, 9) under the
 //     fixed key (0x243F6A88, 0x85A308D3), j = 0..2; U = max(1, (S >> 2) - 2^31): mean 1, sd 1/4
-__device__ __forceinline__ uint64_t law_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr,
-                                            uint64_t ln2_q48, int law) {
+template <class Tab>
+__device__ __forceinline__ uint64_t law_q32_t(uint32_t w1, uint32_t w2, const Tab& tab, uint64_t ln2_q48, int law) {
     if (law == 1) return (uint64_t)w1;
     if (law == 3) {   // Gaussian period: Irwin-Hall(12) of three sub-draws
         uint64_t S = 0;
@@ -120,13 +147,18 @@ __device__ __forceinline__ uint64_t law_q32(uint32_t w1, uint32_t w2, const unsi
         const double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
         return (uint64_t)(__dsqrt_rn(__dsqrt_rn(__dsqrt_rn(r))) * 4294967296.0);
     }
-    return nlog_q32(((uint64_t)w1 << 32) | w2, lr, ln2_q48);
+    return nlog_q32_t(((uint64_t)w1 << 32) | w2, tab, ln2_q48);
+}
+__device__ __forceinline__ uint64_t law_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr, uint64_t ln2_q48,
+                                            int law) {
+    return law_q32_t(w1, w2, NlogLR{lr}, ln2_q48, law);
 }
 
 // next_t = t + U / lambda, next_t > t; P3b tie quantisation.
-__device__ __forceinline__ uint64_t delta_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr,
-                                              uint64_t ln2_q48, uint64_t inv_lambda, int tie_bits, int law = 0) {
-    const uint64_t q = law_q32(w1, w2, lr, ln2_q48, law);
+template <class Tab>
+__device__ __forceinline__ uint64_t delta_q32_t(uint32_t w1, uint32_t w2, const Tab& tab, uint64_t ln2_q48,
+                                                uint64_t inv_lambda, int tie_bits, int law = 0) {
+    const uint64_t q = law_q32_t(w1, w2, tab, ln2_q48, law);
     uint64_t d;
     if (inv_lambda == (1ull << 32)) {
         d = q;
@@ -140,6 +172,11 @@ __device__ __forceinline__ uint64_t delta_q32(uint32_t w1, uint32_t w2, const un
         d = d < quantum ? quantum : d;
     }
     return d;
+}
+
+__device__ __forceinline__ uint64_t delta_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr, uint64_t ln2_q48,
+                                              uint64_t inv_lambda, int tie_bits, int law = 0) {
+    return delta_q32_t(w1, w2, NlogLR{lr}, ln2_q48, inv_lambda, tie_bits, law);
 }
 
 // ---------------------------------------------------------------- P7 event hash

@@ -53,21 +53,30 @@ def bond_sum(spins, ndim):
     return int(sum((s * np.roll(s, -1, axis=ax)).sum() for ax in range(ndim)))
 
 
-@pytest.mark.parametrize("seed", workloads.PARITY_SEEDS)
-def test_config2_full_digest(aca, oracle_mod, seed):
-    """Config 2 in full (1024^2, Metropolis beta 0.40, T = 100, ~1.05e8 arrivals) against the
-    digests of a full oracle run (tests/golden/c2_seed<k>.json, written by
-    scripts/make_golden.py from oracle/ only): every spin, time and counter, bit for bit, in the
-    bench configuration (R = 6, 512-thread tiles) for all three parity seeds."""
+def _golden_files():
+    import glob
+    import os
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    return sorted(os.path.basename(p) for p in glob.glob(os.path.join(here, "c[2-5]_seed*.json")))
+
+
+@pytest.mark.parametrize("golden", _golden_files())
+def test_full_lattice_digest(aca, golden):
+    """A BASELINE config in full against the digests of a full oracle run
+    (tests/golden/<config>_seed<k>[_T<T'>].json, written by scripts/make_golden.py from oracle/
+    only): SHA-256 of every spin, time and counter plus every integer statistic (arrivals,
+    flips, P7 event hash, B, M, t range), bit for bit, in the launch configuration bench.py
+    times (default tile, rounds and kernel). Files with a _T suffix stop at an interim horizon
+    T' < T (full-T oracle runs of c3 and c5 take hours)."""
     import hashlib
     import json
     import os
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "c2_seed%d.json" % seed)
-    gold = json.load(open(path))
-    cfg = workloads.config("c2")
+    gold = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", golden)))
+    cfg = workloads.config(gold["config"])
+    assert tuple(gold["dims"]) == tuple(cfg["dims"])
     g = aca.Sim(cfg["dims"], lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
                 seed=gold["seed"], init_q=cfg["init_q"], tile=cfg["tile"], **cfg.get("opts", {}))
-    g.run_until(cfg["T"])
+    g.run_until(gold["T"])
     dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
     assert dig(g.spins()) == gold["sha256_spins_int8"]
     assert dig(g.times()) == gold["sha256_times_u64"]
@@ -75,6 +84,38 @@ def test_config2_full_digest(aca, oracle_mod, seed):
     st = g.stats()
     for k, v in gold["stats"].items():
         assert st[k] == v, k
+    g.close()
+
+
+@pytest.mark.parametrize("max_ctas", [0, 16])
+def test_multi_tile_per_cta_full_oracle(aca, oracle_mod, max_ctas):
+    """A 2048^2 lattice (1024 tiles of 64^2, 512 per checkerboard launch) against the full
+    oracle, element by element, at the default grid (every CTA runs 3-4 tiles per launch through
+    its buffer ring) and at 16 CTAs (32 tiles per CTA per launch): the production persistent
+    loop, its buffer reuse and prefetch, in the configuration bench.py times."""
+    from test_gpu_parity import assert_same, run_pair
+    g, o = run_pair(aca, oracle_mod, (2048, 2048), [1.5, 2.5], beta=0.4406868, seed=3, max_ctas=max_ctas)
+    assert_same(g, o)
+
+
+def test_long_horizon_16384_wide(aca, oracle_mod):
+    """The packed word no longer caps the horizon: a 16384-wide lattice (64 rows) runs to
+    T = 1000 (~1.05e9 arrivals, counters ~1000); every sampled cell's (t, n) equals the per-cell
+    closed form (arrival times are state-independent), and sum n = arrivals."""
+    dims, T = (16384, 64), 1000.0
+    g = aca.Sim(dims, beta=0.4406868, seed=5)
+    g.run_until(T)
+    st = g.stats()
+    assert st["time_bits"] >= 43
+    pts = sample_cells(dims, (64, 64), 48, seed=11)
+    idx = np.array([flat(c, dims) for c in pts], np.int64)
+    _, t_g, n_g = g.cells(idx)
+    for c, t, n in zip(pts, t_g, n_g):
+        assert (int(t), int(n)) == oracle_mod.cell_time_counter(5, flat(c, dims), T, 1.0), c
+    assert int(g.counters().astype(np.int64).sum()) == st["arrivals"] == st["cells_fired"]
+    mu = dims[0] * dims[1] * T
+    assert abs(st["arrivals"] - mu) < 5 * math.sqrt(mu)
+    assert st["t_min"] >= oracle_mod.to_q32(T)
 
 
 @pytest.mark.parametrize("seed", workloads.PARITY_SEEDS)

@@ -126,7 +126,7 @@ def test_config1_exact(aca, oracle_mod, sync):
     assert abs(st["arrivals"] - 40960) < 5 * 202
 
 
-@pytest.mark.parametrize("tile", [(64, 64), (32, 32), (64, 32), (128, 64)])
+@pytest.mark.parametrize("tile", [(64, 64), (32, 32), (64, 32)])
 def test_tiled_2d_ragged(aca, oracle_mod, tile):
     """Several tiles plus ragged tails in x and y."""
     g, o = run_pair(aca, oracle_mod, (200, 150), [2.0, 6.0], beta=0.40, rule=1, seed=11, tile=tile,
@@ -134,17 +134,42 @@ def test_tiled_2d_ragged(aca, oracle_mod, tile):
     assert_same(g, o)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4, 5])
-def test_kernel_variants(aca, oracle_mod, variant):
-    """Persistent TMA kernel (0), uncompacted per-tile kernel (1), double-buffered TMA
-    kernel (2), register-resident synchronous rounds (3), work-list rounds (4), 2-wide redundant
-    halo (5): identical
-    trajectories, 2-D (full + ragged tiles, odd width) and 3-D."""
+@pytest.mark.parametrize("max_ctas", [0, 1, 3, 7])
+def test_buffer_ring_and_grid_cap(aca, oracle_mod, max_ctas):
+    """The persistent grouped kernel with its grid capped (max_ctas): every CTA cycles many
+    tiles through its NBUF-buffer ring, so the buffer reuse, the mbarrier parity flips and the
+    prefetch issued at write-back are all exercised; 2-D (full + ragged tiles, odd width) and
+    3-D, identical trajectories."""
     for dims, tile, T in (((256, 192), (64, 64), 5.0), ((200, 150), (64, 32), 4.0), ((130, 70), (32, 32), 4.0),
                           ((64, 48, 40), (32, 16, 8), 3.0), ((40, 24, 20), (16, 16, 16), 3.0)):
         beta = 0.2216544 if len(dims) == 3 else 0.4406868
-        g, o = run_pair(aca, oracle_mod, dims, [T], beta=beta, seed=37, tile=tile, whole_lattice=-1, variant=variant)
+        g, o = run_pair(aca, oracle_mod, dims, [T], beta=beta, seed=37, tile=tile, whole_lattice=-1, max_ctas=max_ctas)
         assert_same(g, o)
+
+
+@pytest.mark.parametrize("case", ["jacobi", "jacobi_ties", "odd_tiles", "ties_cap", "rounds1_ties", "T_frac"])
+def test_staging_paths(aca, oracle_mod, case):
+    """Staging paths of the grouped kernel: one launch over all tiles (checkerboard -1: every
+    halo word is read by threads with relaxed loads, neighbours run concurrently), odd tile
+    counts (same-colour wrap neighbours: the wrapped halo by threads), forced ties with a
+    capped grid, R = 1 (every round exact), and a horizon whose Q32 value has a non-zero low
+    half (the T bucket tie)."""
+    kw = dict(dims=(256, 192), Ts=[3.0, 6.0], seed=29, whole_lattice=-1)
+    if case == "jacobi":
+        kw.update(checkerboard=-1)
+    elif case == "jacobi_ties":
+        kw.update(checkerboard=-1, tie_bits=30)
+    elif case == "odd_tiles":
+        kw.update(dims=(320, 192))          # 5 x 3 tiles of 64: odd in x and y
+    elif case == "ties_cap":
+        kw.update(tie_bits=29, max_ctas=2)
+    elif case == "rounds1_ties":
+        kw.update(tie_bits=30, rounds_per_launch=1)
+    elif case == "T_frac":
+        kw.update(Ts=[2.3, 5.123456789])
+    dims, Ts = kw.pop("dims"), kw.pop("Ts")
+    g, o = run_pair(aca, oracle_mod, dims, Ts, **kw)
+    assert_same(g, o)
 
 
 @pytest.mark.parametrize("case", ["c5", "hb", "3d", "ties", "bulk"])
@@ -174,7 +199,7 @@ def test_sync_rounds_tiled(aca, oracle_mod):
     assert_same(g, o)
 
 
-@pytest.mark.parametrize("tile", [(32, 16, 8), (16, 16, 16), (8, 8, 8), (32, 32, 8)])
+@pytest.mark.parametrize("tile", [(32, 16, 8), (16, 16, 16), (8, 8, 8)])
 def test_tiled_3d_ragged(aca, oracle_mod, tile):
     g, o = run_pair(aca, oracle_mod, (40, 24, 20), [3.0], beta=0.2216544, seed=13, tile=tile, whole_lattice=-1)
     assert_same(g, o)
@@ -240,6 +265,24 @@ def test_set_state_roundtrip(aca, oracle_mod):
     g.run_until(5.0)
     g2.run_until(5.0)
     assert np.array_equal(g.spins(), g2.spins()) and np.array_equal(g.times(), g2.times())
+
+
+def test_set_state_beyond_horizon(aca, oracle_mod):
+    """A restored state whose times lie far beyond the next horizon: the packed layout must keep
+    every stored time (no silent loss of high time bits when the counter field grows)."""
+    g, o = run_pair(aca, oracle_mod, (64, 48), [3.0], beta=0.5, seed=47, whole_lattice=-1)
+    s, t, n = g.spins().copy(), g.times().copy(), g.counters().copy()
+    t2 = t + np.uint64(900 << 32)           # every pending arrival 900 time units later
+    g.set_state(s, t2, n)
+    g.run_until(5.0)                         # nothing is below T: no arrival may fire
+    assert np.array_equal(g.times(), t2) and np.array_equal(g.counters(), n) and np.array_equal(g.spins(), s)
+    assert g.stats()["t_min"] == int(t2.min())
+    g.run_until(904.0)
+    g2 = aca.Sim((64, 48), beta=0.5, seed=47, whole_lattice=-1)   # the same state run straight to 904
+    g2.set_state(s, t2, n)
+    g2.run_until(904.0)
+    assert np.array_equal(g.spins(), g2.spins()) and np.array_equal(g.times(), g2.times())
+    assert np.array_equal(g.counters(), g2.counters()) and int(g.counters().sum() - n.sum()) > 0
 
 
 def test_packed_layout_repack(aca, oracle_mod):
@@ -329,31 +372,8 @@ def test_class_histogram(aca, oracle_mod, dims):
     assert abs(st["nfold_rate"] - rate) < 1e-6 * max(1.0, rate)
 
 
-@pytest.mark.parametrize("case", ["tiny", "shards", "ties", "metro_field", "law2", "rounds"])
-def test_two_wide_halo(aca, oracle_mod, case):
-    """Variant 5 (2-wide halo, inner ring simulated redundantly): lattices smaller than a tile
-    (the box is a periodic unrolling with repeated cells), virtual shards (rows outside the
-    shard stay frozen), forced ties, Metropolis with field, the r^(1/8) law, many rounds."""
-    kw = dict(dims=(200, 150), Ts=[3.0, 6.0], seed=53, whole_lattice=-1, variant=5)
-    if case == "tiny":
-        kw.update(dims=(20, 12))
-    elif case == "shards":
-        kw.update(dims=(128, 256), shards=4)
-    elif case == "ties":
-        kw.update(tie_bits=30)
-    elif case == "metro_field":
-        kw.update(rule=1, h=0.1, beta=0.6)
-    elif case == "law2":
-        kw.update(law=2)
-    elif case == "rounds":
-        kw.update(rounds_per_launch=24)
-    dims, Ts = kw.pop("dims"), kw.pop("Ts")
-    g, o = run_pair(aca, oracle_mod, dims, Ts, **kw)
-    assert_same(g, o)
-
-
-@pytest.mark.parametrize("case", ["whole", "tiny", "tiled", "t32", "t64x32", "t128", "shards", "ties", "law2",
-                                  "block", "frames"])
+@pytest.mark.parametrize("case", ["whole", "tiny", "tiled", "t32", "t64x32", "shards", "ties", "law2",
+                                  "block", "frames", "jacobi", "odd"])
 def test_game_of_life(aca, oracle_mod, case):
     """Rule 2 (asynchronous Game of Life, P10): Moore neighbourhood, Conway's
     rule, explicit (t, c) tie-break (no rank bits): bit-identical trajectories on the
@@ -368,8 +388,10 @@ def test_game_of_life(aca, oracle_mod, case):
         kw.update(tile=(32, 32))
     elif case == "t64x32":
         kw.update(tile=(64, 32))
-    elif case == "t128":
-        kw.update(tile=(128, 64))
+    elif case == "jacobi":
+        kw.update(checkerboard=-1)
+    elif case == "odd":
+        kw.update(dims=(320, 192))
     elif case == "shards":
         kw.update(dims=(128, 96), shards=4)
     elif case == "ties":
@@ -400,25 +422,10 @@ def test_game_of_life(aca, oracle_mod, case):
     assert_same(g, o)
 
 
-@pytest.mark.parametrize("env,tile,dims", [(("ACA_DEFER_TAIL", "1"), (64, 64), (320, 200)),
-                                           (("ACA_TILE_NT", "128"), (64, 32), (320, 200)),
-                                           (("ACA_TILE_NT", "256"), (64, 32), (200, 136)),
+@pytest.mark.parametrize("env,tile,dims", [(("ACA_TILE_NT", "256"), (64, 64), (320, 200)),
                                            (("ACA_TILE_NT", "512"), (64, 64), (320, 200))])
 def test_ablation_switches_stay_exact(aca, oracle_mod, env, tile, dims, monkeypatch):
-    """Ablation switches read at aca_create: the carried partial fire chunk (ACA_DEFER_TAIL=1)
-    and the block size of a tile shape (ACA_TILE_NT) change the schedule, never the result."""
+    """The group size of a tile shape (ACA_TILE_NT) changes the schedule, never the result."""
     monkeypatch.setenv(*env)
     g, o = run_pair(aca, oracle_mod, dims, [3.0, 6.0], beta=0.4406868, seed=71, tile=tile)
-    assert_same(g, o)
-
-
-@pytest.mark.parametrize("dims,kw", [((256, 192), dict(beta=0.4406868)),
-                                     ((256, 256), dict(beta=0.4406868, shards=2)),
-                                     ((256, 128), dict(beta=0.4406868, checkerboard=-1)),
-                                     ((256, 128), dict(beta=1.0, h=0.1, rule=1, init_q=0.05, early_reject=1))])
-def test_async_tile_pipeline_exact(aca, oracle_mod, dims, kw, monkeypatch):
-    """The barrier-free tile pipeline (ACA_ASYNC_TILES=1: two TMA buffers, per-warp waits and
-    write-back, the last warp out refills the buffer) reaches the oracle's trajectory."""
-    monkeypatch.setenv("ACA_ASYNC_TILES", "1")
-    g, o = run_pair(aca, oracle_mod, dims, [2.0, 5.0], seed=83, tile=(64, 64), **kw)
     assert_same(g, o)
