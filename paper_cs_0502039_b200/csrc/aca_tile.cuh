@@ -606,25 +606,29 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         return TY * ((int)face_ok(o, true, true) + (int)face_ok(o, true, false)) +
                TZ * ((int)face_ok(o, false, true) + (int)face_ok(o, false, false));
     };
-    // One whole warp stages tile k into buffer b (or, for a tile that is not all-TMA, just
-    // arrives on the buffer's barrier so the phases stay aligned with the tile count).
-    auto issue = [&](int k, int b) {
+    // Staging of tile k into buffer b in two steps. arm (one thread): announce the bytes the
+    // bulk copies will deliver on bar[b] (or just arrive, for a tile that is not all-TMA, so the
+    // phases stay aligned with the tile count) and publish that phase k / NBUF is armed.
+    // copy_rows (every thread of a group or warp, `t` of `nt`): issue the row copies.
+    auto arm = [&](int k, int b) {
         const Org o = origin(k);
         const bool fast = o.full && vec_ok;
-        const bool xs = fast && x_tma(o);
-        const int rw = xs ? TX + 4 : TX;                  // words per staged row
-        const int nrows = fast ? NROWS + face_rows_tma(o) : 0;
-        if (lane == 0) {
-            if (fast) mbar_arrive_expect_tx(&bar[b], (uint32_t)(nrows * rw * 8));
-            else mbar_arrive(&bar[b]);
-            __threadfence_block();
-            armed[b] = (unsigned int)(k / NBUF) + 1u;   // phase k / NBUF of bar[b] is armed
+        if (fast) {
+            const int rw = x_tma(o) ? TX + 4 : TX;       // words per staged row
+            mbar_arrive_expect_tx(&bar[b], (uint32_t)((NROWS + face_rows_tma(o)) * rw * 8));
+        } else {
+            mbar_arrive(&bar[b]);
         }
-        if (!fast) return;
-        __syncwarp();
-        fence_proxy_async();
+        __threadfence_block();
+        armed[b] = (unsigned int)(k / NBUF) + 1u;   // phase k / NBUF of bar[b] is armed
+    };
+    auto copy_rows = [&](int k, int b, int t, int nt) {
+        const Org o = origin(k);
+        if (!(o.full && vec_ok)) return;
+        const bool xs = x_tma(o);
         unsigned long long* S = Sb + b * NSLOTP;
-        for (int row = lane; row < NROWS + NFACE; row += 32) {
+        bool fenced = false;
+        for (int row = t; row < NROWS + NFACE; row += nt) {
             int ly, lz;
             const unsigned long long* rowp;
             if (row < NROWS) {
@@ -636,6 +640,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                 face_coords(row - NROWS, ly, lz);
                 rowp = word_ptr_t<true>(P, 0, o.y0 + ly, o.z0 + lz);
             }
+            if (!fenced) { fence_proxy_async(); fenced = true; }
             unsigned long long* d0 = &S[slot(0, ly, lz)];
             ACA_CHECK(slot(-2, ly, lz) >= 0 && slot(TX + 2, ly, lz) <= NSLOTP, row, ly);
             ACA_CHECK(rowp != nullptr && ((uintptr_t)rowp & 15) == 0, (uintptr_t)rowp, row);
@@ -652,8 +657,14 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         }
     };
 
-    if (warp == 0)
-        for (int k = 0; k < NBUF && k < K; ++k) issue(k, k);
+    if (warp == 0) {   // the first NBUF tiles of this CTA
+        for (int k = 0; k < NBUF && k < K; ++k) {
+            if (lane == 0) arm(k, k);
+            __syncwarp();
+            copy_rows(k, k, lane, 32);
+        }
+    }
+
 
     TileStats st;
     TileTotals tot;
@@ -756,9 +767,12 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
             }
         }
         ACA_TRACE(6, k);
-        group_bar(1 + gid, NTG);   // the buffer is free: refill it with tile k + NBUF
+        // refill the buffer with tile k + NBUF: armed before the barrier (the arrive does not
+        // touch the buffer), copied after it by every thread of the group (at most a row each)
+        if (gt == 0 && k + NBUF < K) arm(k + NBUF, b);
+        group_bar(1 + gid, NTG);   // the buffer is free
         ACA_TRACE(7, k);
-        if (wg == 0 && k + NBUF < K) issue(k + NBUF, b);
+        if (k + NBUF < K) copy_rows(k + NBUF, b, gt, NTG);
     }
     ACA_TRACE(8, 0);
     __syncthreads();
