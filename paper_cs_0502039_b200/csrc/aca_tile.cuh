@@ -35,11 +35,12 @@ __host__ __device__ constexpr int grp_slots(int ndim, int tx, int ty, int tz) {
 // Shared-memory layout of tile_grp_kernel (host and device): NBUF tile buffers, the P4 (16) and
 // a10 (112) tables, the NLOG-2 tables split as L u64[256] and R u32[256], the reduction
 // scratch, NBUF mbarriers, 32 u32 of ring control (claim counter, the tile of each group, the
-// phases armed on each buffer), then the per-warp fire queues.
+// phases armed on each buffer), the origin of the tile in each buffer (32 B each), then the
+// per-warp fire queues.
 __host__ __device__ constexpr size_t grp_smem_bytes(int ndim, int tx, int ty, int tz, int ntg, int ng, int nbuf,
                                                     bool early) {
     return ((size_t)nbuf * grp_slots(ndim, tx, ty, tz) + 16 + 112 + 256 + 128 + (size_t)(ntg * ng) / 32 + nbuf) * 8 +
-           128 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15);
+           128 + 16 + (size_t)nbuf * 32 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15);
 }
 
 // Commit the pending arrivals of the cell in slot s for as long as that is exact (a10):
@@ -531,7 +532,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     unsigned long long* bar = red + NW;                     // NBUF full barriers
     unsigned int* cs = (unsigned int*)(bar + NBUF);         // [0] claim counter, [1 + g] tile of group g
     volatile unsigned int* armed = cs + 1 + NG;             // [b] phases of bar[b] armed so far
-    unsigned short* Q = (unsigned short*)(cs + 32);         // NW x QW fire queue entries
+    int4* orgs = (int4*)(((uintptr_t)(cs + 32) + 15) & ~(uintptr_t)15);   // [2b], [2b+1]: origin of buffer b's tile
+    unsigned short* Q = (unsigned short*)(orgs + 2 * NBUF); // NW x QW fire queue entries
 
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -610,8 +612,18 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     // bulk copies will deliver on bar[b] (or just arrive, for a tile that is not all-TMA, so the
     // phases stay aligned with the tile count) and publish that phase k / NBUF is armed.
     // copy_rows (every thread of a group or warp, `t` of `nt`): issue the row copies.
+    // The origin of the tile in buffer b is computed once (integer divisions by runtime tile
+    // counts) by the arming thread and read by everyone else from shared memory.
+    auto org_load = [&](int b) -> Org {
+        const int4 a = orgs[2 * b], c = orgs[2 * b + 1];
+        Org o;
+        o.x0 = a.x; o.y0 = a.y; o.z0 = a.z; o.tx = a.w; o.ty = c.x; o.tz = c.y; o.valid = c.z != 0; o.full = c.w != 0;
+        return o;
+    };
     auto arm = [&](int k, int b) {
         const Org o = origin(k);
+        orgs[2 * b] = make_int4(o.x0, o.y0, o.z0, o.tx);
+        orgs[2 * b + 1] = make_int4(o.ty, o.tz, o.valid ? 1 : 0, o.full ? 1 : 0);
         const bool fast = o.full && vec_ok;
         if (fast) {
             const int rw = x_tma(o) ? TX + 4 : TX;       // words per staged row
@@ -622,8 +634,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         __threadfence_block();
         armed[b] = (unsigned int)(k / NBUF) + 1u;   // phase k / NBUF of bar[b] is armed
     };
-    auto copy_rows = [&](int k, int b, int t, int nt) {
-        const Org o = origin(k);
+    auto copy_rows = [&](int b, int t, int nt) {   // after arm(k, b) is visible to the caller
+        const Org o = org_load(b);
         if (!(o.full && vec_ok)) return;
         const bool xs = x_tma(o);
         unsigned long long* S = Sb + b * NSLOTP;
@@ -661,7 +673,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         for (int k = 0; k < NBUF && k < K; ++k) {
             if (lane == 0) arm(k, k);
             __syncwarp();
-            copy_rows(k, k, lane, 32);
+            copy_rows(k, lane, 32);
         }
     }
 
@@ -680,8 +692,6 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         ACA_TRACE(1, k);
         const int b = k % NBUF;
         unsigned long long* S = Sb + b * NSLOTP;
-        const Org o = origin(k);
-        const bool fast = o.full && vec_ok;
         // Tile k is phase u = k / NBUF of bar[b]. A fast group may claim tile k while tile k - NBUF
         // (the same buffer) is still being processed by a slow group, i.e. before phase u is even
         // armed; a parity wait then would alias phase u - 1 (already complete). So wait until
@@ -691,6 +701,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
             while (armed[b] <= use) __nanosleep(64);
             mbar_wait(&bar[b], use & 1u);
         }
+        const Org o = org_load(b);
+        const bool fast = o.full && vec_ok;
         if (fast) {   // the words the bulk copies left out: x-halo columns, unsafe face rows
             if (!x_tma(o)) {
                 for (int h = gt; h < 2 * NROWS; h += NTG) {
@@ -702,12 +714,20 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                     S[slot(lx, ly, 0)] = ld_word_t<true>(P, o.x0 + lx, o.y0 + ly, 0);
                 }
             }
-            for (int f = 0; f < NFACE; ++f) {
-                if (face_tma(o, f)) continue;
-                int ly, lz;
-                face_coords(f, ly, lz);
-                for (int lx = gt - 1; lx <= TX; lx += NTG)
+            // face rows of a category (2-D: y-; y+. 3-D: z-, z+ (TY rows each); y-, y+ (TZ rows each))
+            // whose bulk copy was unsafe: by threads
+            const int ncat = NDIM == 2 ? 2 : 4;
+            for (int c = 0; c < ncat; ++c) {
+                const bool zface = NDIM == 3 && c < 2, lo = (c & 1) == 0;
+                if (face_ok(o, zface, lo)) continue;
+                const int f0 = NDIM == 2 ? c : (c < 2 ? c * TY : 2 * TY + (c - 2) * TZ);
+                const int nf = NDIM == 2 ? 1 : (c < 2 ? TY : TZ);
+                for (int h = gt; h < nf * (TX + 2); h += NTG) {
+                    int ly, lz;
+                    face_coords(f0 + h / (TX + 2), ly, lz);
+                    const int lx = h % (TX + 2) - 1;
                     S[slot(lx, ly, lz)] = ld_word_t<true>(P, o.x0 + lx, o.y0 + ly, o.z0 + lz);
+                }
             }
         } else if (o.valid) {   // ragged or odd-width tile: the whole slot set by threads
             for (int i = gt; i < NSLOT; i += NTG) {
@@ -772,7 +792,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         if (gt == 0 && k + NBUF < K) arm(k + NBUF, b);
         group_bar(1 + gid, NTG);   // the buffer is free
         ACA_TRACE(7, k);
-        if (k + NBUF < K) copy_rows(k + NBUF, b, gt, NTG);
+        if (k + NBUF < K) copy_rows(b, gt, NTG);
     }
     ACA_TRACE(8, 0);
     __syncthreads();
