@@ -505,7 +505,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
 template <int NDIM, int TX, int TY, int TZ, int NTG, int NG, int NBUF, bool EARLY, bool MOORE>
 __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) {
     static_assert(!MOORE || NDIM == 2, "Moore neighbourhood: 2-D");
-    static_assert(NG >= 1 && NG <= 15 && NBUF >= 1 && 1 + NG + NBUF <= 32, "groups / buffers");
+    static_assert(NG >= 1 && NG <= 15 && NBUF >= 1 && 1 + 2 * NG + NBUF <= 32, "groups / buffers");
     constexpr int NT = NTG * NG;
     constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
     constexpr int SXY = SX * SY;
@@ -530,8 +530,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     unsigned int* Rt = (unsigned int*)(Lt + 256);           // 256 u32 (NLOG-2 R, low words)
     unsigned long long* red = Lt + 256 + 128;               // NW
     unsigned long long* bar = red + NW;                     // NBUF full barriers
-    unsigned int* cs = (unsigned int*)(bar + NBUF);         // [0] claim counter, [1 + g] tile of group g
-    volatile unsigned int* armed = cs + 1 + NG;             // [b] phases of bar[b] armed so far
+    unsigned int* cs = (unsigned int*)(bar + NBUF);         // [0] claim counter, [1 + 2g + p] tiles of group g
+    volatile unsigned int* armed = cs + 1 + 2 * NG;         // [b] phases of bar[b] armed so far
     int4* orgs = (int4*)(((uintptr_t)(cs + 32) + 15) & ~(uintptr_t)15);   // [2b], [2b+1]: origin of buffer b's tile
     unsigned short* Q = (unsigned short*)(orgs + 2 * NBUF); // NW x QW fire queue entries
 
@@ -683,10 +683,15 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     unsigned int active = 0;   // cells of this CTA still below T (< 2^32: N < 2^32)
     unsigned int rounds_max = 0;
     unsigned short* q = Q + warp * QW;
+    // A group's next tile is claimed by its thread 0 before the write-back barrier that ends
+    // the current one, into the other of the group's two slots (everybody has read the current
+    // slot by then), so one group barrier per tile visit suffices when no thread patches the
+    // staged buffer.
+    int par = 0;
+    if (gt == 0) cs[1 + 2 * gid] = atomicAdd(&cs[0], 1u);
+    group_bar(1 + gid, NTG);
     for (;;) {
-        if (gt == 0) cs[1 + gid] = atomicAdd(&cs[0], 1u);
-        group_bar(1 + gid, NTG);
-        const int k = (int)cs[1 + gid];
+        const int k = (int)cs[1 + 2 * gid + par];
         if (k >= K) break;
         ACA_CHECK(k >= 0, k, gid);
         ACA_TRACE(1, k);
@@ -703,7 +708,9 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         }
         const Org o = org_load(b);
         const bool fast = o.full && vec_ok;
+        bool patched = !fast && o.valid;   // threads wrote words into the buffer: barrier before use
         if (fast) {   // the words the bulk copies left out: x-halo columns, unsafe face rows
+            patched = !x_tma(o);
             if (!x_tma(o)) {
                 for (int h = gt; h < 2 * NROWS; h += NTG) {
                     const int row = h >> 1, lx = (h & 1) ? TX : -1, ly = row % TY, lz = row / TY;
@@ -720,6 +727,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
             for (int c = 0; c < ncat; ++c) {
                 const bool zface = NDIM == 3 && c < 2, lo = (c & 1) == 0;
                 if (face_ok(o, zface, lo)) continue;
+                patched = true;
                 const int f0 = NDIM == 2 ? c : (c < 2 ? c * TY : 2 * TY + (c - 2) * TZ);
                 const int nf = NDIM == 2 ? 1 : (c < 2 ? TY : TZ);
                 for (int h = gt; h < nf * (TX + 2); h += NTG) {
@@ -737,7 +745,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                 if (MOORE || out <= 1) S[i] = ld_word(P, o.x0 + lx, o.y0 + ly, o.z0 + lz);
             }
         }
-        group_bar(1 + gid, NTG);
+        if (patched) group_bar(1 + gid, NTG);
         ACA_TRACE(2, ((unsigned long long)o.x0 << 32) | (unsigned)o.y0);
 
         if (o.valid) {
@@ -789,9 +797,13 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         ACA_TRACE(6, k);
         // refill the buffer with tile k + NBUF: armed before the barrier (the arrive does not
         // touch the buffer), copied after it by every thread of the group (at most a row each)
-        if (gt == 0 && k + NBUF < K) arm(k + NBUF, b);
+        if (gt == 0) {
+            if (k + NBUF < K) arm(k + NBUF, b);
+            cs[1 + 2 * gid + (par ^ 1)] = atomicAdd(&cs[0], 1u);   // the group's next tile
+        }
         group_bar(1 + gid, NTG);   // the buffer is free
         ACA_TRACE(7, k);
+        par ^= 1;
         if (k + NBUF < K) copy_rows(b, gt, NTG);
     }
     ACA_TRACE(8, 0);
