@@ -243,6 +243,17 @@ __device__ __forceinline__ ulonglong2 lds128v(const volatile unsigned long long*
     asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(smem_u32((const void*)p)) : "memory");
     return v;
 }
+// the same through a 32-bit shared-window address
+__device__ __forceinline__ ulonglong2 lds128a(uint32_t a) {
+    ulonglong2 v;
+    asm volatile("ld.volatile.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned int lds32a(uint32_t a) {
+    unsigned int v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

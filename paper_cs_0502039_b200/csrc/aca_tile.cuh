@@ -195,14 +195,16 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         if constexpr (!EARLY && PAIRMAP) {
             unsigned int tiec = ~0u;
             // rows of the lane's column pair, top to bottom; `a` holds row rr, `b` row rr + 1
-            const ulonglong2 up = lds128v(&VS[s0 - SX]);
+            // (32-bit shared-window addresses: no generic-to-shared conversion per load)
+            const uint32_t sa0 = smem_u32(S) + 8u * (uint32_t)s0;
+            const ulonglong2 up = lds128a(sa0 - 8u * SX);
             unsigned int uh0 = hi32(up.x), uh1 = hi32(up.y);
-            ulonglong2 a = lds128v(&VS[s0]);
+            ulonglong2 a = lds128a(sa0);
 #define ACA_PAIR_ROWS(TEST)                                                                          \
     _Pragma("unroll") for (int rr = 0; rr < RPW; ++rr) {                                             \
-        const int sr = s0 + rr * SX;                                                                 \
-        const ulonglong2 b = lds128v(&VS[sr + SX]); /* row rr + 1 (the halo row for the last) */     \
-        const unsigned int lh = VH[2 * (sr - 1) + 1], rh = VH[2 * (sr + 2) + 1];                     \
+        const uint32_t ar = sa0 + 8u * SX * (uint32_t)rr;                                            \
+        const ulonglong2 b = lds128a(ar + 8u * SX); /* row rr + 1 (the halo row for the last) */     \
+        const unsigned int lh = lds32a(ar - 4u), rh = lds32a(ar + 20u);                              \
         const unsigned int ah0 = hi32(a.x), ah1 = hi32(a.y);                                         \
         const unsigned int m0 = min(min(lh, ah1), min(uh0, hi32(b.x)));                              \
         const unsigned int m1 = min(min(ah0, rh), min(uh1, hi32(b.y)));                              \
