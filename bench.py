@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true", help="skip the P7 event hash (diagnostics only)")
+    ap.add_argument("--shards", type=int, default=1,
+                    help="virtual row strips / z slabs on this GPU (bounds the per-shard boundary cost of the "
+                         "multi-GPU partition on one device; push-mode halos, same kernels)")
     return ap.parse_args()
 
 
@@ -113,29 +116,48 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_tag):
-    """dram bytes per sweep of the dominant kernel (both checkerboard launches) from the
-    committed ncu --set full summary (profiles/ncu_full_summary.json)."""
+def ncu_entry(config):
+    """The committed ncu --set full summary of this config's tile kernel
+    (profiles/ncu_full_summary.json, keyed by config; written by scripts/ncu_summary.py)."""
     p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
-    if not os.path.exists(p):
-        return None
     try:
-        d = json.load(open(p)).get(kernel_tag, {})
-        if "dram_bytes_per_sweep" in d:
-            return d["dram_bytes_per_sweep"]
-        return None
+        return json.load(open(p)).get(config)
     except Exception:
         return None
 
 
-def issue_roofline(kernel_tag):
+def ncu_traffic(config):
+    """dram bytes per launch of the tile kernel from this config's committed ncu capture."""
+    d = ncu_entry(config) or {}
+    return d.get("dram_bytes_per_launch")
+
+
+def l2_copy_gbs(torch):
+    """Measured L2 bandwidth for the L2-resident config: torch copy_ between two 16 MiB buffers
+    (both stay in the 126 MB L2), read + write bytes, best of 20 (CUDA events)."""
+    a = torch.empty(16 << 20, dtype=torch.uint8, device="cuda")
+    b = torch.empty_like(a)
+    best = 0.0
+    for _ in range(3):
+        b.copy_(a)
+    for _ in range(20):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(50):
+            b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, 50 * 2 * a.numel() / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
+
+
+def issue_roofline(config):
     """Secondary roofline of the tile kernel, which is issue/ALU-bound: warp instructions issued
     per second in the committed ncu --set full capture against the issue limit of the chip
     (4 SMSPs x 1 warp-instruction/cycle per SM, B300_MICROARCH.md 'Per-warp issue scheduler';
     148 SMs at the captured SM clock)."""
-    p = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
     try:
-        d = json.load(open(p)).get(kernel_tag, {})
+        d = ncu_entry(config) or {}
         inst, ms, clk = d["warp_inst_per_launch"], d["launch_ms"], d["sm_clock_hz"]
         ach = inst / (ms * 1e-3)
         peak = 148 * 4 * clk
@@ -147,8 +169,9 @@ def issue_roofline(kernel_tag):
 
 
 def algorithmic_bytes_per_cell(ndim, tile):
-    """Per launch (in place, 1-cell halo): read each cell's packed word (t, rank, n, s: 8 B)
-    and write it back (8 B), plus the halo words of the tile faces. DESIGN.md 'Roofline'."""
+    """Per sweep (in place, 1-cell halo): read each cell's packed word (t, n, s: 8 B) and write it
+    back (8 B), plus the halo words of the tile faces. DESIGN.md 'Roofline' (the builder's
+    convention; SURVEY.md section 8(d) counts 13 B/cell SoA state instead: SURVEY_BYTES)."""
     if ndim == 2:
         tx, ty = tile[0], tile[1]
         halo = 8.0 * 2 * (tx + ty) / (tx * ty)
@@ -156,6 +179,11 @@ def algorithmic_bytes_per_cell(ndim, tile):
         tx, ty, tz = tile
         halo = 8.0 * 2 * (tx * ty + ty * tz + tx * tz) / (tx * ty * tz)
     return 16.0 + halo
+
+
+# bytes per cell per outer round of the SoA layout it assumed (t, n, s:
+# 13 B read + 13 B written, + 0.56 B tile-halo re-read for 64^2 tiles; 3-D tiles 29.4 B)
+SURVEY_BYTES = {2: 26.6, 3: 29.4}
 
 
 def oracle_sample(cfg, seconds_target=10.0):
@@ -245,6 +273,10 @@ def main():
     ndim = len(dims)
     tile = tuple(int(x) for x in args.tile.split("x")) if args.tile else tuple(cfg["tile"])
     opts = dict(init_q=cfg["init_q"], device=local, tile=tile, event_hash=0 if args.no_hash else 1)
+    if args.shards > 1:
+        if world > 1:
+            raise SystemExit("--shards is a single-process mode (virtual shards on one GPU)")
+        opts["shards"] = args.shards
     opts.update(cfg.get("opts", {}))
     if args.early_reject >= 0:
         opts["early_reject"] = args.early_reject
@@ -272,13 +304,10 @@ def main():
         except aca.AcaError as e:   # e.g. no peer mapping between these GPUs
             failed = 1
             print("rank %d: CUDA-IPC push transport unavailable (%s)" % (rank, e), file=sys.stderr)
-        if adist.reduce_sum_int(failed) > 0:   # every rank switches to the NCCL exchange together
-            sim.close()
-            uid = aca.aca_nccl_unique_id() if rank == 0 else bytes(128)
-            opts.update(nccl_id=adist.broadcast_bytes(uid), halo_mode=1)
-            args.transport = "nccl"
-            sim = aca.Sim(dims, lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
-                          seed=args.seed, **opts)
+        if adist.reduce_sum_int(failed) > 0:
+            # no silent switch of transport: the NCCL exchange is a different (slower) schedule,
+            # so a number measured with it must be asked for explicitly (--transport nccl)
+            raise SystemExit("CUDA-IPC push transport unavailable on some rank; rerun with --transport nccl")
     n_local = aca.aca_num_cells(sim.handle)
 
     def step(seed):
@@ -326,12 +355,22 @@ def main():
     mean_sweep = ks / max(1, launches)
     kl_per_sweep = (kl / max(1, launches * 1.0)) if launches else 1.0
     achieved = (n_local * bpc / mean_sweep) / 1e9 if mean_sweep > 0 else None
-    tag = "tile_kernel_%dd" % ndim
-    traffic = ncu_traffic(tag)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+    tag = "tile_grp_kernel (%d-D)" % ndim
+    traffic = ncu_traffic(args.config)
+    state_bytes = n_local * 8
+    l2_resident = state_bytes * 2 < 64e6          # config 2: 8 MB of state, far below the 126 MB L2
+    if l2_resident:
+        peak, peak_src = l2_copy_gbs(torch), "measured in this run: L2-resident torch copy_ (2 x 16 MiB)"
+    sbytes = SURVEY_BYTES[ndim]
+    achieved_s = (n_local * sbytes / mean_sweep) / 1e9 if mean_sweep > 0 else None
+    roof = {"bound": "l2" if l2_resident else "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "kernel": tag, "peak_source": peak_src,
-            "algorithmic_bytes_per_cell_per_sweep": bpc, "cells_per_sweep": n_local,
+            "algorithmic_bytes_per_cell_per_sweep": bpc,
+            "survey_8d": {"bytes_per_cell_per_sweep": sbytes, "achieved": achieved_s,
+                          "frac": (achieved_s / peak) if achieved_s else None,
+                          "note": "SURVEY.md 8(d) convention (13 B/cell SoA state read + written + tile halo)"},
+            "cells_per_sweep": n_local,
             "mean_sweep_ms": mean_sweep * 1e3, "sweeps_per_step": launches / args.steps,
             "kernel_launches_per_sweep": round(kl_per_sweep, 2),
             "kernel_share_of_step": ks / elapsed if elapsed else None}
@@ -346,10 +385,13 @@ def main():
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
                        "halo_transport": (("cuda-ipc push" if args.transport == "ipc" else "nccl exchange")
                                           if world > 1 else "none (one shard)"),
-                       "l2": "state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (n_local * 12 / 1e9),
+                       "l2": ("state %.1f MB per GPU: L2-resident (roofline against measured L2 bandwidth)" %
+                              (state_bytes / 1e6)) if l2_resident else
+                             ("state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (state_bytes / 1e9)),
+                       "shards": args.shards,
                        "event_hash": not args.no_hash},
             "roofline": roof,
-            "roofline_issue": issue_roofline(tag),
+            "roofline_issue": issue_roofline(args.config),
             "firing_fraction": fired / tested if tested else None,
             "arrivals_per_cell_per_sweep": (fired / launches / n_local) if launches else None,
             "gpu_launches": int(kl + 2 * args.steps),
@@ -361,7 +403,9 @@ def main():
     # is staged while step k runs, and step k's output drains while step k+1 runs.
     if not args.no_e2e:
         import torch as _t
-        host_in = [_t.from_numpy(workloads.host_spins((n_local,), seed=7 + j)).pin_memory() for j in range(2)]
+        # the config's own initial distribution (c5: all +1 but an i.i.d. 5 %)
+        host_in = [_t.from_numpy(workloads.host_spins((n_local,), seed=7 + j, q_minus=cfg["init_q"])).pin_memory()
+                   for j in range(2)]
         host_out = [_t.empty(n_local, dtype=_t.int8).pin_memory() for _ in range(2)]
         e_arr = 0
         if world > 1:
@@ -390,6 +434,14 @@ def main():
         v, arr, dt, sample = oracle_sample(cfg)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                                 "cpu": cpu_name(), "host_cores": os.cpu_count()}
+    uuid = str(torch.cuda.get_device_properties(local).uuid)
+    if world > 1:
+        import torch.distributed as tdist
+        uuids = [None] * world
+        tdist.all_gather_object(uuids, uuid)
+        line["config"]["device_uuids"] = uuids
+    else:
+        line["config"]["device_uuids"] = [uuid]
     if rank == 0:
         print(json.dumps(line), flush=True)
     sim.close()

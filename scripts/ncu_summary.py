@@ -2,7 +2,8 @@
   * the launch list (gpu__time_duration per launch) -> per-kernel totals and shares;
   * an `ncu --set full` capture -> key metrics of the dominant kernel (JSON + markdown),
     and profiles/ncu_full_summary.json (dram bytes per launch, read by bench.py as `traffic`).
-usage: python scripts/ncu_summary.py <tag> <launches.csv> <prof.ncu-rep> [kernel_tag]"""
+usage: python scripts/ncu_summary.py <tag> <launches.csv|-> <prof.ncu-rep> [config] [launches_per_sweep]
+The entry of profiles/ncu_full_summary.json is keyed by the config (c2 .. c5) bench.py measures."""
 import csv
 import io
 import json
@@ -22,6 +23,8 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__grid_size", "launch__block_size", "launch__occupancy_limit_shared_mem",
         "launch__occupancy_limit_registers", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
         "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_bytes.sum", "sm__cycles_elapsed.avg.per_second"]
+STALLS = ["barrier", "wait", "short_scoreboard", "not_selected", "math_pipe_throttle", "long_scoreboard", "mio_throttle",
+          "branch_resolving", "dispatch_stall", "no_instruction", "lg_throttle", "membar", "sleeping"]
 
 
 def launches(path):
@@ -53,6 +56,10 @@ def full(path):
         for k in KEYS:
             if k in hdr:
                 d[k] = r[hdr.index(k)] + " " + units[hdr.index(k)]
+        for st in STALLS:
+            k = "smsp__average_warps_issue_stalled_%s_per_issue_active.ratio" % st
+            if k in hdr:
+                d["stall_" + st] = float(r[hdr.index(k)] or 0)
         res.append(d)
     return res
 
@@ -67,11 +74,11 @@ def num(s):
 
 def main():
     tag, lpath, fpath = sys.argv[1:4]
-    ktag = sys.argv[4] if len(sys.argv) > 4 else "tile_kernel_2d"
+    ktag = sys.argv[4] if len(sys.argv) > 4 else "c3"
     per_sweep = int(sys.argv[5]) if len(sys.argv) > 5 else 2   # kernel launches per sweep (checkerboard: 2)
     d = os.path.join(ROOT, "profiles", tag)
     os.makedirs(d, exist_ok=True)
-    L = launches(lpath)
+    L = launches(lpath) if lpath != "-" else {}
     F = full(fpath)
     json.dump({"launch_list": L, "full_capture": F}, open(os.path.join(d, "ncu_summary.json"), "w"), indent=1)
     with open(os.path.join(d, "ncu_summary.md"), "w") as f:
@@ -85,11 +92,15 @@ def main():
             for k in KEYS:
                 if k in c:
                     f.write("  * %s: %s\n" % (k, c[k]))
+            st = sorted(((k[6:], v) for k, v in c.items() if k.startswith("stall_")), key=lambda kv: -kv[1])
+            if st:
+                f.write("  * stalls (warps per issue): %s\n" % ", ".join("%s %.2f" % kv for kv in st[:8]))
     if F:
         rb = sum(num(c["dram__bytes_read.sum"]) for c in F) / len(F)
         wb = sum(num(c["dram__bytes_write.sum"]) for c in F) / len(F)
         summ = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
         cur = json.load(open(summ)) if os.path.exists(summ) else {}
+        cur = {k: v for k, v in cur.items() if k in ("c1", "c2", "c3", "c4", "c5")}   # round-1 kernel keys retired
         def avg(key):
             vals = [num(c[key]) for c in F if key in c]
             return sum(vals) / len(vals) if vals else None
@@ -106,6 +117,8 @@ def main():
                      "issue_active_pct": avg("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                      "alu_pipe_pct": avg("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
                      "sm_clock_hz": avg("sm__cycles_elapsed.avg.per_second"),
+                     "stalls_per_issue": {k[6:]: round(v, 3) for k, v in F[0].items() if k.startswith("stall_")},
+                     "kernel": F[0]["kernel"][:120],
                      "source": "profiles/%s" % tag}
         json.dump(cur, open(summ, "w"), indent=1)
     print("wrote", d)

@@ -77,6 +77,18 @@ def test_nlog_bit_identical_to_oracle(aca, oracle_mod):
         assert list(d) == want
 
 
+def test_nlog_bit_identical_1e8(aca, oracle_mod):
+    """SURVEY 8(c)'s volume: the device's NLOG-2 (the shared-memory table view the tile kernels use,
+    checked against the interleaved view inside the self-test) equals the oracle's on 10^8 random
+    inputs, in chunks of 10^7."""
+    rng = np.random.default_rng(12)
+    for _ in range(10):
+        X = rng.integers(0, 2 ** 63, size=10 ** 7, dtype=np.uint64) * np.uint64(2) + \
+            rng.integers(0, 2, size=10 ** 7).astype(np.uint64)
+        q, d = aca.aca_selftest_nlog(X)
+        assert np.array_equal(q, oracle_mod.nlog_batch(X))
+
+
 @pytest.mark.parametrize("law", [0, 1, 2, 3])
 def test_law_bit_identical_to_oracle(aca, oracle_mod, law):
     """P3L asynchrony laws: the device's unscaled increment and

@@ -92,6 +92,27 @@ def test_nlog_within_one_unit_of_mpmath(oracle_mod):
     assert worst <= 1.0, worst
 
 
+def test_nlog_within_one_unit_1e7(oracle_mod):
+    """The P3 contract at SURVEY 8(c)'s volume: 10^7 random inputs (plus the edge set), the oracle's
+    q against -ln(x / 2^64) 2^32 evaluated in x87 extended precision (64-bit mantissa: x is exact,
+    the reference's absolute error is ~1e-8 units); the few inputs whose error lies within 1e-6 of
+    the bound are re-checked with mpmath at 50 digits."""
+    rng = np.random.default_rng(11)
+    X = np.concatenate([rng.integers(0, 2 ** 63, size=10 ** 7, dtype=np.uint64) * np.uint64(2) +
+                        rng.integers(0, 2, size=10 ** 7).astype(np.uint64),
+                        np.array(_nlog_inputs(n_random=0), np.uint64)])
+    q = oracle_mod.nlog_batch(X)
+    x = (X | np.uint64(1)).astype(np.longdouble)
+    ref = -np.log(x / np.longdouble(2) ** 64) * np.longdouble(2) ** 32
+    err = np.abs(q.astype(np.longdouble) - ref)
+    border = np.nonzero(err > 1 - 1e-6)[0]
+    for i in border:
+        mpmath.mp.dps = 50
+        assert abs(int(q[i]) - _exact_nlog(int(X[i]))) <= 1, int(X[i])
+    assert float(err.max()) <= 1 + 1e-6
+    assert len(border) < 100
+
+
 def test_nlog_edge_values(oracle_mod):
     assert oracle_mod.nlog_q32((1 << 64) - 1) == 0            # u -> 1: -ln u -> 0, Delta clamps to 1
     assert oracle_mod.delta(0xFFFFFFFF, 0xFFFFFFFF) == 1
