@@ -106,6 +106,8 @@ struct Shard {
     unsigned long long* halo_hi = nullptr;
     unsigned long long* push_lo = nullptr;  // push mode: the lower neighbour's halo_hi
     unsigned long long* push_hi = nullptr;  // ... and the upper neighbour's halo_lo
+    unsigned long long* stats_lo = nullptr; // multi-process: the halos as they were at the end of the last run
+    unsigned long long* stats_hi = nullptr; //   (the bond term of the statistics reads these)
     Ctl* ctl = nullptr;
     size_t n = 0;          // owned cells
     size_t face = 0;       // cells of one row / plane of the sharded axis
@@ -160,7 +162,8 @@ struct aca_sim {
     bool push = false;             // sharded: boundary rows pushed into the neighbours' halos by the kernel
     bool ipc = false;              // multi-process push mode: halos of the neighbour ranks mapped by CUDA IPC
     bool ipc_ready = false;        // aca_ipc_import done
-    unsigned long long* d_slot = nullptr;              // this rank's {epoch, active} (exported)
+    unsigned long long* d_slot = nullptr;              // this rank's {epoch, active, snapshot epoch} (exported)
+    bool snap_valid = false;       // multi-process: stats_lo/hi hold the neighbours' current boundary rows
     std::vector<unsigned long long*> peer_slot;        // every rank's slot (own = d_slot)
     std::vector<void*> ipc_opened;                     // mappings to close in aca_destroy
     uint64_t epoch = 0;
@@ -476,6 +479,8 @@ int check_count(const aca_sim* S, size_t count, const void* p) {
 
 constexpr size_t CHUNK = (size_t)1 << 25;   // cells per getter chunk (256 MB of u64)
 
+int init_peer_halos(aca_sim* S);
+
 // P5 initial state on the device + zeroed control blocks.
 int init_state(aca_sim* S) {
     RoundKeys K;
@@ -488,6 +493,31 @@ int init_state(aca_sim* S) {
     }
     S->T_last = 0;
     S->t_hi = S->max_delta + 1;
+    if (S->ipc && S->shards[0].stats_lo) return init_peer_halos(S);
+    return ACA_OK;
+}
+
+// Multi-process (IPC) handles after a (re)initialisation: the neighbours' boundary rows are
+// their P5 initial states, a function of (seed, cell) alone, so each rank fills its halo buffers
+// (and the statistics' snapshot of them) itself: the P5 kernel on a one-row (one-plane) shard
+// at the neighbour's global offset.
+int init_peer_halos(aca_sim* S) {
+    RoundKeys K;
+    philox_round_keys((uint32_t)(S->seed & 0xffffffffu), (uint32_t)(S->seed >> 32), K.rk);
+    Shard& sh = S->shards[0];
+    const bool d2 = sh.g.ndim == 2;
+    const int n_axis = d2 ? sh.g.NY : sh.g.NZ, a0 = d2 ? sh.g.y0 : sh.g.z0, na = d2 ? sh.g.ny : sh.g.nz;
+    for (int side = 0; side < 2; ++side) {
+        Geo gh = sh.g;
+        const int at = side == 0 ? (a0 - 1 + n_axis) % n_axis : (a0 + na) % n_axis;
+        if (d2) { gh.ny = 1; gh.y0 = at; } else { gh.nz = 1; gh.z0 = at; }
+        unsigned long long* dst = side == 0 ? sh.halo_lo : sh.halo_hi;
+        init_kernel<<<148, 256, 0, S->stream>>>(dst, gh, S->d_lr, K, S->thr_init, S->inv_lambda, S->opt.tie_bits,
+                                                 (unsigned long long)sh.face, S->opt.law);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(side == 0 ? sh.stats_lo : sh.stats_hi, dst, sh.face * 8, cudaMemcpyDeviceToDevice, S->stream));
+    }
+    S->snap_valid = true;
     return ACA_OK;
 }
 
@@ -498,8 +528,15 @@ int device_stats(aca_sim* S) {
     CK(cudaMemcpyAsync(S->d_stat, S->h_stat, sizeof(StatAcc), cudaMemcpyHostToDevice, S->stream));
     int rc = exchange(S);
     if (rc) return rc;
+    if (S->ipc && !S->snap_valid)
+        return fail(ACA_ESTATE, "multi-process statistics after set_state / set_spins need a run_until first "
+                                "(the neighbours' boundary rows are not known yet)");
     for (auto& sh : S->shards) {
         KParams P = make_params(S, sh);
+        if (S->ipc) {   // the neighbours' rows as of the end of the last run (or their P5 state)
+            P.halo_lo = sh.stats_lo;
+            P.halo_hi = sh.stats_hi;
+        }
         stats_kernel<256><<<1184, 256, 0, S->stream>>>(P, S->d_stat, (unsigned long long)sh.n);
         CK(cudaGetLastError());
     }
@@ -578,6 +615,8 @@ void aca_destroy(aca_sim* S) {
         cudaFree(sh.halo_lo);
         cudaFree(sh.halo_hi);
         cudaFree(sh.ctl);
+        cudaFree(sh.stats_lo);
+        cudaFree(sh.stats_hi);
     }
     if (S->comm && nccl().ok) nccl().destroy(S->comm);
     for (void* p : S->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -845,8 +884,12 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (S->ipc && !(S->persistent_ctas > 0 && !S->whole))
         return bail(fail(ACA_EINVAL, "multi-process push mode needs the persistent tile kernel (not sync_rounds)"));
     if (S->ipc) {   // this rank's {epoch, active} slot, read by every rank through CUDA IPC
-        if (cudaMalloc(&S->d_slot, 16) != cudaSuccess) return bail(fail(ACA_ENOMEM, "ipc slot"));
-        if (cudaMemset(S->d_slot, 0, 16) != cudaSuccess) return bail(fail(ACA_ECUDA, "ipc slot"));
+        if (cudaMalloc(&S->d_slot, 32) != cudaSuccess) return bail(fail(ACA_ENOMEM, "ipc slot"));
+        if (cudaMemset(S->d_slot, 0, 32) != cudaSuccess) return bail(fail(ACA_ECUDA, "ipc slot"));
+        Shard& sh0 = S->shards[0];
+        if (cudaMalloc(&sh0.stats_lo, sh0.face * 8) != cudaSuccess || cudaMalloc(&sh0.stats_hi, sh0.face * 8) != cudaSuccess)
+            return bail(fail(ACA_ENOMEM, "stats halo allocation failed"));
+        if (int r = init_peer_halos(S)) return bail(r);
         S->push = true;   // push pointers are set by aca_ipc_import
     }
     if (S->use_nccl) {
@@ -884,6 +927,17 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         // slots); from then on no rank waits for another until termination
         if (!S->ipc_ready) return fail(ACA_ESTATE, "multi-process push mode: call aca_ipc_import first");
         Shard& sh = S->shards[0];
+        // every peer has snapshotted its halos at the end of the previous run before this rank's
+        // boundary rows overwrite them
+        for (int r = 0; r < S->world; ++r) {
+            for (long spins = 0;; ++spins) {
+                unsigned long long v[3];
+                CK(cudaMemcpy(v, S->peer_slot[r], 24, cudaMemcpyDeviceToHost));
+                if (v[2] >= S->epoch) break;
+                if (spins > 20000000) return fail(ACA_ESTATE, "rank %d never finished run %llu", r, (unsigned long long)S->epoch);
+                std::this_thread::sleep_for(std::chrono::microseconds(20));
+            }
+        }
         CK(cudaMemcpyAsync(sh.push_lo, sh.words, sh.face * 8, cudaMemcpyDeviceToDevice, S->stream));
         CK(cudaMemcpyAsync(sh.push_hi, sh.words + (sh.n - sh.face), sh.face * 8, cudaMemcpyDeviceToDevice, S->stream));
         CK(cudaStreamSynchronize(S->stream));
@@ -1001,6 +1055,17 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         bool dummy;
         rc = retire(outstanding, &dummy);
         if (rc) return rc;
+    }
+    if (S->ipc) {
+        // every rank is done, so every boundary row pushed into this rank's halos is final:
+        // snapshot them for the statistics, then let the peers start their next run
+        Shard& sh = S->shards[0];
+        CK(cudaMemcpyAsync(sh.stats_lo, sh.halo_lo, sh.face * 8, cudaMemcpyDeviceToDevice, S->stream));
+        CK(cudaMemcpyAsync(sh.stats_hi, sh.halo_hi, sh.face * 8, cudaMemcpyDeviceToDevice, S->stream));
+        CK(cudaStreamSynchronize(S->stream));
+        const unsigned long long snap = S->epoch;
+        CK(cudaMemcpy(S->d_slot + 2, &snap, 8, cudaMemcpyHostToDevice));
+        S->snap_valid = true;
     }
     CK(cudaEventRecord(S->ev1, S->stream));
     CK(cudaEventSynchronize(S->ev1));
@@ -1151,6 +1216,7 @@ int aca_get_stats(aca_sim* S, aca_stats* o) {
 int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const uint32_t* counters, size_t count) {
     int rc = check_count(S, count, spins);
     if (rc) return rc;
+    if (S->ipc) S->snap_valid = false;   // the neighbours' boundary rows are unknown until a run
     if (!times || !counters) return fail(ACA_EINVAL, "null times/counters");
     CK(cudaSetDevice(S->device));
     uint64_t tmax = 0;
@@ -1195,6 +1261,7 @@ int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const 
 int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
     int rc = check_count(S, count, spins);
     if (rc) return rc;
+    if (S->ipc) S->snap_valid = false;   // the neighbours' boundary rows are unknown until a run
     CK(cudaSetDevice(S->device));
     rc = ensure_scratch(S, CHUNK);
     if (rc) return rc;
@@ -1246,6 +1313,7 @@ int aca_stage_spins(aca_sim* S, const int8_t* spins, size_t count, int slot) {
 
 int aca_set_spins_staged(aca_sim* S, int slot) {
     if (!S) return fail(ACA_EINVAL, "null handle");
+    if (S->ipc) S->snap_valid = false;
     if (slot < 0 || slot > 1) return fail(ACA_EINVAL, "slot must be 0 or 1");
     if (!S->cstream) return fail(ACA_ESTATE, "nothing staged (call aca_stage_spins first)");
     CK(cudaSetDevice(S->device));

@@ -38,14 +38,16 @@ def _worker(rank, world, port, q, dims, Ts, kw):
         torch.cuda.set_device(0)
         sim = aca.Sim(dims, world=world, rank=rank, device=0, **kw)
         adist.ipc_connect(sim.handle)
+        st0 = sim.stats()            # right after create: the halos hold the neighbours' P5 rows
         for T in Ts:
             sim.run_until(T)
         st = sim.stats()
-        q.put((rank, sim.spins().copy(), sim.times().copy(), sim.counters().copy(), st["cells_fired"], None))
+        q.put((rank, sim.spins().copy(), sim.times().copy(), sim.counters().copy(), st["cells_fired"], None,
+               {k: st0[k] for k in ("bond_sum", "class_hist")}, {k: st[k] for k in ("bond_sum", "class_hist")}))
         dist.barrier()   # keep the mappings alive until every rank has read its result
         sim.close()
     except Exception as e:  # report instead of hanging the parent
-        q.put((rank, None, None, None, 0, repr(e)))
+        q.put((rank, None, None, None, 0, repr(e), None, None))
     finally:
         dist.destroy_process_group()
 
@@ -67,6 +69,7 @@ def _run_world(dims, Ts, world=2, **kw):
     for r in res:
         assert r[5] is None, r[5]
     cat = lambda i: np.concatenate([r[i].reshape(-1) for r in res]).reshape(tuple(dims)[::-1])
+    _run_world.stats = [(r[6], r[7]) for r in res]   # per rank: (after create, after the runs)
     return cat(1), cat(2), cat(3), sum(r[4] for r in res)
 
 
@@ -77,8 +80,12 @@ def test_ipc_push_two_processes(oracle_mod, dims, beta, tile):
     Ts = [1.0, 3.0, 5.0]
     s, t, n, fired = _run_world(dims, Ts, beta=beta, seed=61, tile=tile)
     o = oracle_mod.OracleSim(dims, lam=1.0, beta=beta, J=1.0, h=0.0, rule=0, seed=61, init_q=0.5)
+    # statistics read the neighbours' boundary rows: right after create (their P5 rows) and after
+    # the runs (the snapshot taken when every rank was done); the bond sums add up exactly
+    assert sum(a["bond_sum"] for a, _ in _run_world.stats) == o.stats()["bond_sum"]
     for T in Ts:
         o.run_until(T)
+    assert sum(b["bond_sum"] for _, b in _run_world.stats) == o.stats()["bond_sum"]
     assert np.array_equal(s, o.spins())
     assert np.array_equal(t, o.times())
     assert np.array_equal(n, o.counters())
