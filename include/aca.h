@@ -273,6 +273,18 @@ int aca_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J
  * Errors: ACA_EINVAL (arguments), ACA_ENOMEM, ACA_ENODEV, ACA_ECUDA. */
 int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                        uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds);
+/* fig:perfbl model (docs/PRIMITIVES.md P11): the simplified many-cells-per-PE model of
+ * PAPER.md:1491-1546 (Eq. hC) on a px x py torus of PEs, each carrying an m x m subarray, in the
+ * reading where a blocked PE keeps its selected cell (fig:amcpoi Steps 2-3),
+ * with the lag bound of fig:perfbl in units of a cell's mean inter-arrival
+ * time (lag 0 = unbounded). ups[r] (caller-owned, `rounds` entries) = PEs that advanced in round
+ * r; the efficiency (Eq. effi) is their mean over PEs. Optional h_out (u64[px py], Q32) and n_out
+ * (u32[px py]): the final state. device < 0: the current device. ACA_EINVAL on bad arguments
+ * (1 <= px py <= 2^24, 2 <= m <= 65535), ACA_ENODEV without a GPU. Bit-identical to the
+ * oracle's oracle_perfbl_run. */
+int aca_perfbl_run(int64_t px, int64_t py, int m, double lag, uint64_t seed, int64_t rounds, uint64_t* ups,
+                   uint64_t* h_out, uint32_t* n_out, int device);
+
 /* The same with the q-th degree neighbourhood neighbors^q (Eq. neiq: all
  * cells within Manhattan distance q, |neighbors^q| - 1 = 2q(q+1) on the square array), q in
  * [1, 8]; aca_efficiency_run is q = 1. */

@@ -114,6 +114,8 @@ def lib():
                                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.POINTER(Stats)]
         L.oracle_bkl_run.argtypes = L.oracle_agg_run.argtypes
+        L.oracle_perfbl_run.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
+                                         ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_efficiency_run_q.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
                                               ctypes.c_double, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int,
                                               ctypes.c_void_p, ctypes.c_void_p]
@@ -294,6 +296,20 @@ def efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False,
                                        t.ctypes.data if want_times else None)
     assert rc == 0
     return (fired, t) if want_times else fired
+
+
+def perfbl_run(px, py, m, rounds, lag=0.0, seed=1):
+    """fig:perfbl model (docs/PRIMITIVES.md P11): PEs that advanced
+    in each round, final h (Q32) and n. lag in units of a cell's mean inter-arrival time
+    (0 = unbounded)."""
+    N = int(px) * int(py)
+    ups = np.zeros(rounds, np.uint64)
+    hh = np.zeros(N, np.uint64)
+    nn = np.zeros(N, np.uint32)
+    rc = lib().oracle_perfbl_run(px, py, m, to_q32(lag) if lag else 0, seed, rounds, ups.ctypes.data, hh.ctypes.data,
+                                 nn.ctypes.data)
+    assert rc == 0
+    return ups, hh, nn
 
 
 def agg_run(dims, m, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1, init_q=0.5, bkl=False):

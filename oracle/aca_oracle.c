@@ -634,6 +634,72 @@ int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda,
     return oracle_efficiency_run_q(ndim, dims, law, lambda, seed, rounds, 1, fired_per_round, t_out);
 }
 
+/* ---------------------------------------------------------------- fig:perfbl model (P11)
+ * The simplified many-cells-per-PE model of PAPER.md:1491-1546 (Eq. hC), in the reading where a
+ * PE that selected a cell keeps it while blocked (fig:amcpoi Steps 2-3), with
+ * the lag bound of PAPER.md:1573-1605. A px x py torus of PEs; PE C (= y px + x) holds h(C) (Q32)
+ * and n(C). Its event n uses the draw (w0..w3) = Philox ctr (n, C, 0, 7): category 0 (the cell
+ * has no outside neighbour, probability (m-2)^2/m^2) iff w0 < E1, category 1 (an edge cell,
+ * 4(m-2)/m^2) iff E1 <= w0 < E2, else category 2 (a corner, 4/m^2), with
+ * E1 = floor((m-2)^2 2^32 / m^2), E2 = floor((m^2-4) 2^32 / m^2); neighbour directions
+ * a = w1 >> 30 and b = (a + 1 + (((w1 & 0xffff) * 3) >> 16)) & 3 (0 -x, 1 +x, 2 -y, 3 +y); the
+ * increment max(1, NLOG-2((w2 << 32) | w3)) (Exp(1) in Q32: h = lambda T, time measured in
+ * units of a cell's mean inter-arrival time, the unit of the lag in fig:perfbl). h0(C) = the
+ * increment of the draw ctr (0, C, 0, 8). A round reads one snapshot hs of every h: hmin = min
+ * hs; PE C advances (h = hs(C) + increment, n += 1) iff (lag = 0 or hs(C) < hmin + lag) and every
+ * neighbour its category checks (a; a and b) has hs(C') >= hs(C) (Eq. hC conditions (i)-(iii));
+ * otherwise it keeps its event. ups[r] = PEs that advanced in round r: the efficiency is their
+ * mean over PEs (Eq. effi). Plain loops; test infrastructure only. 0, or -1 on bad arguments. */
+int oracle_perfbl_run(int64_t px, int64_t py, int m, uint64_t lag_q32, uint64_t seed, int64_t rounds, uint64_t* ups,
+                      uint64_t* h_out, uint32_t* n_out) {
+    if (px < 1 || py < 1 || m < 2 || m > 65535 || rounds < 0) return -1;
+    const int64_t N = px * py;
+    const uint64_t mm = (uint64_t)m * (uint64_t)m;
+    const uint64_t E1 = ((uint64_t)(m - 2) * (uint64_t)(m - 2) << 32) / mm, E2 = ((mm - 4) << 32) / mm;
+    const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint64_t* h = (uint64_t*)malloc((size_t)N * 8);
+    uint64_t* hs = (uint64_t*)malloc((size_t)N * 8);
+    uint32_t* n = (uint32_t*)calloc((size_t)N, 4);
+    if (!h || !hs || !n) { free(h); free(hs); free(n); return -1; }
+    for (int64_t C = 0; C < N; C++) {
+        uint32_t ctr[4] = {0, (uint32_t)C, (uint32_t)((uint64_t)C >> 32), 8u}, w[4];
+        oracle_philox4x32_10(ctr, key, w);
+        uint64_t d = oracle_nlog_q32(((uint64_t)w[2] << 32) | w[3]);
+        h[C] = d < 1 ? 1 : d;
+    }
+    for (int64_t r = 0; r < rounds; r++) {
+        memcpy(hs, h, (size_t)N * 8);
+        uint64_t hmin = hs[0], cnt = 0;
+        for (int64_t C = 1; C < N; C++) hmin = hs[C] < hmin ? hs[C] : hmin;
+        for (int64_t C = 0; C < N; C++) {
+            if (lag_q32 && hs[C] - hmin >= lag_q32) continue;          /* beyond the lag window */
+            uint32_t ctr[4] = {n[C], (uint32_t)C, (uint32_t)((uint64_t)C >> 32), 7u}, w[4];
+            oracle_philox4x32_10(ctr, key, w);
+            const int cat = (uint64_t)w[0] < E1 ? 0 : ((uint64_t)w[0] < E2 ? 1 : 2);
+            const int a = (int)(w[1] >> 30), b = (a + 1 + (int)(((w[1] & 0xffffu) * 3u) >> 16)) & 3;
+            const int64_t x = C % px, y = C / px;
+            int64_t nb[4];
+            nb[0] = y * px + (x + px - 1) % px;
+            nb[1] = y * px + (x + 1) % px;
+            nb[2] = ((y + py - 1) % py) * px + x;
+            nb[3] = ((y + 1) % py) * px + x;
+            int go = 1;
+            if (cat >= 1 && hs[nb[a]] < hs[C]) go = 0;
+            if (cat == 2 && hs[nb[b]] < hs[C]) go = 0;
+            if (!go) continue;
+            uint64_t d = oracle_nlog_q32(((uint64_t)w[2] << 32) | w[3]);
+            h[C] = hs[C] + (d < 1 ? 1 : d);
+            n[C] += 1;
+            cnt++;
+        }
+        if (ups) ups[r] = cnt;
+    }
+    if (h_out) memcpy(h_out, h, (size_t)N * 8);
+    if (n_out) memcpy(n_out, n, (size_t)N * 4);
+    free(h); free(hs); free(n);
+    return 0;
+}
+
 /* q-th degree neighbourhood (Eq. neiq): neighbors^q(c) =
  * neighbors(neighbors^(q-1)(c)), i.e. every cell within Manhattan distance q; a cell passes the
  * test when its (t, c) is below all of them. q = 1 is the model above. */

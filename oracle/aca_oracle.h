@@ -98,6 +98,11 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
                            int64_t radius, int refine, int8_t* s_out, uint64_t* t_out, uint32_t* n_out,
                            int* exact_out, int law);
 
+/* fig:perfbl model (docs/PRIMITIVES.md P11): rounds of the simplified many-cells-per-PE model
+ * with a lag bound (0 = unbounded). ups[rounds]. */
+int oracle_perfbl_run(int64_t px, int64_t py, int m, uint64_t lag_q32, uint64_t seed, int64_t rounds, uint64_t* ups,
+                      uint64_t* h_out, uint32_t* n_out);
+
 /* Time-only efficiency model: synchronous iterations on local times,
  * ndim 1..3, law P3L. fired_per_round[rounds] (N0 per iteration) and t_out[N] may be NULL. */
 int oracle_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,

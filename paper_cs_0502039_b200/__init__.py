@@ -121,6 +121,8 @@ def lib():
     L.aca_run_frames.argtypes = [vp, ctypes.c_double, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]
     L.aca_efficiency_run.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
                                      ctypes.c_int64, vp, vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    L.aca_perfbl_run.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_uint64,
+                                 ctypes.c_int64, vp, vp, vp, ctypes.c_int]
     L.aca_selftest_law.argtypes = [ctypes.c_uint64, vp, ctypes.c_int, ctypes.c_uint64, ctypes.c_int, vp, vp]
     _lib = L
     return L
@@ -355,6 +357,17 @@ def aca_run_frames(p, dt, K0, count, B=4):
     _check(lib().aca_run_frames(p, float(dt), int(K0), int(count), int(B), _ptr(bits)))
     pm = np.unpackbits(bits.reshape(count, fb), axis=1, bitorder="little")[:, :n]
     return np.where(pm > 0, 1, -1).astype(np.int8)
+
+
+def aca_perfbl_run(px, py, m, rounds, lag=0.0, seed=1, device=-1):
+    """fig:perfbl model on the GPU (include/aca.h aca_perfbl_run): (ups per round, h, n)."""
+    n = int(px) * int(py)
+    ups = np.zeros(max(rounds, 1), np.uint64)
+    hh = np.zeros(n, np.uint64)
+    nn = np.zeros(n, np.uint32)
+    _check(lib().aca_perfbl_run(px, py, m, float(lag), seed, rounds, ups.ctypes.data, hh.ctypes.data, nn.ctypes.data,
+                                device))
+    return ups[:rounds], hh, nn
 
 
 def aca_efficiency_run(dims, rounds, law=POISSON, lam=1.0, seed=1, want_times=False, device=-1, q=1):

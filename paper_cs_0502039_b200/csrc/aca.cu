@@ -1470,6 +1470,41 @@ int aca_selftest_nlog(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* delt
     return ACA_OK;
 }
 
+// ---------------------------------------------------------------- fig:perfbl model (P11)
+int aca_perfbl_run(int64_t px, int64_t py, int m, double lag, uint64_t seed, int64_t rounds, uint64_t* ups,
+                   uint64_t* h_out, uint32_t* n_out, int device) {
+    if (px < 1 || py < 1 || px * py > ((int64_t)1 << 24)) return fail(ACA_EINVAL, "PE grid must have 1 .. 2^24 PEs");
+    if (m < 2 || m > 65535) return fail(ACA_EINVAL, "m must be in [2, 65535]");
+    if (!(lag >= 0) || !std::isfinite(lag)) return fail(ACA_EINVAL, "lag must be >= 0 (0 = unbounded)");
+    if (rounds < 0 || (rounds > 0 && !ups)) return fail(ACA_EINVAL, "bad rounds / null ups");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
+    if (device >= 0) CK(cudaSetDevice(device));
+    const int64_t N = px * py;
+    PerfblParams A{};
+    A.px = (int)px; A.py = (int)py;
+    const unsigned long long mm = (unsigned long long)m * (unsigned long long)m;
+    A.E1 = ((unsigned long long)(m - 2) * (unsigned long long)(m - 2) << 32) / mm;
+    A.E2 = ((mm - 4) << 32) / mm;
+    A.lag = lag > 0 ? (unsigned long long)std::floor(lag * 4294967296.0 + 0.5) : 0ull;
+    philox_round_keys((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), A.rk);
+    A.rounds = rounds;
+    unsigned long long* dlr = nullptr;
+    CK(cudaMalloc(&A.hb, (size_t)N * 16));
+    CK(cudaMalloc(&A.n, (size_t)N * 4));
+    CK(cudaMalloc(&A.ups, (size_t)(rounds > 0 ? rounds : 1) * 8));
+    CK(cudaMalloc(&dlr, sizeof(ACA_NLOG_LR)));
+    CK(cudaMemcpy(dlr, ACA_NLOG_LR, sizeof(ACA_NLOG_LR), cudaMemcpyHostToDevice));
+    perfbl_kernel<1024><<<1, 1024>>>(A, dlr);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    if (rounds > 0) CK(cudaMemcpy(ups, A.ups, (size_t)rounds * 8, cudaMemcpyDeviceToHost));
+    if (h_out) CK(cudaMemcpy(h_out, A.hb + (size_t)(rounds & 1) * N, (size_t)N * 8, cudaMemcpyDeviceToHost));
+    if (n_out) CK(cudaMemcpy(n_out, A.n, (size_t)N * 4, cudaMemcpyDeviceToHost));
+    cudaFree(A.hb); cudaFree(A.n); cudaFree(A.ups); cudaFree(dlr);
+    return ACA_OK;
+}
+
 // ---------------------------------------------------------------- time-only efficiency model
 int aca_efficiency_run(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                        uint64_t* fired_per_round, uint64_t* t_out, int device, double* gpu_seconds) {

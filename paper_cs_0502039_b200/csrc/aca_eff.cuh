@@ -298,4 +298,91 @@ __global__ void __launch_bounds__(EFF_W) eff_round_kernel_2d(const unsigned long
     }
 }
 
+// ------------------------------------------------------------ fig:perfbl model (P11)
+// The simplified many-cells-per-PE model with the lag bound of fig:perfbl
+// (PAPER.md:1573-1605), docs/PRIMITIVES.md P11: a PE that selected a cell keeps it while blocked
+// (fig:amcpoi Steps 2-3), so its pending event is a function of its counter
+// alone. One CTA runs every round: the round reads the snapshot buffer hb[r & 1] and writes
+// hb[(r + 1) & 1]; a block reduction gives the snapshot's minimum for the lag window.
+struct PerfblParams {
+    int px, py;
+    unsigned long long E1, E2;          // category thresholds (floor((m-2)^2 2^32 / m^2), floor((m^2-4) 2^32 / m^2))
+    unsigned long long lag;             // Q32, 0 = unbounded
+    uint32_t rk[20];
+    long long rounds;
+    unsigned long long* hb;             // 2 x N
+    unsigned int* n;                    // N
+    unsigned long long* ups;            // rounds
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) perfbl_kernel(const PerfblParams A, const unsigned long long* __restrict__ lr_g) {
+    __shared__ unsigned long long lr[512];
+    __shared__ unsigned long long red[NT / 32];
+    __shared__ unsigned long long bmin;
+    for (int i = threadIdx.x; i < 512; i += NT) lr[i] = lr_g[i];
+    const int N = A.px * A.py;
+    for (int C = threadIdx.x; C < N; C += NT) {
+        const u32x4 r = philox4x32_10_rk(0u, (uint32_t)C, 0u, 8u, A.rk);
+        const uint64_t d = nlog_q32(((uint64_t)r.z << 32) | r.w, lr_g, ACA_LN2_Q48);
+        A.hb[C] = d < 1 ? 1 : d;
+        A.n[C] = 0u;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (long long r = 0; r < A.rounds; ++r) {
+        const unsigned long long* hs = A.hb + (size_t)(r & 1) * N;
+        unsigned long long* hn = A.hb + (size_t)((r + 1) & 1) * N;
+        unsigned long long mn = ~0ull;
+        for (int C = threadIdx.x; C < N; C += NT) mn = min(mn, hs[C]);
+        for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        if (lane == 0) red[warp] = mn;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long m2 = red[0];
+            for (int w = 1; w < NT / 32; ++w) m2 = min(m2, red[w]);
+            bmin = m2;
+        }
+        __syncthreads();
+        const unsigned long long hmin = bmin;
+        unsigned long long cnt = 0;
+        for (int C = threadIdx.x; C < N; C += NT) {
+            const unsigned long long h = hs[C];
+            unsigned long long out = h;
+            if (!(A.lag && h - hmin >= A.lag)) {
+                const unsigned int k = A.n[C];
+                const u32x4 w = philox4x32_10_rk(k, (uint32_t)C, 0u, 7u, A.rk);
+                const int cat = (unsigned long long)w.x < A.E1 ? 0 : ((unsigned long long)w.x < A.E2 ? 1 : 2);
+                const int a = (int)(w.y >> 30), b = (a + 1 + (int)(((w.y & 0xffffu) * 3u) >> 16)) & 3;
+                const int x = C % A.px, y = C / A.px;
+                auto nbr = [&](int dir) {
+                    const int xx = dir == 0 ? (x == 0 ? A.px - 1 : x - 1) : dir == 1 ? (x == A.px - 1 ? 0 : x + 1) : x;
+                    const int yy = dir == 2 ? (y == 0 ? A.py - 1 : y - 1) : dir == 3 ? (y == A.py - 1 ? 0 : y + 1) : y;
+                    return hs[yy * A.px + xx];
+                };
+                bool go = true;
+                if (cat >= 1 && nbr(a) < h) go = false;
+                if (cat == 2 && nbr(b) < h) go = false;
+                if (go) {
+                    const uint64_t d = nlog_q32(((uint64_t)w.z << 32) | w.w, lr, ACA_LN2_Q48);
+                    out = h + (d < 1 ? 1 : d);
+                    A.n[C] = k + 1;
+                    ++cnt;
+                }
+            }
+            hn[C] = out;
+        }
+        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        __syncthreads();                                   // red[] is reused
+        if (lane == 0) red[warp] = cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long s2 = 0;
+            for (int w = 0; w < NT / 32; ++w) s2 += red[w];
+            A.ups[r] = s2;
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace aca

@@ -61,3 +61,15 @@ def test_efficiency_2d_streaming_kernel(aca, oracle_mod, dims):
     f_g, t_g, _ = aca.aca_efficiency_run(dims, 60, law=1, seed=43, want_times=True)
     f_o, t_o = oracle_mod.efficiency_run(dims, 60, law=1, seed=43, want_times=True)
     assert np.array_equal(f_g, f_o) and np.array_equal(t_g, t_o)
+
+
+@pytest.mark.parametrize("px,py,m,lag,rounds", [(5, 5, 24, 0.0, 3000), (32, 32, 12, 0.3, 1500), (32, 32, 12, 16.0, 1500),
+                                               (7, 3, 2, 0.0, 500), (100, 100, 100, 0.0, 300), (1, 1, 12, 0.0, 50),
+                                               (6, 5, 12, 1.0 / 2 ** 32, 400)])
+def test_perfbl_model_bit_identical_to_oracle(aca, oracle_mod, px, py, m, lag, rounds):
+    """fig:perfbl model (P11): the GPU's per-round advance counts and final (h, n) equal the
+    oracle's, including the paper's configurations (25 PEs / m = 24; 1024 PEs / m = 12 with a lag
+    bound; 10^4 PEs / m = 100)."""
+    ug, hg, ng = aca.aca_perfbl_run(px, py, m, rounds, lag=lag, seed=4)
+    uo, ho, no = oracle_mod.perfbl_run(px, py, m, rounds, lag=lag, seed=4)
+    assert np.array_equal(ug, uo) and np.array_equal(hg, ho) and np.array_equal(ng, no)
