@@ -24,7 +24,7 @@ EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
            "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q", "aca_ipc_export", "aca_ipc_import",
-           "aca_stage_spins", "aca_set_spins_staged", "aca_get_spins_async", "aca_sync"]
+           "aca_stage_spins", "aca_set_spins_staged", "aca_get_spins_async", "aca_sync", "aca_perfbl_run"]
 ACA_IPC_BLOB_BYTES = 192
 DEFAULT_ROUNDS = 5   # in-tile rounds per tile visit when aca_options.rounds_per_launch = 0 (aca.cu)
 POISSON, UNIFORM, ROOT8, GAUSS = 0, 1, 2, 3   # asynchrony laws (aca_options.law)
