@@ -103,6 +103,13 @@ typedef struct {
                                    CTA per SM). Small caps make every CTA cycle many tiles
                                    through its buffer ring (tests of that path on small
                                    lattices). Same results. */
+    double lag;                 /* > 0: bounded lag: a launch fires only
+                                   arrivals below min(T, t_min + lag/lambda), t_min the minimum
+                                   pending time when the launch starts (per shard after the first
+                                   launch of a run_until), lag in units of a cell's mean
+                                   inter-arrival time 1/lambda. A scheduling
+                                   bound only: same results; 0 (default) = unbounded. Not with
+                                   multi-process handles. */
 } aca_options;
 
 typedef struct {

@@ -45,7 +45,8 @@ class aca_options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("event_hash", ctypes.c_int32),
                 ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("early_reject", ctypes.c_int32), ("checkerboard", ctypes.c_int32),
-                ("law", ctypes.c_int32), ("halo_mode", ctypes.c_int32), ("max_ctas", ctypes.c_int32)]
+                ("law", ctypes.c_int32), ("halo_mode", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
+                ("lag", ctypes.c_double)]
 
 
 class aca_stats(ctypes.Structure):

@@ -128,6 +128,7 @@ struct aca_sim {
     int NB = 1, TB = 1;            // packed word: counter bits, time bits (+1 spin bit)
     uint64_t t_hi = 0;             // exclusive upper bound of every stored time (Q32)
     bool sync_debug = false;       // ACA_SYNC_DEBUG=1: synchronise after every tile launch
+    unsigned long long lag_q = 0;  // bounded lag (aca_options.lag / lambda) in Q32; 0 = off
     unsigned long long* h_trace = nullptr;   // ACA_TRACE_FROM=n (debug builds): host-mapped stage trace
     unsigned long long* h_dbg = nullptr;     // ACA_SYNC_DEBUG (debug builds): host-mapped failed-check record
     long long trace_from = -1;
@@ -316,6 +317,7 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     P.early = S->opt.early_reject;
     P.bulk = S->bulk;
     P.halo_peer = S->ipc ? 1 : 0;
+    P.lag_q = (S->whole || S->sync) ? 0ull : S->lag_q;
     P.dbg_trace = nullptr;
     P.dbg_map = nullptr;
     if (S->h_dbg) {
@@ -683,6 +685,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     if (opt.variant != 0)
         return fail(ACA_EINVAL, "variant must be 0 (the kernel ablations of round 1 were retired; DESIGN.md section 6)");
     if (opt.max_ctas < 0) return fail(ACA_EINVAL, "max_ctas must be >= 0");
+    if (!(opt.lag >= 0) || !std::isfinite(opt.lag)) return fail(ACA_EINVAL, "lag must be >= 0 and finite (0 = off)");
 
     int64_t N = 1;
     for (int a = 0; a < ndim; ++a) {
@@ -733,6 +736,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
 
     // P3 constants, P4 table, P5 threshold, packed-word layout
     S->inv_lambda = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
+    if (opt.lag > 0) S->lag_q = std::max(1ull, (unsigned long long)std::floor(opt.lag / lambda * 4294967296.0 + 0.5));
     flip_table(ndim, beta, J, h, rule, S->thr);
     early_table(ndim, S->thr, opt.early_reject != 0, S->thm);
     S->bulk = 1;   // one committed arrival per cell per fire step: longer in-thread chains
@@ -915,10 +919,28 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
     S->T_last = Tq;
     S->t_hi = std::max<uint64_t>(S->t_hi, Tq + S->max_delta);   // every time the run can store
     const int TSH = S->NB + 1;
+    // bounded lag: the first launch fires below min(T, global minimum time + lag); the tile
+    // kernels then move the bound with the minimum (finish_launch). The minimum over all shards.
+    unsigned long long wfirst = (unsigned long long)Tq << TSH, wmin0 = ~0ull;
+    if (S->lag_q && !S->whole && !S->sync) {
+        if (S->ipc) return fail(ACA_EINVAL, "the lag window is a single-process option");
+        rc = device_stats(S);
+        if (rc) return rc;
+        const unsigned long long tmin = S->h_stat->tmin;
+        if (tmin != ~0ull) {
+            wmin0 = tmin << TSH;
+            if (tmin + S->lag_q < Tq) wfirst = (tmin + S->lag_q) << TSH;
+        }
+    }
     for (size_t i = 0; i < S->shards.size(); ++i) {
-        S->h_ctl[i].wlim = (unsigned long long)Tq << TSH;
-        CK(cudaMemcpyAsync(&S->shards[i].ctl->wlim, &S->h_ctl[i].wlim, sizeof(unsigned long long),
-                           cudaMemcpyHostToDevice, S->stream));
+        Ctl& h = S->h_ctl[i];
+        h.wlim = wfirst;
+        h.wlim_T = (unsigned long long)Tq << TSH;
+        h.wmin[0] = h.wmin[1] = wmin0;
+        CK(cudaMemcpyAsync(&S->shards[i].ctl->wlim, &h.wlim, sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                           S->stream));
+        CK(cudaMemcpyAsync(&S->shards[i].ctl->wlim_T, &h.wlim_T, 3 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                           S->stream));
         CK(cudaMemsetAsync(&S->shards[i].ctl->done, 0, sizeof(unsigned int), S->stream));
     }
     if (S->ipc) {

@@ -78,6 +78,10 @@ struct Ctl {                            // device control block, one per shard
     unsigned long long active_carry;    // checkerboard: active cells of the phase-0 tiles
     unsigned int dbg_line, dbg_pad;     // ACA_DEBUG builds: first failed device check
     unsigned long long dbg_a, dbg_b;
+    // bounded lag (aca_options.lag): the firing limit wlim of the next launch
+    // is min(T, global minimum time + lag); wlim_T keeps T (termination counts cells below it)
+    unsigned long long wlim_T;
+    unsigned long long wmin[2];         // minimum word of the tiles of each colour at their last write-back
 };
 
 struct Geo {
@@ -175,6 +179,7 @@ struct KParams {
     FrameParams fr;                      // output frames (off unless aca_run_frames)
     int fast;                            // fire_fast applies (law 0, lambda 1, no ties, no frames, N < 2^32)
     int life;                            // rule 2: asynchronous Game of Life (Moore neighbourhood, P10)
+    unsigned long long lag_q;            // bounded lag in Q32 (0 = off)
     unsigned long long* dbg_trace;       // ACA_DEBUG: host-mapped stage trace (nullptr = off)
     unsigned long long* dbg_map;         // ACA_DEBUG: host-mapped record of the first failed check
 };
@@ -344,7 +349,8 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
 // termination is decided) with phase 1.
 __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long active, unsigned long long fired,
                                               unsigned long long flips, unsigned long long tested,
-                                              unsigned long long hash, unsigned int rounds, int phase = -1) {
+                                              unsigned long long hash, unsigned int rounds, int phase = -1,
+                                              unsigned long long lag_q = 0, int tsh = 0) {
     atomicAdd(&ctl->active_accum, active);
     if (fired) atomicAdd(&ctl->fired, fired);
     if (flips) atomicAdd(&ctl->flips, flips);
@@ -367,6 +373,14 @@ __device__ __forceinline__ void finish_launch(Ctl* ctl, unsigned long long activ
             ctl->launches += 1ull;
         }
         ctl->rounds_max = 0u;
+        if (lag_q) {   // next launch: fire only below (global minimum time + lag), and below T
+            const int q = phase < 0 ? 0 : phase;
+            const unsigned long long wm = phase < 0 ? ctl->wmin[0] : min(ctl->wmin[0], ctl->wmin[1]);
+            const unsigned long long tl = (wm >> tsh) + lag_q;
+            const unsigned long long wl = tl < (ctl->wlim_T >> tsh) ? tl << tsh : ctl->wlim_T;
+            ctl->wlim = wl;
+            ctl->wmin[phase < 0 ? 0 : 1 - q] = ~0ull;   // recomputed by the launch that comes next
+        }
         __threadfence();
         ctl->ticket = 0u;
     }

@@ -553,7 +553,9 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     const uint32_t thr_a = smem_u32(thr);
 
     auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3 ? 1 : 0)) * SXY + (ly + 1) * SX + lx + 2; };
-    const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;
+    const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;      // firing limit
+    const unsigned long long wlimT = *(volatile unsigned long long*)&P.ctl->wlim_T;   // T (termination)
+    unsigned long long wmin = ~0ull;   // bounded lag: the minimum word this CTA writes back
     // work items: every tile (phase < 0), or the tiles of one checkerboard colour: item k is
     // column pair j = k % hx of tile row k / hx, tx = 2j + ((row parity + phase) & 1)
     const int hx = (P.tiles_x + 1) >> 1;
@@ -771,7 +773,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                     const ulonglong2 v = lds128v(&S[slot(lx, ly, lz)]);
                     ACA_CHECK(gi + 1 < (size_t)g.nx * g.ny * g.nz, gi, oo);
                     *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
-                    active += (v.x < wlim) + (v.y < wlim);
+                    active += (v.x < wlimT) + (v.y < wlimT);
+                    if (P.lag_q) wmin = min(wmin, min(v.x, v.y));
                     if (P.push_lo) {
                         const int a = NDIM == 2 ? o.y0 + ly : o.z0 + lz, n = NDIM == 2 ? g.ny : g.nz;
                         if (a == 0 || a == n - 1) {
@@ -791,7 +794,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                         const unsigned long long w = S[slot(lx, ly, lz)];
                         P.words[gi] = w;
                         push_word(P, gx, gy, gz, w);
-                        active += w < wlim;
+                        active += w < wlimT;
+                        if (P.lag_q) wmin = min(wmin, w);
                     }
                 }
             }
@@ -810,11 +814,16 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     }
     ACA_TRACE(8, 0);
     __syncthreads();
+    if (P.lag_q) {   // one atomic per warp into this colour's minimum
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+        if (lane == 0 && wmin != ~0ull) atomicMin(&P.ctl->wmin[P.phase > 0 ? 1 : 0], wmin);
+    }
     const unsigned long long s_act = block_sum<NT>((unsigned long long)active, red);
     tot.fold(st);
     const unsigned long long s_fir = block_sum<NT>(tot.fired, red);
     const unsigned long long s_flp = block_sum<NT>(tot.flips, red);
     const unsigned long long s_tst = block_sum<NT>(tot.tested, red);
     const unsigned long long s_hsh = block_sum<NT>(st.hacc, red);
-    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase);
+    if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase, P.lag_q, g.TSH);
 }

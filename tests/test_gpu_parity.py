@@ -159,6 +159,39 @@ def test_buffer_ring_and_grid_cap(aca, oracle_mod, max_ctas):
         assert_same(g, o)
 
 
+@pytest.mark.parametrize("lag,kw", [(16.0, {}), (1.0, {}), (0.3, {}), (0.05, {}), (1.0, dict(max_ctas=3)),
+                                    (0.3, dict(checkerboard=-1)), (0.5, dict(lam=2.5)), (0.3, dict(tie_bits=30)),
+                                    (0.3, dict(dims=(48, 32, 40), beta=0.2216544)),
+                                    (0.3, dict(beta=1.0, h=0.1, rule=1, init_q=0.05, early_reject=1)),
+                                    (0.3, dict(shards=4, dims=(256, 256)))])
+def test_lag_window_exact(aca, oracle_mod, lag, kw):
+    """The bounded-lag window on the main path (aca_options.lag): a launch
+    fires only below min(T, t_min + lag), a scheduling bound, so the trajectory is the oracle's
+    for every lag (checkerboard and Jacobi launches, grid cap, lambda != 1, forced ties, 3-D,
+    a10, virtual shards)."""
+    kw = dict(kw)
+    dims = kw.pop("dims", (256, 192))
+    beta = kw.pop("beta", 0.4406868)
+    g, o = run_pair(aca, oracle_mod, dims, [2.0, 5.0], beta=beta, seed=77, whole_lattice=-1, lag=lag, **kw)
+    assert_same(g, o)
+
+
+def test_lag_window_bounds_the_spread(aca, oracle_mod):
+    """With a lag window the sweeps needed grow as the bound tightens (the efficiency loss of
+    fig:perfbl on the real algorithm), and the result does not change."""
+    sweeps = []
+    for lag in (0.0, 4.0, 1.0, 0.3):
+        g = aca.Sim((512, 512), beta=0.4406868, seed=3, lag=lag)
+        g.run_until(6.0)
+        st = g.stats()
+        sweeps.append(st["launches"])
+        if lag == 0.0:
+            ref = (g.spins().copy(), g.times().copy())
+        else:
+            assert np.array_equal(g.spins(), ref[0]) and np.array_equal(g.times(), ref[1])
+    assert sweeps[0] <= sweeps[1] <= sweeps[2] < sweeps[3], sweeps
+
+
 @pytest.mark.parametrize("case", ["jacobi", "jacobi_ties", "odd_tiles", "ties_cap", "rounds1_ties", "T_frac"])
 def test_staging_paths(aca, oracle_mod, case):
     """Staging paths of the grouped kernel: one launch over all tiles (checkerboard -1: every
