@@ -35,12 +35,12 @@ __host__ __device__ constexpr int grp_slots(int ndim, int tx, int ty, int tz) {
 // Shared-memory layout of tile_grp_kernel (host and device): NBUF tile buffers, the P4 (16) and
 // a10 (112) tables, the NLOG-2 tables split as L u64[256] and R u32[256], the reduction
 // scratch, NBUF mbarriers, 32 u32 of ring control (claim counter, the tile of each group, the
-// phases armed on each buffer), the origin of the tile in each buffer (32 B each), then the
-// per-warp fire queues.
+// phases armed on each buffer), the CTA's bounded-lag minimum and T limit (2 u64), the origin
+// of the tile in each buffer (32 B each), then the per-warp fire queues.
 __host__ __device__ constexpr size_t grp_smem_bytes(int ndim, int tx, int ty, int tz, int ntg, int ng, int nbuf,
                                                     bool early) {
     return ((size_t)nbuf * grp_slots(ndim, tx, ty, tz) + 16 + 112 + 256 + 128 + (size_t)(ntg * ng) / 32 + nbuf) * 8 +
-           128 + 16 + (size_t)nbuf * 32 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15);
+           160 + 16 + (size_t)nbuf * 32 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15);
 }
 
 // Commit the pending arrivals of the cell in slot s for as long as that is exact (a10):
@@ -534,7 +534,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     unsigned long long* bar = red + NW;                     // NBUF full barriers
     unsigned int* cs = (unsigned int*)(bar + NBUF);         // [0] claim counter, [1 + 2g + p] tiles of group g
     volatile unsigned int* armed = cs + 1 + 2 * NG;         // [b] phases of bar[b] armed so far
-    int4* orgs = (int4*)(((uintptr_t)(cs + 32) + 15) & ~(uintptr_t)15);   // [2b], [2b+1]: origin of buffer b's tile
+    unsigned long long* lagw = (unsigned long long*)(cs + 32);   // [0] bounded lag: min word written back, [1] wlim_T
+    int4* orgs = (int4*)(((uintptr_t)(cs + 40) + 15) & ~(uintptr_t)15);   // [2b], [2b+1]: origin of buffer b's tile
     unsigned short* Q = (unsigned short*)(orgs + 2 * NBUF); // NW x QW fire queue entries
 
     const Geo& g = P.g;
@@ -547,15 +548,17 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         Rt[i] = (unsigned int)P.lr[2 * i + 1];
     }
     if (tid < NBUF) { mbar_init(&bar[tid], 1); armed[tid] = 0u; }
-    if (tid == 0) cs[0] = 0u;
+    if (tid == 0) {
+        cs[0] = 0u;
+        lagw[0] = ~0ull;
+        lagw[1] = *(volatile unsigned long long*)&P.ctl->wlim_T;
+    }
     __syncthreads();
     const NlogSmem tab{smem_u32(Lt), smem_u32(Rt)};
     const uint32_t thr_a = smem_u32(thr);
 
     auto slot = [](int lx, int ly, int lz) { return (lz + (NDIM == 3 ? 1 : 0)) * SXY + (ly + 1) * SX + lx + 2; };
     const unsigned long long wlim = *(volatile unsigned long long*)&P.ctl->wlim;      // firing limit
-    const unsigned long long wlimT = *(volatile unsigned long long*)&P.ctl->wlim_T;   // T (termination)
-    unsigned long long wmin = ~0ull;   // bounded lag: the minimum word this CTA writes back
     // work items: every tile (phase < 0), or the tiles of one checkerboard colour: item k is
     // column pair j = k % hx of tile row k / hx, tx = 2j + ((row parity + phase) & 1)
     const int hx = (P.tiles_x + 1) >> 1;
@@ -765,6 +768,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                 // are final once its round loop ends, so each warp stores its rows while the
                 // others may still be firing.
                 const int wb0 = wg * CPW;
+                const unsigned long long wT = lagw[1];   // T (termination counts cells below it)
+                unsigned long long wm = ~0ull;
                 for (int idx = lane; idx < CPW / 2; idx += 32) {
                     const int oo = wb0 + 2 * idx;
                     const int lx = oo % TX, ly = (oo / TX) % TY, lz = oo / (TX * TY);
@@ -773,8 +778,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                     const ulonglong2 v = lds128v(&S[slot(lx, ly, lz)]);
                     ACA_CHECK(gi + 1 < (size_t)g.nx * g.ny * g.nz, gi, oo);
                     *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
-                    active += (v.x < wlimT) + (v.y < wlimT);
-                    if (P.lag_q) wmin = min(wmin, min(v.x, v.y));
+                    active += (v.x < wT) + (v.y < wT);
+                    wm = min(wm, min(v.x, v.y));
                     if (P.push_lo) {
                         const int a = NDIM == 2 ? o.y0 + ly : o.z0 + lz, n = NDIM == 2 ? g.ny : g.nz;
                         if (a == 0 || a == n - 1) {
@@ -784,6 +789,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                         }
                     }
                 }
+                if (P.lag_q) atomicMin(&lagw[0], wm);
             } else {
                 group_bar(1 + gid, NTG);   // other warps' cells are read below
                 for (int oo = gt; oo < NCELL; oo += NTG) {
@@ -794,8 +800,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                         const unsigned long long w = S[slot(lx, ly, lz)];
                         P.words[gi] = w;
                         push_word(P, gx, gy, gz, w);
-                        active += w < wlimT;
-                        if (P.lag_q) wmin = min(wmin, w);
+                        active += w < lagw[1];
+                        if (P.lag_q) atomicMin(&lagw[0], w);
                     }
                 }
             }
@@ -814,11 +820,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     }
     ACA_TRACE(8, 0);
     __syncthreads();
-    if (P.lag_q) {   // one atomic per warp into this colour's minimum
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
-        if (lane == 0 && wmin != ~0ull) atomicMin(&P.ctl->wmin[P.phase > 0 ? 1 : 0], wmin);
-    }
+    if (P.lag_q && tid == 0 && lagw[0] != ~0ull) atomicMin(&P.ctl->wmin[P.phase > 0 ? 1 : 0], lagw[0]);
     const unsigned long long s_act = block_sum<NT>((unsigned long long)active, red);
     tot.fold(st);
     const unsigned long long s_fir = block_sum<NT>(tot.fired, red);
