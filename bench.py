@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hash", action="store_true", help="skip the P7 event hash (diagnostics only)")
+    ap.add_argument("--rows-div", type=int, default=1,
+                    help="run the config on 1/G of its rows (2-D) / planes (3-D): the per-GPU lattice of a G-GPU "
+                         "strip partition, to bound the per-GPU launch/tail cost of the multi-GPU runs on one device")
     ap.add_argument("--shards", type=int, default=1,
                     help="virtual row strips / z slabs on this GPU (bounds the per-shard boundary cost of the "
                          "multi-GPU partition on one device; push-mode halos, same kernels)")
@@ -270,6 +273,8 @@ def main():
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = workloads.config(args.config)
     dims = tuple(cfg["dims"])
+    if args.rows_div > 1:
+        dims = dims[:-1] + (dims[-1] // args.rows_div,)
     ndim = len(dims)
     tile = tuple(int(x) for x in args.tile.split("x")) if args.tile else tuple(cfg["tile"])
     opts = dict(init_q=cfg["init_q"], device=local, tile=tile, event_hash=0 if args.no_hash else 1)
@@ -333,7 +338,7 @@ def main():
         arrivals += st["arrivals"]
         tested += st["cells_tested"]
         fired += st["cells_fired"]
-        launches += st["launches"]
+        launches += st["launches"] // max(1, args.shards)   # every virtual shard counts its own sweeps
     e1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -388,7 +393,7 @@ def main():
                        "l2": ("state %.1f MB per GPU: L2-resident (roofline against measured L2 bandwidth)" %
                               (state_bytes / 1e6)) if l2_resident else
                              ("state %.2f GB per GPU >> 126 MB L2 (no flush needed)" % (state_bytes / 1e9)),
-                       "shards": args.shards,
+                       "shards": args.shards, "rows_div": args.rows_div,
                        "event_hash": not args.no_hash},
             "roofline": roof,
             "roofline_issue": issue_roofline(args.config),

@@ -278,7 +278,7 @@ struct TileKey {
      sync_smem_bytes(ND, TX, TY, TZ, NTS), NTG * NG, NTG * NGE, NTS}
 
 const TileKey kTiles[] = {
-    TKG(2, 64, 64, 1, 256, 4, 5, 4, 5, 256), TKG(2, 64, 64, 1, 512, 2, 3, 2, 3, 512),
+    TKG(2, 64, 64, 1, 256, 4, 5, 4, 5, 256), TKG(2, 64, 64, 1, 512, 1, 2, 1, 2, 512),
     TKG(2, 32, 32, 1, 256, 4, 8, 4, 8, 256), TKG(2, 64, 32, 1, 256, 4, 8, 4, 8, 256),
     TKG(3, 32, 16, 8, 256, 3, 4, 3, 3, 256), TKG(3, 8, 8, 8, 128, 8, 12, 8, 12, 128),
     TKG(3, 16, 16, 16, 256, 3, 4, 3, 3, 256),

@@ -233,19 +233,21 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
         } else if constexpr (!EARLY && COLMAP) {
             unsigned int tiec = ~0u;
-            unsigned int uh = VH[2 * (s0 - SX) + 1];
-            unsigned long long a = VS[s0];
+            // high halves only, through 32-bit shared-window addresses (byte offset +4 of a word)
+            const uint32_t ha0 = smem_u32(S) + 8u * (uint32_t)s0 + 4u;
+            unsigned int uh = lds32a(ha0 - 8u * SX);
+            unsigned int ah_ = lds32a(ha0);
 #define ACA_COL_ROWS(TEST)                                                                           \
     _Pragma("unroll") for (int rr = 0; rr < TY; ++rr) {                                              \
-        const int sr = s0 + rr * SX;                                                                 \
-        const unsigned long long b = VS[sr + SX];                                                    \
-        const unsigned int ah = hi32(a);                                                             \
-        const unsigned int m = min(min(min(VH[2 * (sr - 1) + 1], VH[2 * (sr + 1) + 1]),              \
-                                       min(VH[2 * (sr - SXY) + 1], VH[2 * (sr + SXY) + 1])),         \
-                                   min(uh, hi32(b)));                                                \
+        const uint32_t hr = ha0 + 8u * SX * (uint32_t)rr;                                            \
+        const unsigned int bh = lds32a(hr + 8u * SX);                                                \
+        const unsigned int ah = ah_;                                                                 \
+        const unsigned int m = min(min(min(lds32a(hr - 8u), lds32a(hr + 8u)),                        \
+                                       min(lds32a(hr - 8u * SXY), lds32a(hr + 8u * SXY))),           \
+                                   min(uh, bh));                                                     \
         TEST;                                                                                        \
         uh = ah;                                                                                     \
-        a = b;                                                                                       \
+        ah_ = bh;                                                                                    \
     }
             if (!exact) {
                 ACA_COL_ROWS(one_test_strict(ah, m, wh, 1u << rr, emask, ntest))
@@ -394,6 +396,17 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 emask ^= 1u << j;
                 const uint32_t e = base | ((j << 5) & 0x1c0u) | (j & 1u);
                 asm volatile("st.shared.u16 [%0], %1;" ::"r"(qp), "h"((unsigned short)e) : "memory");
+                qp += 2u;
+            }
+        } else if constexpr (COLMAP) {
+            // entry of cell j = wbase + lane + 32 j
+            uint32_t qp = smem_u32(q) + 2u * (uint32_t)pos;
+            const uint32_t base = (uint32_t)(wbase + lane);
+            while (emask) {
+                uint32_t j;
+                asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(emask));
+                emask ^= 1u << j;
+                asm volatile("st.shared.u16 [%0], %1;" ::"r"(qp), "h"((unsigned short)(base + (j << 5))) : "memory");
                 qp += 2u;
             }
         } else {
@@ -646,6 +659,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         if (!(o.full && vec_ok)) return;
         const bool xs = x_tma(o);
         unsigned long long* S = Sb + b * NSLOTP;
+        const uint32_t barA = smem_u32(&bar[b]);
         bool fenced = false;
         for (int row = t; row < NROWS + NFACE; row += nt) {
             int ly, lz;
@@ -663,16 +677,17 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
             unsigned long long* d0 = &S[slot(0, ly, lz)];
             ACA_CHECK(slot(-2, ly, lz) >= 0 && slot(TX + 2, ly, lz) <= NSLOTP, row, ly);
             ACA_CHECK(rowp != nullptr && ((uintptr_t)rowp & 15) == 0, (uintptr_t)rowp, row);
+            const uint32_t da = smem_u32(d0);
             if (!xs) {
-                bulk_g2s(d0, rowp + o.x0, TX * 8, &bar[b]);
+                bulk_g2s_a(da, rowp + o.x0, TX * 8, barA);
                 continue;
             }
             // columns x0-2 .. x0+TX+1; the parts across the periodic x wrap come separately
             const bool lo_in = o.x0 >= 2, hi_in = o.x0 + TX + 2 <= g.nx;
             const int st = lo_in ? o.x0 - 2 : o.x0, en = hi_in ? o.x0 + TX + 2 : o.x0 + TX;
-            bulk_g2s(d0 + (st - o.x0), rowp + st, (uint32_t)(en - st) * 8u, &bar[b]);
-            if (!lo_in) bulk_g2s(d0 - 2, rowp + g.nx - 2, 16u, &bar[b]);
-            if (!hi_in) bulk_g2s(d0 + TX, rowp, 16u, &bar[b]);
+            bulk_g2s_a(da + 8u * (uint32_t)(st - o.x0), rowp + st, (uint32_t)(en - st) * 8u, barA);
+            if (!lo_in) bulk_g2s_a(da - 16u, rowp + g.nx - 2, 16u, barA);
+            if (!hi_in) bulk_g2s_a(da + 8u * TX, rowp, 16u, barA);
         }
     };
 
