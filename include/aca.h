@@ -7,7 +7,8 @@
  * (Eq. newt1i); next_state from the neighbourhood just before the arrival
  * (Eq. newst), here continuous-time Glauber / Metropolis Ising
  * (Appendix); simulate until end_time
- * (fig:a1c1pe). All arithmetic on the path is integer and follows
+ * (fig:a1c1pe). All arithmetic on the path is integer (the optional Gaussian laws
+ * add correctly rounded IEEE double steps that host and device perform identically) and follows
  * docs/PRIMITIVES.md (P1 Philox4x32-10, P3 NLOG-2, P4 threshold table, P5 init, P6 (t, c)
  * tie-break, P7 event hash), so results are bit-identical to the serial oracle for every
  * tile shape, rounds-per-launch and shard count.
@@ -89,9 +90,11 @@ typedef struct {
                                    0 (default) Poisson, next_t = t - ln(r)/lambda (Eq. newt1i,
                                    PAPER.md:485-488); 1 uniform, next_t - t = r/lambda
                                    (PAPER.md:1389-1393); 2 next_t - t = r^(1/8)/lambda
-                                   (PAPER.md:1425-1430); 3 Gaussian period of mean 1/lambda
-                                   and sd 1/(4 lambda) (Irwin-Hall(12), negative periods
-                                   clamped). r from the arrival's draw. */
+                                   (PAPER.md:1425-1430); 3 a Gaussian period of mean 1/lambda and
+                                   sd 1/(4 lambda) drawn at every arrival (the normal quantile of
+                                   r, periods below one unit redrawn); 4 the
+                                   strict reading of PAPER.md:404-410: a fixed Gaussian period per
+                                   cell. r from the arrival's draw (law 4: the cell's initial draw). */
     int32_t halo_mode;          /* sharded handles: 0 (default) = push, the tile kernel stores its
                                    boundary rows into the neighbour shard's halo as it writes them
                                    back (no exchange step; exact because words only grow and are
@@ -138,7 +141,7 @@ int aca_default_options(aca_options* opt);
 
 /* Create a simulation and initialise it on the device (P5: one Philox draw per cell).
  * ndim in {2, 3}; dims[a] >= 2; periodic must be 1;
- * lambda > 0 finite; beta >= 0 finite; rule ACA_HEATBATH or ACA_METROPOLIS;
+ * lambda > 0 finite; beta >= 0 finite; rule ACA_HEATBATH, ACA_METROPOLIS or (2-D) ACA_LIFE;
  * opt may be NULL (defaults). On success *out owns device memory until aca_destroy. */
 int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, double lambda,
                double beta, double J, double h, int rule, uint64_t seed, const aca_options* opt);
@@ -306,8 +309,9 @@ int aca_selftest_philox(uint64_t n, const uint32_t* ctr, const uint32_t* key, ui
 /* P3: q[i] = NLOG-2(X[i]); delta[i] = Delta(X[i]) for inv_lambda, tie_bits. */
 int aca_selftest_nlog(uint64_t n, const uint64_t* X, uint64_t* q, uint64_t* delta,
                       uint64_t inv_lambda, int tie_bits);
-/* P3L: u[i] = unscaled increment of `law` for (w1, w2) = (X[i] >> 32, X[i] & 0xffffffff);
- * delta[i] = the increment after 1/lambda, the clamp and P3b. ACA_EINVAL for law outside 0..2. */
+/* P3L: u[i] = unscaled increment of `law` for (w1, w2) = (X[i] >> 32, X[i] & 0xffffffff) (law 4: the
+ * period gauss_u(w1, w1, w2, 10) of a cell whose initial draw has w3 = w1 and c_lo = w2);
+ * delta[i] = the increment after 1/lambda, the clamp and P3b. ACA_EINVAL for law outside 0..4. */
 int aca_selftest_law(uint64_t n, const uint64_t* X, int law, uint64_t inv_lambda, int tie_bits, uint64_t* u,
                      uint64_t* delta);
 

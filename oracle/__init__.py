@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = [os.path.join(_HERE, "aca_oracle.c")]
-_HDR = [os.path.join(_HERE, "aca_oracle.h"), os.path.join(_HERE, "nlog_tables.h")]
+_HDR = [os.path.join(_HERE, "aca_oracle.h"), os.path.join(_HERE, "nlog_tables.h"), os.path.join(_HERE, "gauss_tables.h")]
 
 HEATBATH, METROPOLIS = 0, 1
 
@@ -114,6 +114,12 @@ def lib():
                                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                      ctypes.POINTER(Stats)]
         L.oracle_bkl_run.argtypes = L.oracle_agg_run.argtypes
+        L.oracle_gauss_z.argtypes = [ctypes.c_uint32]
+        L.oracle_gauss_z.restype = ctypes.c_double
+        L.oracle_gauss_u.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
+        L.oracle_gauss_u.restype = ctypes.c_uint64
+        L.oracle_cell_period_q32.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        L.oracle_cell_period_q32.restype = ctypes.c_uint64
         L.oracle_perfbl_run.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64,
                                          ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         L.oracle_efficiency_run_q.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int,
@@ -150,7 +156,7 @@ def nlog_batch(X):
     return q
 
 
-POISSON, UNIFORM, ROOT8, GAUSS = 0, 1, 2, 3   # P3L asynchrony laws
+POISSON, UNIFORM, ROOT8, GAUSS, GAUSS_CELL = 0, 1, 2, 3, 4   # P3L asynchrony laws
 
 
 def cell_time_counter(seed, c, T, lam=1.0, tie_bits=0, law=POISSON):
@@ -168,6 +174,20 @@ def delta(w1, w2, lam=1.0, tie_bits=0, law=POISSON):
 
 def law_q32(w1, w2, law):
     return lib().oracle_law_q32(w1, w2, law)
+
+
+def gauss_z(w):
+    """The normal quantile of (w + 1/2) 2^-32 as P3L defines it (double)."""
+    return lib().oracle_gauss_z(w)
+
+
+def gauss_u(w, sa, sb, tag):
+    return lib().oracle_gauss_u(w, sa, sb, tag)
+
+
+def cell_period_q32(seed, c):
+    """Law 4: the fixed Gaussian period of cell c (Q32)."""
+    return lib().oracle_cell_period_q32(seed, c)
 
 
 def flip_table(ndim, beta, J=1.0, h=0.0, rule=HEATBATH):

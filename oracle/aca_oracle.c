@@ -13,6 +13,7 @@
 #include <string.h>
 
 #include "nlog_tables.h"
+#include "gauss_tables.h"
 
 /* ---------------------------------------------------------------- P1: Philox4x32-10 */
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
@@ -58,29 +59,50 @@ uint64_t oracle_inv_lambda(double lambda) { return (uint64_t)floor(4294967296.0 
  *   law 1, uniform on (0,1):         U = w1
  *   law 2, next_t - t = r^(1/8):     U = floor(sqrt(sqrt(sqrt(r))) * 2^32),
  *          r = (w1 + 0.5) * 2^-32 in IEEE double (sqrt is correctly rounded). */
-uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law) {
-    if (law == 1) return (uint64_t)w1;
-    if (law == 3) {   /* Gaussian period: Irwin-Hall(12), mean 1, sd 1/4 (P3L) */
-        const uint32_t kg[2] = {0x243F6A88u, 0x85A308D3u};
-        uint64_t S = 0;
-        for (uint32_t j = 0; j < 3; j++) {
-            uint32_t ctr[4] = {w1, w2, j, 9u}, o[4];
-            oracle_philox4x32_10(ctr, kg, o);
-            S += (uint64_t)o[0] + o[1] + o[2] + o[3];
-        }
-        int64_t U = (int64_t)(S >> 2) - (int64_t)(1ULL << 31);
-        return U < 1 ? 1 : (uint64_t)U;
-    }
-    if (law == 2) {
-        double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
-        return (uint64_t)floor(sqrt(sqrt(sqrt(r))) * 4294967296.0);
-    }
-    return oracle_nlog_q32(((uint64_t)w1 << 32) | w2);
+/* The standard normal quantile z = Phi^{-1}((w + 1/2) 2^-32) of P3L laws 3 and 4: by symmetry on
+ * p' = min(p, 1 - p), s = sqrt(-ln p') with -ln p' from NLOG-2 (exact integers), |z| = G(s) by the
+ * cubic pieces of oracle/gauss_tables.h (Horner in IEEE double, in this order, no fused ops). */
+double oracle_gauss_z(uint32_t w) {
+    const uint32_t wp = w < 0x80000000u ? w : 0xffffffffu - w;
+    const uint64_t q = oracle_nlog_q32(((uint64_t)(2ull * wp + 1ull)) << 31);   /* -ln p' in Q32 */
+    const double s = sqrt((double)q * (1.0 / 4294967296.0));
+    const double u = (s - 0.828125) * 256.0;
+    int i = (int)u;
+    if (i < 0) i = 0;
+    if (i > 1023) i = 1023;
+    const double t = u - (double)i;
+    const double* c = ORACLE_GAUSS_C[i];
+    const double g = ((c[3] * t + c[2]) * t + c[1]) * t + c[0];
+    return w < 0x80000000u ? -g : g;
 }
 
-/* next_t = t + U / lambda; next_t > t (PAPER.md:340). */
-uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits, int law) {
-    uint64_t q = oracle_law_q32(w1, w2, law);
+/* A Gaussian period of mean 1 and standard deviation 1/4 in Q32: U = floor((1 + z/4) 2^32) for the
+ * uniform word w; a period below one unit is rejected and redrawn from the sub-draws a0 of
+ * Philox ctr (sa, sb, j, tag), j = 1..31, under the fixed key (0x243F6A88, 0x85A308D3); U = 1 if all
+ * 32 draws fail. */
+uint64_t oracle_gauss_u(uint32_t w, uint32_t sa, uint32_t sb, uint32_t tag) {
+    const uint32_t kg[2] = {0x243F6A88u, 0x85A308D3u};
+    for (uint32_t j = 0;; j++) {
+        const double x = (1.0 + 0.25 * oracle_gauss_z(w)) * 4294967296.0;
+        if (x >= 1.0) return (uint64_t)floor(x);
+        if (j == 31) return 1;
+        uint32_t ctr[4] = {sa, sb, j + 1, tag}, o[4];
+        oracle_philox4x32_10(ctr, kg, o);
+        w = o[0];
+    }
+}
+
+/* Law 4, the strict reading of PAPER.md:404-410 (sigma_c = 0, m_c itself Gaussian): the fixed
+ * period of cell c, from the spare word w3 of its initial draw (Philox ctr (0, c, 0, 1)). */
+uint64_t oracle_cell_period_q32(uint64_t seed, uint64_t c) {
+    const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {0, (uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 1u}, w[4];
+    oracle_philox4x32_10(ctr, key, w);
+    return oracle_gauss_u(w[3], w[3], (uint32_t)(c & 0xffffffffu), 10u);
+}
+
+/* Delta = max(1, (U INV) >> 32) with the tie quantisation of P3b. */
+static uint64_t delta_of_u(uint64_t q, uint64_t inv_lambda, int tie_bits) {
     unsigned __int128 prod = (unsigned __int128)q * inv_lambda;
     uint64_t d = (uint64_t)(prod >> 32);
     if (d < 1) d = 1;
@@ -90,6 +112,29 @@ uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie
         if (d < quantum) d = quantum;
     }
     return d;
+}
+
+uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law) {
+    if (law == 1) return (uint64_t)w1;
+    if (law == 3) return oracle_gauss_u(w1, w1, w2, 9u);   /* Gaussian period, liberal */
+    if (law == 2) {
+        double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
+        return (uint64_t)floor(sqrt(sqrt(sqrt(r))) * 4294967296.0);
+    }
+    return oracle_nlog_q32(((uint64_t)w1 << 32) | w2);
+}
+
+/* next_t = t + U / lambda; next_t > t (PAPER.md:340). */
+uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits, int law) {
+    return delta_of_u(oracle_law_q32(w1, w2, law), inv_lambda, tie_bits);
+}
+
+/* The increment of cell c at any arrival: law 4 uses the cell's fixed period, every other law the
+ * arrival's draw (w1, w2). */
+static uint64_t cell_delta(uint64_t seed, uint64_t c, uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits,
+                           int law) {
+    if (law == 4) return delta_of_u(oracle_cell_period_q32(seed, c), inv_lambda, tie_bits);
+    return oracle_delta_law(w1, w2, inv_lambda, tie_bits, law);
 }
 
 /* Eq. newt1i: next_t = t - ln(r)/lambda (the Poisson law). */
@@ -189,7 +234,7 @@ oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double b
 oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, double beta, double J,
                               double h, int rule, uint64_t seed, double init_q, int tie_bits, int law) {
     if (ndim != 2 && ndim != 3) return NULL;
-    if (law < 0 || law > 3) return NULL;
+    if (law < 0 || law > 4) return NULL;
     if (!(lambda > 0) || !isfinite(lambda) || !(beta >= 0) || !isfinite(beta)) return NULL;
     if (rule != 0 && rule != 1 && !(rule == 2 && ndim == 2)) return NULL;
     if (!(init_q >= 0 && init_q <= 1)) return NULL;
@@ -217,7 +262,7 @@ oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, doub
         uint32_t w[4];
         draw(S, 0, c, 1u, w);
         S->s[c] = ((uint64_t)w[0] < S->thr_init) ? -1 : 1;
-        S->t[c] = oracle_delta_law(w[1], w[2], S->inv_lambda, tie_bits, law);
+        S->t[c] = cell_delta(seed, (uint64_t)c, w[1], w[2], S->inv_lambda, tie_bits, law);
         S->n[c] = 0;
     }
     return S;
@@ -254,7 +299,7 @@ static void arrival(oracle_sim* S, int64_t c, int8_t* new_s, uint64_t* new_t) {
     uint64_t tev = S->t[c];
     S->event_hash += oracle_ev_hash(w[3], tev, 0, ns);
     *new_s = (int8_t)ns;
-    *new_t = tev + oracle_delta_law(w[1], w[2], S->inv_lambda, S->tie_bits, S->law);
+    *new_t = tev + cell_delta(S->seed, (uint64_t)c, w[1], w[2], S->inv_lambda, S->tie_bits, S->law);
 }
 
 /* lexicographic (t, c) order (P6). */
@@ -476,12 +521,12 @@ void oracle_cell_time_counter_law(uint64_t seed, uint64_t c, uint64_t T_q32, uin
     uint32_t ctr[4] = {0, (uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 1u};
     uint32_t w[4];
     oracle_philox4x32_10(ctr, key, w);
-    uint64_t t = oracle_delta_law(w[1], w[2], inv_lambda, tie_bits, law);
+    uint64_t t = cell_delta(seed, c, w[1], w[2], inv_lambda, tie_bits, law);
     uint32_t k = 0;
     while (t < T_q32) {
         uint32_t ce[4] = {k, (uint32_t)(c & 0xffffffffu), (uint32_t)(c >> 32), 0u};
         oracle_philox4x32_10(ce, key, w);
-        t += oracle_delta_law(w[1], w[2], inv_lambda, tie_bits, law);
+        t += cell_delta(seed, c, w[1], w[2], inv_lambda, tie_bits, law);
         k++;
     }
     *t_out = t;
@@ -557,7 +602,7 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
         uint32_t ctr[4] = {0, (uint32_t)(gid[l] & 0xffffffffu), (uint32_t)(gid[l] >> 32), 1u}, w[4];
         oracle_philox4x32_10(ctr, key, w);
         s[l] = ((uint64_t)w[0] < thr_init) ? -1 : 1;
-        t[l] = oracle_delta_law(w[1], w[2], inv, tie_bits, law);
+        t[l] = cell_delta(seed, gid[l], w[1], w[2], inv, tie_bits, law);
     }
     /* binary heap of (t, global id, local id) */
     int64_t hn = 0;
@@ -599,7 +644,7 @@ int oracle_window_cell_law(int ndim, const int64_t* dims, double lambda, double 
                 unk[c] = 1;
             }
         }
-        t[c] += oracle_delta_law(w[1], w[2], inv, tie_bits, law);
+        t[c] += cell_delta(seed, gid[c], w[1], w[2], inv, tie_bits, law);
         n[c] += 1;
         heap[0].t = t[c];
         int64_t i = 0;
@@ -706,7 +751,7 @@ int oracle_perfbl_run(int64_t px, int64_t py, int m, uint64_t lag_q32, uint64_t 
 int oracle_efficiency_run_q(int ndim, const int64_t* dims, int law, double lambda, uint64_t seed, int64_t rounds,
                             int q, uint64_t* fired_per_round, uint64_t* t_out) {
     if (q < 1 || q > 8) return -1;
-    if (ndim < 1 || ndim > 3 || law < 0 || law > 3 || !(lambda > 0) || rounds < 0) return -1;
+    if (ndim < 1 || ndim > 3 || law < 0 || law > 3 || !(lambda > 0) || rounds < 0) return -1;   /* law 4: n/a */
     int64_t d[3] = {1, 1, 1}, N = 1;
     for (int a = 0; a < ndim; a++) { if (dims[a] < 2) return -1; d[a] = dims[a]; N *= dims[a]; }
     uint64_t inv = oracle_inv_lambda(lambda);

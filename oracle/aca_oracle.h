@@ -36,6 +36,11 @@ uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bit
 uint64_t oracle_inv_lambda(double lambda);
 /* P3L: asynchrony laws. law 0 Poisson (= oracle_delta), 1 uniform on (0,1), 2 r^(1/8).
  * oracle_law_q32 is the unscaled increment U in Q32 (before 1/lambda, the clamp and P3b). */
+/* P3L laws 3/4: the normal quantile of (w + 1/2) 2^-32, a Gaussian period (mean 1, sd 1/4, Q32) with
+ * redraws below one unit, and the fixed period of cell c under law 4. */
+double oracle_gauss_z(uint32_t w);
+uint64_t oracle_gauss_u(uint32_t w, uint32_t sa, uint32_t sb, uint32_t tag);
+uint64_t oracle_cell_period_q32(uint64_t seed, uint64_t c);
 uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law);
 uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits, int law);
 /* P4: thresholds, 2*(2*ndim+1) entries written to out. */

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libaca.so")
 SOURCES = [os.path.join(CSRC, "aca.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("aca_kernels.cuh", "aca_tile.cuh", "aca_misc.cuh", "aca_prim.cuh", "nlog_tables.cuh", "aca_eff.cuh", "aca_agg.cuh")] + \
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("aca_kernels.cuh", "aca_tile.cuh", "aca_misc.cuh", "aca_prim.cuh", "nlog_tables.cuh", "gauss_tables.cuh", "aca_eff.cuh", "aca_agg.cuh")] + \
     [os.path.join(ROOT, "include", "aca.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -21,9 +21,9 @@ def build(force=False, verbose=False):
     newest = max(os.path.getmtime(p) for p in DEPS)
     if not force and os.path.exists(SO) and os.path.getmtime(SO) >= newest:
         return SO
-    tables = os.path.join(CSRC, "nlog_tables.cuh")
-    if not os.path.exists(tables):
-        subprocess.check_call([sys.executable, os.path.join(CSRC, "gen_nlog_tables.py")])
+    for tab, gen in (("nlog_tables.cuh", "gen_nlog_tables.py"), ("gauss_tables.cuh", "gen_gauss_tables.py")):
+        if not os.path.exists(os.path.join(CSRC, tab)):
+            subprocess.check_call([sys.executable, os.path.join(CSRC, gen)])
     log = os.path.join(PKG, "build_ptxas.log")
     cmd = [NVCC] + FLAGS + ["-o", SO] + SOURCES + ["-ldl"]
     with open(log, "w") as f:

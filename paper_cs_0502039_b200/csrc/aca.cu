@@ -671,8 +671,9 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     }
     if (!(opt.init_q >= 0 && opt.init_q <= 1)) return fail(ACA_EINVAL, "init_q must be in [0, 1]");
     if (opt.tie_bits < 0 || opt.tie_bits > 40) return fail(ACA_EINVAL, "tie_bits must be in [0, 40]");
-    if (opt.law < 0 || opt.law > 3)
-        return fail(ACA_EINVAL, "law must be 0 (Poisson), 1 (uniform), 2 (r^1/8) or 3 (Gaussian period)");
+    if (opt.law < 0 || opt.law > 4)
+        return fail(ACA_EINVAL, "law must be 0 (Poisson), 1 (uniform), 2 (r^1/8), 3 (Gaussian period) or 4 (fixed "
+                                "Gaussian period per cell)");
     if (rule == ACA_LIFE && (opt.early_reject || opt.sync_rounds))
         return fail(ACA_EINVAL, "the Game of Life rule has no early rejection / sync-round kernel");
     if (opt.shards < 1) opt.shards = 1;
@@ -745,7 +746,8 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     S->thr_init = (unsigned long long)std::floor(opt.init_q * 4294967296.0);
     {
         // largest unscaled increment of the law: NLOG-2(1) for Poisson, < 2^32 otherwise
-        const unsigned long long umax = opt.law == 0 ? 190530846196ull : opt.law == 3 ? (3ull << 32) : (1ull << 32);
+        // (laws 3 and 4: 1 + 6.34/4 < 3 periods)
+        const unsigned long long umax = opt.law == 0 ? 190530846196ull : opt.law >= 3 ? (3ull << 32) : (1ull << 32);
         const unsigned __int128 p = (unsigned __int128)umax * S->inv_lambda;
         S->max_delta = (unsigned long long)(p >> 32) + 1 + (opt.tie_bits ? (1ull << opt.tie_bits) : 0ull);
         const int tb = bits_for(S->max_delta);
@@ -1428,6 +1430,12 @@ __global__ void law_test_kernel(uint64_t n, const uint64_t* X, uint64_t* u, uint
     const NlogSmem tab{smem_u32(Lt), smem_u32(Rt)};
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t w1 = (uint32_t)(X[i] >> 32), w2 = (uint32_t)X[i];
+        if (law == 4) {   // the period of law 4 from (w3, c_lo) = (w1, w2): gauss_u(w3, w3, c_lo, 10)
+            const uint64_t ua = gauss_u(w1, w1, w2, 10u, tab, ACA_LN2_Q48), ub = gauss_u(w1, w1, w2, 10u, NlogLR{lr_g}, ACA_LN2_Q48);
+            u[i] = ua == ub ? ua : ~ua;
+            d[i] = delta_of_u(ua, inv_lambda, tie_bits);
+            continue;
+        }
         const uint64_t ua = law_q32_t(w1, w2, tab, ACA_LN2_Q48, law), ub = law_q32(w1, w2, lr_g, ACA_LN2_Q48, law);
         u[i] = ua == ub ? ua : ~ua;
         const uint64_t da = delta_q32_t(w1, w2, tab, ACA_LN2_Q48, inv_lambda, tie_bits, law);
@@ -1441,7 +1449,7 @@ extern "C" {
 int aca_selftest_law(uint64_t n, const uint64_t* X, int law, uint64_t inv_lambda, int tie_bits, uint64_t* u,
                      uint64_t* delta) {
     if (!X || !u || !delta) return fail(ACA_EINVAL, "null buffer");
-    if (law < 0 || law > 3) return fail(ACA_EINVAL, "bad law");
+    if (law < 0 || law > 4) return fail(ACA_EINVAL, "bad law");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
     uint64_t *dx = nullptr, *du = nullptr, *dd = nullptr;

@@ -334,7 +334,7 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
     // z = 8: asynchronous Game of Life (P10), Conway's rule on the Moore neighbourhood
     const uint32_t flip = z == 8 ? ((ones == 3u || (sb && ones == 2u)) ? 1u : 0u) ^ sb
                                  : ((unsigned long long)r.x < thr[idx] ? 1u : 0u);
-    const unsigned long long d = delta_q32_t(r.y, r.z, tab, ACA_LN2_Q48, inv_lambda, tie_bits, law);
+    const unsigned long long d = delta_cell_t(c, rk, r.y, r.z, tab, ACA_LN2_Q48, inv_lambda, tie_bits, law);
     o.wnew = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;   // t += d, n += 1, s ^= flip
     o.flip = flip;
     if (fr && fr->nb) {

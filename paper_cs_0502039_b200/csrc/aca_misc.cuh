@@ -128,7 +128,7 @@ __global__ void init_kernel(unsigned long long* __restrict__ words, Geo g, const
             const unsigned long long c = cbase + x;
             const u32x4 r = philox4x32_10_rk(0u, (uint32_t)c, (uint32_t)(c >> 32), 1u, K.rk);
             const unsigned long long sb = ((unsigned long long)r.x < thr_init) ? 0ull : 1ull;
-            const unsigned long long t0 = delta_q32(r.y, r.z, lr, ACA_LN2_Q48, inv_lambda, tie_bits, law);
+            const unsigned long long t0 = delta_cell_t(c, K.rk, r.y, r.z, NlogLR{lr}, ACA_LN2_Q48, inv_lambda, tie_bits, law);
             words[(size_t)row * nx + x] = w_pack(t0, 0ull, sb, g);
         }
     }

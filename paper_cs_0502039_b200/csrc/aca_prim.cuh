@@ -3,6 +3,8 @@
 #pragma once
 #include <stdint.h>
 
+#include "gauss_tables.cuh"
+
 namespace aca {
 
 // ---------------------------------------------------------------- P1 Philox4x32-10
@@ -123,26 +125,49 @@ __device__ __forceinline__ uint64_t nlog_q32(uint64_t X, const unsigned long lon
     return nlog_q32_t(X, NlogLR{lr}, ln2_q48);
 }
 
+// The standard normal quantile z = Phi^{-1}((w + 1/2) 2^-32) of P3L laws 3 and 4 (docs/PRIMITIVES.md
+// P3L): by symmetry on p' = min(p, 1 - p), s = sqrt(-ln p') with -ln p' from NLOG-2 (exact integers),
+// |z| = G(s) by the cubic pieces of ACA_GAUSS_C (Horner in IEEE double through the _rn intrinsics,
+// which are never contracted into FMAs: the same roundings as the oracle's plain C).
+template <class Tab>
+__device__ __forceinline__ double gauss_z(uint32_t w, const Tab& tab, uint64_t ln2_q48) {
+    const uint32_t wp = w < 0x80000000u ? w : 0xffffffffu - w;
+    const uint64_t q = nlog_q32_t(((uint64_t)(2ull * wp + 1ull)) << 31, tab, ln2_q48);
+    const double s = __dsqrt_rn(__dmul_rn((double)q, 1.0 / 4294967296.0));
+    const double u = __dmul_rn(__dadd_rn(s, -0.828125), 256.0);
+    int i = (int)u;
+    i = i < 0 ? 0 : (i > 1023 ? 1023 : i);
+    const double t = __dadd_rn(u, -(double)i);
+    const double* c = ACA_GAUSS_C + 4 * i;
+    const double g = __dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(__dadd_rn(__dmul_rn(c[3], t), c[2]), t), c[1]), t), c[0]);
+    return w < 0x80000000u ? -g : g;
+}
+// A Gaussian period of mean 1 and sd 1/4 in Q32, U = floor((1 + z/4) 2^32); a period below one unit
+// is redrawn from the sub-draws a0 of Philox ctr (sa, sb, j, tag), j = 1..31, under the fixed key
+// (0x243F6A88, 0x85A308D3); U = 1 if all 32 draws fail.
+template <class Tab>
+__device__ __forceinline__ uint64_t gauss_u(uint32_t w, uint32_t sa, uint32_t sb, uint32_t tag, const Tab& tab,
+                                            uint64_t ln2_q48) {
+    for (uint32_t j = 0;; ++j) {
+        const double x = __dmul_rn(__dadd_rn(1.0, __dmul_rn(0.25, gauss_z(w, tab, ln2_q48))), 4294967296.0);
+        if (x >= 1.0) return (uint64_t)floor(x);
+        if (j == 31) return 1ull;
+        w = philox4x32_10(sa, sb, j + 1u, tag, 0x243F6A88u, 0x85A308D3u).x;
+    }
+}
+
 // P3L asynchrony law: the unscaled increment U in Q32 (docs/PRIMITIVES.md P3L).
 //   0 Poisson, Eq. newt1i:   U = NLOG-2((w1 << 32) | w2)
 //   1 uniform on (0,1):    U = w1
 //   2 r^(1/8):             U = floor(sqrt(sqrt(sqrt(r))) * 2^32), r = (w1 + 0.5) 2^-32
 //     (IEEE double; sqrt is correctly rounded on the device as on the host)
-//   3 Gaussian period:        S = sum of the 12 words of Philox (w1, w2, j, 9) under the
-//     fixed key (0x243F6A88, 0x85A308D3), j = 0..2; U = max(1, (S >> 2) - 2^31): mean 1, sd 1/4
+//   3 Gaussian period (the liberal reading): U = gauss_u(w1, w1, w2, 9), a fresh
+//     period of mean 1/lambda and sd 1/(4 lambda) at every arrival
+//   4 (the strict reading) needs the cell: cell_period_q32
 template <class Tab>
 __device__ __forceinline__ uint64_t law_q32_t(uint32_t w1, uint32_t w2, const Tab& tab, uint64_t ln2_q48, int law) {
     if (law == 1) return (uint64_t)w1;
-    if (law == 3) {   // Gaussian period: Irwin-Hall(12) of three sub-draws
-        uint64_t S = 0;
-#pragma unroll
-        for (uint32_t j = 0; j < 3; ++j) {
-            const u32x4 o = philox4x32_10(w1, w2, j, 9u, 0x243F6A88u, 0x85A308D3u);
-            S += (uint64_t)o.x + o.y + o.z + o.w;
-        }
-        const long long U = (long long)(S >> 2) - (1ll << 31);
-        return U < 1 ? 1ull : (uint64_t)U;
-    }
+    if (law == 3) return gauss_u(w1, w1, w2, 9u, tab, ln2_q48);
     if (law == 2) {
         const double r = ((double)w1 + 0.5) * (1.0 / 4294967296.0);
         return (uint64_t)(__dsqrt_rn(__dsqrt_rn(__dsqrt_rn(r))) * 4294967296.0);
@@ -154,11 +179,17 @@ __device__ __forceinline__ uint64_t law_q32(uint32_t w1, uint32_t w2, const unsi
     return law_q32_t(w1, w2, NlogLR{lr}, ln2_q48, law);
 }
 
-// next_t = t + U / lambda, next_t > t; P3b tie quantisation.
+// Law 4, the strict reading of PAPER.md:404-410 (sigma_c = 0, m_c itself Gaussian): the fixed period
+// of cell c from the spare word w3 of its initial draw (Philox ctr (0, c_lo, c_hi, 1), run key).
 template <class Tab>
-__device__ __forceinline__ uint64_t delta_q32_t(uint32_t w1, uint32_t w2, const Tab& tab, uint64_t ln2_q48,
-                                                uint64_t inv_lambda, int tie_bits, int law = 0) {
-    const uint64_t q = law_q32_t(w1, w2, tab, ln2_q48, law);
+__device__ __forceinline__ uint64_t cell_period_q32(uint32_t c_lo, uint32_t c_hi, const uint32_t* rk, const Tab& tab,
+                                                    uint64_t ln2_q48) {
+    const u32x4 r = philox4x32_10_rk(0u, c_lo, c_hi, 1u, rk);
+    return gauss_u(r.w, r.w, c_lo, 10u, tab, ln2_q48);
+}
+
+// Delta = max(1, (U INV) >> 32) and the P3b tie quantisation.
+__device__ __forceinline__ uint64_t delta_of_u(uint64_t q, uint64_t inv_lambda, int tie_bits) {
     uint64_t d;
     if (inv_lambda == (1ull << 32)) {
         d = q;
@@ -172,6 +203,22 @@ __device__ __forceinline__ uint64_t delta_q32_t(uint32_t w1, uint32_t w2, const 
         d = d < quantum ? quantum : d;
     }
     return d;
+}
+
+// next_t = t + U / lambda, next_t > t.
+template <class Tab>
+__device__ __forceinline__ uint64_t delta_q32_t(uint32_t w1, uint32_t w2, const Tab& tab, uint64_t ln2_q48,
+                                                uint64_t inv_lambda, int tie_bits, int law = 0) {
+    return delta_of_u(law_q32_t(w1, w2, tab, ln2_q48, law), inv_lambda, tie_bits);
+}
+// The increment of cell c at any arrival: law 4 the cell's fixed period, every other law the draw.
+template <class Tab>
+__device__ __forceinline__ uint64_t delta_cell_t(unsigned long long c, const uint32_t* rk, uint32_t w1, uint32_t w2,
+                                                 const Tab& tab, uint64_t ln2_q48, uint64_t inv_lambda, int tie_bits,
+                                                 int law) {
+    if (law == 4) return delta_of_u(cell_period_q32((uint32_t)c, (uint32_t)(c >> 32), rk, tab, ln2_q48), inv_lambda,
+                                    tie_bits);
+    return delta_q32_t(w1, w2, tab, ln2_q48, inv_lambda, tie_bits, law);
 }
 
 __device__ __forceinline__ uint64_t delta_q32(uint32_t w1, uint32_t w2, const unsigned long long* lr, uint64_t ln2_q48,

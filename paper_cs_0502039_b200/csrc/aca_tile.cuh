@@ -94,7 +94,7 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
             d = nlog_q32_t(((uint64_t)r.y << 32) | r.z, tab, ACA_LN2_Q48);
             d = d < 1ull ? 1ull : d;
         } else {
-            d = delta_q32_t(r.y, r.z, tab, ACA_LN2_Q48, P.inv_lambda, P.tie_bits, P.law);
+            d = delta_cell_t(cid, P.rk, r.y, r.z, tab, ACA_LN2_Q48, P.inv_lambda, P.tie_bits, P.law);
         }
         if (P.do_hash) st.hacc += ev_hash(r.w, w >> g.TSH, (unsigned long long)(sb ^ flip));
         if (!FASTP && P.fr.nb) {

@@ -89,7 +89,7 @@ def test_nlog_bit_identical_1e8(aca, oracle_mod):
         assert np.array_equal(q, oracle_mod.nlog_batch(X))
 
 
-@pytest.mark.parametrize("law", [0, 1, 2, 3])
+@pytest.mark.parametrize("law", [0, 1, 2, 3, 4])
 def test_law_bit_identical_to_oracle(aca, oracle_mod, law):
     """P3L asynchrony laws: the device's unscaled increment and
     Delta equal the oracle's on random and edge inputs, for several lambda / tie settings."""
@@ -99,13 +99,17 @@ def test_law_bit_identical_to_oracle(aca, oracle_mod, law):
     X = np.concatenate([np.array(edges, np.uint64), X])
     for lam, tb in ((1.0, 0), (2.5, 0), (0.3, 0), (1.0, 28)):
         u, d = aca.aca_selftest_law(X[:20000], law, lam, tb)
+        if law == 4:   # the period of law 4 from (w3, c_lo): gauss_u(w3, w3, c_lo, 10)
+            want_u = [oracle_mod.gauss_u(int(x) >> 32, int(x) >> 32, int(x) & 0xFFFFFFFF, 10) for x in X[:20000]]
+            assert list(u) == want_u
+            continue
         want_u = [oracle_mod.law_q32(int(x) >> 32, int(x) & 0xFFFFFFFF, law) for x in X[:20000]]
         want_d = [oracle_mod.delta(int(x) >> 32, int(x) & 0xFFFFFFFF, lam, tb, law) for x in X[:20000]]
         assert list(u) == want_u
         assert list(d) == want_d
 
 
-@pytest.mark.parametrize("law", [1, 2, 3])
+@pytest.mark.parametrize("law", [1, 2, 3, 4])
 def test_law_trajectories(aca, oracle_mod, law):
     """Whole trajectories under the uniform and r^(1/8) laws: whole-lattice, tiled 2-D with
     ragged tiles, 3-D tiles, with field and both rules."""

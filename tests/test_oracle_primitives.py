@@ -282,22 +282,30 @@ def test_law_closed_form_times(oracle_mod, law):
         assert (int(t.flat[c]), int(n.flat[c])) == (tc, nc)
 
 
-def _irwin_hall_cdf(x, n=12):
-    """Exact Irwin-Hall CDF, using the symmetry F(x) = 1 - F(n - x) to keep the alternating sum
-    well conditioned."""
-    x = np.asarray(x, float)
-    lo = np.minimum(x, n - x)
-    f = np.zeros_like(lo)
-    for k in range(n + 1):
-        term = (-1) ** k * math.comb(n, k) * np.clip(lo - k, 0, None) ** n
-        f += term
-    f /= math.factorial(n)
-    return np.where(x <= n / 2, f, 1 - f)
+def test_gauss_quantile_within_one_unit_of_mpmath(oracle_mod):
+    """P3L law 3: U = floor(2^32 (1 + Phi^{-1}((w + 1/2) 2^-32) / 4)) within one unit of mpmath's exact
+    value on random words, both tails (w near 0 and 2^32 - 1, |z| up to 6.3) and the centre; the
+    quantile itself is odd about w = 2^31 - 1/2."""
+    mpmath.mp.dps = 30
+    rnd = random.Random(21)
+    ws = [rnd.getrandbits(32) for _ in range(20000)]
+    ws += list(range(0, 64)) + [2 ** 32 - 1 - k for k in range(64)] + [2 ** 31 + d for d in range(-64, 64)]
+    ws += [rnd.getrandbits(12) for _ in range(500)] + [2 ** 32 - 1 - rnd.getrandbits(12) for _ in range(500)]
+    worst = 0
+    for w in ws:
+        p = (mpmath.mpf(w) + mpmath.mpf(1) / 2) / 2 ** 32
+        z = mpmath.sqrt(2) * mpmath.erfinv(2 * p - 1)
+        x = (1 + z / 4) * 2 ** 32
+        if x >= 1:
+            worst = max(worst, abs(oracle_mod.gauss_u(w, w, 0, 9) - int(mpmath.floor(x))))
+        assert oracle_mod.gauss_z(w) == -oracle_mod.gauss_z(2 ** 32 - 1 - w)
+    assert worst <= 1, worst
 
 
 def test_law_gauss_distribution(oracle_mod):
-    """Law 3 (Gaussian period): U/2^32 = S/4 - 1/2 with S ~ Irwin-Hall(12):
-    mean 1 and sd 1/4 exactly in distribution; KS against the exact Irwin-Hall CDF."""
+    """Law 3 (Gaussian period, the liberal reading): U / 2^32 ~ N(1, 1/4^2)
+    (the rare periods below one unit are redrawn, P(z < -4) = 3e-5): mean, sd and a KS test against
+    the normal CDF."""
     from scipy import stats
     v = []
     for c in range(20000):
@@ -306,9 +314,35 @@ def test_law_gauss_distribution(oracle_mod):
     v = np.array(v)
     assert abs(v.mean() - 1.0) < 4 * 0.25 / math.sqrt(len(v))
     assert abs(v.std() - 0.25) < 0.01
-    ks = stats.kstest(4 * (v + 0.5), lambda x: _irwin_hall_cdf(x))
+    ks = stats.kstest(v, stats.norm(loc=1.0, scale=0.25).cdf)
     assert ks.pvalue > 1e-4, ks
     assert v.min() > 0
+
+
+def test_law_gauss_redraws_nonpositive_periods(oracle_mod):
+    """A period below one unit is never used: the words whose quantile gives 1 + z/4 <= 0
+    (z <= -4, w below ~2^32 3.2e-5) are redrawn from the keyed sub-draws, deterministically."""
+    lo = [w for w in range(0, 200000, 997) if 1 + oracle_mod.gauss_z(w) / 4 <= 0]
+    assert lo, "expected words in the z <= -4 tail"
+    for w in lo[:50]:
+        u = oracle_mod.gauss_u(w, w, 77, 9)
+        assert u >= 1 and u == oracle_mod.gauss_u(w, w, 77, 9) and u != oracle_mod.gauss_u(w, w, 78, 9)
+
+
+def test_law4_fixed_period_per_cell(oracle_mod):
+    """Law 4 (the strict reading: sigma_c = 0, m_c Gaussian): every increment of a
+    cell is its fixed period, so its closed form is an arithmetic progression: t = (n + 1) P_c,
+    n = the number of periods below T; the periods are N(1, 1/4^2) across cells."""
+    from scipy import stats
+    T = 7.0
+    Tq = oracle_mod.to_q32(T)
+    P = []
+    for c in range(3000):
+        pc = oracle_mod.cell_period_q32(5, c)
+        t, n = oracle_mod.cell_time_counter(5, c, T, law=4)
+        assert t == (n + 1) * pc and n * pc < Tq <= t
+        P.append(pc / 2.0 ** 32)
+    assert stats.kstest(np.array(P), stats.norm(loc=1.0, scale=0.25).cdf).pvalue > 1e-4
 
 
 def test_law_gauss_is_a_function_of_the_draw(oracle_mod):
