@@ -240,7 +240,8 @@ int aca_run_frames(aca_sim* s, double dt, int64_t K0, int64_t count, int B, uint
 
 /* ---- Aggregated Poisson stream (fig:amcpoi; docs/PRIMITIVES.md P8) ----
  * The 2-D periodic lattice (dims[0] x dims[1], multiples of m) is partitioned into m x m
- * subarrays (m = 1, 2, 4, 8). Each subarray carries one Poisson stream of rate lambda m^2; at
+ * subarrays (1 <= m <= 32; the paper's experiments use m = 12 and 24, PAPER.md:1476-1488,
+ * 1586-1589). Each subarray carries one Poisson stream of rate lambda m^2; at
  * each arrival one of its cells, chosen uniformly at random, is updated (heat-bath or
  * Metropolis, P4), after waiting for the subarrays that hold the cell's outside neighbours.
  * One GPU thread per subarray, conservative launches until every T(C) >= T. The trajectory
@@ -260,7 +261,7 @@ int aca_agg_run(const int64_t* dims, int m, double lambda, double beta, double J
                 aca_agg_stats* st, int device);
 
 /* ---- Modified BKL (docs/PRIMITIVES.md P9) ----
- * Same partition, arguments and outputs as aca_agg_run (m = 2, 4, 8; lambda >= 1e-6). In
+ * Same partition, arguments and outputs as aca_agg_run (2 <= m <= 32; lambda >= 1e-6). In
  * every subarray the boundary layer Gamma_0 (fixed class, weight |Gamma_0|) follows the
  * standard model and waits for the neighbouring subarrays; the (m-2) x (m-2) kernel runs the
  * BKL n-fold way (classes by flip probability, the selected kernel cell always flips), so no

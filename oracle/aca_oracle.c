@@ -838,10 +838,9 @@ int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, doubl
                    uint64_t seed, double init_q, uint64_t T_q32, int8_t* spins_out, uint64_t* T_out,
                    uint32_t* n_out, oracle_stats* st) {
     int64_t nx = dims[0], ny = dims[1];
-    if (m < 1 || (m & (m - 1)) || m > 8 || nx % m || ny % m || nx < 2 || ny < 2) return -1;
+    if (m < 1 || m > 32 || nx % m || ny % m || nx < 2 || ny < 2) return -1;
     if (!(lambda > 0) || !(beta >= 0) || (rule != 0 && rule != 1)) return -1;
-    int lg = 0;
-    while ((1 << lg) < m * m) lg++;
+    const uint64_t mm = (uint64_t)m * (uint64_t)m;
     const uint32_t tag_e = m == 1 ? 0u : 3u, tag_i = m == 1 ? 1u : 4u;
     int64_t mx = nx / m, my = ny / m, NC = mx * my, N = nx * ny;
     uint64_t thr[14];
@@ -873,7 +872,7 @@ int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, doubl
         uint32_t k = n[C];
         uint32_t ctr[4] = {k, (uint32_t)((uint64_t)C & 0xffffffffu), (uint32_t)((uint64_t)C >> 32), tag_e}, w[4];
         oracle_philox4x32_10(ctr, key, w);
-        int64_t l = lg == 0 ? 0 : (int64_t)(w[3] >> (32 - lg));   /* Step 2: uniform cell of C */
+        int64_t l = (int64_t)(((uint64_t)w[3] * mm) >> 32);       /* Step 2: uniform cell of C (P8) */
         int64_t X = C % mx, Y = C / mx;
         int64_t x = X * m + l % m, y = Y * m + l / m;
         int64_t c = y * nx + x;
@@ -910,7 +909,7 @@ int oracle_agg_run(const int64_t* dims, int m, double lambda, double beta, doubl
 }
 
 /* ---------------------------------------------------------------- modified BKL (P9)
- * every m x m subarray (m in {2, 4, 8}) of the 2-D torus runs the BKL
+ * every m x m subarray (2 <= m <= 32) of the 2-D torus runs the BKL
  * n-fold way on its kernel (the (m-2) x (m-2) interior) and the standard procedure on its
  * boundary layer Gamma_0 (fixed class, weight |Gamma_0|, may or may not change; waits for the
  * neighbouring subarrays like fig:amcpoi). Kernel classes Gamma_k are the P4 table indices
@@ -952,7 +951,7 @@ int oracle_bkl_run(const int64_t* dims, int m, double lambda, double beta, doubl
                    uint64_t seed, double init_q, uint64_t T_q32, int8_t* spins_out, uint64_t* T_out,
                    uint32_t* n_out, oracle_stats* st) {
     int64_t nx = dims[0], ny = dims[1];
-    if ((m != 2 && m != 4 && m != 8) || nx % m || ny % m || nx < 2 || ny < 2) return -1;
+    if (m < 2 || m > 32 || nx % m || ny % m || nx < 2 || ny < 2) return -1;
     if (!(lambda > 0) || !(beta >= 0) || (rule != 0 && rule != 1)) return -1;
     int64_t mx = nx / m, my = ny / m, NC = mx * my, N = nx * ny;
     uint64_t thr[14];
@@ -963,7 +962,7 @@ int oracle_bkl_run(const int64_t* dims, int m, double lambda, double beta, doubl
     uint64_t* T = (uint64_t*)malloc((size_t)NC * 8);
     uint32_t* n = (uint32_t*)calloc((size_t)NC, 4);
     uint32_t* H = (uint32_t*)malloc((size_t)NC * 4);
-    int cls[64];
+    int cls[1024];
     if (!s || !T || !n || !H) { free(s); free(T); free(n); free(H); return -1; }
     for (int64_t c = 0; c < N; c++) {
         uint32_t ctr[4] = {0, (uint32_t)((uint64_t)c & 0xffffffffu), (uint32_t)((uint64_t)c >> 32), 1u}, w[4];

@@ -1698,8 +1698,8 @@ static int agg_run_impl(bool bkl, const int64_t* dims, int m, double lambda, dou
                         uint64_t seed, double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out,
                         uint32_t* n_out, aca_agg_stats* st, int device) {
     if (!dims) return fail(ACA_EINVAL, "null dims");
-    if (m != 1 && m != 2 && m != 4 && m != 8) return fail(ACA_EINVAL, "m must be 1, 2, 4 or 8");
-    if (bkl && m == 1) return fail(ACA_EINVAL, "modified BKL needs m = 2, 4 or 8");
+    if (m < 1 || m > 32) return fail(ACA_EINVAL, "m must be in [1, 32]");
+    if (bkl && m == 1) return fail(ACA_EINVAL, "modified BKL needs m >= 2");
     if (bkl && !(lambda >= 1e-6)) return fail(ACA_EINVAL, "modified BKL needs lambda >= 1e-6");
     const int64_t nx = dims[0], ny = dims[1];
     if (nx < 2 || ny < 2 || nx % m || ny % m || nx * ny > ((int64_t)1 << 32) || nx > (1 << 30) || ny > (1 << 30))
@@ -1716,8 +1716,6 @@ static int agg_run_impl(bool bkl, const int64_t* dims, int m, double lambda, dou
     if (device >= 0) CK(cudaSetDevice(device));
     AggParams A{};
     A.nx = (int)nx; A.ny = (int)ny; A.m = m;
-    A.lg = 0;
-    while ((1 << A.lg) < m * m) ++A.lg;
     A.mx = (int)(nx / m); A.my = (int)(ny / m);
     philox_round_keys((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), A.rk);
     A.inv = (unsigned long long)std::floor(4294967296.0 / (lambda * (double)(m * m)) + 0.5);
@@ -1732,12 +1730,8 @@ static int agg_run_impl(bool bkl, const int64_t* dims, int m, double lambda, dou
     A.thr_init = (unsigned long long)std::floor(init_q * 4294967296.0);
     BklExtra E{};
     E.lambda = lambda;
-    for (int l = 0; l < m * m; ++l) {
-        const int i = l % m, j = l / m;
-        if (i == 0 || j == 0 || i == m - 1 || j == m - 1) E.B |= 1ull << l;
-        else E.K |= 1ull << l;
-    }
-    E.W0 = (unsigned long long)__builtin_popcountll(E.B) << 32;
+    E.kcol = m > 2 ? (((1u << (m - 1)) - 1u) & ~1u) : 0u;   // columns 1 .. m - 2
+    E.W0 = (unsigned long long)(4 * m - 4) << 32;
     const int64_t NC = (int64_t)A.mx * A.my;
     unsigned long long* dlr = nullptr;
     AggAcc* dacc = nullptr;
@@ -1746,12 +1740,12 @@ static int agg_run_impl(bool bkl, const int64_t* dims, int m, double lambda, dou
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     auto cleanup = [&]() {
         if (str) cudaStreamSynchronize(str);
-        cudaFree(A.mask); cudaFree(A.T); cudaFree(A.n); cudaFree(dlr); cudaFree(dacc); cudaFree(dsp);
+        cudaFree(A.rows); cudaFree(A.T); cudaFree(A.n); cudaFree(dlr); cudaFree(dacc); cudaFree(dsp);
         if (e0) cudaEventDestroy(e0);
         if (e1) cudaEventDestroy(e1);
         if (str) cudaStreamDestroy(str);
     };
-    if (cudaMalloc(&A.mask, NC * 8) != cudaSuccess || cudaMalloc(&A.T, NC * 8) != cudaSuccess ||
+    if (cudaMalloc(&A.rows, (size_t)NC * m * 4) != cudaSuccess || cudaMalloc(&A.T, NC * 8) != cudaSuccess ||
         cudaMalloc(&A.n, NC * 4) != cudaSuccess || cudaMalloc(&dlr, sizeof(ACA_NLOG_LR)) != cudaSuccess ||
         cudaMalloc(&dacc, sizeof(AggAcc)) != cudaSuccess) {
         cleanup();

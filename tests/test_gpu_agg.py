@@ -19,7 +19,8 @@ def _same(g, o):
 
 
 @pytest.mark.parametrize("dims,m", [((64, 64), 8), ((64, 48), 4), ((40, 24), 2), ((16, 16), 1), ((8, 8), 8),
-                                    ((16, 8), 8), ((12, 6), 2), ((256, 128), 8)])
+                                    ((16, 8), 8), ((12, 6), 2), ((256, 128), 8), ((9, 6), 3), ((48, 36), 12),
+                                    ((120, 120), 24), ((384, 384), 12), ((96, 64), 32)])
 @pytest.mark.parametrize("rule", [0, 1])
 def test_agg_bit_identical(aca, oracle_mod, dims, m, rule):
     kw = dict(beta=0.44 if rule == 0 else 0.6, h=0.0 if rule == 0 else 0.1, rule=rule, seed=5 + m)
@@ -45,13 +46,14 @@ def test_agg_m1_equals_main_path(aca, oracle_mod):
 
 
 def test_agg_rejects_bad_arguments(aca):
-    for dims, m in (((10, 8), 4), ((8, 8), 3), ((8, 8), 16)):
+    for dims, m in (((10, 8), 4), ((8, 8), 3), ((8, 8), 16), ((66, 66), 33)):
         with pytest.raises(aca.AcaError):
             aca.aca_agg_run(dims, m, 1.0)
 
 
 @pytest.mark.parametrize("dims,m", [((64, 64), 8), ((64, 48), 4), ((40, 24), 2), ((8, 8), 8), ((16, 8), 8),
-                                    ((256, 128), 8), ((4, 4), 4)])
+                                    ((256, 128), 8), ((4, 4), 4), ((9, 6), 3), ((48, 36), 12), ((120, 120), 24),
+                                    ((96, 64), 32)])
 @pytest.mark.parametrize("rule", [0, 1])
 def test_bkl_bit_identical(aca, oracle_mod, dims, m, rule):
     """Modified BKL: bit-identical to its serial oracle for the partition."""

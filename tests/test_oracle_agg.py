@@ -26,7 +26,6 @@ def test_agg_m1_is_the_main_oracle(oracle_mod, dims, rule, h):
 
 def _stream(seed, C, m, lam, T_end):
     """(T, n) of subarray C from its own stream (P8), without the simulation."""
-    lg = (m * m).bit_length() - 1
     tag_e, tag_i = (0, 1) if m == 1 else (3, 4)
     inv = int(np.floor(4294967296.0 / (lam * m * m) + 0.5))
     key = (seed & 0xFFFFFFFF, seed >> 32)
@@ -59,7 +58,6 @@ def _random_order(dims, m, T, beta, seed, rule, h, choice_seed):
     nx, ny = dims
     mx, my = nx // m, ny // m
     NC = mx * my
-    lg = (m * m).bit_length() - 1
     tag_e, tag_i = (0, 1) if m == 1 else (3, 4)
     key = (seed & 0xFFFFFFFF, seed >> 32)
     inv = int(np.floor(4294967296.0 / (m * m) + 0.5))
@@ -80,7 +78,7 @@ def _random_order(dims, m, T, beta, seed, rule, h, choice_seed):
             if Tt[C] >= Tend:
                 continue
             w = O.philox((n[C], C, 0, tag_e), key)
-            l = 0 if lg == 0 else w[3] >> (32 - lg)
+            l = (w[3] * m * m) >> 32                     # P8 Step 2 (= w3 >> (32 - log2 m^2) for powers of 2)
             X, Y = C % mx, C // mx
             x, y = X * m + l % m, Y * m + l // m
             ok = True
@@ -102,7 +100,7 @@ def _random_order(dims, m, T, beta, seed, rule, h, choice_seed):
     return s.astype(np.int8), np.array(Tt, np.uint64), np.array(n, np.uint32)
 
 
-@pytest.mark.parametrize("dims,m", [((8, 8), 2), ((8, 4), 4), ((6, 6), 2)])
+@pytest.mark.parametrize("dims,m", [((8, 8), 2), ((8, 4), 4), ((6, 6), 2), ((9, 6), 3), ((24, 12), 12)])
 def test_agg_order_independence(oracle_mod, dims, m):
     sp, Tt, n, st = oracle_mod.agg_run(dims, m, 4.0, beta=0.5, seed=17, rule=1, h=0.1)
     for cs in (1, 2):
@@ -269,7 +267,7 @@ def _bkl_random_order(dims, m, T, beta, h, rule, seed, choice_seed):
     return s.astype(np.int8), np.array(Tt, np.uint64), np.array(n, np.uint32)
 
 
-@pytest.mark.parametrize("dims,m", [((8, 8), 4), ((16, 8), 8), ((8, 8), 2)])
+@pytest.mark.parametrize("dims,m", [((8, 8), 4), ((16, 8), 8), ((8, 8), 2), ((9, 6), 3), ((24, 12), 12)])
 def test_bkl_order_independence(oracle_mod, dims, m):
     sp, Tt, n, st = oracle_mod.agg_run(dims, m, 3.0, beta=0.6, h=0.1, rule=1, seed=31, bkl=True)
     s2, T2, n2 = _bkl_random_order(dims, m, 3.0, 0.6, 0.1, 1, 31, 7)
