@@ -171,6 +171,7 @@ struct aca_sim {
     size_t smem = 0;
     int persistent_ctas = 0;       // > 0: grid size of the persistent tile kernel
     void* kern = nullptr;          // selected tile/whole kernel
+    void* kern_gen = nullptr;      // its instance with the general arrival (launched when !KParams::fast)
     int nthreads = 256;
     cudaGraphExec_t graph = nullptr;
     int graph_rounds = 0;
@@ -260,8 +261,10 @@ int bits_for(uint64_t v) {
 // fig:s1c1pe reference (sync_rounds = 1).
 struct TileKey {
     int ndim, tx, ty, tz, ntg;
-    void* fn;         // production kernel
+    void* fn;         // production kernel (the fast arrival only: Poisson law, lambda = 1, no ties/frames)
     void* fn_early;   // with the a10 early-rejection path
+    void* fn_gen;     // the same two with the general arrival compiled in (any law, lambda, ties, frames)
+    void* fn_early_gen;
     void* fn_life;    // with the Moore neighbourhood (rule 2, 2-D only; nullptr in 3-D)
     void* fn_sync;    // fig:s1c1pe reference kernel
     size_t smem, smem_early, smem_sync;
@@ -270,9 +273,11 @@ struct TileKey {
 
 #define TKG(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS)                                              \
     {ND, TX, TY, TZ, NTG,                                                                              \
-     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, false>,                             \
-     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, true, false>,                            \
-     (ND == 2 ? (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, (ND == 2)> : nullptr),   \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, false, false>,                      \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, true, false, false>,                     \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, false, true>,                       \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, true, false, true>,                      \
+     (ND == 2 ? (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, (ND == 2), true> : nullptr), \
      (void*)tile_sync_kernel<ND, TX, TY, TZ, NTS>,                                                     \
      grp_smem_bytes(ND, TX, TY, TZ, NTG, NG, NBUF, false), grp_smem_bytes(ND, TX, TY, TZ, NTG, NGE, NBUFE, true), \
      sync_smem_bytes(ND, TX, TY, TZ, NTS), NTG * NG, NTG * NGE, NTS}
@@ -392,7 +397,8 @@ int launch_round(aca_sim* S) {
                                       : ((sh.tiles_x + 1) / 2) * sh.tiles_y * sh.tiles_z;
             dim3 grid = S->whole ? dim3(1)
                                  : dim3(S->persistent_ctas > 0 ? std::min(ntiles, S->persistent_ctas) : ntiles);
-            CK(cudaLaunchKernel(S->kern, grid, dim3(S->nthreads), args, S->smem, S->stream));
+            void* fn = (S->kern_gen && !P.fast) ? S->kern_gen : S->kern;
+            CK(cudaLaunchKernel(fn, grid, dim3(S->nthreads), args, S->smem, S->stream));
             if (S->sync_debug) {   // ACA_SYNC_DEBUG=1: locate a failing launch (no graphs)
                 cudaError_t e = cudaStreamSynchronize(S->stream);
                 if (e != cudaSuccess && S->h_dbg && S->h_dbg[0])
@@ -826,6 +832,10 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         } else {
             const bool early = opt.early_reject != 0 && rule != ACA_LIFE;
             S->kern = rule == ACA_LIFE ? sel->fn_life : early ? sel->fn_early : sel->fn;
+            S->kern_gen = rule == ACA_LIFE ? nullptr : early ? sel->fn_early_gen : sel->fn_gen;
+            if (S->kern_gen &&
+                cudaFuncSetAttribute(S->kern_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
+                return bail(fail(ACA_ECUDA, "smem attribute (tile, general)"));
             S->nthreads = early ? sel->nt_early : sel->nt;
             S->smem = early ? sel->smem_early : sel->smem;
             if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)

@@ -123,7 +123,10 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
 // the neighbour row of the next (1.5 loads per cell instead of 5). COLMAP (3-D, 32-wide tiles,
 // one z-plane per warp): lane l owns column l of the warp's plane. Otherwise lane l owns
 // tile-linear cells wbase + l + 32 j.
-template <int NDIM, int TX, int TY, int TZ, int NTG, bool FULL, bool EARLY, bool MOORE>
+// GEN: the general arrival (any law, lambda, tie stress, frames, N >= 2^32) is compiled in; without
+// it only the fast arrival is (P.fast holds; the host picks the instance per launch), which keeps
+// the general path's code out of the production kernel's register allocation.
+template <int NDIM, int TX, int TY, int TZ, int NTG, bool FULL, bool EARLY, bool MOORE, bool GEN>
 __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned long long* S, unsigned short* q, int wg,
                                                     uint32_t thr_a, const unsigned long long* thr,
                                                     const unsigned long long* thm, const NlogSmem& tab, int x0, int y0,
@@ -418,7 +421,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
         }
         __syncwarp();
-        if ((PAIRMAP || COLMAP) && !EARLY && P.fast) {
+        if ((PAIRMAP || COLMAP) && !EARLY && (!GEN || P.fast)) {
             // The common case (64-wide 2-D / 32-wide 3-D tiles, Poisson, lambda = 1, no frames):
             // the queue, the words and the tables are addressed with 32-bit shared-window offsets.
             const uint32_t qa = smem_u32(q), sa = smem_u32(S);
@@ -464,10 +467,10 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 if (EARLY) {
                     int gx, gy, gz;
                     gcoord(o, gx, gy, gz);
-                    if (P.fast)
+                    if (!GEN || P.fast)
                         commit_loop<NDIM, SX, SXY, true>(P, VS, s, cell_id32t<NDIM>(g, x0 + lx, y0 + ly, z0 + lz), thr_a,
                                                          thr, thm, tab, wlim, st, gx, gy, gz);
-                    else
+                    else if constexpr (GEN)
                         commit_loop<NDIM, SX, SXY>(P, VS, s, cell_id(g, x0 + lx, y0 + ly, z0 + lz), thr_a, thr, thm,
                                                    tab, wlim, st, gx, gy, gz);
                     continue;
@@ -479,7 +482,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 if (MOORE)
                     ones += (VH[2 * (s - SX - 1)] & 1u) + (VH[2 * (s - SX + 1)] & 1u) + (VH[2 * (s + SX - 1)] & 1u) +
                             (VH[2 * (s + SX + 1)] & 1u);
-                if (P.fast) {   // Poisson law, lambda = 1, no tie stress, no frames, N < 2^32
+                if (!GEN || P.fast) {   // Poisson law, lambda = 1, no tie stress, no frames, N < 2^32
                     const FireOut f = fire_fast(w, ones, Z, cell_id32t<NDIM>(g, x0 + lx, y0 + ly, z0 + lz), g, thr_a,
                                                 tab, P.rk, P.do_hash);
                     if (!f.ok) { atomicOr(&P.ctl->overflow, 1u); continue; }
@@ -489,13 +492,15 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                     ++fi32;
                     continue;
                 }
-                const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, tab, P.rk,
-                                       P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
-                if (!f.ok) continue;
-                VS[s] = f.wnew;
-                st.hacc += f.h;
-                st.flips += f.flip;
-                ++st.fired;
+                if constexpr (GEN) {
+                    const FireOut f = fire(w, ones, Z, cell_id(g, x0 + lx, y0 + ly, z0 + lz), g, thr, tab, P.rk,
+                                           P.inv_lambda, P.tie_bits, P.do_hash, P.ctl, P.law, &P.fr);
+                    if (!f.ok) continue;
+                    VS[s] = f.wnew;
+                    st.hacc += f.h;
+                    st.flips += f.flip;
+                    ++st.fired;
+                }
             }
         }
         ACA_TRACE(5, r);
@@ -517,7 +522,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
 }
 
 // ------------------------------------------------------------ grouped persistent tile kernel
-template <int NDIM, int TX, int TY, int TZ, int NTG, int NG, int NBUF, bool EARLY, bool MOORE>
+template <int NDIM, int TX, int TY, int TZ, int NTG, int NG, int NBUF, bool EARLY, bool MOORE, bool GEN>
 __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) {
     static_assert(!MOORE || NDIM == 2, "Moore neighbourhood: 2-D");
     static_assert(NG >= 1 && NG <= 15 && NBUF >= 1 && 1 + 2 * NG + NBUF <= 32, "groups / buffers");
@@ -772,10 +777,10 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
 
         if (o.valid) {
             const unsigned int rounds =
-                o.full ? tile_rounds<NDIM, TX, TY, TZ, NTG, true, EARLY, MOORE>(P, S, q, wg, thr_a, thr, thm, tab, o.x0,
-                                                                               o.y0, o.z0, wlim, st)
-                       : tile_rounds<NDIM, TX, TY, TZ, NTG, false, EARLY, MOORE>(P, S, q, wg, thr_a, thr, thm, tab, o.x0,
-                                                                                o.y0, o.z0, wlim, st);
+                o.full ? tile_rounds<NDIM, TX, TY, TZ, NTG, true, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
+                                                                                    o.x0, o.y0, o.z0, wlim, st)
+                       : tile_rounds<NDIM, TX, TY, TZ, NTG, false, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
+                                                                                     o.x0, o.y0, o.z0, wlim, st);
             rounds_max = rounds > rounds_max ? rounds : rounds_max;
             tot.fold(st);
             if (fast) {
