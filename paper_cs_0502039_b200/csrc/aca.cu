@@ -833,13 +833,13 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
             const bool early = opt.early_reject != 0 && rule != ACA_LIFE;
             S->kern = rule == ACA_LIFE ? sel->fn_life : early ? sel->fn_early : sel->fn;
             S->kern_gen = rule == ACA_LIFE ? nullptr : early ? sel->fn_early_gen : sel->fn_gen;
-            if (S->kern_gen &&
-                cudaFuncSetAttribute(S->kern_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
-                return bail(fail(ACA_ECUDA, "smem attribute (tile, general)"));
             S->nthreads = early ? sel->nt_early : sel->nt;
             S->smem = early ? sel->smem_early : sel->smem;
             if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
                 return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
+            if (S->kern_gen &&
+                cudaFuncSetAttribute(S->kern_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
+                return bail(fail(ACA_ECUDA, "smem attribute (tile, general arrival)"));
             int nsm = 0, occ = 0;
             cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
             if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->kern, S->nthreads, S->smem) != cudaSuccess || occ < 1)
