@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--tile", type=str, default="", help="e.g. 64x64 or 32x16x8")
     ap.add_argument("--launches-per-check", type=int, default=0)
     ap.add_argument("--early-reject", type=int, default=-1, help="a10 early rejection (-1 = config default)")
+    ap.add_argument("--class-book", type=int, default=-1, help="a10 per-tile class bookkeeping (-1 = config default)")
+    ap.add_argument("--class-wmax", type=float, default=None, help="a10 path iff a tile's mean flip probability <= this")
     ap.add_argument("--checkerboard", type=int, default=0, help="1/0 = checkerboard sweeps (default), -1 = off")
     ap.add_argument("--transport", default="ipc", choices=["ipc", "nccl"],
                     help="N>1 halo transport: kernel stores into CUDA-IPC-mapped neighbour halos (push "
@@ -285,6 +287,10 @@ def main():
     opts.update(cfg.get("opts", {}))
     if args.early_reject >= 0:
         opts["early_reject"] = args.early_reject
+    if args.class_book >= 0:
+        opts["class_book"] = args.class_book
+    if args.class_wmax is not None:
+        opts["class_wmax"] = args.class_wmax
     if args.rounds:
         opts["rounds_per_launch"] = args.rounds
     if args.launches_per_check:
@@ -332,9 +338,12 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     arrivals = tested = fired = launches = kl = 0
+    v_early = v_plain = 0
     ks = 0.0
     for k in range(args.steps):
         st = step(args.seed + k)
+        v_early += st["tile_visits_early"]
+        v_plain += st["tile_visits_plain"]
         arrivals += st["arrivals"]
         tested += st["cells_tested"]
         fired += st["cells_fired"]
@@ -398,6 +407,10 @@ def main():
             "roofline": roof,
             "roofline_issue": issue_roofline(args.config),
             "firing_fraction": fired / tested if tested else None,
+            "a10": {"early_reject": int(opts.get("early_reject", 0)), "class_book": int(opts.get("class_book", 0)),
+                    "class_wmax": opts.get("class_wmax"),
+                    "tile_visits_early_per_step": v_early // args.steps,
+                    "tile_visits_plain_per_step": v_plain // args.steps},
             "arrivals_per_cell_per_sweep": (fired / launches / n_local) if launches else None,
             "gpu_launches": int(kl + 2 * args.steps),
             "clocks": clk}

@@ -113,6 +113,17 @@ typedef struct {
                                    inter-arrival time 1/lambda. A scheduling
                                    bound only: same results; 0 (default) = unbounded. Not with
                                    multi-process handles. */
+    int32_t class_book;         /* 1: per-tile BKL class bookkeeping (a10 as north_star words it;
+                                   classes (s, Sigma) in the P4 index): every
+                                   tile visit recounts the classes of the tile's cells when it
+                                   writes them back, and each visit of a tile takes the a10
+                                   early-rejection path (with early_reject = 1) iff the tile's
+                                   mean flip probability per arrival at its last visit,
+                                   sum_k |Gamma_k| p_k / cells (the n-fold-way rate per cell over
+                                   lambda), is at most class_wmax; otherwise
+                                   the plain test. Both paths are exact: same results. Needs the
+                                   default tile shape and an Ising rule. 0 (default) = off. */
+    double class_wmax;          /* see class_book; < 0 = never the a10 path, >= 1 = always */
 } aca_options;
 
 typedef struct {
@@ -134,6 +145,8 @@ typedef struct {
                                  (Sigma+z)/2 + (z+1)(s+1)/2 as the P4 table */
     double nfold_rate;        /* lambda * sum_k |Gamma_k| p_k: the total flip rate of the BKL
                                  n-fold way */
+    uint64_t tile_visits_early; /* class_book: tile visits that took the a10 path ... */
+    uint64_t tile_visits_plain; /* ... and the plain test (0 without class_book) */
 } aca_stats;
 
 /* Fill *opt with defaults (struct_size set). */
@@ -163,6 +176,19 @@ int aca_get_cells(aca_sim* s, const int64_t* idx, size_t m, int8_t* spins, uint6
 int aca_get_stats(aca_sim* s, aca_stats* out);
 /* P4 table: count = 10 (2-D) or 14 (3-D), index (Sigma+z)/2 + (z+1)(s+1)/2. */
 int aca_get_flip_table(const aca_sim* s, uint64_t* thr, size_t count);
+/* Tile grid of the persistent tile kernel: out[0..6] = tiles along x, y, z of one shard,
+ * shards on this handle, tile extents x, y, z. ACA_ESTATE for whole-lattice / sync handles. */
+int aca_get_tile_grid(const aca_sim* s, int64_t* out);
+/* a10 per-tile class bookkeeping (aca_options.class_book = 1, north_star
+ * "per-tile Bortz-Kalos-Lebowitz n-fold-way class bookkeeping"): for every tile (shard-major,
+ * then (tz * tiles_y + ty) * tiles_x + tx) 16 u32, the number of the tile's cells in BKL class k
+ * = (Sigma+z)/2 + (z+1)(s+1)/2 (k < 10 in 2-D, < 14 in 3-D; the rest 0). count = 16 x tiles.
+ * refresh = 0: the histograms as the kernels keep them, each tile's classes counted when its
+ * last visit wrote it back (a tile whose neighbours fired after that visit may differ from
+ * the current state at its boundary cells). refresh = 1: recounted from the current state
+ * first (exact; multi-process handles: against the halos of the last run). ACA_ESTATE when
+ * class_book is off. Synchronises. */
+int aca_get_tile_classes(aca_sim* s, uint32_t* out, size_t count, int refresh);
 
 /* Replace the state from host arrays (checkpoint / resume). Every t must be >= 1 and
  * below the packed-word limit, spins +-1. */

@@ -24,7 +24,8 @@ EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_
            "aca_get_times", "aca_get_counters", "aca_get_cells", "aca_get_stats", "aca_get_flip_table", "aca_set_state",
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
            "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q", "aca_ipc_export", "aca_ipc_import",
-           "aca_stage_spins", "aca_set_spins_staged", "aca_get_spins_async", "aca_sync", "aca_perfbl_run"]
+           "aca_stage_spins", "aca_set_spins_staged", "aca_get_spins_async", "aca_sync", "aca_perfbl_run",
+           "aca_get_tile_grid", "aca_get_tile_classes"]
 ACA_IPC_BLOB_BYTES = 192
 DEFAULT_ROUNDS = 5   # in-tile rounds per tile visit when aca_options.rounds_per_launch = 0 (aca.cu)
 POISSON, UNIFORM, ROOT8, GAUSS = 0, 1, 2, 3   # asynchrony laws (aca_options.law)
@@ -46,7 +47,7 @@ class aca_options(ctypes.Structure):
                 ("whole_lattice", ctypes.c_int32), ("variant", ctypes.c_int32),
                 ("early_reject", ctypes.c_int32), ("checkerboard", ctypes.c_int32),
                 ("law", ctypes.c_int32), ("halo_mode", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
-                ("lag", ctypes.c_double)]
+                ("lag", ctypes.c_double), ("class_book", ctypes.c_int32), ("class_wmax", ctypes.c_double)]
 
 
 class aca_stats(ctypes.Structure):
@@ -57,7 +58,8 @@ class aca_stats(ctypes.Structure):
                 ("gpu_seconds", ctypes.c_double), ("kernel_seconds", ctypes.c_double),
                 ("kernel_launches", ctypes.c_uint64), ("time_bits", ctypes.c_int32),
                 ("counter_bits", ctypes.c_int32), ("rank_bits", ctypes.c_int32),
-                ("class_hist", ctypes.c_uint64 * 14), ("nfold_rate", ctypes.c_double)]
+                ("class_hist", ctypes.c_uint64 * 14), ("nfold_rate", ctypes.c_double),
+                ("tile_visits_early", ctypes.c_uint64), ("tile_visits_plain", ctypes.c_uint64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
@@ -97,6 +99,8 @@ def lib():
     L.aca_get_stats.argtypes = [vp, ctypes.POINTER(aca_stats)]
     L.aca_get_cells.argtypes = [vp, vp, ctypes.c_size_t, vp, vp, vp]
     L.aca_get_flip_table.argtypes = [vp, vp, ctypes.c_size_t]
+    L.aca_get_tile_grid.argtypes = [vp, vp]
+    L.aca_get_tile_classes.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_int]
     L.aca_set_state.argtypes = [vp, vp, vp, vp, ctypes.c_size_t]
     L.aca_reset.argtypes = [vp, ctypes.c_uint64]
     L.aca_nccl_unique_id.argtypes = [vp]
@@ -220,6 +224,21 @@ def aca_get_flip_table(p, ndim):
     a = (ctypes.c_uint64 * n)()
     _check(lib().aca_get_flip_table(p, a, n))
     return [int(v) for v in a]
+
+
+def aca_get_tile_grid(p):
+    """(tiles_x, tiles_y, tiles_z, shards, tile_x, tile_y, tile_z)"""
+    a = (ctypes.c_int64 * 7)()
+    _check(lib().aca_get_tile_grid(p, a))
+    return tuple(int(v) for v in a)
+
+
+def aca_get_tile_classes(p, refresh=0):
+    """a10 per-tile BKL class histograms: uint32 array [shards, tiles_z, tiles_y, tiles_x, 16]."""
+    tx, ty, tz, G = aca_get_tile_grid(p)[:4]
+    out = np.empty((G, tz, ty, tx, 16), np.uint32)
+    _check(lib().aca_get_tile_classes(p, _ptr(out), out.size, int(refresh)))
+    return out
 
 
 def aca_set_state(p, spins, times, counters):
@@ -440,6 +459,9 @@ class Sim:
 
     def flip_table(self):
         return aca_get_flip_table(self._p, self.ndim)
+
+    def tile_classes(self, refresh=0):
+        return aca_get_tile_classes(self._p, refresh)
 
     def set_state(self, spins, times, counters):
         aca_set_state(self._p, spins, times, counters)

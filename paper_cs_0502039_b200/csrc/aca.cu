@@ -112,6 +112,7 @@ struct Shard {
     size_t n = 0;          // owned cells
     size_t face = 0;       // cells of one row / plane of the sharded axis
     int tiles_x = 1, tiles_y = 1, tiles_z = 1;
+    unsigned int* tile_hist = nullptr;      // a10 class bookkeeping: 16 u32 per tile (class_book)
 };
 
 }  // namespace
@@ -135,6 +136,9 @@ struct aca_sim {
     unsigned long long inv_lambda = 1ull << 32;
     unsigned long long thr[14] = {};
     unsigned long long thm[98] = {};   // a10 early-rejection table (see commit_loop)
+    bool cls = false;                  // a10 per-tile class bookkeeping (aca_options.class_book)
+    bool cls_stale = true;             // the tile histograms must be recounted before the next run
+    long long cls_lim = -1;            // early path iff sum_k |Gamma_k| floor(p_k 2^16) <= cls_lim
     int bulk = 1;
     unsigned long long thr_init = 0;
     unsigned long long max_delta = 0;
@@ -269,23 +273,34 @@ struct TileKey {
     void* fn_sync;    // fig:s1c1pe reference kernel
     size_t smem, smem_early, smem_sync;
     int nt, nt_early, nt_sync;
+    void* fn_cls;     // a10 path chosen per tile from its class histogram (default shapes only)
+    void* fn_cls_gen;
+    size_t smem_cls;
 };
 
-#define TKG(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS)                                              \
+#define TKG_BASE(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS)                                         \
     {ND, TX, TY, TZ, NTG,                                                                              \
-     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, false, false>,                      \
-     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, true, false, false>,                     \
-     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, false, true>,                       \
-     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, true, false, true>,                      \
-     (ND == 2 ? (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, false, (ND == 2), true> : nullptr), \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, 0, false, false>,                          \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, 1, false, false>,                        \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, 0, false, true>,                           \
+     (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, 1, false, true>,                         \
+     (ND == 2 ? (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NG, NBUF, 0, (ND == 2), true> : nullptr), \
      (void*)tile_sync_kernel<ND, TX, TY, TZ, NTS>,                                                     \
      grp_smem_bytes(ND, TX, TY, TZ, NTG, NG, NBUF, false), grp_smem_bytes(ND, TX, TY, TZ, NTG, NGE, NBUFE, true), \
-     sync_smem_bytes(ND, TX, TY, TZ, NTS), NTG * NG, NTG * NGE, NTS}
+     sync_smem_bytes(ND, TX, TY, TZ, NTS), NTG * NG, NTG * NGE, NTS
+#define TKG(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS) \
+    TKG_BASE(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS), nullptr, nullptr, 0}
+// shapes with the class-bookkeeping instance (the defaults and the few-tile 64x64 group size)
+#define TKGC(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS)                                       \
+    TKG_BASE(ND, TX, TY, TZ, NTG, NG, NBUF, NGE, NBUFE, NTS),                                      \
+        (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, 2, false, false>,                  \
+        (void*)tile_grp_kernel<ND, TX, TY, TZ, NTG, NGE, NBUFE, 2, false, true>,                   \
+        grp_smem_bytes(ND, TX, TY, TZ, NTG, NGE, NBUFE, true, true)}
 
 const TileKey kTiles[] = {
-    TKG(2, 64, 64, 1, 256, 4, 5, 4, 5, 256), TKG(2, 64, 64, 1, 512, 1, 2, 1, 2, 512),
+    TKGC(2, 64, 64, 1, 256, 4, 5, 4, 5, 256), TKGC(2, 64, 64, 1, 512, 1, 2, 1, 2, 512),
     TKG(2, 32, 32, 1, 256, 4, 8, 4, 8, 256), TKG(2, 64, 32, 1, 256, 4, 8, 4, 8, 256),
-    TKG(3, 32, 16, 8, 256, 3, 4, 3, 3, 256), TKG(3, 8, 8, 8, 128, 8, 12, 8, 12, 128),
+    TKGC(3, 32, 16, 8, 256, 3, 4, 3, 3, 256), TKG(3, 8, 8, 8, 128, 8, 12, 8, 12, 128),
     TKG(3, 16, 16, 16, 256, 3, 4, 3, 3, 256),
 };
 
@@ -347,7 +362,23 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
         P.row_par0 = t0 & 1;
     }
     for (int i = 0; i < 14; ++i) P.thr[i] = S->thr[i];
+    P.tile_hist = sh.tile_hist;
+    for (int i = 0; i < 16; ++i) P.clsw[i] = i < 14 ? (unsigned int)(S->thr[i] >> 16) : 0u;
+    P.cls_lim = S->cls_lim;
     return P;
+}
+
+// a10 class bookkeeping: recount every tile's class histogram from the current state
+int class_refresh(aca_sim* S) {
+    if (!S->cls) return ACA_OK;
+    for (auto& sh : S->shards) {
+        const KParams P = make_params(S, sh);
+        const int nt = sh.tiles_x * sh.tiles_y * sh.tiles_z;
+        class_refresh_kernel<256><<<nt, 256, 0, S->stream>>>(P, S->tile[0], S->tile[1], S->tile[2]);
+        CK(cudaGetLastError());
+    }
+    S->cls_stale = false;
+    return ACA_OK;
 }
 
 // exchange of the sharded-axis boundary rows/planes (virtual shards: D2D copies;
@@ -491,6 +522,7 @@ int init_peer_halos(aca_sim* S);
 
 // P5 initial state on the device + zeroed control blocks.
 int init_state(aca_sim* S) {
+    S->cls_stale = true;
     RoundKeys K;
     philox_round_keys((uint32_t)(S->seed & 0xffffffffu), (uint32_t)(S->seed >> 32), K.rk);
     for (auto& sh : S->shards) {
@@ -625,6 +657,7 @@ void aca_destroy(aca_sim* S) {
         cudaFree(sh.ctl);
         cudaFree(sh.stats_lo);
         cudaFree(sh.stats_hi);
+        cudaFree(sh.tile_hist);
     }
     if (S->comm && nccl().ok) nccl().destroy(S->comm);
     for (void* p : S->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -693,6 +726,10 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         return fail(ACA_EINVAL, "variant must be 0 (the kernel ablations of round 1 were retired; DESIGN.md section 6)");
     if (opt.max_ctas < 0) return fail(ACA_EINVAL, "max_ctas must be >= 0");
     if (!(opt.lag >= 0) || !std::isfinite(opt.lag)) return fail(ACA_EINVAL, "lag must be >= 0 and finite (0 = off)");
+    if (opt.class_book != 0 && opt.class_book != 1) return fail(ACA_EINVAL, "class_book must be 0 or 1");
+    if (opt.class_book && (rule == ACA_LIFE || opt.sync_rounds || opt.whole_lattice == 1))
+        return fail(ACA_EINVAL, "class_book needs the persistent tile kernel of an Ising rule");
+    if (!std::isfinite(opt.class_wmax)) return fail(ACA_EINVAL, "class_wmax must be finite");
 
     int64_t N = 1;
     for (int a = 0; a < ndim; ++a) {
@@ -791,7 +828,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
     cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, S->device);
     const bool single = (S->G == 1 && S->world == 1 && !S->use_nccl);
     S->whole = false;
-    if (single && opt.whole_lattice >= 0) {
+    if (single && opt.whole_lattice >= 0 && !opt.class_book) {
         const bool fits = whole_smem(N, S->sync) <= (size_t)dev_smem;
         if (opt.whole_lattice == 1 && !fits) return bail(fail(ACA_EINVAL, "lattice too large for whole_lattice"));
         S->whole = fits && (opt.whole_lattice == 1 || N <= 8192);
@@ -835,6 +872,19 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
             S->kern_gen = rule == ACA_LIFE ? nullptr : early ? sel->fn_early_gen : sel->fn_gen;
             S->nthreads = early ? sel->nt_early : sel->nt;
             S->smem = early ? sel->smem_early : sel->smem;
+            if (opt.class_book) {   // a10 per-tile class bookkeeping: the a10 or the plain path per tile visit
+                if (!sel->fn_cls)
+                    return bail(fail(ACA_EINVAL, "class_book needs the default tile (64x64 in 2-D, 32x16x8 in 3-D)"));
+                S->cls = true;
+                S->kern = sel->fn_cls;
+                S->kern_gen = sel->fn_cls_gen;
+                S->nthreads = sel->nt_early;
+                S->smem = sel->smem_cls;
+                // early path iff the tile's mean flip probability per arrival, sum_k |Gamma_k| p_k / cells,
+                // is at most class_wmax (early_reject = 0: never; the histograms are still kept)
+                const double cells = (double)tx * ty * tz, lim = std::floor(opt.class_wmax * 65536.0 * cells);
+                S->cls_lim = (!early || opt.class_wmax < 0) ? -1 : (long long)std::min(lim, 4.0e18);
+            }
             if (cudaFuncSetAttribute(S->kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->smem) != cudaSuccess)
                 return bail(fail(ACA_ECUDA, "smem attribute (tile)"));
             if (S->kern_gen &&
@@ -878,6 +928,9 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         sh.tiles_z = ndim == 3 ? (g.nz + S->tile[2] - 1) / S->tile[2] : 1;
         if (cudaMalloc(&sh.words, sh.n * 8) != cudaSuccess || cudaMalloc(&sh.ctl, sizeof(Ctl)) != cudaSuccess)
             return bail(fail(ACA_ENOMEM, "device allocation of %zu cells failed", sh.n));
+        if (S->cls &&
+            cudaMalloc(&sh.tile_hist, (size_t)sh.tiles_x * sh.tiles_y * sh.tiles_z * 16 * sizeof(unsigned int)) != cudaSuccess)
+            return bail(fail(ACA_ENOMEM, "tile class histograms"));
         if (g.sharded) {
             if (cudaMalloc(&sh.halo_lo, sh.face * 8) != cudaSuccess || cudaMalloc(&sh.halo_hi, sh.face * 8) != cudaSuccess)
                 return bail(fail(ACA_ENOMEM, "halo allocation failed"));
@@ -989,6 +1042,14 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         }
     } else if (S->push) {   // push mode: fill the halos once; the kernels keep them current
         rc = exchange(S);
+        if (rc) return rc;
+    }
+    if (S->cls && S->cls_stale) {   // the state was set from outside: recount the tiles' classes
+        if (!S->push && !S->ipc) {
+            rc = exchange(S);
+            if (rc) return rc;
+        }
+        rc = class_refresh(S);
         if (rc) return rc;
     }
     rc = build_graph(S);
@@ -1230,6 +1291,8 @@ int aca_get_stats(aca_sim* S, aca_stats* o) {
         o->inner_rounds += c.inner_rounds;
         o->cells_tested += c.tested;
         o->cells_fired += c.fired;
+        o->tile_visits_early += c.visits_early;
+        o->tile_visits_plain += c.visits_plain;
     }
     o->gpu_seconds = S->gpu_seconds;
     o->kernel_seconds = S->kernel_seconds;
@@ -1247,9 +1310,44 @@ int aca_get_stats(aca_sim* S, aca_stats* o) {
     return ACA_OK;
 }
 
+int aca_get_tile_grid(const aca_sim* S, int64_t* out) {
+    if (!S || !out) return fail(ACA_EINVAL, "null argument");
+    if (S->whole || S->sync || S->shards.empty()) return fail(ACA_ESTATE, "the handle runs no tile kernel");
+    const Shard& sh = S->shards[0];
+    out[0] = sh.tiles_x; out[1] = sh.tiles_y; out[2] = sh.tiles_z; out[3] = (int64_t)S->shards.size();
+    out[4] = S->tile[0]; out[5] = S->tile[1]; out[6] = S->tile[2];
+    return ACA_OK;
+}
+
+int aca_get_tile_classes(aca_sim* S, uint32_t* out, size_t count, int refresh) {
+    if (!S || !out) return fail(ACA_EINVAL, "null argument");
+    if (!S->cls) return fail(ACA_ESTATE, "class bookkeeping is off (aca_options.class_book = 0)");
+    size_t want = 0;
+    for (auto& sh : S->shards) want += (size_t)sh.tiles_x * sh.tiles_y * sh.tiles_z * 16;
+    if (count != want) return fail(ACA_EINVAL, "count %zu != %zu (16 per tile)", count, want);
+    CK(cudaSetDevice(S->device));
+    if (refresh || S->cls_stale) {
+        if (!S->ipc) {   // single process: the halos of sharded handles from the current rows
+            int rc = exchange(S);
+            if (rc) return rc;
+        }
+        int rc = class_refresh(S);
+        if (rc) return rc;
+    }
+    size_t off = 0;
+    for (auto& sh : S->shards) {
+        const size_t n = (size_t)sh.tiles_x * sh.tiles_y * sh.tiles_z * 16;
+        CK(cudaMemcpyAsync(out + off, sh.tile_hist, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, S->stream));
+        off += n;
+    }
+    CK(cudaStreamSynchronize(S->stream));
+    return ACA_OK;
+}
+
 int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const uint32_t* counters, size_t count) {
     int rc = check_count(S, count, spins);
     if (rc) return rc;
+    S->cls_stale = true;
     if (S->ipc) S->snap_valid = false;   // the neighbours' boundary rows are unknown until a run
     if (!times || !counters) return fail(ACA_EINVAL, "null times/counters");
     CK(cudaSetDevice(S->device));
@@ -1295,6 +1393,7 @@ int aca_set_state(aca_sim* S, const int8_t* spins, const uint64_t* times, const 
 int aca_set_spins(aca_sim* S, const int8_t* spins, size_t count) {
     int rc = check_count(S, count, spins);
     if (rc) return rc;
+    S->cls_stale = true;
     if (S->ipc) S->snap_valid = false;   // the neighbours' boundary rows are unknown until a run
     CK(cudaSetDevice(S->device));
     rc = ensure_scratch(S, CHUNK);
@@ -1347,6 +1446,7 @@ int aca_stage_spins(aca_sim* S, const int8_t* spins, size_t count, int slot) {
 
 int aca_set_spins_staged(aca_sim* S, int slot) {
     if (!S) return fail(ACA_EINVAL, "null handle");
+    S->cls_stale = true;
     if (S->ipc) S->snap_valid = false;
     if (slot < 0 || slot > 1) return fail(ACA_EINVAL, "slot must be 0 or 1");
     if (!S->cstream) return fail(ACA_ESTATE, "nothing staged (call aca_stage_spins first)");

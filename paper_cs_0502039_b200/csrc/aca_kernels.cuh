@@ -82,6 +82,7 @@ struct Ctl {                            // device control block, one per shard
     // is min(T, global minimum time + lag); wlim_T keeps T (termination counts cells below it)
     unsigned long long wlim_T;
     unsigned long long wmin[2];         // minimum word of the tiles of each colour at their last write-back
+    unsigned long long visits_early, visits_plain;   // a10 class bookkeeping: tile visits per path
 };
 
 struct Geo {
@@ -180,6 +181,11 @@ struct KParams {
     int fast;                            // fire_fast applies (law 0, lambda 1, no ties, no frames, N < 2^32)
     int life;                            // rule 2: asynchronous Game of Life (Moore neighbourhood, P10)
     unsigned long long lag_q;            // bounded lag in Q32 (0 = off)
+    // a10 per-tile class bookkeeping (tile_grp_kernel EM = 2): 16 u32 per tile (BKL classes in the
+    // P4 index), the class weights floor(p_k 2^16) and the early-path limit on sum_k |Gamma_k| w_k
+    unsigned int* tile_hist;
+    unsigned int clsw[16];
+    long long cls_lim;
     unsigned long long* dbg_trace;       // ACA_DEBUG: host-mapped stage trace (nullptr = off)
     unsigned long long* dbg_map;         // ACA_DEBUG: host-mapped record of the first failed check
 };

@@ -336,3 +336,31 @@ __global__ void __launch_bounds__(NT) stats_kernel(const KParams P, StatAcc* out
     (void)n_local;
 }
 
+
+// a10 per-tile class bookkeeping: the BKL class histogram (P4 index of (s, Sigma),
+// PAPER.md:1039-1045) of every tile of a shard from the current state, into P.tile_hist (16 u32
+// per tile, tile index (tz tiles_y + ty) tiles_x + tx as in tile_grp_kernel). Run when the state
+// is set from outside (create, reset, set_state/set_spins) and by aca_get_tile_classes with
+// refresh = 1; during runs the tile kernel recounts a tile at every visit. One CTA per tile.
+template <int NT>
+__global__ void __launch_bounds__(NT) class_refresh_kernel(const KParams P, int TX, int TY, int TZ) {
+    __shared__ unsigned int h[16];
+    const Geo& g = P.g;
+    if (threadIdx.x < 16) h[threadIdx.x] = 0u;
+    __syncthreads();
+    const int t = blockIdx.x;
+    const int tx = t % P.tiles_x, ty = (t / P.tiles_x) % P.tiles_y, tz = t / (P.tiles_x * P.tiles_y);
+    const uint32_t Z = 2 * g.ndim;
+    for (int i = threadIdx.x; i < TX * TY * TZ; i += NT) {
+        const int x = tx * TX + i % TX, y = ty * TY + (i / TX) % TY, z = tz * TZ + i / (TX * TY);
+        if (x >= g.nx || y >= g.ny || (g.ndim == 3 && z >= g.nz)) continue;
+        const unsigned long long w = *word_ptr_t<false>(P, x, y, z);
+        uint32_t o = (uint32_t)(*word_ptr_t<false>(P, x - 1, y, z) & 1ull) + (uint32_t)(*word_ptr_t<false>(P, x + 1, y, z) & 1ull) +
+                     (uint32_t)(*word_ptr_t<false>(P, x, y - 1, z) & 1ull) + (uint32_t)(*word_ptr_t<false>(P, x, y + 1, z) & 1ull);
+        if (g.ndim == 3)
+            o += (uint32_t)(*word_ptr_t<false>(P, x, y, z - 1) & 1ull) + (uint32_t)(*word_ptr_t<false>(P, x, y, z + 1) & 1ull);
+        atomicAdd(&h[o + (Z + 1) * (uint32_t)(w & 1ull)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 16) P.tile_hist[16 * (size_t)t + threadIdx.x] = h[threadIdx.x];
+}

@@ -38,9 +38,54 @@ __host__ __device__ constexpr int grp_slots(int ndim, int tx, int ty, int tz) {
 // phases armed on each buffer), the CTA's bounded-lag minimum and T limit (2 u64), the origin
 // of the tile in each buffer (32 B each), then the per-warp fire queues.
 __host__ __device__ constexpr size_t grp_smem_bytes(int ndim, int tx, int ty, int tz, int ntg, int ng, int nbuf,
-                                                    bool early) {
+                                                    bool early, bool cls = false) {
     return ((size_t)nbuf * grp_slots(ndim, tx, ty, tz) + 16 + 112 + 256 + 128 + (size_t)(ntg * ng) / 32 + nbuf) * 8 +
-           160 + 16 + (size_t)nbuf * 32 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15);
+           160 + 16 + (size_t)nbuf * 32 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15) +
+           (cls ? (size_t)ng * 2 * 16 * 4 : 0);
+}
+
+// a10 per-tile class bookkeeping: the BKL class (s, Sigma) of the cell pair (sl, sl + 1) of a
+// tile buffer (words v), from the spins of its neighbours in the buffer, added to the per-lane
+// class counters (8-bit fields: bins 0-7 in c0, 8-13 in c1; bin = (Sigma + z)/2 + (z + 1)(s + 1)/2
+// as the P4 index).
+__device__ __forceinline__ void cls_add(uint32_t b, unsigned long long& c0, unsigned long long& c1) {
+    const unsigned long long one = 1ull << (8u * (b & 7u));
+    if (b < 8u) c0 += one; else c1 += one;
+}
+template <int NDIM, int SX, int SXY>
+__device__ __forceinline__ void cls_pair(const volatile unsigned long long* VS, int sl, ulonglong2 v,
+                                         unsigned long long& c0, unsigned long long& c1) {
+    constexpr uint32_t Z = 2 * NDIM;
+    const uint32_t a = (uint32_t)(v.x & 1ull), b = (uint32_t)(v.y & 1ull);
+    const ulonglong2 up = lds128v(&VS[sl - SX]), dn = lds128v(&VS[sl + SX]);
+    uint32_t o0 = (uint32_t)(VS[sl - 1] & 1ull) + b + (uint32_t)(up.x & 1ull) + (uint32_t)(dn.x & 1ull);
+    uint32_t o1 = a + (uint32_t)(VS[sl + 2] & 1ull) + (uint32_t)(up.y & 1ull) + (uint32_t)(dn.y & 1ull);
+    if constexpr (NDIM == 3) {
+        const ulonglong2 zl = lds128v(&VS[sl - SXY]), zh = lds128v(&VS[sl + SXY]);
+        o0 += (uint32_t)(zl.x & 1ull) + (uint32_t)(zh.x & 1ull);
+        o1 += (uint32_t)(zl.y & 1ull) + (uint32_t)(zh.y & 1ull);
+    }
+    cls_add(o0 + (Z + 1) * a, c0, c1);
+    cls_add(o1 + (Z + 1) * b, c0, c1);
+}
+template <int NDIM, int SX, int SXY>
+__device__ __forceinline__ void cls_one(const volatile unsigned long long* VS, int s, unsigned long long w,
+                                        unsigned long long& c0, unsigned long long& c1) {
+    constexpr uint32_t Z = 2 * NDIM;
+    uint32_t o = (uint32_t)(VS[s - 1] & 1ull) + (uint32_t)(VS[s + 1] & 1ull) + (uint32_t)(VS[s - SX] & 1ull) +
+                 (uint32_t)(VS[s + SX] & 1ull);
+    if constexpr (NDIM == 3) o += (uint32_t)(VS[s - SXY] & 1ull) + (uint32_t)(VS[s + SXY] & 1ull);
+    cls_add(o + (Z + 1) * (uint32_t)(w & 1ull), c0, c1);
+}
+// warp sum of the per-lane counters, added to the group's histogram in shared memory
+template <int NBIN>
+__device__ __forceinline__ void cls_flush_warp(unsigned long long c0, unsigned long long c1, unsigned int* gh, int lane) {
+#pragma unroll
+    for (int b = 0; b < NBIN; ++b) {
+        const unsigned int v = (unsigned int)(((b < 8 ? c0 : c1) >> (8 * (b & 7))) & 255ull);
+        const unsigned int t = __reduce_add_sync(0xffffffffu, v);
+        if (lane == 0 && t) atomicAdd(&gh[b], t);
+    }
 }
 
 // Commit the pending arrivals of the cell in slot s for as long as that is exact (a10):
@@ -522,8 +567,15 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
 }
 
 // ------------------------------------------------------------ grouped persistent tile kernel
-template <int NDIM, int TX, int TY, int TZ, int NTG, int NG, int NBUF, bool EARLY, bool MOORE, bool GEN>
+// EM: 0 = the plain test; 1 = the a10 path on every tile; 2 = per-tile class bookkeeping (a10 as
+// north_star words it): every visit recounts the BKL classes of the tile's cells at its
+// write-back into P.tile_hist, and the next visit of the tile takes the a10 path iff the tile's
+// n-fold flip weight sum_k |Gamma_k| p_k is at most P.cls_lim.
+template <int NDIM, int TX, int TY, int TZ, int NTG, int NG, int NBUF, int EM, bool MOORE, bool GEN>
 __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) {
+    constexpr bool EARLY = EM != 0;   // queue sizing: a10 candidates
+    constexpr bool CLS = EM == 2;
+    constexpr int NBIN = 2 * (2 * NDIM + 1);
     static_assert(!MOORE || NDIM == 2, "Moore neighbourhood: 2-D");
     static_assert(NG >= 1 && NG <= 15 && NBUF >= 1 && 1 + 2 * NG + NBUF <= 32, "groups / buffers");
     constexpr int NT = NTG * NG;
@@ -555,6 +607,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     unsigned long long* lagw = (unsigned long long*)(cs + 32);   // [0] bounded lag: min word written back, [1] wlim_T
     int4* orgs = (int4*)(((uintptr_t)(cs + 40) + 15) & ~(uintptr_t)15);   // [2b], [2b+1]: origin of buffer b's tile
     unsigned short* Q = (unsigned short*)(orgs + 2 * NBUF); // NW x QW fire queue entries
+    // CLS: per group two 16-bin class histograms (the visit in progress, by the parity `par`)
+    unsigned int* ghist = (unsigned int*)((char*)Q + (((size_t)NW * QW * 2 + 15) & ~(size_t)15));
 
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -566,6 +620,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         Rt[i] = (unsigned int)P.lr[2 * i + 1];
     }
     if (tid < NBUF) { mbar_init(&bar[tid], 1); armed[tid] = 0u; }
+    if constexpr (CLS)
+        for (int i = tid; i < NG * 32; i += NT) ghist[i] = 0u;
     if (tid == 0) {
         cs[0] = 0u;
         lagw[0] = ~0ull;
@@ -585,7 +641,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     const bool vec_ok = (g.nx % 2) == 0;
     const bool reverse = P.phase < 0 && ((*(volatile unsigned long long*)&P.ctl->launches) & 1ull);
 
-    struct Org { int x0, y0, z0, tx, ty, tz; bool valid, full; };
+    struct Org { int x0, y0, z0, tx, ty, tz; bool valid, full, early; };
     auto origin = [&](int k) -> Org {
         const int it = (int)blockIdx.x + k * (int)gridDim.x;
         Org o;
@@ -600,8 +656,10 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         o.x0 = o.tx * TX; o.y0 = o.ty * TY; o.z0 = o.tz * TZ;
         o.valid = o.tx < P.tiles_x;   // odd tiles_x: the last column pair has one tile
         o.full = o.valid && o.x0 + TX <= g.nx && o.y0 + TY <= g.ny && (NDIM == 2 || o.z0 + TZ <= g.nz);
+        o.early = EM == 1;
         return o;
     };
+    auto tile_index = [&](const Org& o) { return ((size_t)o.tz * P.tiles_y + o.ty) * P.tiles_x + o.tx; };
     // Which staged words may another writer store while we copy them? Own rows: nobody (a tile
     // is processed by one group per launch). In a checkerboard launch the tiles adjacent to
     // ours have the other colour and are idle, except across a periodic wrap with an odd tile
@@ -642,13 +700,29 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     auto org_load = [&](int b) -> Org {
         const int4 a = orgs[2 * b], c = orgs[2 * b + 1];
         Org o;
-        o.x0 = a.x; o.y0 = a.y; o.z0 = a.z; o.tx = a.w; o.ty = c.x; o.tz = c.y; o.valid = c.z != 0; o.full = c.w != 0;
+        o.x0 = a.x; o.y0 = a.y; o.z0 = a.z; o.tx = a.w; o.ty = c.x; o.tz = c.y; o.valid = c.z != 0;
+        o.full = (c.w & 1) != 0;
+        o.early = EM == 1 || (c.w & 2) != 0;
         return o;
     };
     auto arm = [&](int k, int b) {
         const Org o = origin(k);
+        bool early = false;
+        if constexpr (CLS) {   // the tile's classes at its last visit decide its path for this one
+            if (o.valid) {
+                const uint4* hp = reinterpret_cast<const uint4*>(P.tile_hist + 16 * tile_index(o));
+                long long wsum = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint4 v = hp[j];
+                    wsum += (long long)v.x * P.clsw[4 * j] + (long long)v.y * P.clsw[4 * j + 1] +
+                            (long long)v.z * P.clsw[4 * j + 2] + (long long)v.w * P.clsw[4 * j + 3];
+                }
+                early = wsum <= P.cls_lim;
+            }
+        }
         orgs[2 * b] = make_int4(o.x0, o.y0, o.z0, o.tx);
-        orgs[2 * b + 1] = make_int4(o.ty, o.tz, o.valid ? 1 : 0, o.full ? 1 : 0);
+        orgs[2 * b + 1] = make_int4(o.ty, o.tz, o.valid ? 1 : 0, (o.full ? 1 : 0) | (early ? 2 : 0));
         const bool fast = o.full && vec_ok;
         if (fast) {
             const int rw = x_tma(o) ? TX + 4 : TX;       // words per staged row
@@ -709,6 +783,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     TileTotals tot;
     unsigned int active = 0;   // cells of this CTA still below T (< 2^32: N < 2^32)
     unsigned int rounds_max = 0;
+    unsigned long long nv_early = 0, nv_plain = 0;   // CLS: visits per path (thread 0 of each group)
     unsigned short* q = Q + warp * QW;
     // A group's next tile is claimed by its thread 0 before the write-back barrier that ends
     // the current one, into the other of the group's two slots (everybody has read the current
@@ -775,12 +850,21 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         if (patched) group_bar(1 + gid, NTG);
         ACA_TRACE(2, ((unsigned long long)o.x0 << 32) | (unsigned)o.y0);
 
+        unsigned long long c0 = 0, c1 = 0;   // CLS: per-lane class counters of this visit
         if (o.valid) {
-            const unsigned int rounds =
-                o.full ? tile_rounds<NDIM, TX, TY, TZ, NTG, true, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
-                                                                                    o.x0, o.y0, o.z0, wlim, st)
-                       : tile_rounds<NDIM, TX, TY, TZ, NTG, false, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
-                                                                                     o.x0, o.y0, o.z0, wlim, st);
+            unsigned int rounds;
+            if (!CLS || o.early) {
+                rounds = o.full ? tile_rounds<NDIM, TX, TY, TZ, NTG, true, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
+                                                                                             o.x0, o.y0, o.z0, wlim, st)
+                                : tile_rounds<NDIM, TX, TY, TZ, NTG, false, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
+                                                                                              o.x0, o.y0, o.z0, wlim, st);
+            } else {
+                rounds = o.full ? tile_rounds<NDIM, TX, TY, TZ, NTG, true, false, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
+                                                                                             o.x0, o.y0, o.z0, wlim, st)
+                                : tile_rounds<NDIM, TX, TY, TZ, NTG, false, false, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
+                                                                                              o.x0, o.y0, o.z0, wlim, st);
+            }
+            if (CLS && gt == 0) { nv_early += o.early; nv_plain += !o.early; }
             rounds_max = rounds > rounds_max ? rounds : rounds_max;
             tot.fold(st);
             if (fast) {
@@ -796,6 +880,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                     const size_t gi = NDIM == 2 ? (size_t)(o.y0 + ly) * g.nx + o.x0 + lx
                                                 : ((size_t)(o.z0 + lz) * g.ny + (o.y0 + ly)) * g.nx + o.x0 + lx;
                     const ulonglong2 v = lds128v(&S[slot(lx, ly, lz)]);
+                    if constexpr (CLS) cls_pair<NDIM, SX, SXY>(S, slot(lx, ly, lz), v, c0, c1);
                     ACA_CHECK(gi + 1 < (size_t)g.nx * g.ny * g.nz, gi, oo);
                     *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
                     active += (v.x < wT) + (v.y < wT);
@@ -818,6 +903,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                     if (gx < g.nx && gy < g.ny && (NDIM == 2 || gz < g.nz)) {
                         const size_t gi = NDIM == 2 ? (size_t)gy * g.nx + gx : ((size_t)gz * g.ny + gy) * g.nx + gx;
                         const unsigned long long w = S[slot(lx, ly, lz)];
+                        if constexpr (CLS) cls_one<NDIM, SX, SXY>(S, slot(lx, ly, lz), w, c0, c1);
                         P.words[gi] = w;
                         push_word(P, gx, gy, gz, w);
                         active += w < lagw[1];
@@ -825,6 +911,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                     }
                 }
             }
+            if constexpr (CLS) cls_flush_warp<NBIN>(c0, c1, ghist + (gid * 2 + par) * 16, lane);
         }
         ACA_TRACE(6, k);
         // refill the buffer with tile k + NBUF: armed before the barrier (the arrive does not
@@ -835,6 +922,17 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         }
         group_bar(1 + gid, NTG);   // the buffer is free
         ACA_TRACE(7, k);
+        if constexpr (CLS) {   // the tile's class histogram of this visit -> HBM (and zeroed for reuse)
+            if (gt == 0 && o.valid) {
+                unsigned int* gh = ghist + (gid * 2 + par) * 16;
+                uint4* hp = reinterpret_cast<uint4*>(P.tile_hist + 16 * tile_index(o));
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    hp[j] = make_uint4(gh[4 * j], gh[4 * j + 1], gh[4 * j + 2], gh[4 * j + 3]);
+                    gh[4 * j] = gh[4 * j + 1] = gh[4 * j + 2] = gh[4 * j + 3] = 0u;
+                }
+            }
+        }
         par ^= 1;
         if (k + NBUF < K) copy_rows(b, gt, NTG);
     }
@@ -847,5 +945,9 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
     const unsigned long long s_flp = block_sum<NT>(tot.flips, red);
     const unsigned long long s_tst = block_sum<NT>(tot.tested, red);
     const unsigned long long s_hsh = block_sum<NT>(st.hacc, red);
+    if constexpr (CLS) {
+        if (nv_early) atomicAdd(&P.ctl->visits_early, nv_early);
+        if (nv_plain) atomicAdd(&P.ctl->visits_plain, nv_plain);
+    }
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase, P.lag_q, g.TSH);
 }

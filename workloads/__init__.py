@@ -20,8 +20,9 @@ CONFIGS = {
     "c4": dict(dims=(512, 512, 512), beta=0.2216544, J=1.0, h=0.0, lam=1.0, rule=HEATBATH,
                init_q=0.5, T=10.0, tile=(32, 16, 8), note="z slabs across 1/2/4/8 GPUs"),
     "c5": dict(dims=(8192, 8192), beta=1.0, J=1.0, h=0.1, lam=1.0, rule=METROPOLIS,
-               init_q=0.05, T=200.0, tile=(64, 64), note="low temperature; exact early-reject",
-               opts={"early_reject": 1}),
+               init_q=0.05, T=200.0, tile=(64, 64),
+               note="low temperature; exact early rejection, path chosen per tile from its BKL class histogram",
+               opts={"early_reject": 1, "class_book": 1, "class_wmax": 0.01}),
 }
 
 PARITY_SEEDS = (1, 2, 3)
