@@ -4,6 +4,7 @@
 // statistics and getters. Every step of the method runs in the kernels of aca_kernels.cuh;
 // nothing here computes a trajectory.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <curand_kernel.h>
 #include <dlfcn.h>
 
@@ -113,6 +114,8 @@ struct Shard {
     size_t face = 0;       // cells of one row / plane of the sharded axis
     int tiles_x = 1, tiles_y = 1, tiles_z = 1;
     unsigned int* tile_hist = nullptr;      // a10 class bookkeeping: 16 u32 per tile (class_book)
+    CUtensorMap tmap{};                     // TMA box of one tile over `words` (box_ok = 1 when encoded)
+    int box_ok = 0;
 };
 
 }  // namespace
@@ -363,9 +366,40 @@ KParams make_params(const aca_sim* S, const Shard& sh) {
     }
     for (int i = 0; i < 14; ++i) P.thr[i] = S->thr[i];
     P.tile_hist = sh.tile_hist;
+    P.tmap = sh.tmap;
+    P.box_ok = sh.box_ok;
     for (int i = 0; i < 16; ++i) P.clsw[i] = i < 14 ? (unsigned int)(S->thr[i] >> 16) : 0u;
     P.cls_lim = S->cls_lim;
     return P;
+}
+
+// TMA tensor map of a shard's words with the tile box (tile + 2-word x halo + 1-cell y / z halo):
+// interior tiles are staged by one cp.async.bulk.tensor (driver entry point, no libcuda link)
+void encode_tile_box(aca_sim* S, Shard& sh) {
+    static void* fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            fn = nullptr;
+        }
+    }
+    sh.box_ok = 0;
+    if (!fn || getenv("ACA_NO_TMA_BOX") || (sh.g.nx & 1)) return;
+    const int nd = sh.g.ndim;
+    cuuint64_t dims[3] = {(cuuint64_t)sh.g.nx, (cuuint64_t)sh.g.ny, (cuuint64_t)sh.g.nz};
+    cuuint64_t strides[2] = {(cuuint64_t)sh.g.nx * 8, (cuuint64_t)sh.g.nx * sh.g.ny * 8};
+    cuuint32_t box[3] = {(cuuint32_t)S->tile[0] + 4, (cuuint32_t)S->tile[1] + 2, (cuuint32_t)S->tile[2] + 2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (box[0] > 256 || box[1] > 256 || box[2] > 256) return;
+    auto enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    CUresult r = enc(&sh.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, (cuuint32_t)nd, sh.words, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    sh.box_ok = r == CUDA_SUCCESS ? 1 : 0;
 }
 
 // a10 class bookkeeping: recount every tile's class histogram from the current state
@@ -928,6 +962,7 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         sh.tiles_z = ndim == 3 ? (g.nz + S->tile[2] - 1) / S->tile[2] : 1;
         if (cudaMalloc(&sh.words, sh.n * 8) != cudaSuccess || cudaMalloc(&sh.ctl, sizeof(Ctl)) != cudaSuccess)
             return bail(fail(ACA_ENOMEM, "device allocation of %zu cells failed", sh.n));
+        if (!S->whole && !S->sync) encode_tile_box(S, sh);
         if (S->cls &&
             cudaMalloc(&sh.tile_hist, (size_t)sh.tiles_x * sh.tiles_y * sh.tiles_z * 16 * sizeof(unsigned int)) != cudaSuccess)
             return bail(fail(ACA_ENOMEM, "tile class histograms"));

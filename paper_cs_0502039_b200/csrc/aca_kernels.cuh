@@ -22,6 +22,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <cuda.h>   // CUtensorMap (the tile box of the TMA tensor copies)
+
 #include "aca_prim.cuh"
 #include "nlog_tables.cuh"
 
@@ -151,6 +153,11 @@ __device__ __forceinline__ void frame_write(const FrameParams& F, unsigned long 
 }
 
 struct KParams {
+    // TMA tensor map of the shard's words (2-D [ny][nx] / 3-D [nz][ny][nx] u64, box = a tile with
+    // its 2-word x halo and 1-cell y (z) halo); tile_grp_kernel stages interior tiles with ONE
+    // cp.async.bulk.tensor per tile. Zeroed (box_ok = 0) when the host could not encode it.
+    CUtensorMap tmap;
+    int box_ok;
     Geo g;
     unsigned long long* words;
     const unsigned long long* halo_lo;   // sharded axis: row/plane just below the shard
@@ -273,6 +280,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}"
                  ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+// announce `bytes` of async-proxy transfers for the current phase without arriving
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -292,6 +303,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+// the tile box at (x, y[, z]) of the tensor map -> shared memory (128-B aligned), completes on bar
+__device__ __forceinline__ void tma_box_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint32_t bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_box_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z, uint32_t bar) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                 ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar) : "memory");
 }
 // order earlier generic-proxy accesses of shared memory before later async-proxy (TMA) ones
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

@@ -572,7 +572,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
 // write-back into P.tile_hist, and the next visit of the tile takes the a10 path iff the tile's
 // n-fold flip weight sum_k |Gamma_k| p_k is at most P.cls_lim.
 template <int NDIM, int TX, int TY, int TZ, int NTG, int NG, int NBUF, int EM, bool MOORE, bool GEN>
-__global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) {
+__global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_constant__ KParams P) {
     constexpr bool EARLY = EM != 0;   // queue sizing: a10 candidates
     constexpr bool CLS = EM == 2;
     constexpr int NBIN = 2 * (2 * NDIM + 1);
@@ -705,6 +705,12 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         o.early = EM == 1 || (c.w & 2) != 0;
         return o;
     };
+    auto box_ok = [&](const Org& o) {
+        if (!P.box_ok || P.phase < 0 || !(o.full && vec_ok)) return false;
+        if (o.x0 < 2 || o.x0 + TX + 2 > g.nx || o.y0 < 1 || o.y0 + TY + 1 > g.ny) return false;
+        return NDIM == 2 || (o.z0 >= 1 && o.z0 + TZ + 1 <= g.nz);
+    };
+    constexpr uint32_t BOX_BYTES = (uint32_t)(TX + 4) * (TY + 2) * (NDIM == 3 ? TZ + 2 : 1) * 8u;
     auto arm = [&](int k, int b) {
         const Org o = origin(k);
         bool early = false;
@@ -724,7 +730,9 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         orgs[2 * b] = make_int4(o.x0, o.y0, o.z0, o.tx);
         orgs[2 * b + 1] = make_int4(o.ty, o.tz, o.valid ? 1 : 0, (o.full ? 1 : 0) | (early ? 2 : 0));
         const bool fast = o.full && vec_ok;
-        if (fast) {
+        if (box_ok(o)) {
+            mbar_arrive_expect_tx(&bar[b], BOX_BYTES);
+        } else if (fast) {
             const int rw = x_tma(o) ? TX + 4 : TX;       // words per staged row
             mbar_arrive_expect_tx(&bar[b], (uint32_t)((NROWS + face_rows_tma(o)) * rw * 8));
         } else {
@@ -739,6 +747,14 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
         const bool xs = x_tma(o);
         unsigned long long* S = Sb + b * NSLOTP;
         const uint32_t barA = smem_u32(&bar[b]);
+        if (box_ok(o)) {
+            if (t == 0) {
+                fence_proxy_async();
+                if constexpr (NDIM == 2) tma_box_2d(smem_u32(S), &P.tmap, o.x0 - 2, o.y0 - 1, barA);
+                else tma_box_3d(smem_u32(S), &P.tmap, o.x0 - 2, o.y0 - 1, o.z0 - 1, barA);
+            }
+            return;
+        }
         bool fenced = false;
         for (int row = t; row < NROWS + NFACE; row += nt) {
             int ly, lz;
@@ -874,6 +890,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                 const int wb0 = wg * CPW;
                 const unsigned long long wT = lagw[1];   // T (termination counts cells below it)
                 unsigned long long wm = ~0ull;
+                const bool lag = P.lag_q != 0;
                 for (int idx = lane; idx < CPW / 2; idx += 32) {
                     const int oo = wb0 + 2 * idx;
                     const int lx = oo % TX, ly = (oo / TX) % TY, lz = oo / (TX * TY);
@@ -884,7 +901,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const KParams P) 
                     ACA_CHECK(gi + 1 < (size_t)g.nx * g.ny * g.nz, gi, oo);
                     *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
                     active += (v.x < wT) + (v.y < wT);
-                    wm = min(wm, min(v.x, v.y));
+                    if (lag) wm = min(wm, min(v.x, v.y));
                     if (P.push_lo) {
                         const int a = NDIM == 2 ? o.y0 + ly : o.z0 + lz, n = NDIM == 2 ? g.ny : g.nz;
                         if (a == 0 || a == n - 1) {
