@@ -369,7 +369,9 @@ def main():
     mean_sweep = ks / max(1, launches)
     kl_per_sweep = (kl / max(1, launches * 1.0)) if launches else 1.0
     achieved = (n_local * bpc / mean_sweep) / 1e9 if mean_sweep > 0 else None
-    tag = "tile_grp_kernel (%d-D)" % ndim
+    resident = kl_per_sweep < 0.5     # one cooperative launch per run_until: the resident-tile kernel
+    tag = "res_kernel (2-D, tiles resident in shared memory, one cooperative launch per run_until)" if resident \
+        else "tile_grp_kernel (%d-D)" % ndim
     traffic = ncu_traffic(args.config)
     state_bytes = n_local * 8
     l2_resident = state_bytes * 2 < 64e6          # config 2: 8 MB of state, far below the 126 MB L2
@@ -384,6 +386,9 @@ def main():
             "survey_8d": {"bytes_per_cell_per_sweep": sbytes, "achieved": achieved_s,
                           "frac": (achieved_s / peak) if achieved_s else None,
                           "note": "SURVEY.md 8(d) convention (13 B/cell SoA state read + written + tile halo)"},
+            "resident_note": ("the tiles stay in shared memory across sweeps: per sweep only their boundary lines "
+                              "(0.25 B/cell) cross L2, so the byte roofline is nominal; the kernel is bound by the "
+                              "issue rate and the grid barriers") if resident else None,
             "cells_per_sweep": n_local,
             "mean_sweep_ms": mean_sweep * 1e3, "sweeps_per_step": launches / args.steps,
             "kernel_launches_per_sweep": round(kl_per_sweep, 2),
@@ -395,7 +400,8 @@ def main():
             "config": {"workload": "%s: %s" % (args.config, cfg["note"]), "dims": list(dims), "T": cfg["T"],
                        "beta": cfg["beta"], "h": cfg["h"], "rule": ["heatbath", "metropolis"][cfg["rule"]],
                        "tile": list(tile), "rounds_per_tile_visit": args.rounds or cfg.get("opts", {}).get("rounds_per_launch", aca.DEFAULT_ROUNDS),
-                       "sweep": "checkerboard: 2 kernel launches per outer round (tile colours 0, 1)",
+                       "sweep": ("checkerboard: 2 grid-barrier phases per outer round inside one cooperative launch"
+                                 if resident else "checkerboard: 2 kernel launches per outer round (tile colours 0, 1)"),
                        "parallelism": "row strips x %d" % world if ndim == 2 else "z slabs x %d" % world,
                        "halo_transport": (("cuda-ipc push" if args.transport == "ipc" else "nccl exchange")
                                           if world > 1 else "none (one shard)"),

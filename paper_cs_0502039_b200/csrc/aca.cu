@@ -140,6 +140,10 @@ struct aca_sim {
     unsigned long long thr[14] = {};
     unsigned long long thm[98] = {};   // a10 early-rejection table (see commit_loop)
     bool cls = false;                  // a10 per-tile class bookkeeping (aca_options.class_book)
+    // resident-tile kernel (small 2-D lattices): the whole run_until in one cooperative launch
+    bool res_ok = false;
+    int res_grid = 0;
+    size_t res_smem = 0;
     bool cls_stale = true;             // the tile histograms must be recounted before the next run
     long long cls_lim = -1;            // early path iff sum_k |Gamma_k| floor(p_k 2^16) <= cls_lim
     int bulk = 1;
@@ -981,6 +985,27 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
             S->shards[s2].push_hi = S->shards[(s2 + 1) % S->G].halo_lo;
         }
     }
+    // resident-tile kernel: 2-D, one shard, whole 64 x 64 tiles, at most two tiles per colour per SM,
+    // the plain test (no a10, no class bookkeeping, Ising rules), Poisson law at lambda = 1, no tie
+    // stress, checkerboard sweeps (ACA_NO_RES=1: never, for ablations and parity tests)
+    if (ndim == 2 && S->G == 1 && S->world == 1 && !S->use_nccl && !S->whole && !S->sync && !S->cls &&
+        S->persistent_ctas > 0 && S->phased && S->tile[0] == 64 && S->tile[1] == 64 && dims[0] % 64 == 0 &&
+        dims[1] % 64 == 0 && !opt.early_reject && rule != ACA_LIFE && opt.law == 0 && opt.tie_bits == 0 &&
+        S->inv_lambda == (1ull << 32) && N < ((int64_t)1 << 32) && opt.max_ctas == 0 && !getenv("ACA_NO_RES")) {
+        int nsm = 0, occ = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
+        const size_t sm = res_smem_bytes(512);
+        const int items = (int)((S->shards[0].tiles_x + 1) / 2) * S->shards[0].tiles_y;
+        const int per = (items + nsm - 1) / nsm;
+        if (per <= res_tiles_max() / 2 &&
+            cudaFuncSetAttribute((void*)res_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (void*)res_kernel<512>, 512, sm) == cudaSuccess && occ >= 1) {
+            S->res_ok = true;
+            S->res_grid = (items + per - 1) / per;
+            S->res_smem = sm;
+        }
+        cudaGetLastError();
+    }
     if (int r = init_state(S)) return bail(r);
     if (cudaMallocHost(&S->h_ctl, 2 * sizeof(Ctl) * S->shards.size()) != cudaSuccess)
         return bail(fail(ACA_ENOMEM, "pinned ctl"));
@@ -1087,8 +1112,12 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         rc = class_refresh(S);
         if (rc) return rc;
     }
-    rc = build_graph(S);
-    if (rc) return rc;
+    // the resident-tile kernel when the run has the plain fast arrival and no lag window
+    const bool use_res = S->res_ok && S->fr.nb == 0 && S->lag_q == 0;
+    if (!use_res) {
+        rc = build_graph(S);
+        if (rc) return rc;
+    }
     CK(cudaEventRecord(S->ev0, S->stream));
     const size_t nsh = S->shards.size();
     // One batch = K outer rounds (a CUDA-graph replay) followed by a copy of the control
@@ -1097,7 +1126,14 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
     // (every launch returns at its first instruction when ctl->done is set).
     auto issue = [&](int slot) -> int {
         CK(cudaEventRecord(S->evb[slot][0], S->stream));
-        if (S->graph) {
+        if (use_res) {   // one launch runs to termination; a second one returns at once
+            KParams P = make_params(S, S->shards[0]);
+            P.phase = 0;
+            void* args[] = {&P};
+            CK(cudaLaunchCooperativeKernel((void*)res_kernel<512>, dim3(S->res_grid), dim3(512), args, S->res_smem,
+                                           S->stream));
+            S->kernel_launches += 1;
+        } else if (S->graph) {
             CK(cudaGraphLaunch(S->graph, S->stream));
             S->kernel_launches += (uint64_t)S->graph_rounds * nsh * (S->phased ? 2 : 1);
         } else {

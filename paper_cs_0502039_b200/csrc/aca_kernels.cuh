@@ -85,6 +85,10 @@ struct Ctl {                            // device control block, one per shard
     unsigned long long wlim_T;
     unsigned long long wmin[2];         // minimum word of the tiles of each colour at their last write-back
     unsigned long long visits_early, visits_plain;   // a10 class bookkeeping: tile visits per path
+    // resident-tile kernel (res_kernel): grid barrier (arrivals, generation) and the active-cell
+    // counts of three consecutive sweeps
+    unsigned int bar_count, bar_gen;
+    unsigned long long res_act[3];
 };
 
 struct Geo {
@@ -719,6 +723,8 @@ __host__ __device__ constexpr size_t sync_smem_bytes(int ndim, int tx, int ty, i
 }
 
 #include "aca_tile.cuh"
+
+#include "aca_res.cuh"
 
 #include "aca_misc.cuh"
 

@@ -13,7 +13,7 @@ CONFIGS = {
     "c1": dict(dims=(64, 64), beta=0.4406868, J=1.0, h=0.0, lam=1.0, rule=HEATBATH,
                init_q=0.5, T=10.0, tile=(64, 64), note="one cell per PE rule; whole lattice = one CTA"),
     "c2": dict(dims=(1024, 1024), beta=0.40, J=1.0, h=0.0, lam=1.0, rule=METROPOLIS,
-               init_q=0.5, T=100.0, tile=(64, 64), note="single B200, 64x64 CTA tiles, 1-cell halo",
+               init_q=0.5, T=100.0, tile=(64, 64), note="single B200, 64x64 CTA tiles, 1-cell halo (resident in shared memory across sweeps)",
                opts={"rounds_per_launch": 6}),   # 256 tiles only: more rounds per visit (measured best)
     "c3": dict(dims=(16384, 16384), beta=0.4406868, J=1.0, h=0.0, lam=1.0, rule=HEATBATH,
                init_q=0.5, T=20.0, tile=(64, 64), note="row strips across 1/2/4/8 GPUs"),
