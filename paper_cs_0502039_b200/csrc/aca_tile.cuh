@@ -40,7 +40,7 @@ __host__ __device__ constexpr int grp_slots(int ndim, int tx, int ty, int tz) {
 __host__ __device__ constexpr size_t grp_smem_bytes(int ndim, int tx, int ty, int tz, int ntg, int ng, int nbuf,
                                                     bool early, bool cls = false) {
     return ((size_t)nbuf * grp_slots(ndim, tx, ty, tz) + 16 + 112 + 256 + 128 + (size_t)(ntg * ng) / 32 + nbuf) * 8 +
-           160 + 16 + (size_t)nbuf * 32 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15) +
+           160 + 16 + (size_t)nbuf * 64 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15) +
            (cls ? (size_t)ng * 2 * 16 * 4 : 0);
 }
 
@@ -605,8 +605,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     unsigned int* cs = (unsigned int*)(bar + NBUF);         // [0] claim counter, [1 + 2g + p] tiles of group g
     volatile unsigned int* armed = cs + 1 + 2 * NG;         // [b] phases of bar[b] armed so far
     unsigned long long* lagw = (unsigned long long*)(cs + 32);   // [0] bounded lag: min word written back, [1] wlim_T
-    int4* orgs = (int4*)(((uintptr_t)(cs + 40) + 15) & ~(uintptr_t)15);   // [2b], [2b+1]: origin of buffer b's tile
-    unsigned short* Q = (unsigned short*)(orgs + 2 * NBUF); // NW x QW fire queue entries
+    int4* orgs = (int4*)(((uintptr_t)(cs + 40) + 15) & ~(uintptr_t)15);   // [2s], [2s+1]: origin of tile k, s = k % (2 NBUF)
+    unsigned short* Q = (unsigned short*)(orgs + 4 * NBUF); // NW x QW fire queue entries
     // CLS: per group two 16-bin class histograms (the visit in progress, by the parity `par`)
     unsigned int* ghist = (unsigned int*)((char*)Q + (((size_t)NW * QW * 2 + 15) & ~(size_t)15));
 
@@ -697,8 +697,12 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     // copy_rows (every thread of a group or warp, `t` of `nt`): issue the row copies.
     // The origin of the tile in buffer b is computed once (integer divisions by runtime tile
     // counts) by the arming thread and read by everyone else from shared memory.
-    auto org_load = [&](int b) -> Org {
-        const int4 a = orgs[2 * b], c = orgs[2 * b + 1];
+    // The origin of tile k lives in slot k % (2 NBUF), not in its buffer's slot: a warp of the
+    // group processing tile k may read it after the group's thread 0 has armed tile k + NBUF (same
+    // buffer) — the arm precedes the visit's closing barrier, not its opening.
+    auto org_load = [&](int k) -> Org {
+        const int os = k % (2 * NBUF);
+        const int4 a = orgs[2 * os], c = orgs[2 * os + 1];
         Org o;
         o.x0 = a.x; o.y0 = a.y; o.z0 = a.z; o.tx = a.w; o.ty = c.x; o.tz = c.y; o.valid = c.z != 0;
         o.full = (c.w & 1) != 0;
@@ -727,8 +731,9 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
                 early = wsum <= P.cls_lim;
             }
         }
-        orgs[2 * b] = make_int4(o.x0, o.y0, o.z0, o.tx);
-        orgs[2 * b + 1] = make_int4(o.ty, o.tz, o.valid ? 1 : 0, (o.full ? 1 : 0) | (early ? 2 : 0));
+        const int os = k % (2 * NBUF);
+        orgs[2 * os] = make_int4(o.x0, o.y0, o.z0, o.tx);
+        orgs[2 * os + 1] = make_int4(o.ty, o.tz, o.valid ? 1 : 0, (o.full ? 1 : 0) | (early ? 2 : 0));
         const bool fast = o.full && vec_ok;
         if (box_ok(o)) {
             mbar_arrive_expect_tx(&bar[b], BOX_BYTES);
@@ -741,8 +746,9 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         __threadfence_block();
         armed[b] = (unsigned int)(k / NBUF) + 1u;   // phase k / NBUF of bar[b] is armed
     };
-    auto copy_rows = [&](int b, int t, int nt) {   // after arm(k, b) is visible to the caller
-        const Org o = org_load(b);
+    auto copy_rows = [&](int k, int t, int nt) {   // tile k, after arm(k, k % NBUF) is visible to the caller
+        const int b = k % NBUF;
+        const Org o = org_load(k);
         if (!(o.full && vec_ok)) return;
         const bool xs = x_tma(o);
         unsigned long long* S = Sb + b * NSLOTP;
@@ -824,7 +830,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
             while (armed[b] <= use) __nanosleep(64);
             mbar_wait(&bar[b], use & 1u);
         }
-        const Org o = org_load(b);
+        const Org o = org_load(k);
         const bool fast = o.full && vec_ok;
         bool patched = !fast && o.valid;   // threads wrote words into the buffer: barrier before use
         if (fast) {   // the words the bulk copies left out: x-halo columns, unsafe face rows
@@ -951,7 +957,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
             }
         }
         par ^= 1;
-        if (k + NBUF < K) copy_rows(b, gt, NTG);
+        if (k + NBUF < K) copy_rows(k + NBUF, gt, NTG);
     }
     ACA_TRACE(8, 0);
     __syncthreads();

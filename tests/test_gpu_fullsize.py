@@ -187,3 +187,24 @@ def test_energy_matches_onsager_at_scale(aca, beta, rule):
             es.append(-g.stats()["bond_sum"] / 1024 ** 2)
     u = _onsager_u(beta)
     assert abs(np.mean(es) - u) < 0.004, (np.mean(es), u)
+
+
+@pytest.mark.parametrize("name,reps", [("c3", 40), ("c4", 20)])
+def test_repeated_runs_identical(aca, name, reps):
+    """Race regression: the same run repeated must give the same final state every time. A warp
+    that read its tile's origin after the group's thread 0 had armed the next tile of the same
+    buffer (origins were kept per buffer) wrote 512 cells of one tile into another about once in
+    30 c3 runs (found by this loop; origins are now kept per tile, slot k % 2 NBUF)."""
+    cfg = workloads.config(name)
+    kw = dict(lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"])
+    g = aca.Sim(tuple(cfg["dims"]), seed=2, init_q=cfg["init_q"], tile=cfg["tile"], **cfg.get("opts", {}), **kw)
+    ref = None
+    for r in range(reps):
+        g.reset(2)
+        g.run_until(cfg["T"])
+        st = g.stats()
+        got = (st["arrivals"], st["cells_fired"], st["event_hash"], st["bond_sum"], st["magnetisation"])
+        assert got[0] == got[1], (r, got)
+        if ref is None:
+            ref = got
+        assert got == ref, (r, got, ref)
