@@ -76,6 +76,7 @@ def lib():
         L.oracle_destroy.argtypes = [ctypes.c_void_p]
         L.oracle_run_until_q32.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
         L.oracle_run_until_random_order.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]
+        L.oracle_run_until_calendar.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
         L.oracle_run_until_sync.argtypes = [ctypes.c_void_p, ctypes.c_uint64,
                                             ctypes.POINTER(ctypes.c_uint64), ctypes.c_int64]
         L.oracle_run_until_sync.restype = ctypes.c_int64
@@ -233,6 +234,10 @@ class OracleSim:
     def run_until_q32(self, Tq, order="pq", choice_seed=0, fired_per_round=None):
         if order == "pq":
             rc = lib().oracle_run_until_q32(self._p, Tq)
+        elif order == "calendar":   # (D): the same queue as "pq", bucketed
+            rc = lib().oracle_run_until_calendar(self._p, Tq)
+            if rc == -2:
+                raise MemoryError("calendar queue allocation")
         elif order == "random":
             rc = lib().oracle_run_until_random_order(self._p, Tq, choice_seed)
         elif order == "sync":

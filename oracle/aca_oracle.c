@@ -344,6 +344,99 @@ int oracle_run_until_q32(oracle_sim* S, uint64_t T) {
     return 0;
 }
 
+/* (D) The same global priority queue on (t, c) as (A), organised as a calendar queue (SURVEY
+ * 8(c) step 2: "a calendar/bucket queue that is exact on (t, c)"): pending arrivals are kept in
+ * buckets of width 2^BSH Q32 units by t >> BSH, on a ring longer than any increment; the bucket in
+ * progress is a binary heap on (t, c), later buckets are unsorted lists. Every arrival of an
+ * earlier bucket precedes every arrival of a later one, and within the bucket the heap pops in
+ * (t, c) order, so the events are processed in exactly the order of (A) — the same trajectory,
+ * bit for bit (tests/test_oracle_sim.py pins (D) == (A)) — with memory traffic local to one
+ * bucket instead of a heap over the whole lattice. Used for the long full-lattice golden runs. */
+typedef struct { uint64_t t; uint32_t c; } cq_ev;
+typedef struct { cq_ev* v; int64_t n, cap; } cq_list;
+
+static int cq_less(cq_ev a, cq_ev b) { return a.t < b.t || (a.t == b.t && a.c < b.c); }
+static int cq_push(cq_list* L, cq_ev e) {
+    if (L->n == L->cap) {
+        int64_t nc = L->cap ? 2 * L->cap : 64;
+        cq_ev* nv = (cq_ev*)realloc(L->v, (size_t)nc * sizeof(cq_ev));
+        if (!nv) return -1;
+        L->v = nv; L->cap = nc;
+    }
+    L->v[L->n++] = e;
+    return 0;
+}
+static void cq_sift_down(cq_ev* H, int64_t n, int64_t i) {
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < n && cq_less(H[l], H[m])) m = l;
+        if (r < n && cq_less(H[r], H[m])) m = r;
+        if (m == i) return;
+        cq_ev tmp = H[i]; H[i] = H[m]; H[m] = tmp;
+        i = m;
+    }
+}
+static void cq_sift_up(cq_ev* H, int64_t i) {
+    while (i > 0) {
+        int64_t p = (i - 1) / 2;
+        if (!cq_less(H[i], H[p])) return;
+        cq_ev tmp = H[i]; H[i] = H[p]; H[p] = tmp;
+        i = p;
+    }
+}
+
+int oracle_run_until_calendar(oracle_sim* S, uint64_t T) {
+    if (T < S->T_last) return -1;
+    S->T_last = T;
+    S->heap_valid = 0;   /* (A) rebuilds its heap from the state next time */
+    const int BSH = 26;  /* bucket width 2^26 Q32 units = 1/64 of a time unit */
+    /* ring length: more buckets than the largest increment spans (law 0: NLOG-2 <= 190530846196
+     * at lambda = 1; every law's increment is below 64 ln 2 / lambda time units) */
+    uint64_t maxd = ((uint64_t)190530846196ULL >> 16) * (S->inv_lambda >> 16) + (1ULL << 33);
+    if (S->tie_bits) maxd += 1ULL << S->tie_bits;
+    int64_t R = 1;
+    while ((uint64_t)R <= (maxd >> BSH) + 2) R <<= 1;
+    cq_list* B = (cq_list*)calloc((size_t)R, sizeof(cq_list));
+    if (!B) return -2;
+    uint64_t tmin = ~0ULL;
+    for (int64_t c = 0; c < S->N; c++) {
+        if (S->t[c] >= T) continue;
+        cq_ev e = {S->t[c], (uint32_t)c};
+        if (cq_push(&B[(S->t[c] >> BSH) & (uint64_t)(R - 1)], e)) return -2;
+        if (S->t[c] < tmin) tmin = S->t[c];
+    }
+    int rc = 0;
+    if (tmin != ~0ULL) {
+        uint64_t b = tmin >> BSH;          /* absolute index of the bucket in progress */
+        const uint64_t bend = (T - 1) >> BSH;
+        for (; b <= bend; b++) {
+            cq_list* L = &B[b & (uint64_t)(R - 1)];
+            cq_ev* H = L->v;
+            for (int64_t i = L->n / 2 - 1; i >= 0; i--) cq_sift_down(H, L->n, i);
+            while (L->n > 0) {
+                H = L->v;
+                const int64_t c = H[0].c;
+                H[0] = H[--L->n];
+                cq_sift_down(H, L->n, 0);
+                int8_t ns; uint64_t nt;
+                arrival(S, c, &ns, &nt);
+                S->s[c] = ns; S->t[c] = nt; S->n[c] += 1;
+                if (nt >= T) continue;
+                cq_ev e = {nt, (uint32_t)c};
+                const uint64_t nb = nt >> BSH;
+                if (nb == b) {   /* the same bucket: into its heap */
+                    if (cq_push(L, e)) { rc = -2; break; }
+                    cq_sift_up(L->v, L->n - 1);
+                } else if (cq_push(&B[nb & (uint64_t)(R - 1)], e)) { rc = -2; break; }
+            }
+            if (rc) break;
+        }
+    }
+    for (int64_t i = 0; i < R; i++) free(B[i].v);
+    free(B);
+    return rc;
+}
+
 /* eligibility: fig:a1c1pe step 2 with the (t, c) tie-break (P6).
  * naive_leq = 1 is a NEGATIVE CONTROL only: the bare "t(c) <= min t(c')" test of
  * fig:s1c1pe without a tie-break, which lets tied neighbours fire in the same round. */

@@ -281,3 +281,33 @@ def test_onsager_energy(oracle_mod, beta, init_q):
     sigma = bm.std(ddof=1) / math.sqrt(nb)
     u = onsager_u(beta)
     assert abs(e.mean() - u) < 5 * sigma + 0.002, (e.mean(), u, sigma)
+
+
+@pytest.mark.parametrize("dims,kw,Ts", [
+    ((64, 48), dict(beta=0.4406868), [3.0, 7.25]),
+    ((96, 64), dict(beta=1.0, h=0.1, rule=1, init_q=0.05), [12.0]),
+    ((13, 7), dict(beta=0.6, lam=2.5), [2.0, 5.0]),
+    ((12, 10, 8), dict(beta=0.2216544), [4.0]),
+    ((32, 32), dict(beta=0.5, tie_bits=30), [6.0]),          # forced ties: the (t, c) order inside buckets
+    ((32, 32), dict(beta=0.5, tie_bits=36), [40.0]),         # ties wider than a bucket
+    ((24, 24), dict(beta=0.5, law=3), [5.0]),
+    ((24, 24), dict(beta=0.5, law=1, lam=0.3), [9.0]),
+])
+def test_calendar_queue_equals_heap(oracle_mod, dims, kw, Ts):
+    """(D) the calendar-queue form of the global priority queue processes the arrivals in the
+    same (t, c) order as the binary heap (A): identical spins, times, counters, flips, hash."""
+    a = oracle_mod.OracleSim(dims, seed=17, **kw)
+    b = oracle_mod.OracleSim(dims, seed=17, **kw)
+    for T in Ts:
+        a.run_until(T)
+        b.run_until(T, order="calendar")
+    assert np.array_equal(a.spins(), b.spins())
+    assert np.array_equal(a.times(), b.times())
+    assert np.array_equal(a.counters(), b.counters())
+    sa, sb = a.stats(), b.stats()
+    for k in ("arrivals", "flips", "event_hash", "bond_sum", "magnetisation"):
+        assert sa[k] == sb[k], k
+    # composition across the two queues: heap after calendar and calendar after heap
+    a.run_until(Ts[-1] + 1.5, order="calendar")
+    b.run_until(Ts[-1] + 1.5)
+    assert np.array_equal(a.times(), b.times()) and np.array_equal(a.spins(), b.spins())
