@@ -192,25 +192,40 @@ SURVEY_BYTES = {2: 26.6, 3: 29.4}
 
 
 def oracle_sample(cfg, seconds_target=10.0):
-    """The oracle as it stands on a bounded sample of the workload: same physics (beta, h,
-    rule, init, T) on a smaller lattice, single thread. Returns (arrivals/s, sample text)."""
+    """The oracle as it stands on a bounded sample of the workload: the same physics (beta, h,
+    rule, init) on a lattice larger than the host's caches (2-D 4096 x 2048, 3-D 256 x 256 x 128,
+    or the whole lattice if smaller), run to T' = min(T, the time that gives ~2.5e6 arrivals per
+    second of target), on ONE core (the process is pinned to one CPU for the call).
+    Returns (arrivals/s, arrivals, seconds, sample text)."""
     import oracle
     dims = tuple(cfg["dims"])
+    big = seconds_target >= 8
     if len(dims) == 2:
-        side = 1024 if seconds_target >= 8 else 512
-        sdims = (min(dims[0], side), min(dims[1], side // 2 if seconds_target >= 8 else side // 2))
+        sdims = (min(dims[0], 4096 if big else 2048), min(dims[1], 2048 if big else 1024))
     else:
-        side = 64 if seconds_target >= 8 else 48
-        sdims = tuple(min(d, side) for d in dims)
-    T = cfg["T"]
+        sdims = (min(dims[0], 256), min(dims[1], 256 if big else 128), min(dims[2], 128 if big else 64))
+    n = 1
+    for d in sdims:
+        n *= d
+    T = min(cfg["T"], max(0.5, round(2.5e6 * seconds_target / (n * cfg["lam"]), 2)))
     o = oracle.OracleSim(sdims, lam=cfg["lam"], beta=cfg["beta"], J=cfg["J"], h=cfg["h"], rule=cfg["rule"],
                          seed=1, init_q=cfg["init_q"])
-    t0 = time.perf_counter()
-    o.run_until(T)
-    dt = time.perf_counter() - t0
+    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    core = min(old) if old else None
+    if old:
+        os.sched_setaffinity(0, {core})
+    try:
+        t0 = time.perf_counter()
+        o.run_until(T)
+        dt = time.perf_counter() - t0
+    finally:
+        if old:
+            os.sched_setaffinity(0, old)
     arr = o.stats()["arrivals"]
-    return arr / dt, arr, dt, "oracle (serial PQ, 1 thread) on %s lattice, same beta/h/rule/init, T=%g: %d arrivals in %.2f s" % (
-        "x".join(map(str, sdims)), T, arr, dt)
+    o.close()
+    return arr / dt, arr, dt, ("oracle (serial binary-heap PQ, 1 thread pinned to CPU %s) on a %s lattice (%.0f MB of "
+                               "state), same beta/h/rule/init, T'=%g of T=%g: %d arrivals in %.2f s" % (
+                                   core, "x".join(map(str, sdims)), n * 13 / 1e6, T, cfg["T"], arr, dt))
 
 
 def cpu_name():
