@@ -143,6 +143,8 @@ struct aca_sim {
     // resident-tile kernel (small 2-D lattices): the whole run_until in one cooperative launch
     bool res_ok = false;
     int res_grid = 0;
+    int res_nt = 512;                  // threads per CTA (one tile at a time)
+    void* res_fn = nullptr;
     size_t res_smem = 0;
     bool cls_stale = true;             // the tile histograms must be recounted before the next run
     long long cls_lim = -1;            // early path iff sum_k |Gamma_k| floor(p_k 2^16) <= cls_lim
@@ -994,12 +996,17 @@ int aca_create(aca_sim** out, int ndim, const int64_t* dims, int periodic, doubl
         S->inv_lambda == (1ull << 32) && N < ((int64_t)1 << 32) && opt.max_ctas == 0 && !getenv("ACA_NO_RES")) {
         int nsm = 0, occ = 0;
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, S->device);
-        const size_t sm = res_smem_bytes(512);
+        int nt = 512;
+        if (const char* e = getenv("ACA_RES_NT")) nt = atoi(e) == 1024 ? 1024 : 512;   // ablation
+        void* fn = nt == 1024 ? (void*)res_kernel<1024> : (void*)res_kernel<512>;
+        const size_t sm = res_smem_bytes(nt);
         const int items = (int)((S->shards[0].tiles_x + 1) / 2) * S->shards[0].tiles_y;
         const int per = (items + nsm - 1) / nsm;
         if (per <= res_tiles_max() / 2 &&
-            cudaFuncSetAttribute((void*)res_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (void*)res_kernel<512>, 512, sm) == cudaSuccess && occ >= 1) {
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nt, sm) == cudaSuccess && occ >= 1) {
+            S->res_nt = nt;
+            S->res_fn = fn;
             S->res_ok = true;
             S->res_grid = (items + per - 1) / per;
             S->res_smem = sm;
@@ -1130,7 +1137,7 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
             KParams P = make_params(S, S->shards[0]);
             P.phase = 0;
             void* args[] = {&P};
-            CK(cudaLaunchCooperativeKernel((void*)res_kernel<512>, dim3(S->res_grid), dim3(512), args, S->res_smem,
+            CK(cudaLaunchCooperativeKernel(S->res_fn, dim3(S->res_grid), dim3(S->res_nt), args, S->res_smem,
                                            S->stream));
             S->kernel_launches += 1;
         } else if (S->graph) {
