@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(NT, 1) res_kernel(const __grid_constant__ KPar
     unsigned short* Q = (unsigned short*)(red + NW);                  // NW x QW
 
     const Geo& g = P.g;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5;
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
     for (int i = tid; i < 112; i += NT) thm[i] = ~0ull;
     for (int i = tid; i < 256; i += NT) {
