@@ -28,8 +28,10 @@ def build(force=False):
     newest = max(os.path.getmtime(p) for p in _SRC + _HDR)
     if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= newest:
         return _SO
-    cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math", "-o", _SO] + _SRC + ["-lm"]
+    tmp = _SO + ".tmp%d" % os.getpid()
+    cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math", "-o", tmp] + _SRC + ["-lm"]
     subprocess.check_call(cmd)
+    os.replace(tmp, _SO)   # atomic: a process that has the old library mapped keeps it
     return _SO
 
 
@@ -73,6 +75,16 @@ def lib():
         L.oracle_create.restype = ctypes.c_void_p
         L.oracle_create_law.argtypes = L.oracle_create.argtypes + [ctypes.c_int]
         L.oracle_create_law.restype = ctypes.c_void_p
+        L.oracle_create_q.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, ctypes.c_double,
+                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_int,
+                                      ctypes.c_uint64, ctypes.c_double, ctypes.c_int, ctypes.c_int]
+        L.oracle_create_q.restype = ctypes.c_void_p
+        L.oracle_q_offsets.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+        L.oracle_q_offsets.restype = ctypes.c_int
+        L.oracle_neighbours.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p]
+        L.oracle_neighbours.restype = ctypes.c_int
+        L.oracle_flip_table_z.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_int, ctypes.POINTER(ctypes.c_uint64)]
         L.oracle_destroy.argtypes = [ctypes.c_void_p]
         L.oracle_run_until_q32.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
         L.oracle_run_until_random_order.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64]
@@ -198,6 +210,22 @@ def flip_table(ndim, beta, J=1.0, h=0.0, rule=HEATBATH):
     return [int(v) for v in out]
 
 
+def flip_table_z(zc, beta, J=1.0, h=0.0, rule=HEATBATH):
+    """P4 table for zc neighbours (2 (zc + 1) entries); zc = |neighbors^q| - 1 for P12."""
+    out = (ctypes.c_uint64 * (2 * (zc + 1)))()
+    lib().oracle_flip_table_z(zc, beta, J, h, rule, out)
+    return [int(v) for v in out]
+
+
+def q_offsets(ndim, q):
+    """Eq. neiq as the oracle applies it: the offsets of neighbors^q(c) minus c."""
+    out = (ctypes.c_int * (3 * 256))()
+    n = lib().oracle_q_offsets(ndim, q, out, 256)
+    if n < 0:
+        raise ValueError("too many offsets")
+    return [tuple(out[3 * i:3 * i + ndim]) for i in range(n)]
+
+
 def ev_hash(w3, t, l, new_spin):
     """P7 event hash term of one arrival."""
     return lib().oracle_ev_hash(w3, t, l, new_spin)
@@ -211,11 +239,12 @@ class OracleSim:
     """One serial simulation. Methods mirror the C-ABI names of the product path."""
 
     def __init__(self, dims, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=HEATBATH, seed=1,
-                 init_q=0.5, tie_bits=0, law=POISSON):
+                 init_q=0.5, tie_bits=0, law=POISSON, q=1):
         self.dims = tuple(int(d) for d in dims)
         self.ndim = len(self.dims)
-        self._p = lib().oracle_create_law(self.ndim, _dims(self.dims), lam, beta, J, h, rule,
-                                          seed, init_q, tie_bits, law)
+        self.q = int(q)
+        self._p = lib().oracle_create_q(self.ndim, _dims(self.dims), self.q, lam, beta, J, h, rule,
+                                        seed, init_q, tie_bits, law)
         if not self._p:
             raise ValueError("oracle_create rejected the arguments")
         self.N = int(np.prod(self.dims))
@@ -274,6 +303,12 @@ class OracleSim:
         a = np.empty(self.N, np.uint32)
         lib().oracle_get_counters(self._p, a.ctypes.data)
         return a.reshape(self.dims[::-1])
+
+    def neighbours(self, c):
+        """The cells whose spins enter Sigma(c) and whose (t, c) gate c's arrival."""
+        out = (ctypes.c_int64 * 128)()
+        n = lib().oracle_neighbours(self._p, int(c), out)
+        return [int(out[i]) for i in range(n)]
 
     def stats(self):
         s = Stats()

@@ -15,6 +15,8 @@
 #include "nlog_tables.h"
 #include "gauss_tables.h"
 
+#define ORACLE_MAXZ 128   /* the most neighbours: 3-D, q = 4 */
+
 /* ---------------------------------------------------------------- P1: Philox4x32-10 */
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
     uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
@@ -146,8 +148,7 @@ uint64_t oracle_delta(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bit
 /* Appendix: dE = 2(J s Sigma + H s), x = exp(-dE/T), p = x/(1+x),
  * index = (Sigma+4)/2 + 5(s+1)/2; generalised to z = 2*ndim neighbours. Metropolis
  * acceptance min(1, exp(-beta dE)) is the MRRTT rule the paper names. */
-void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint64_t* out) {
-    int zc = 2 * ndim;
+void oracle_flip_table_z(int zc, double beta, double J, double h, int rule, uint64_t* out) {
     for (int sb = 0; sb < 2; sb++) {
         int s = 2 * sb - 1;
         for (int k = 0; k <= zc; k++) {
@@ -168,6 +169,10 @@ void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint
     }
 }
 
+void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint64_t* out) {
+    oracle_flip_table_z(2 * ndim, beta, J, h, rule, out);
+}
+
 /* ---------------------------------------------------------------- P7 */
 /* P7 event hash term (docs/PRIMITIVES.md): h = (w3 | 1) * (t ^ (l << 1) ^ s') mod 2^64, with w3
  * the fourth Philox word of the arrival's draw, t the arrival time, l the cell within the
@@ -183,7 +188,9 @@ struct oracle_sim {
     int64_t dims[3], N;
     double lambda, beta, J, h, init_q;
     int rule, tie_bits, law;
-    uint64_t seed, inv_lambda, thr_init, thr[14];
+    int q, nofs;                       /* q-th degree neighbourhood (Eq. neiq); q = 1: the 2 ndim neighbours */
+    int ofs[ORACLE_MAXZ][3];           /* q > 1: the offsets of neighbors^q(c) minus c itself */
+    uint64_t seed, inv_lambda, thr_init, thr[2 * (ORACLE_MAXZ + 1)];
     uint32_t key[2];
     int8_t* s;
     uint64_t* t;
@@ -203,6 +210,15 @@ int64_t oracle_num_cells(const oracle_sim* s) { return s->N; }
 static int neighbours(const oracle_sim* S, int64_t c, int64_t* nb) {
     int64_t nx = S->dims[0], ny = S->dims[1];
     int64_t x = c % nx, y = (c / nx) % ny, zz = (S->ndim == 3) ? c / (nx * ny) : 0;
+    if (S->q > 1) {   /* neighbors^q(c) \ {c}: the offset set of q_offsets, wrapped */
+        int64_t nz = S->dims[2];
+        for (int j = 0; j < S->nofs; j++) {
+            int64_t X = (x + S->ofs[j][0] + S->q * nx) % nx, Y = (y + S->ofs[j][1] + S->q * ny) % ny;
+            int64_t Z = (zz + S->ofs[j][2] + S->q * nz) % nz;
+            nb[j] = (Z * ny + Y) * nx + X;
+        }
+        return S->nofs;
+    }
     int64_t base = c - x;
     nb[0] = base + (x + nx - 1) % nx;
     nb[1] = base + (x + 1) % nx;
@@ -221,6 +237,8 @@ static int neighbours(const oracle_sim* S, int64_t c, int64_t* nb) {
     return S->zc;
 }
 
+int oracle_neighbours(const oracle_sim* S, int64_t c, int64_t* nb) { return neighbours(S, c, nb); }
+
 static void draw(const oracle_sim* S, uint32_t k, int64_t c, uint32_t tag, uint32_t w[4]) {
     uint32_t ctr[4] = {k, (uint32_t)((uint64_t)c & 0xffffffffu), (uint32_t)((uint64_t)c >> 32), tag};
     oracle_philox4x32_10(ctr, S->key, w);
@@ -228,12 +246,59 @@ static void draw(const oracle_sim* S, uint32_t k, int64_t c, uint32_t tag, uint3
 
 oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double beta, double J,
                           double h, int rule, uint64_t seed, double init_q, int tie_bits) {
-    return oracle_create_law(ndim, dims, lambda, beta, J, h, rule, seed, init_q, tie_bits, 0);
+    return oracle_create_q(ndim, dims, 1, lambda, beta, J, h, rule, seed, init_q, tie_bits, 0);
 }
 
 oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, double beta, double J,
                               double h, int rule, uint64_t seed, double init_q, int tie_bits, int law) {
+    return oracle_create_q(ndim, dims, 1, lambda, beta, J, h, rule, seed, init_q, tie_bits, law);
+}
+
+/* Eq. neiq applied literally to offset vectors: neighbors^1 = the cell and
+ * its 2 ndim first-degree neighbours; neighbors^q = neighbors(neighbors^(q-1)), the union of the
+ * first-degree neighbourhoods of its members. Returns the members other than the cell itself
+ * (their number is |neighbors^q(c)| - 1), or -1 if there are more than `cap`. On the torus the
+ * set is the same around every cell (translation), so it is computed once around the origin. */
+int oracle_q_offsets(int ndim, int q, int (*out)[3], int cap) {
+    int set[2 * ORACLE_MAXZ + 2][3], n = 1, nxt[2 * ORACLE_MAXZ + 2][3];
+    set[0][0] = set[0][1] = set[0][2] = 0;
+    for (int k = 1; k <= q; k++) {
+        int m = 0;
+        for (int i = 0; i < n; i++) {
+            for (int d = -1; d < 2 * ndim; d++) {   /* d = -1: the member itself (c is in neighbors(c)) */
+                int v[3] = {set[i][0], set[i][1], set[i][2]};
+                if (d >= 0) v[d / 2] += (d % 2) ? 1 : -1;
+                int dup = 0;
+                for (int j = 0; j < m && !dup; j++)
+                    dup = nxt[j][0] == v[0] && nxt[j][1] == v[1] && nxt[j][2] == v[2];
+                if (dup) continue;
+                if (m == 2 * ORACLE_MAXZ + 2) return -1;
+                nxt[m][0] = v[0]; nxt[m][1] = v[1]; nxt[m][2] = v[2]; m++;
+            }
+        }
+        memcpy(set, nxt, sizeof(int) * 3 * (size_t)m);
+        n = m;
+    }
+    int r = 0;
+    for (int i = 0; i < n; i++) {
+        if (!set[i][0] && !set[i][1] && !set[i][2]) continue;
+        if (r == cap) return -1;
+        out[r][0] = set[i][0]; out[r][1] = set[i][1]; out[r][2] = set[i][2]; r++;
+    }
+    return r;
+}
+
+/* q >= 2: the Ising model on neighbors^q (docs/PRIMITIVES.md P12): Sigma sums
+ * the spins of neighbors^q(c) \ {c}, the P4 table has z = |neighbors^q| - 1, a cell fires when its
+ * (t, c) is below every member's. Every side must be >= 2q + 1 so the members are distinct cells. */
+oracle_sim* oracle_create_q(int ndim, const int64_t* dims, int q, double lambda, double beta, double J,
+                            double h, int rule, uint64_t seed, double init_q, int tie_bits, int law) {
     if (ndim != 2 && ndim != 3) return NULL;
+    if (q < 1 || q > 4) return NULL;
+    if (q > 1) {
+        if (rule == 2) return NULL;
+        for (int a = 0; a < ndim; a++) if (dims[a] < 2 * q + 1) return NULL;
+    }
     if (law < 0 || law > 4) return NULL;
     if (!(lambda > 0) || !isfinite(lambda) || !(beta >= 0) || !isfinite(beta)) return NULL;
     if (rule != 0 && rule != 1 && !(rule == 2 && ndim == 2)) return NULL;
@@ -244,12 +309,18 @@ oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, doub
     if (N >= (1LL << 32)) return NULL;
     oracle_sim* S = (oracle_sim*)calloc(1, sizeof(oracle_sim));
     S->ndim = ndim; S->zc = rule == 2 ? 8 : 2 * ndim; S->N = N;
+    S->q = q;
+    if (q > 1) {
+        S->nofs = oracle_q_offsets(ndim, q, S->ofs, ORACLE_MAXZ);
+        if (S->nofs < 0) { free(S); return NULL; }
+        S->zc = S->nofs;
+    }
     for (int a = 0; a < 3; a++) S->dims[a] = a < ndim ? dims[a] : 1;
     S->lambda = lambda; S->beta = beta; S->J = J; S->h = h; S->rule = rule;
     S->seed = seed; S->init_q = init_q; S->tie_bits = tie_bits; S->law = law;
     S->inv_lambda = oracle_inv_lambda(lambda);
     S->thr_init = (uint64_t)floor(init_q * 4294967296.0);
-    oracle_flip_table(ndim, beta, J, h, rule, S->thr);
+    oracle_flip_table_z(S->zc, beta, J, h, rule, S->thr);
     S->key[0] = (uint32_t)(seed & 0xffffffffu);
     S->key[1] = (uint32_t)(seed >> 32);
     S->s = (int8_t*)malloc((size_t)N);
@@ -279,7 +350,7 @@ void oracle_destroy(oracle_sim* S) {
  * flip iff w0 < thr[idx], then t += Delta, n += 1. new_s / new_t are returned so the
  * synchronous variant can commit them later. */
 static void arrival(oracle_sim* S, int64_t c, int8_t* new_s, uint64_t* new_t) {
-    int64_t nb[8];
+    int64_t nb[ORACLE_MAXZ];
     int z = neighbours(S, c, nb);
     int sigma = 0;
     for (int j = 0; j < z; j++) sigma += S->s[nb[j]];
@@ -442,7 +513,7 @@ int oracle_run_until_calendar(oracle_sim* S, uint64_t T) {
  * fig:s1c1pe without a tie-break, which lets tied neighbours fire in the same round. */
 static int eligible_rule(const oracle_sim* S, int64_t c, uint64_t T, int naive_leq) {
     if (S->t[c] >= T) return 0;
-    int64_t nb[8];
+    int64_t nb[ORACLE_MAXZ];
     int z = neighbours(S, c, nb);
     for (int j = 0; j < z; j++) {
         if (naive_leq ? !(S->t[c] <= S->t[nb[j]]) : !lex_less(S, c, nb[j])) return 0;
@@ -473,7 +544,7 @@ int oracle_run_until_random_order(oracle_sim* S, uint64_t T, uint64_t choice_see
         int8_t ns; uint64_t nt;
         arrival(S, c, &ns, &nt);
         S->s[c] = ns; S->t[c] = nt; S->n[c] += 1;
-        int64_t touch[9];
+        int64_t touch[ORACLE_MAXZ + 1];
         touch[0] = c;
         int z = neighbours(S, c, touch + 1);
         for (int j = 0; j <= z; j++) {
@@ -532,22 +603,30 @@ void oracle_get_times(const oracle_sim* S, uint64_t* out) { memcpy(out, S->t, (s
 void oracle_get_counters(const oracle_sim* S, uint32_t* out) { memcpy(out, S->n, (size_t)S->N * 4); }
 
 /* Energy bookkeeping, Appendix comment "Energy = -J sum spin spin' - H sum spin"
- * (PAPER.md:1680): B counts each bond once along +e_a, periodic. */
+ * (PAPER.md:1680): B counts each bond once along +e_a, periodic; with neighbors^q (q > 1) each
+ * pair of cells within it once. */
 void oracle_get_stats(const oracle_sim* S, oracle_stats* o) {
     memset(o, 0, sizeof(*o));
-    int64_t nb[8];
+    int64_t nb[ORACLE_MAXZ];
     uint64_t tmin = ~0ULL, tmax = 0, arr = 0;
-    int64_t B = 0, M = 0;
+    int64_t B = 0, B2 = 0, M = 0;
     for (int64_t c = 0; c < S->N; c++) {
-        neighbours(S, c, nb);
+        int z = neighbours(S, c, nb);
         int sc = S->s[c];
-        int plus = S->s[nb[1]] + S->s[nb[3]] + (S->ndim == 3 ? S->s[nb[5]] : 0);
-        B += sc * plus;
+        if (S->q > 1) {   /* each pair {c, c'} of neighbors^q appears twice in the double sum */
+            int all = 0;
+            for (int j = 0; j < z; j++) all += S->s[nb[j]];
+            B2 += sc * all;
+        } else {
+            int plus = S->s[nb[1]] + S->s[nb[3]] + (S->ndim == 3 ? S->s[nb[5]] : 0);
+            B += sc * plus;
+        }
         M += sc;
         arr += S->n[c];
         if (S->t[c] < tmin) tmin = S->t[c];
         if (S->t[c] > tmax) tmax = S->t[c];
     }
+    if (S->q > 1) B = B2 / 2;
     o->arrivals = arr; o->flips = S->flips; o->event_hash = S->event_hash;
     o->bond_sum = B; o->magnetisation = M; o->t_min = tmin; o->t_max = tmax;
     o->rounds = S->rounds;

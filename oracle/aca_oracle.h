@@ -43,8 +43,9 @@ uint64_t oracle_gauss_u(uint32_t w, uint32_t sa, uint32_t sb, uint32_t tag);
 uint64_t oracle_cell_period_q32(uint64_t seed, uint64_t c);
 uint64_t oracle_law_q32(uint32_t w1, uint32_t w2, int law);
 uint64_t oracle_delta_law(uint32_t w1, uint32_t w2, uint64_t inv_lambda, int tie_bits, int law);
-/* P4: thresholds, 2*(2*ndim+1) entries written to out. */
+/* P4: thresholds, 2*(2*ndim+1) entries written to out; _z: 2*(zc+1) entries for zc neighbours. */
 void oracle_flip_table(int ndim, double beta, double J, double h, int rule, uint64_t* out);
+void oracle_flip_table_z(int zc, double beta, double J, double h, int rule, uint64_t* out);
 /* P7 event hash term: (w3 | 1) * (t ^ (l << 1) ^ [new_spin > 0]) mod 2^64 */
 uint64_t oracle_ev_hash(uint32_t w3, uint64_t t, uint64_t l, int new_spin);
 
@@ -53,6 +54,16 @@ oracle_sim* oracle_create(int ndim, const int64_t* dims, double lambda, double b
                           double h, int rule, uint64_t seed, double init_q, int tie_bits);
 oracle_sim* oracle_create_law(int ndim, const int64_t* dims, double lambda, double beta, double J,
                               double h, int rule, uint64_t seed, double init_q, int tie_bits, int law);
+/* q-th degree neighbourhood (Eq. neiq; docs/PRIMITIVES.md P12): q in [1, 4];
+ * q > 1 needs rule 0/1 and every side >= 2q + 1. q = 1 is oracle_create_law. */
+oracle_sim* oracle_create_q(int ndim, const int64_t* dims, int q, double lambda, double beta, double J,
+                            double h, int rule, uint64_t seed, double init_q, int tie_bits, int law);
+/* Eq. neiq applied literally around the origin: writes the offsets of neighbors^q(c) \ {c} to
+ * out (at most cap) and returns their number, -1 if more than cap. */
+int oracle_q_offsets(int ndim, int q, int (*out)[3], int cap);
+/* The cells of neighbors^q(c) \ {c} (with multiplicity for q = 1 on sides of 2) the oracle
+ * uses; nb must hold 128 entries. Returns their number. */
+int oracle_neighbours(const oracle_sim* s, int64_t c, int64_t* nb);
 void oracle_destroy(oracle_sim* s);
 
 /* (A) global priority queue on (t, c): the oracle. Returns 0, or -1 if T decreased. */
