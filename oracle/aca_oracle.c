@@ -501,6 +501,9 @@ int oracle_run_until_calendar(oracle_sim* S, uint64_t T) {
                 } else if (cq_push(&B[nb & (uint64_t)(R - 1)], e)) { rc = -2; break; }
             }
             if (rc) break;
+            free(L->v);   /* drained: release it, or every ring slot keeps its peak capacity */
+            L->v = NULL;
+            L->cap = 0;
         }
     }
     for (int64_t i = 0; i < R; i++) free(B[i].v);
