@@ -297,6 +297,28 @@ int aca_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J
                 double init_q, double T, int budget, int8_t* spins_out, uint64_t* T_out, uint32_t* n_out,
                 aca_agg_stats* st, int device);
 
+/* ---- The q-th degree neighbourhood (Eq. nei2 / neiq; docs/PRIMITIVES.md P12) ----
+ * The Ising model on neighbors^q(c), the L1 ball of radius q around c (|neighbors^q| - 1 = 2q(q+1)
+ * in 2-D): Sigma sums the spins of every member, the P4 table has
+ * z = |neighbors^q| - 1 (2 (z + 1) entries), a cell fires only when its (t, c) is below every
+ * member's (P6). Draws, increments (law 0..3, P3L; tie_bits P3b), P5 (init_q) and P7 as the main path;
+ * q = 1 gives the main path's trajectory. ndim 2 or 3, 1 <= q <= 4, every side >= 2q + 1, N <= 2^32;
+ * rounds: synchronous rounds per tile visit (<= 0: 32). Runs from the P5 state to T (fires every
+ * arrival t < round-half-up(T 2^32)). Outputs (host, caller-owned, each may be NULL): spins_out[N]
+ * int8, t_out[N] Q32 pending times, n_out[N] counters, row-major; st: arrivals, flips, event hash,
+ * B (each pair of cells within neighbors^q once), M, launches, sweeps and the device time of the
+ * sweeps (initialisation excluded). Device memory (13 N bytes) is allocated and freed inside the
+ * call. Errors: ACA_EINVAL (arguments), ACA_ENOMEM, ACA_ENODEV, ACA_ECUDA, ACA_ESTATE. */
+typedef struct {
+    uint64_t arrivals, flips, event_hash;
+    int64_t bond_sum, magnetisation;
+    uint64_t launches, sweeps;
+    double gpu_seconds;
+} aca_qnbr_stats;
+int aca_qnbr_run(int ndim, const int64_t* dims, int q, double lambda, double beta, double J, double h, int rule,
+                 uint64_t seed, double init_q, int tie_bits, int law, double T, int rounds, int8_t* spins_out,
+                 uint64_t* t_out, uint32_t* n_out, aca_qnbr_stats* st, int device);
+
 /* ---- Time-only efficiency model ----
  * Synchronous iterations of fig:s1c1pe on the local times only (valid because next_t does
  * not depend on the states for the Ising model): each iteration every

@@ -25,7 +25,7 @@ EXPORTS = ["aca_default_options", "aca_create", "aca_run_until", "aca_run_until_
            "aca_set_spins", "aca_reset", "aca_nccl_unique_id", "aca_destroy", "aca_last_error", "aca_num_cells", "aca_selftest_philox",
            "aca_selftest_nlog", "aca_selftest_law", "aca_efficiency_run", "aca_run_frames", "aca_agg_run", "aca_bkl_run", "aca_efficiency_run_q", "aca_ipc_export", "aca_ipc_import",
            "aca_stage_spins", "aca_set_spins_staged", "aca_get_spins_async", "aca_sync", "aca_perfbl_run",
-           "aca_get_tile_grid", "aca_get_tile_classes"]
+           "aca_get_tile_grid", "aca_get_tile_classes", "aca_qnbr_run"]
 ACA_IPC_BLOB_BYTES = 192
 DEFAULT_ROUNDS = 5   # in-tile rounds per tile visit when aca_options.rounds_per_launch = 0 (aca.cu)
 POISSON, UNIFORM, ROOT8, GAUSS = 0, 1, 2, 3   # asynchrony laws (aca_options.law)
@@ -48,6 +48,12 @@ class aca_options(ctypes.Structure):
                 ("early_reject", ctypes.c_int32), ("checkerboard", ctypes.c_int32),
                 ("law", ctypes.c_int32), ("halo_mode", ctypes.c_int32), ("max_ctas", ctypes.c_int32),
                 ("lag", ctypes.c_double), ("class_book", ctypes.c_int32), ("class_wmax", ctypes.c_double)]
+
+
+class aca_qnbr_stats(ctypes.Structure):
+    _fields_ = [("arrivals", ctypes.c_uint64), ("flips", ctypes.c_uint64), ("event_hash", ctypes.c_uint64),
+                ("bond_sum", ctypes.c_int64), ("magnetisation", ctypes.c_int64), ("launches", ctypes.c_uint64),
+                ("sweeps", ctypes.c_uint64), ("gpu_seconds", ctypes.c_double)]
 
 
 class aca_stats(ctypes.Structure):
@@ -115,6 +121,10 @@ def lib():
                               ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_double, ctypes.c_int, vp, vp, vp,
                               ctypes.POINTER(aca_agg_stats), ctypes.c_int]
     L.aca_bkl_run.argtypes = L.aca_agg_run.argtypes
+    L.aca_qnbr_run.argtypes = [ctypes.c_int, vp, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_int, ctypes.c_uint64, ctypes.c_double, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_double, ctypes.c_int, vp, vp, vp,
+                               ctypes.POINTER(aca_qnbr_stats), ctypes.c_int]
     L.aca_ipc_export.argtypes = [vp, vp, ctypes.c_size_t]
     L.aca_stage_spins.argtypes = [vp, vp, ctypes.c_size_t, ctypes.c_int]
     L.aca_set_spins_staged.argtypes = [vp, ctypes.c_int]
@@ -367,6 +377,28 @@ def aca_agg_run(dims, m, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=ACA_HEATBATH, 
                              _ptr(nn) if want_state else None, ctypes.byref(st), int(device)))
     stats = {k: getattr(st, k) for k, _ in st._fields_}
     return (sp.reshape(ny, nx) if want_state else None), Tt, nn, stats
+
+
+def aca_qnbr_run(dims, q, T, lam=1.0, beta=0.0, J=1.0, h=0.0, rule=ACA_HEATBATH, seed=1, init_q=0.5, tie_bits=0,
+                 law=POISSON, rounds=0, want_state=True, device=-1):
+    """The Ising model on the q-th degree neighbourhood (P12) on the GPU: (spins, times, counters,
+    stats), the arrays shaped dims[::-1] (None when want_state is False)."""
+    dims = tuple(int(v) for v in dims)
+    N = int(np.prod(dims))
+    d = (ctypes.c_int64 * len(dims))(*dims)
+    sp = np.zeros(N, np.int8) if want_state else None
+    tt = np.zeros(N, np.uint64) if want_state else None
+    nn = np.zeros(N, np.uint32) if want_state else None
+    st = aca_qnbr_stats()
+    _check(lib().aca_qnbr_run(len(dims), ctypes.cast(d, ctypes.c_void_p), int(q), float(lam), float(beta), float(J),
+                              float(h), int(rule), int(seed), float(init_q), int(tie_bits), int(law), float(T),
+                              int(rounds), _ptr(sp) if want_state else None, _ptr(tt) if want_state else None,
+                              _ptr(nn) if want_state else None, ctypes.byref(st), int(device)))
+    stats = {k: getattr(st, k) for k, _ in st._fields_}
+    shp = dims[::-1]
+    if not want_state:
+        return None, None, None, stats
+    return sp.reshape(shp), tt.reshape(shp), nn.reshape(shp), stats
 
 
 def aca_run_frames(p, dt, K0, count, B=4):

@@ -8,7 +8,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libaca.so")
 SOURCES = [os.path.join(CSRC, "aca.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("aca_kernels.cuh", "aca_tile.cuh", "aca_misc.cuh", "aca_prim.cuh", "nlog_tables.cuh", "gauss_tables.cuh", "aca_eff.cuh", "aca_agg.cuh", "aca_res.cuh")] + \
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("aca_kernels.cuh", "aca_tile.cuh", "aca_misc.cuh", "aca_prim.cuh", "nlog_tables.cuh", "gauss_tables.cuh", "aca_eff.cuh", "aca_agg.cuh", "aca_res.cuh", "aca_qnbr.cuh")] + \
     [os.path.join(ROOT, "include", "aca.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -22,6 +22,7 @@
 #include "aca_kernels.cuh"
 #include "aca_eff.cuh"
 #include "aca_agg.cuh"
+#include "aca_qnbr.cuh"
 #include "nlog_tables.cuh"
 
 using namespace aca;
@@ -209,8 +210,8 @@ namespace {
 
 // ---------------------------------------------------------------- P4 table (host, double)
 // Appendix PAPER.md:1691-1701 generalised (docs/PRIMITIVES.md P4).
-void flip_table(int ndim, double beta, double J, double h, int rule, unsigned long long* out) {
-    const int zc = 2 * ndim;
+// zc neighbours: 2 ndim, or |neighbors^q| - 1 for the q-th degree neighbourhood (P12).
+void flip_table_z(int zc, double beta, double J, double h, int rule, unsigned long long* out) {
     for (int sb = 0; sb < 2; ++sb) {
         const int s = 2 * sb - 1;
         for (int k = 0; k <= zc; ++k) {
@@ -233,6 +234,10 @@ void flip_table(int ndim, double beta, double J, double h, int rule, unsigned lo
             out[(sigma + zc) / 2 + (zc + 1) * (s + 1) / 2] = thr;
         }
     }
+}
+
+void flip_table(int ndim, double beta, double J, double h, int rule, unsigned long long* out) {
+    flip_table_z(2 * ndim, beta, J, h, rule, out);
 }
 
 // a10 table: thm[(s*(Z+1) + u)*(Z+1) + k] for a cell with spin bit s, u neighbours that may
@@ -2020,6 +2025,160 @@ int aca_bkl_run(const int64_t* dims, int m, double lambda, double beta, double J
                 aca_agg_stats* st, int device) {
     return agg_run_impl(true, dims, m, lambda, beta, J, h, rule, seed, init_q, T, budget, spins_out, T_out, n_out, st,
                         device);
+}
+
+// ---------------------------------------------------------------- q-th degree neighbourhood (P12)
+int aca_qnbr_run(int ndim, const int64_t* dims, int q, double lambda, double beta, double J, double h, int rule,
+                 uint64_t seed, double init_q, int tie_bits, int law, double T, int rounds, int8_t* spins_out,
+                 uint64_t* t_out, uint32_t* n_out, aca_qnbr_stats* st, int device) {
+    if (!dims) return fail(ACA_EINVAL, "null dims");
+    if (ndim != 2 && ndim != 3) return fail(ACA_EINVAL, "ndim must be 2 or 3");
+    if (q < 1 || q > 4) return fail(ACA_EINVAL, "q must be in [1, 4]");
+    long long N = 1;
+    for (int a = 0; a < ndim; ++a) {
+        if (dims[a] < 2 * q + 1 || dims[a] > (1 << 30)) return fail(ACA_EINVAL, "every side must be >= 2q + 1");
+        N *= dims[a];
+    }
+    if (N > ((long long)1 << 32)) return fail(ACA_EINVAL, "N must be <= 2^32");
+    if (!(lambda > 0) || !std::isfinite(lambda) || !(beta >= 0) || !std::isfinite(beta) || !std::isfinite(J) ||
+        !std::isfinite(h))
+        return fail(ACA_EINVAL, "bad lambda / beta / J / h");
+    if (rule != ACA_HEATBATH && rule != ACA_METROPOLIS) return fail(ACA_EINVAL, "rule must be 0 or 1");
+    if (law < 0 || law > 3) return fail(ACA_EINVAL, "law must be in [0, 3]");
+    if (tie_bits < 0 || tie_bits > 40) return fail(ACA_EINVAL, "tie_bits must be in [0, 40]");
+    if (!(init_q >= 0 && init_q <= 1)) return fail(ACA_EINVAL, "init_q must be in [0, 1]");
+    if (!(T >= 0) || !std::isfinite(T) || T * 4294967296.0 > 1.8e19) return fail(ACA_EINVAL, "bad T");
+    if (rounds < 1) rounds = 32;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || !ndev) { cudaGetLastError(); return fail(ACA_ENODEV, "no CUDA device"); }
+    if (device >= 0) CK(cudaSetDevice(device));
+    QParams P{};
+    P.ndim = ndim; P.q = q; P.R = rounds; P.tie_bits = tie_bits; P.law = law;
+    // neighbors^q(c) \ {c} = the L1 ball of radius q (closed form; the oracle builds Eq. neiq literally)
+    std::vector<int> ofs;
+    for (int dz = ndim == 3 ? -q : 0; dz <= (ndim == 3 ? q : 0); ++dz)
+        for (int dy = -q; dy <= q; ++dy)
+            for (int dx = -q; dx <= q; ++dx) {
+                const int l1 = std::abs(dx) + std::abs(dy) + std::abs(dz);
+                if (l1 == 0 || l1 > q) continue;
+                ofs.push_back(dx); ofs.push_back(dy); ofs.push_back(dz);
+            }
+    P.nofs = (int)ofs.size() / 3;
+    std::vector<unsigned long long> thr(2 * (P.nofs + 1));
+    flip_table_z(P.nofs, beta, J, h, rule, thr.data());
+    const int blk[3] = {ndim == 3 ? 8 : 32, ndim == 3 ? 8 : 32, 8};
+    int ncolour = 1;
+    for (int a = 0; a < 3; ++a) {
+        if (a >= ndim) { P.dim[a] = 1; P.ntl[a] = 1; P.ncol[a] = 1; P.tmax[a] = 1; continue; }
+        P.dim[a] = (int)dims[a];
+        P.ntl[a] = std::max(2, P.dim[a] / blk[a]);
+        P.ncol[a] = P.ntl[a] % 2 ? 3 : 2;
+        P.tmax[a] = (P.dim[a] + P.ntl[a] - 1) / P.ntl[a];
+        ncolour *= P.ncol[a];
+    }
+    const size_t nreg = (size_t)(P.tmax[0] + 2 * q) * (P.tmax[1] + 2 * q) * (ndim == 3 ? P.tmax[2] + 2 * q : 1);
+    const size_t nimax = (size_t)P.tmax[0] * P.tmax[1] * P.tmax[2];
+    const size_t smem = nreg * 9 + nimax * 13;
+    if (smem > 200 * 1024) return fail(ACA_EINVAL, "tile too large for shared memory (%zu B)", smem);
+    philox_round_keys((uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32), P.rk);
+    P.inv = (unsigned long long)std::floor(4294967296.0 / lambda + 0.5);
+    P.Tend = (unsigned long long)std::floor(T * 4294967296.0 + 0.5);
+    P.thr_init = (unsigned long long)std::floor(init_q * 4294967296.0);
+    unsigned long long* dlr = nullptr;
+    QAcc* dacc = nullptr;
+    int* dofs = nullptr;
+    unsigned long long* dthr = nullptr;
+    cudaStream_t str = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    auto cleanup = [&]() {
+        if (str) cudaStreamSynchronize(str);
+        cudaFree(P.t); cudaFree(P.s); cudaFree(P.n); cudaFree(dlr); cudaFree(dacc); cudaFree(dofs); cudaFree(dthr);
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        if (str) cudaStreamDestroy(str);
+    };
+    if (cudaMalloc(&P.t, (size_t)N * 8) != cudaSuccess || cudaMalloc(&P.s, (size_t)N) != cudaSuccess ||
+        cudaMalloc(&P.n, (size_t)N * 4) != cudaSuccess || cudaMalloc(&dlr, sizeof(ACA_NLOG_LR)) != cudaSuccess ||
+        cudaMalloc(&dacc, sizeof(QAcc)) != cudaSuccess || cudaMalloc(&dofs, ofs.size() * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&dthr, thr.size() * 8) != cudaSuccess) {
+        cudaGetLastError();
+        cleanup();
+        return fail(ACA_ENOMEM, "device allocation failed");
+    }
+    P.ofs = dofs;
+    P.thr = dthr;
+    int rc = ACA_OK;
+    QAcc hacc{};
+    uint64_t launches = 0, sweeps = 0;
+    do {
+        if (cudaStreamCreateWithFlags(&str, cudaStreamNonBlocking) != cudaSuccess) { rc = fail(ACA_ECUDA, "stream"); break; }
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        if (cudaFuncSetAttribute(qn_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+            rc = fail(ACA_ECUDA, "shared memory attribute: %s", cudaGetErrorString(cudaGetLastError()));
+            break;
+        }
+        cudaMemcpyAsync(dlr, ACA_NLOG_LR, sizeof(ACA_NLOG_LR), cudaMemcpyHostToDevice, str);
+        cudaMemcpyAsync(dofs, ofs.data(), ofs.size() * sizeof(int), cudaMemcpyHostToDevice, str);
+        cudaMemcpyAsync(dthr, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, str);
+        cudaMemsetAsync(dacc, 0, sizeof(QAcc), str);
+        int nsm = 148;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device >= 0 ? device : 0);
+        const unsigned igrid = (unsigned)std::max<long long>(1, std::min<long long>((N + 255) / 256, (long long)nsm * 8));
+        qn_init_kernel<<<igrid, 256, 0, str>>>(P, dlr);
+        cudaEventRecord(e0, str);
+        std::vector<unsigned> grid(ncolour);
+        for (int col = 0; col < ncolour; ++col) {
+            const int cc[3] = {col % P.ncol[0], (col / P.ncol[0]) % P.ncol[1], col / (P.ncol[0] * P.ncol[1])};
+            unsigned g = 1;
+            for (int a = 0; a < ndim; ++a)
+                g *= cc[a] == 2 ? 1u : (unsigned)((P.ncol[a] == 3 ? P.ntl[a] - cc[a] : P.ntl[a] - cc[a] + 1) / 2);
+            grid[col] = g;
+        }
+        for (int batch = 0;; ++batch) {
+            for (int kk = 0; kk < 4; ++kk) {
+                if (kk == 3) cudaMemsetAsync(&dacc->active, 0, 8, str);
+                for (int col = 0; col < ncolour; ++col) {
+                    P.colour = col;
+                    qn_tile_kernel<<<grid[col], QN_THREADS, smem, str>>>(P, dlr, dacc);
+                    ++launches;
+                }
+                ++sweeps;
+            }
+            if (cudaMemcpyAsync(&hacc, dacc, sizeof(QAcc), cudaMemcpyDeviceToHost, str) != cudaSuccess ||
+                cudaStreamSynchronize(str) != cudaSuccess) {
+                rc = fail(ACA_ECUDA, "q-neighbourhood kernels failed: %s", cudaGetErrorString(cudaGetLastError()));
+                break;
+            }
+            if (hacc.active == 0) break;
+            if (batch > (1 << 24)) { rc = fail(ACA_ESTATE, "no termination"); break; }
+        }
+        if (rc) break;
+        cudaEventRecord(e1, str);
+        qn_stats_kernel<<<igrid, QN_THREADS, 0, str>>>(P, dacc);
+        if (cudaMemcpyAsync(&hacc, dacc, sizeof(QAcc), cudaMemcpyDeviceToHost, str) != cudaSuccess ||
+            (spins_out && cudaMemcpyAsync(spins_out, P.s, (size_t)N, cudaMemcpyDeviceToHost, str) != cudaSuccess) ||
+            (t_out && cudaMemcpyAsync(t_out, P.t, (size_t)N * 8, cudaMemcpyDeviceToHost, str) != cudaSuccess) ||
+            (n_out && cudaMemcpyAsync(n_out, P.n, (size_t)N * 4, cudaMemcpyDeviceToHost, str) != cudaSuccess) ||
+            cudaStreamSynchronize(str) != cudaSuccess) {
+            rc = fail(ACA_ECUDA, "copy out: %s", cudaGetErrorString(cudaGetLastError()));
+            break;
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (st) {
+            memset(st, 0, sizeof *st);
+            st->arrivals = hacc.arrivals;
+            st->flips = hacc.flips;
+            st->event_hash = hacc.hash;
+            st->bond_sum = hacc.B2 / 2;
+            st->magnetisation = hacc.M;
+            st->launches = launches;
+            st->sweeps = sweeps;
+            st->gpu_seconds = ms * 1e-3;
+        }
+    } while (0);
+    cleanup();
+    return rc;
 }
 
 // ---------------------------------------------------------------- multi-process push (CUDA IPC)
