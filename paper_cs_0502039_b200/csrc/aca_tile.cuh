@@ -32,6 +32,12 @@ __host__ __device__ constexpr int tile_queue_per_warp(int cpw, bool early) { ret
 __host__ __device__ constexpr int grp_slots(int ndim, int tx, int ty, int tz) {
     return ((tx + 4) * (ty + 2) * (ndim == 3 ? tz + 2 : 1) + 15) & ~15;
 }
+// Words (u32) of one spin-bitmap set of the bit-sliced class recount (2-D 64-wide tiles): the even
+// and the odd columns' spin bits of the TY rows and the two face rows, and one byte per row
+// holding the spins of its two x-halo cells.
+__host__ __device__ constexpr int cls_bm_words(int ndim, int tx, int ty) {
+    return (ndim == 2 && tx == 64) ? 2 * (ty + 2) + (ty + 3) / 4 : 0;
+}
 // Shared-memory layout of tile_grp_kernel (host and device): NBUF tile buffers, the P4 (16) and
 // a10 (112) tables, the NLOG-2 tables split as L u64[256] and R u32[256], the reduction
 // scratch, NBUF mbarriers, 32 u32 of ring control (claim counter, the tile of each group, the
@@ -41,7 +47,7 @@ __host__ __device__ constexpr size_t grp_smem_bytes(int ndim, int tx, int ty, in
                                                     bool early, bool cls = false) {
     return ((size_t)nbuf * grp_slots(ndim, tx, ty, tz) + 16 + 112 + 256 + 128 + (size_t)(ntg * ng) / 32 + nbuf) * 8 +
            160 + 16 + (size_t)nbuf * 64 + (((size_t)(ntg * ng / 32) * tile_queue_per_warp(tx * ty * tz / (ntg / 32), early) * 2 + 15) & ~(size_t)15) +
-           (cls ? (size_t)ng * 2 * 16 * 4 : 0);
+           (cls ? (size_t)ng * 2 * (16 + cls_bm_words(ndim, tx, ty)) * 4 : 0);
 }
 
 // a10 per-tile class bookkeeping: the BKL class (s, Sigma) of the cell pair (sl, sl + 1) of a
@@ -85,6 +91,23 @@ __device__ __forceinline__ void cls_flush_warp(unsigned long long c0, unsigned l
         const unsigned int v = (unsigned int)(((b < 8 ? c0 : c1) >> (8 * (b & 7))) & 255ull);
         const unsigned int t = __reduce_add_sync(0xffffffffu, v);
         if (lane == 0 && t) atomicAdd(&gh[b], t);
+    }
+}
+
+// Bit-sliced class count of 32 cells: self = their spin bits, a..d = the spin bits of their
+// four neighbours (bit l of every mask belongs to cell l). The neighbour sum k in 0..4 is added
+// on bit planes (k = b0 + 2 t0 + 4 t1), then bin k + 5 s gets popc(cells with that k and s):
+// the P4 index of (s, Sigma) as in cls_add, for 32 cells in ~35 instructions.
+__device__ __forceinline__ void cls_count32(uint32_t self, uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                            uint32_t* cnt) {
+    const uint32_t s1 = a ^ b, c1 = a & b, s2 = c ^ d, c2 = c & d;
+    const uint32_t b0 = s1 ^ s2, cy = s1 & s2;
+    const uint32_t t0 = c1 ^ c2 ^ cy, t1 = (c1 & c2) | (cy & (c1 ^ c2));
+    const uint32_t eq[5] = {~b0 & ~t0 & ~t1, b0 & ~t0 & ~t1, ~b0 & t0 & ~t1, b0 & t0 & ~t1, t1};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        cnt[k] += __popc(eq[k] & ~self);
+        cnt[k + 5] += __popc(eq[k] & self);
     }
 }
 
@@ -232,6 +255,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
     };
     const unsigned int wh = hi32(wlim);
     const bool wexact = (unsigned int)wlim == 0u;   // w < wlim <=> high(w) < high(wlim)
+    const bool fastE = EARLY && PAIRMAP && (!GEN || P.fast);   // the a10 fast fire (see the fire step)
     uint32_t fl32 = 0, fi32 = 0;   // fast-path flips / fires (folded into st at the end)
     unsigned int rounds = 0;
     bool exact_next = false;
@@ -240,6 +264,13 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         const bool exact = exact_next || r == P.rounds - 1;
         uint32_t emask = 0;
         int ntest = 0;
+        // a10 fast fire (PAIRMAP): the test's decision table index of each candidate, 7 bits per
+        // cell j (bit 6: u = 0), cells 0-8 in pk0, 9-15 in pk1, carried into its queue entry
+        unsigned long long pk0 = 0ull, pk1 = 0ull;
+        auto pk_set = [&](int j, uint32_t v) {
+            if (j < 9) pk0 |= (unsigned long long)v << (7 * j);
+            else pk1 |= (unsigned long long)v << (7 * (j - 9));
+        };
         if constexpr (!EARLY && PAIRMAP) {
             unsigned int tiec = ~0u;
             // rows of the lane's column pair, top to bottom; `a` holds row rr, `b` row rr + 1
@@ -371,8 +402,10 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 const uint32_t u = b0 + b1 + b2 + b3;
                 const uint32_t k = (b0 ? 0u : (uint32_t)(n0 & 1ull)) + (b1 ? 0u : (uint32_t)(n1 & 1ull)) +
                                    (b2 ? 0u : (uint32_t)(n2 & 1ull)) + (b3 ? 0u : (uint32_t)(n3 & 1ull));
-                const bool e = u == 0u || thm[((uint32_t)(w & 1ull) * (Z + 1) + u) * (Z + 1) + k] <= (1ull << 32);
+                const uint32_t ti = ((uint32_t)(w & 1ull) * (Z + 1) + u) * (Z + 1) + k;
+                const bool e = u == 0u || thm[ti] <= (1ull << 32);
                 emask |= (uint32_t)e << j;
+                if (fastE) pk_set(j, ti | (u == 0u ? 64u : 0u));
             };
 #pragma unroll
             for (int rr = 0; rr < RPW; ++rr) {
@@ -397,8 +430,10 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                     gcoord(cell_o(j), gx, gy, gz);
                     uint32_t u, k;
                     early_uk<NDIM, SX, SXY>(VS, sj, w, g, gx, gy, gz, u, k);
-                    const bool e = u == 0u || thm[((uint32_t)(w & 1ull) * (Z + 1) + u) * (Z + 1) + k] <= (1ull << 32);
+                    const uint32_t ti = ((uint32_t)(w & 1ull) * (Z + 1) + u) * (Z + 1) + k;
+                    const bool e = u == 0u || thm[ti] <= (1ull << 32);
                     emask |= (uint32_t)e << j;
+                    if (fastE) pk_set(j, ti | (u == 0u ? 64u : 0u));
                 }
             }
         } else {
@@ -442,7 +477,13 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 uint32_t j;
                 asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(emask));
                 emask ^= 1u << j;
-                const uint32_t e = base | ((j << 5) & 0x1c0u) | (j & 1u);
+                uint32_t e;
+                if (EARLY && fastE) {   // warp-local cell (9 bits) | table index and u = 0 bit (7 bits)
+                    const unsigned long long src = j < 9u ? pk0 >> (7u * j) : pk1 >> (7u * (j - 9u));
+                    e = (uint32_t)(2 * lane) | ((j << 5) & 0x1c0u) | (j & 1u) | (((uint32_t)src & 127u) << 9);
+                } else {
+                    e = base | ((j << 5) & 0x1c0u) | (j & 1u);
+                }
                 asm volatile("st.shared.u16 [%0], %1;" ::"r"(qp), "h"((unsigned short)e) : "memory");
                 qp += 2u;
             }
@@ -466,7 +507,38 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             }
         }
         __syncwarp();
-        if ((PAIRMAP || COLMAP) && !EARLY && (!GEN || P.fast)) {
+        if (EARLY && PAIRMAP && fastE) {
+            // a10 on 64-wide 2-D tiles with the fast arrival: each entry carries its cell's
+            // decision-table index from the test. Using the test-time (u, k) is exact: a neighbour
+            // that came after the cell then cannot change before the cell's arrival (it is not a
+            // local minimum while the cell precedes it), and one that came before stays counted
+            // as unknown even if it has fired since (commit_loop's rule, on an older snapshot).
+            const uint32_t qa = smem_u32(q), sa = smem_u32(S), ta = smem_u32(thm);
+            const uint32_t cb = (uint32_t)(y0 + g.y0) * (uint32_t)g.nx + (uint32_t)x0;
+            for (int i = lane; i < cnt; i += 32) {
+                uint32_t e;
+                asm volatile("ld.shared.u16 %0, [%1];" : "=r"(e) : "r"(qa + 2u * (uint32_t)i) : "memory");
+                const uint32_t o = (uint32_t)wbase + (e & 511u);
+                const uint32_t lx = o % TX, ly = o / TX;
+                const uint32_t a = sa + 8u * (uint32_t)slot((int)lx, (int)ly, 0);
+                unsigned long long w, tm;
+                asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(a) : "memory");
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(tm) : "r"(ta + 8u * ((e >> 9) & 63u)));
+                const uint32_t n = w_count(w, g);
+                if (n == (uint32_t)((1ull << g.NB) - 1ull)) { atomicOr(&P.ctl->overflow, 1u); continue; }
+                const u32x4 rr = philox4x32_10_rk(n, cb + ly * (uint32_t)g.nx + lx, 0u, 0u, P.rk);
+                const bool lo = (unsigned long long)rr.x < tm;
+                if (lo && (e >> 15) == 0u) continue;   // u > 0 and a flip is possible in some world: wait
+                const uint32_t flip = lo ? 1u : 0u;    // u = 0: the P4 decision; u > 0: rejected in every world
+                unsigned long long d = nlog_q32_t(((uint64_t)rr.y << 32) | rr.z, tab, ACA_LN2_Q48);
+                d = d < 1ull ? 1ull : d;
+                if (P.do_hash) st.hacc += ev_hash(rr.w, w >> g.TSH, (unsigned long long)((uint32_t)(w & 1ull) ^ flip));
+                const unsigned long long wn = (w + (d << g.TSH) + 2ull) ^ (unsigned long long)flip;
+                asm volatile("st.volatile.shared.u64 [%0], %1;" ::"r"(a), "l"(wn) : "memory");
+                fl32 += flip;
+                ++fi32;
+            }
+        } else if ((PAIRMAP || COLMAP) && !EARLY && (!GEN || P.fast)) {
             // The common case (64-wide 2-D / 32-wide 3-D tiles, Poisson, lambda = 1, no frames):
             // the queue, the words and the tables are addressed with 32-bit shared-window offsets.
             const uint32_t qa = smem_u32(q), sa = smem_u32(S);
@@ -609,6 +681,11 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     unsigned short* Q = (unsigned short*)(orgs + 4 * NBUF); // NW x QW fire queue entries
     // CLS: per group two 16-bin class histograms (the visit in progress, by the parity `par`)
     unsigned int* ghist = (unsigned int*)((char*)Q + (((size_t)NW * QW * 2 + 15) & ~(size_t)15));
+    // CLS on 2-D 64-wide tiles: the fast tiles' classes are recounted from spin bitmaps built by
+    // ballots at the write-back (per group two sets, by the parity `par`), the others per cell
+    constexpr int CBMW = cls_bm_words(NDIM, TX, TY);
+    constexpr bool BMC = CLS && CBMW > 0 && (NCELL / NWG) % TX == 0;
+    unsigned int* cbm = ghist + NG * 32;
 
     const Geo& g = P.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -719,7 +796,11 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         const Org o = origin(k);
         bool early = false;
         if constexpr (CLS) {   // the tile's classes at its last visit decide its path for this one
+#ifdef ACA_ABL_NOARM
+            if (false) {
+#else
             if (o.valid) {
+#endif
                 const uint4* hp = reinterpret_cast<const uint4*>(P.tile_hist + 16 * tile_index(o));
                 long long wsum = 0;
 #pragma unroll
@@ -903,7 +984,17 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
                     const size_t gi = NDIM == 2 ? (size_t)(o.y0 + ly) * g.nx + o.x0 + lx
                                                 : ((size_t)(o.z0 + lz) * g.ny + (o.y0 + ly)) * g.nx + o.x0 + lx;
                     const ulonglong2 v = lds128v(&S[slot(lx, ly, lz)]);
-                    if constexpr (CLS) cls_pair<NDIM, SX, SXY>(S, slot(lx, ly, lz), v, c0, c1);
+                    if constexpr (BMC) {   // spin bits of the row's even / odd columns
+                        const unsigned int be = __ballot_sync(0xffffffffu, (unsigned int)v.x & 1u);
+                        const unsigned int bo = __ballot_sync(0xffffffffu, (unsigned int)v.y & 1u);
+                        if (lane == 0) {
+                            unsigned int* bm = cbm + (gid * 2 + par) * CBMW;
+                            bm[ly + 1] = be;
+                            bm[TY + 2 + ly + 1] = bo;
+                        }
+                    } else if constexpr (CLS) {
+                        cls_pair<NDIM, SX, SXY>(S, slot(lx, ly, lz), v, c0, c1);
+                    }
                     ACA_CHECK(gi + 1 < (size_t)g.nx * g.ny * g.nz, gi, oo);
                     *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
                     active += (v.x < wT) + (v.y < wT);
@@ -918,6 +1009,30 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
                     }
                 }
                 if (P.lag_q) atomicMin(&lagw[0], wm);
+                if constexpr (BMC) {   // the x-halo spins of the warp's rows; the face rows
+                    unsigned int* bm = cbm + (gid * 2 + par) * CBMW;
+                    constexpr int RPWB = CPW / TX;
+                    const int r0 = wb0 / TX;
+                    if (lane < RPWB) {
+                        const int row = r0 + lane;
+                        const unsigned int hb = (unsigned int)(S[slot(-1, row, 0)] & 1ull) |
+                                                ((unsigned int)(S[slot(TX, row, 0)] & 1ull) << 1);
+                        reinterpret_cast<unsigned char*>(bm + 2 * (TY + 2))[row] = (unsigned char)hb;
+                    }
+#pragma unroll
+                    for (int f = 0; f < 2; ++f) {
+                        if ((f == 0 && wg == 0) || (f == 1 && wg == NWG - 1)) {
+                            const int ly = f == 0 ? -1 : TY;
+                            const ulonglong2 v = lds128v(&S[slot(2 * lane, ly, 0)]);
+                            const unsigned int be = __ballot_sync(0xffffffffu, (unsigned int)v.x & 1u);
+                            const unsigned int bo = __ballot_sync(0xffffffffu, (unsigned int)v.y & 1u);
+                            if (lane == 0) {
+                                bm[ly + 1] = be;
+                                bm[TY + 2 + ly + 1] = bo;
+                            }
+                        }
+                    }
+                }
             } else {
                 group_bar(1 + gid, NTG);   // other warps' cells are read below
                 for (int oo = gt; oo < NCELL; oo += NTG) {
@@ -934,7 +1049,9 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
                     }
                 }
             }
-            if constexpr (CLS) cls_flush_warp<NBIN>(c0, c1, ghist + (gid * 2 + par) * 16, lane);
+            if constexpr (CLS) {
+                if (!(BMC && fast)) cls_flush_warp<NBIN>(c0, c1, ghist + (gid * 2 + par) * 16, lane);
+            }
         }
         ACA_TRACE(6, k);
         // refill the buffer with tile k + NBUF: armed before the barrier (the arrive does not
@@ -946,7 +1063,31 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         group_bar(1 + gid, NTG);   // the buffer is free
         ACA_TRACE(7, k);
         if constexpr (CLS) {   // the tile's class histogram of this visit -> HBM (and zeroed for reuse)
-            if (gt == 0 && o.valid) {
+            if (BMC && fast && o.valid) {
+#ifndef ACA_ABL_NOCOUNT
+                if (wg == 0) {   // warp 0 of the group: lane l counts rows l, l + 32, ...
+                    const unsigned int* bm = cbm + (gid * 2 + par) * CBMW;
+                    const unsigned char* hb = reinterpret_cast<const unsigned char*>(bm + 2 * (TY + 2));
+                    uint32_t cnt[10] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                    for (int r = lane; r < TY; r += 32) {
+                        const uint32_t E = bm[r + 1], O = bm[TY + 3 + r];
+                        const uint32_t h = hb[r];
+                        // even column 2l: left = odd 2l - 1 (the x-halo for l = 0), right = odd 2l
+                        cls_count32(E, (O << 1) | (h & 1u), O, bm[r], bm[r + 2], cnt);
+                        // odd column 2l + 1: left = even 2l, right = even 2l + 2 (the x-halo for l = 31)
+                        cls_count32(O, E, (E >> 1) | ((h >> 1) << 31), bm[TY + 2 + r], bm[TY + 4 + r], cnt);
+                    }
+                    uint32_t tot[16];
+#pragma unroll
+                    for (int b = 0; b < 16; ++b) tot[b] = b < 10 ? __reduce_add_sync(0xffffffffu, cnt[b]) : 0u;
+                    if (lane == 0) {
+                        uint4* hp = reinterpret_cast<uint4*>(P.tile_hist + 16 * tile_index(o));
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) hp[j] = make_uint4(tot[4 * j], tot[4 * j + 1], tot[4 * j + 2], tot[4 * j + 3]);
+                    }
+                }
+#endif
+            } else if (gt == 0 && o.valid) {
                 unsigned int* gh = ghist + (gid * 2 + par) * 16;
                 uint4* hp = reinterpret_cast<uint4*>(P.tile_hist + 16 * tile_index(o));
 #pragma unroll

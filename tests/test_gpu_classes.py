@@ -84,14 +84,20 @@ def test_class_book_exact(aca, oracle_mod, case):
     assert G >= 1
 
 
-@pytest.mark.parametrize("dims,Ts", [((256, 256), [20.0]), ((256, 192), [5.0, 9.0]), ((64, 64, 32), [3.0])])
-def test_kernel_histograms_of_the_last_colour(aca, oracle_mod, dims, Ts):
+@pytest.mark.parametrize("dims,Ts,extra", [
+    ((256, 256), [20.0], {}), ((256, 192), [5.0, 9.0], {}), ((64, 64, 32), [3.0], {}),
+    # the 2-D bit-sliced recount: many visits per group (both bitmap parities, the buffer ring),
+    # a disordered heat-bath state (every class populated), ragged edge tiles
+    ((512, 512), [4.0, 7.0], dict(max_ctas=3, beta=0.35, rule=0, init_q=0.5, class_wmax=0.05)),
+    ((520, 264), [6.0], dict(beta=0.5, rule=0, init_q=0.5, class_wmax=-1.0)),
+])
+def test_kernel_histograms_of_the_last_colour(aca, oracle_mod, dims, Ts, extra):
     """Without a refresh: each tile of the colour launched last was recounted by the tile kernel
     at its final visit, after which nothing changed, so it equals the recount of the oracle's
     final spins; every tile's histogram counts exactly its cells."""
-    beta = 1.0 if len(dims) == 2 else 0.5
-    g, o = run_pair(aca, oracle_mod, dims, Ts, beta=beta, h=0.1, rule=1, init_q=0.05, seed=67, early_reject=1,
-                    class_book=1, class_wmax=0.002)
+    kw = dict(beta=1.0 if len(dims) == 2 else 0.5, h=0.1, rule=1, init_q=0.05, class_wmax=0.002)
+    kw.update(extra)
+    g, o = run_pair(aca, oracle_mod, dims, Ts, seed=67, early_reject=1, class_book=1, **kw)
     assert_same(g, o)
     tx, ty, tz, G, *tile = aca.aca_get_tile_grid(g.handle)
     assert G == 1
