@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     constexpr bool CLS = EM == 2;
     constexpr int NBIN = 2 * (2 * NDIM + 1);
     static_assert(!MOORE || NDIM == 2, "Moore neighbourhood: 2-D");
-    static_assert(NG >= 1 && NG <= 15 && NBUF >= 1 && 1 + 2 * NG + NBUF <= 32, "groups / buffers");
+    static_assert(NG >= 1 && NG <= 14 && NBUF >= 1 && 1 + 2 * NG + NBUF <= 30, "groups / buffers");
     constexpr int NT = NTG * NG;
     constexpr int SX = TX + 4, SY = TY + 2, SZ = (NDIM == 3) ? TZ + 2 : 1;
     constexpr int SXY = SX * SY;
@@ -701,6 +701,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         for (int i = tid; i < NG * 32; i += NT) ghist[i] = 0u;
     if (tid == 0) {
         cs[0] = 0u;
+        cs[30] = cs[31] = 0u;   // CLS: tile visits per path
         lagw[0] = ~0ull;
         lagw[1] = *(volatile unsigned long long*)&P.ctl->wlim_T;
     }
@@ -886,7 +887,6 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     TileTotals tot;
     unsigned int active = 0;   // cells of this CTA still below T (< 2^32: N < 2^32)
     unsigned int rounds_max = 0;
-    unsigned long long nv_early = 0, nv_plain = 0;   // CLS: visits per path (thread 0 of each group)
     unsigned short* q = Q + warp * QW;
     // A group's next tile is claimed by its thread 0 before the write-back barrier that ends
     // the current one, into the other of the group's two slots (everybody has read the current
@@ -956,7 +956,11 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         unsigned long long c0 = 0, c1 = 0;   // CLS: per-lane class counters of this visit
         if (o.valid) {
             unsigned int rounds;
+#ifdef ACA_ABL_CLS_EARLYONLY
+            if (true) {
+#else
             if (!CLS || o.early) {
+#endif
                 rounds = o.full ? tile_rounds<NDIM, TX, TY, TZ, NTG, true, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
                                                                                              o.x0, o.y0, o.z0, wlim, st)
                                 : tile_rounds<NDIM, TX, TY, TZ, NTG, false, EARLY, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
@@ -967,7 +971,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
                                 : tile_rounds<NDIM, TX, TY, TZ, NTG, false, false, MOORE, GEN>(P, S, q, wg, thr_a, thr, thm, tab,
                                                                                               o.x0, o.y0, o.z0, wlim, st);
             }
-            if (CLS && gt == 0) { nv_early += o.early; nv_plain += !o.early; }
+            if (CLS && gt == 0) atomicAdd(&cs[o.early ? 30 : 31], 1u);   // CLS: visits per path
             rounds_max = rounds > rounds_max ? rounds : rounds_max;
             tot.fold(st);
             if (fast) {
@@ -1110,8 +1114,8 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     const unsigned long long s_tst = block_sum<NT>(tot.tested, red);
     const unsigned long long s_hsh = block_sum<NT>(st.hacc, red);
     if constexpr (CLS) {
-        if (nv_early) atomicAdd(&P.ctl->visits_early, nv_early);
-        if (nv_plain) atomicAdd(&P.ctl->visits_plain, nv_plain);
+        if (tid == 0 && cs[30]) atomicAdd(&P.ctl->visits_early, (unsigned long long)cs[30]);
+        if (tid == 0 && cs[31]) atomicAdd(&P.ctl->visits_plain, (unsigned long long)cs[31]);
     }
     if (tid == 0) finish_launch(P.ctl, s_act, s_fir, s_flp, s_tst, s_hsh, rounds_max, P.phase, P.lag_q, g.TSH);
 }
