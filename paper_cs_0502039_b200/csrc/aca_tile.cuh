@@ -392,31 +392,47 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             const ulonglong2 up = lds128v(&VS[s0 - SX]);
             unsigned long long u0 = up.x, u1 = up.y;
             ulonglong2 a = lds128v(&VS[s0]);
-            auto early_cell = [&](unsigned long long w, unsigned long long n0, unsigned long long n1,
+            // table index ti = 25 s + 5 u + k = 25 s + sum over neighbours of (before ? 5 : spin
+            // bit); the candidate test is one bit of the mask built at kernel start (thm[100])
+            static_assert(Z == 4, "a10 PAIRMAP index");
+            const unsigned long long cmask = thm[100];
+            // Strict rounds count a neighbour with an equal high half as one that may come before
+            // (unknown): conservative for the rejection test, and u = 0 still means a strict local
+            // minimum; exact rounds send such lanes to the exact pass instead.
+            auto early_cell = [&](bool strict, unsigned long long w, unsigned long long n0, unsigned long long n1,
                                   unsigned long long n2, unsigned long long n3, int j) {
                 if (w >= wlim) return;
                 ++ntest;
                 const unsigned int h = hi32(w), h0 = hi32(n0), h1 = hi32(n1), h2 = hi32(n2), h3 = hi32(n3);
-                if (h0 == h || h1 == h || h2 == h || h3 == h) tiec = 0u;
-                const uint32_t b0 = h0 < h, b1 = h1 < h, b2 = h2 < h, b3 = h3 < h;
-                const uint32_t u = b0 + b1 + b2 + b3;
-                const uint32_t k = (b0 ? 0u : (uint32_t)(n0 & 1ull)) + (b1 ? 0u : (uint32_t)(n1 & 1ull)) +
-                                   (b2 ? 0u : (uint32_t)(n2 & 1ull)) + (b3 ? 0u : (uint32_t)(n3 & 1ull));
-                const uint32_t ti = ((uint32_t)(w & 1ull) * (Z + 1) + u) * (Z + 1) + k;
-                const bool e = u == 0u || thm[ti] <= (1ull << 32);
-                emask |= (uint32_t)e << j;
-                if (fastE) pk_set(j, ti | (u == 0u ? 64u : 0u));
+                uint32_t v;
+                if (strict) {
+                    v = (h0 <= h ? 5u : (uint32_t)n0 & 1u) + (h1 <= h ? 5u : (uint32_t)n1 & 1u) +
+                        (h2 <= h ? 5u : (uint32_t)n2 & 1u) + (h3 <= h ? 5u : (uint32_t)n3 & 1u);
+                } else {
+                    if (h0 == h || h1 == h || h2 == h || h3 == h) tiec = 0u;
+                    v = (h0 < h ? 5u : (uint32_t)n0 & 1u) + (h1 < h ? 5u : (uint32_t)n1 & 1u) +
+                        (h2 < h ? 5u : (uint32_t)n2 & 1u) + (h3 < h ? 5u : (uint32_t)n3 & 1u);
+                }
+                const uint32_t ti = (uint32_t)(w & 1ull) * 25u + v;
+                emask |= (uint32_t)((cmask >> ti) & 1ull) << j;
+                if (fastE) pk_set(j, ti | (v < 5u ? 64u : 0u));
             };
-#pragma unroll
-            for (int rr = 0; rr < RPW; ++rr) {
-                const int sr = s0 + rr * SX;
-                const ulonglong2 b = lds128v(&VS[sr + SX]);
-                const unsigned long long lw = VS[sr - 1], rw = VS[sr + 2];
-                early_cell(a.x, lw, a.y, u0, b.x, 2 * rr);
-                early_cell(a.y, a.x, rw, u1, b.y, 2 * rr + 1);
-                u0 = a.x; u1 = a.y;
-                a = b;
+#define ACA_EARLY_ROWS(STRICT)                                                                       \
+    _Pragma("unroll") for (int rr = 0; rr < RPW; ++rr) {                                             \
+        const int sr = s0 + rr * SX;                                                                 \
+        const ulonglong2 b = lds128v(&VS[sr + SX]);                                                  \
+        const unsigned long long lw = VS[sr - 1], rw = VS[sr + 2];                                   \
+        early_cell(STRICT, a.x, lw, a.y, u0, b.x, 2 * rr);                                           \
+        early_cell(STRICT, a.y, a.x, rw, u1, b.y, 2 * rr + 1);                                       \
+        u0 = a.x; u1 = a.y;                                                                          \
+        a = b;                                                                                       \
+    }
+            if (!exact) {
+                ACA_EARLY_ROWS(true)
+            } else {
+                ACA_EARLY_ROWS(false)
             }
+#undef ACA_EARLY_ROWS
             if (tiec == 0u) {
                 emask = 0;
                 ntest = 0;
@@ -691,7 +707,15 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int gid = tid / NTG, gt = tid - gid * NTG, wg = gt >> 5;
     if (tid < 16) thr[tid] = tid < 14 ? P.thr[tid] : 0ull;
-    for (int i = tid; i < 112; i += NT) thm[i] = i < 98 ? P.thm[i] : ~0ull;
+    for (int i = tid; i < 112; i += NT) {
+        unsigned long long v = i < 98 ? P.thm[i] : ~0ull;
+        if (NDIM == 2 && i == 100) {   // 2-D a10 candidate mask: bit ti <=> u = 0 or thm[ti] <= 2^32
+            v = 0ull;
+            for (int t = 0; t < 50; ++t)
+                if (t % 25 < 5 || P.thm[t] <= (1ull << 32)) v |= 1ull << t;
+        }
+        thm[i] = v;
+    }
     for (int i = tid; i < 256; i += NT) {
         Lt[i] = P.lr[2 * i];
         Rt[i] = (unsigned int)P.lr[2 * i + 1];
