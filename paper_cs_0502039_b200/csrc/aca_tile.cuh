@@ -436,6 +436,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             if (tiec == 0u) {
                 emask = 0;
                 ntest = 0;
+                pk0 = pk1 = 0ull;   // the first pass's indices are replaced, not merged
 #pragma unroll 1
                 for (int j = 0; j < JPL; ++j) {
                     const int sj = cell_slot(j);

@@ -120,3 +120,17 @@ def test_class_book_errors(aca):
     with pytest.raises(aca.AcaError):
         g.tile_classes()                                                   # bookkeeping off
     g.close()
+
+
+@pytest.mark.parametrize("opts", [dict(early_reject=1, class_book=1, class_wmax=1.0),
+                                  dict(early_reject=1, class_book=0),
+                                  dict(early_reject=1, class_book=1, class_wmax=0.002),
+                                  dict(early_reject=0, class_book=0)])
+def test_high_half_ties_fast_paths(aca, oracle_mod, monkeypatch, opts):
+    """The fast arrival (Poisson, lambda = 1, no tie stress) with frequent equal high halves: a
+    10-bit counter field leaves the words' high halves a time quantum of 2^-10, so the a10 and
+    plain tests meet tied neighbours on a small lattice (their exact passes and the strict rounds'
+    conservative treatment), as c5 does at 8192^2."""
+    monkeypatch.setenv("ACA_NB_CAP", "10")
+    g, o = run_pair(aca, oracle_mod, (256, 256), [10.0, 25.0], seed=71, **C5, **opts)
+    assert_same(g, o)
