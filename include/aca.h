@@ -243,9 +243,11 @@ int aca_sync(aca_sim* s);
  * aca_ipc_import (world x ACA_IPC_BLOB_BYTES bytes), once, before the first run_until.
  * Errors: ACA_ESTATE (not a push-mode handle / imported twice / run before import), ACA_EINVAL,
  * ACA_ECUDA. Stats, frames and getters are rank-local as for the NCCL mode; the boundary
- * bond term of aca_get_stats reads the halo copy of the neighbour's row, so take stats before
- * any neighbour resets or sets its state (a barrier between runs and resets keeps it exact).
- * Needs the persistent tile kernel (variant 0, 4 or 5; ACA_EINVAL at create otherwise). */
+ * bond term of aca_get_stats reads a snapshot of the neighbours' rows taken when every rank
+ * had finished the last run (or their P5 rows after create / reset), so a neighbour's later
+ * reset or run does not race with it; after set_state / set_spins a run_until must come first
+ * (ACA_ESTATE). Needs the persistent tile kernel (not whole_lattice = 1 or sync_rounds = 1;
+ * ACA_EINVAL at create otherwise). */
 #define ACA_IPC_BLOB_BYTES 192
 int aca_ipc_export(const aca_sim* s, void* out, size_t size);
 int aca_ipc_import(aca_sim* s, const void* blobs, size_t size);
