@@ -77,7 +77,10 @@ typedef struct {
                                    section 6 keeps their numbers. The group size of the 64x64
                                    tile is chosen by the library (512 threads when a launch has
                                    fewer than two tiles per SM). Environment switches for
-                                   ablations only: ACA_TILE_NT, ACA_BULK, ACA_EFF_STREAM. */
+                                   ablations only: ACA_TILE_NT, ACA_BULK, ACA_EFF_STREAM,
+                                   ACA_NO_RES, ACA_RES_NT, ACA_NO_TMA_BOX; for tests only:
+                                   ACA_NB_CAP=b caps the counter field at b bits (the words'
+                                   high halves then tie often: exercises the exact passes). */
     int32_t early_reject;       /* 1: a cell may also commit arrivals that are rejected for
                                    every possible state of the neighbours it still waits for
                                    (exact; pays off at low temperature, config 5). 0 = off */
