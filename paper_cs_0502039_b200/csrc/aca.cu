@@ -1179,6 +1179,8 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
     rc = issue(0);
     if (rc) return rc;
     int outstanding = -1;      // pipelined: slot issued but not yet retired
+    unsigned long long last_fired = ~0ull;
+    int stall_batches = 0;
     for (int iter = 1;; ++iter) {
         const int cur = iter & 1, prev = cur ^ 1;
         if (pipelined) {
@@ -1189,6 +1191,20 @@ int aca_run_until_q32(aca_sim* S, uint64_t Tq) {
         bool done = false;
         rc = retire(pipelined ? prev : 0, &done);
         if (rc) return rc;
+        if (!done && S->world == 1) {
+            // Every sweep fires at least the globally first pending arrival (fig:amcgen progress,
+            // PAPER.md:820-823), so hundreds of batches without one fired arrival mean a broken
+            // kernel, not a slow run: fail loudly instead of spinning. (A multi-process rank may
+            // legitimately wait for its neighbours, so only single-process runs are checked.)
+            unsigned long long f = 0;
+            const int sl = pipelined ? prev : 0;
+            for (size_t i = 0; i < nsh; ++i) f += S->h_ctl[sl * nsh + i].fired;
+            stall_batches = f == last_fired ? stall_batches + 1 : 0;
+            last_fired = f;
+            if (stall_batches > 256)
+                return fail(ACA_ESTATE, "no arrival fired in 256 batches of launches with cells still below T "
+                                        "(a kernel fault: the method always makes progress)");
+        }
         if (S->ipc && done) {
             // this rank has no cell below T any more (monotone: halos only grow); publish that
             // and wait, without issuing more batches, until every rank has. A rank whose epoch is

@@ -264,12 +264,17 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
         const bool exact = exact_next || r == P.rounds - 1;
         uint32_t emask = 0;
         int ntest = 0;
-        // a10 fast fire (PAIRMAP): the test's decision table index of each candidate, 7 bits per
-        // cell j (bit 6: u = 0), cells 0-8 in pk0, 9-15 in pk1, carried into its queue entry
-        unsigned long long pk0 = 0ull, pk1 = 0ull;
+        // a10 fast fire (PAIRMAP): the test's decision-table index ti < 50 of each cell j, one byte
+        // each (byte j & 3 of pk[j >> 2]; one IMAD per cell for a constant j), carried into its
+        // queue entry; the fire step reads u = 0 off ti
+        static_assert(!PAIRMAP || JPL <= 16, "a10 index packing: 16 cells per lane");
+        uint32_t pk0 = 0u, pk1 = 0u, pk2 = 0u, pk3 = 0u;
         auto pk_set = [&](int j, uint32_t v) {
-            if (j < 9) pk0 |= (unsigned long long)v << (7 * j);
-            else pk1 |= (unsigned long long)v << (7 * (j - 9));
+            const uint32_t add = v << (8 * (j & 3));
+            if ((j >> 2) == 0) pk0 += add;
+            else if ((j >> 2) == 1) pk1 += add;
+            else if ((j >> 2) == 2) pk2 += add;
+            else pk3 += add;
         };
         if constexpr (!EARLY && PAIRMAP) {
             unsigned int tiec = ~0u;
@@ -415,7 +420,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 }
                 const uint32_t ti = (uint32_t)(w & 1ull) * 25u + v;
                 emask |= (uint32_t)((cmask >> ti) & 1ull) << j;
-                if (fastE) pk_set(j, ti | (v < 5u ? 64u : 0u));
+                if (fastE) pk_set(j, ti);
             };
 #define ACA_EARLY_ROWS(STRICT)                                                                       \
     _Pragma("unroll") for (int rr = 0; rr < RPW; ++rr) {                                             \
@@ -436,7 +441,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             if (tiec == 0u) {
                 emask = 0;
                 ntest = 0;
-                pk0 = pk1 = 0ull;   // the first pass's indices are replaced, not merged
+                pk0 = pk1 = pk2 = pk3 = 0u;   // the first pass's indices are replaced, not merged
 #pragma unroll 1
                 for (int j = 0; j < JPL; ++j) {
                     const int sj = cell_slot(j);
@@ -450,7 +455,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                     const uint32_t ti = ((uint32_t)(w & 1ull) * (Z + 1) + u) * (Z + 1) + k;
                     const bool e = u == 0u || thm[ti] <= (1ull << 32);
                     emask |= (uint32_t)e << j;
-                    if (fastE) pk_set(j, ti | (u == 0u ? 64u : 0u));
+                    if (fastE) pk_set(j, ti);
                 }
             }
         } else {
@@ -495,9 +500,9 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 asm("bfind.u32 %0, %1;" : "=r"(j) : "r"(emask));
                 emask ^= 1u << j;
                 uint32_t e;
-                if (EARLY && fastE) {   // warp-local cell (9 bits) | table index and u = 0 bit (7 bits)
-                    const unsigned long long src = j < 9u ? pk0 >> (7u * j) : pk1 >> (7u * (j - 9u));
-                    e = (uint32_t)(2 * lane) | ((j << 5) & 0x1c0u) | (j & 1u) | (((uint32_t)src & 127u) << 9);
+                if (EARLY && fastE) {   // warp-local cell (9 bits) | table index (6 bits)
+                    const uint32_t ti = __byte_perm(j < 8u ? pk0 : pk2, j < 8u ? pk1 : pk3, j & 7u) & 0xffu;
+                    e = (uint32_t)(2 * lane) | ((j << 5) & 0x1c0u) | (j & 1u) | (ti << 9);
                 } else {
                     e = base | ((j << 5) & 0x1c0u) | (j & 1u);
                 }
@@ -540,12 +545,15 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 const uint32_t a = sa + 8u * (uint32_t)slot((int)lx, (int)ly, 0);
                 unsigned long long w, tm;
                 asm volatile("ld.volatile.shared.u64 %0, [%1];" : "=l"(w) : "r"(a) : "memory");
-                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(tm) : "r"(ta + 8u * ((e >> 9) & 63u)));
+                const uint32_t ti = (e >> 9) & 63u;
+                asm volatile("ld.shared.u64 %0, [%1];" : "=l"(tm) : "r"(ta + 8u * ti));
                 const uint32_t n = w_count(w, g);
                 if (n == (uint32_t)((1ull << g.NB) - 1ull)) { atomicOr(&P.ctl->overflow, 1u); continue; }
                 const u32x4 rr = philox4x32_10_rk(n, cb + ly * (uint32_t)g.nx + lx, 0u, 0u, P.rk);
                 const bool lo = (unsigned long long)rr.x < tm;
-                if (lo && (e >> 15) == 0u) continue;   // u > 0 and a flip is possible in some world: wait
+                // u = 0 iff ti mod 25 < 5: bits 0-4 and 25-29 of 0x3e00001f (clamped shift: 0 for ti >= 32)
+                const bool u0 = (__funnelshift_rc(0x3e00001fu, 0u, ti) & 1u) != 0u;
+                if (lo && !u0) continue;   // u > 0 and a flip is possible in some world: wait
                 const uint32_t flip = lo ? 1u : 0u;    // u = 0: the P4 decision; u > 0: rejected in every world
                 unsigned long long d = nlog_q32_t(((uint64_t)rr.y << 32) | rr.z, tab, ACA_LN2_Q48);
                 d = d < 1ull ? 1ull : d;
@@ -978,7 +986,6 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         if (patched) group_bar(1 + gid, NTG);
         ACA_TRACE(2, ((unsigned long long)o.x0 << 32) | (unsigned)o.y0);
 
-        unsigned long long c0 = 0, c1 = 0;   // CLS: per-lane class counters of this visit
         if (o.valid) {
             unsigned int rounds;
 #ifdef ACA_ABL_CLS_EARLYONLY
@@ -997,6 +1004,7 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
                                                                                               o.x0, o.y0, o.z0, wlim, st);
             }
             if (CLS && gt == 0) atomicAdd(&cs[o.early ? 30 : 31], 1u);   // CLS: visits per path
+            unsigned long long c0 = 0, c1 = 0;   // CLS: per-lane class counters of this visit (per-cell count)
             rounds_max = rounds > rounds_max ? rounds : rounds_max;
             tot.fold(st);
             if (fast) {
