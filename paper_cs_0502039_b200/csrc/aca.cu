@@ -327,6 +327,7 @@ void set_geo_layout(aca_sim* S) {
     for (auto& sh : S->shards) {
         sh.g.NB = S->NB;
         sh.g.TSH = S->NB + 1;
+        sh.g.nbmask = (1u << S->NB) - 1u;
     }
 }
 
@@ -660,6 +661,7 @@ int fit_layout(aca_sim* S, uint64_t Tq) {
         Geo ga = sh.g;
         ga.NB = old_nb;
         ga.TSH = old_nb + 1;
+        ga.nbmask = (1u << old_nb) - 1u;
         repack_kernel<<<1184, 256, 0, S->stream>>>(sh.words, ga, sh.g, (unsigned long long)sh.n);
         CK(cudaGetLastError());
     }

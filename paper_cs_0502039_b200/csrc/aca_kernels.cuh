@@ -98,11 +98,12 @@ struct Geo {
     int y0, z0;              // global offset of the shard along the sharded axis
     int sharded;             // 0: periodic wrap inside the storage; 1: halo buffers
     int NB, TSH;             // counter bits, time shift (= NB + 1)
+    unsigned int nbmask;     // (1 << NB) - 1: the counter field's mask and its saturated value
 };
 
 __device__ __host__ __forceinline__ unsigned long long w_time(unsigned long long w, const Geo& g) { return w >> g.TSH; }
 __device__ __host__ __forceinline__ unsigned int w_count(unsigned long long w, const Geo& g) {
-    return (unsigned int)((w >> 1) & ((1ull << g.NB) - 1ull));
+    return (unsigned int)(w >> 1) & g.nbmask;   // NB <= 31
 }
 __device__ __host__ __forceinline__ unsigned long long w_pack(unsigned long long t, unsigned long long n,
                                                               unsigned long long sb, const Geo& g) {
@@ -353,7 +354,7 @@ __device__ __forceinline__ FireOut fire(unsigned long long w, uint32_t ones, int
                                         int do_hash, Ctl* ctl, int law = 0, const FrameParams* fr = nullptr) {
     FireOut o;
     const uint32_t k = w_count(w, g);
-    if (k == (uint32_t)((1ull << g.NB) - 1ull)) {
+    if (k == g.nbmask) {
         atomicOr(&ctl->overflow, 1u);
         o.wnew = w; o.flip = 0; o.h = 0; o.ok = false;
         return o;
@@ -438,7 +439,7 @@ __device__ __forceinline__ FireOut fire_fast(unsigned long long w, uint32_t ones
                                              uint32_t thr_a, const NlogSmem& tab, const uint32_t* rk, int do_hash) {
     FireOut o;
     const uint32_t k = w_count(w, g);
-    o.ok = k != (uint32_t)((1ull << g.NB) - 1ull);
+    o.ok = k != g.nbmask;
     const uint32_t sb = (uint32_t)(w & 1ull);
     const uint32_t idx = ones + (uint32_t)(z + 1) * sb;
     const u32x4 r = philox4x32_10_rk(k, c, 0u, 0u, rk);

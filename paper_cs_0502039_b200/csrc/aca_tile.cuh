@@ -150,7 +150,7 @@ __device__ __forceinline__ void commit_loop(const KParams& P, volatile unsigned 
         const unsigned long long tm = thm[(sb * (Z + 1) + u) * (Z + 1) + k];
         if (tm > (1ull << 32)) break;                     // must wait for the u neighbours
         const uint32_t n = w_count(w, g);
-        if (n == (uint32_t)((1ull << g.NB) - 1ull)) { atomicOr(&P.ctl->overflow, 1u); break; }
+        if (n == g.nbmask) { atomicOr(&P.ctl->overflow, 1u); break; }
         // FASTP (P.fast: Poisson, lambda = 1, no tie stress, no frames, N < 2^32): the same
         // integers with the general branches compiled out
         const u32x4 r = philox4x32_10_rk(n, (uint32_t)cid, FASTP ? 0u : (uint32_t)(cid >> 32), 0u, P.rk);
@@ -548,7 +548,7 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
                 const uint32_t ti = (e >> 9) & 63u;
                 asm volatile("ld.shared.u64 %0, [%1];" : "=l"(tm) : "r"(ta + 8u * ti));
                 const uint32_t n = w_count(w, g);
-                if (n == (uint32_t)((1ull << g.NB) - 1ull)) { atomicOr(&P.ctl->overflow, 1u); continue; }
+                if (n == g.nbmask) { atomicOr(&P.ctl->overflow, 1u); continue; }
                 const u32x4 rr = philox4x32_10_rk(n, cb + ly * (uint32_t)g.nx + lx, 0u, 0u, P.rk);
                 const bool lo = (unsigned long long)rr.x < tm;
                 // u = 0 iff ti mod 25 < 5: bits 0-4 and 25-29 of 0x3e00001f (clamped shift: 0 for ti >= 32)
