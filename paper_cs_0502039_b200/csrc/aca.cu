@@ -189,6 +189,7 @@ struct aca_sim {
     int nthreads = 256;
     cudaGraphExec_t graph = nullptr;
     int graph_rounds = 0;
+    bool graph_stale = false;      // same launches, new parameters (reset: the seed's round keys)
     Ctl* h_ctl = nullptr;          // pinned mirror (2 slots per shard)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     cudaEvent_t evb[2][3] = {};    // per in-flight batch: start, end of kernels, end of ctl copy
@@ -508,14 +509,16 @@ int launch_round(aca_sim* S) {
 void drop_graph(aca_sim* S) {
     if (S->graph) cudaGraphExecDestroy(S->graph);
     S->graph = nullptr;
+    S->graph_stale = false;
 }
 
 int build_graph(aca_sim* S) {
-    if (S->graph) return ACA_OK;
+    if (S->graph && !S->graph_stale) return ACA_OK;
     if (S->use_nccl || S->sync_debug) return ACA_OK;   // NCCL path / ACA_SYNC_DEBUG: direct launches
     cudaGraph_t g = nullptr;
     if (cudaStreamBeginCapture(S->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
         cudaGetLastError();
+        drop_graph(S);
         return ACA_OK;
     }
     int rc = ACA_OK;
@@ -524,7 +527,18 @@ int build_graph(aca_sim* S) {
     if (rc != ACA_OK || e != cudaSuccess) {
         cudaGetLastError();
         if (g) cudaGraphDestroy(g);
+        drop_graph(S);
         return ACA_OK;   // fall back to direct launches (same kernels)
+    }
+    if (S->graph) {   // stale parameters only: update the instantiated graph in place (no re-instantiation)
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(S->graph, g, &info) == cudaSuccess) {
+            cudaGraphDestroy(g);
+            S->graph_stale = false;
+            return ACA_OK;
+        }
+        cudaGetLastError();
+        drop_graph(S);
     }
     e = cudaGraphInstantiate(&S->graph, g, 0);
     cudaGraphDestroy(g);
@@ -1294,7 +1308,7 @@ int aca_reset(aca_sim* S, uint64_t seed) {
     if (!S) return fail(ACA_EINVAL, "null handle");
     CK(cudaSetDevice(S->device));
     S->seed = seed;
-    drop_graph(S);   // the key is a kernel parameter
+    if (S->graph) S->graph_stale = true;   // the key is a kernel parameter: updated at the next run
     return init_state(S);
 }
 
