@@ -36,7 +36,7 @@ __host__ __device__ constexpr int grp_slots(int ndim, int tx, int ty, int tz) {
 // and the odd columns' spin bits of the TY rows and the two face rows, and one byte per row
 // holding the spins of its two x-halo cells.
 __host__ __device__ constexpr int cls_bm_words(int ndim, int tx, int ty) {
-    return (ndim == 2 && tx == 64) ? 2 * (ty + 2) + (ty + 3) / 4 : 0;
+    return (ndim == 2 && tx == 64) ? 2 * (ty + 2) + (ty + 3) / 4 + 17 : 0;   // + the deferred count: 16 bins, tile
 }
 // Shared-memory layout of tile_grp_kernel (host and device): NBUF tile buffers, the P4 (16) and
 // a10 (112) tables, the NLOG-2 tables split as L u64[256] and R u32[256], the reduction
@@ -108,6 +108,30 @@ __device__ __forceinline__ void cls_count32(uint32_t self, uint32_t a, uint32_t 
     for (int k = 0; k < 5; ++k) {
         cnt[k] += __popc(eq[k] & ~self);
         cnt[k + 5] += __popc(eq[k] & self);
+    }
+}
+
+// A warp's share of the bit-sliced recount of a visit's bitmap set (2-D 64-wide tiles, TY rows
+// + 2 face rows): lane l < RPW counts row r0 + l, the warp's bin sums are added to the set's
+// deferred histogram (16 u32 after the bitmaps) by lane 0.
+template <int TY, int RPW>
+__device__ __forceinline__ void cls_count_rows(unsigned int* bm, int r0, int lane) {
+    const unsigned char* hb = reinterpret_cast<const unsigned char*>(bm + 2 * (TY + 2));
+    unsigned int* dh = bm + 2 * (TY + 2) + (TY + 3) / 4;
+    uint32_t cnt[10] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    if (lane < RPW) {
+        const int r = r0 + lane;
+        const uint32_t E = bm[r + 1], O = bm[TY + 3 + r];
+        const uint32_t h = hb[r];
+        // even column 2l: left = odd 2l - 1 (the x-halo for l = 0), right = odd 2l
+        cls_count32(E, (O << 1) | (h & 1u), O, bm[r], bm[r + 2], cnt);
+        // odd column 2l + 1: left = even 2l, right = even 2l + 2 (the x-halo for l = 31)
+        cls_count32(O, E, (E >> 1) | ((h >> 1) << 31), bm[TY + 2 + r], bm[TY + 4 + r], cnt);
+    }
+#pragma unroll
+    for (int b = 0; b < 10; ++b) {
+        const uint32_t t = __reduce_add_sync(0xffffffffu, cnt[b]);
+        if (lane == 0 && t) atomicAdd(&dh[b], t);
     }
 }
 
@@ -732,6 +756,11 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
     if (tid < NBUF) { mbar_init(&bar[tid], 1); armed[tid] = 0u; }
     if constexpr (CLS)
         for (int i = tid; i < NG * 32; i += NT) ghist[i] = 0u;
+    if constexpr (BMC)
+        for (int i = tid; i < NG * 2 * 17; i += NT) {   // deferred counts: bins 0, tile -1
+            unsigned int* dh = cbm + (i / 17) * CBMW + 2 * (TY + 2) + (TY + 3) / 4;
+            dh[i % 17] = i % 17 == 16 ? ~0u : 0u;
+        }
     if (tid == 0) {
         cs[0] = 0u;
         cs[30] = cs[31] = 0u;   // CLS: tile visits per path
@@ -1091,6 +1120,17 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
             }
         }
         ACA_TRACE(6, k);
+        if constexpr (BMC) {
+            // The classes of the group's previous visit (bitmap set par ^ 1, final since that
+            // visit's closing barrier) are counted now, by every warp for its own rows, in the
+            // time it would otherwise wait at this visit's closing barrier; the group's thread 0
+            // writes them to HBM after that barrier. This visit's set is marked for the next one.
+            unsigned int* pb = cbm + (gid * 2 + (par ^ 1)) * CBMW;
+            if (pb[2 * (TY + 2) + (TY + 3) / 4 + 16] != ~0u) cls_count_rows<TY, NCELL / NWG / TX>(pb, wg * (NCELL / NWG / TX), lane);
+            if (gt == 0)
+                cbm[(gid * 2 + par) * CBMW + 2 * (TY + 2) + (TY + 3) / 4 + 16] =
+                    (fast && o.valid) ? (unsigned int)tile_index(o) : ~0u;
+        }
         // refill the buffer with tile k + NBUF: armed before the barrier (the arrive does not
         // touch the buffer), copied after it by every thread of the group (at most a row each)
         if (gt == 0) {
@@ -1100,30 +1140,20 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         group_bar(1 + gid, NTG);   // the buffer is free
         ACA_TRACE(7, k);
         if constexpr (CLS) {   // the tile's class histogram of this visit -> HBM (and zeroed for reuse)
-            if (BMC && fast && o.valid) {
-#ifndef ACA_ABL_NOCOUNT
-                if (wg == 0) {   // warp 0 of the group: lane l counts rows l, l + 32, ...
-                    const unsigned int* bm = cbm + (gid * 2 + par) * CBMW;
-                    const unsigned char* hb = reinterpret_cast<const unsigned char*>(bm + 2 * (TY + 2));
-                    uint32_t cnt[10] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-                    for (int r = lane; r < TY; r += 32) {
-                        const uint32_t E = bm[r + 1], O = bm[TY + 3 + r];
-                        const uint32_t h = hb[r];
-                        // even column 2l: left = odd 2l - 1 (the x-halo for l = 0), right = odd 2l
-                        cls_count32(E, (O << 1) | (h & 1u), O, bm[r], bm[r + 2], cnt);
-                        // odd column 2l + 1: left = even 2l, right = even 2l + 2 (the x-halo for l = 31)
-                        cls_count32(O, E, (E >> 1) | ((h >> 1) << 31), bm[TY + 2 + r], bm[TY + 4 + r], cnt);
-                    }
-                    uint32_t tot[16];
+            if (BMC && gt == 0) {   // the previous visit's deferred histogram (counted before this barrier)
+                unsigned int* dh = cbm + (gid * 2 + (par ^ 1)) * CBMW + 2 * (TY + 2) + (TY + 3) / 4;
+                if (dh[16] != ~0u) {
+                    uint4* hp = reinterpret_cast<uint4*>(P.tile_hist + 16 * (size_t)dh[16]);
 #pragma unroll
-                    for (int b = 0; b < 16; ++b) tot[b] = b < 10 ? __reduce_add_sync(0xffffffffu, cnt[b]) : 0u;
-                    if (lane == 0) {
-                        uint4* hp = reinterpret_cast<uint4*>(P.tile_hist + 16 * tile_index(o));
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) hp[j] = make_uint4(tot[4 * j], tot[4 * j + 1], tot[4 * j + 2], tot[4 * j + 3]);
+                    for (int j = 0; j < 4; ++j) {
+                        hp[j] = make_uint4(dh[4 * j], dh[4 * j + 1], dh[4 * j + 2], dh[4 * j + 3]);
+                        dh[4 * j] = dh[4 * j + 1] = dh[4 * j + 2] = dh[4 * j + 3] = 0u;
                     }
+                    dh[16] = ~0u;
                 }
-#endif
+            }
+            if (BMC && fast && o.valid) {
+                // counted during the group's next visit (or after the loop)
             } else if (gt == 0 && o.valid) {
                 unsigned int* gh = ghist + (gid * 2 + par) * 16;
                 uint4* hp = reinterpret_cast<uint4*>(P.tile_hist + 16 * tile_index(o));
@@ -1138,6 +1168,17 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
         if (k + NBUF < K) copy_rows(k + NBUF, gt, NTG);
     }
     ACA_TRACE(8, 0);
+    if constexpr (BMC) {   // the group's last visit: count its set (par ^ 1) and write it
+        unsigned int* pb = cbm + (gid * 2 + (par ^ 1)) * CBMW;
+        unsigned int* dh = pb + 2 * (TY + 2) + (TY + 3) / 4;
+        if (dh[16] != ~0u) cls_count_rows<TY, NCELL / NWG / TX>(pb, wg * (NCELL / NWG / TX), lane);
+        group_bar(1 + gid, NTG);
+        if (gt == 0 && dh[16] != ~0u) {
+            uint4* hp = reinterpret_cast<uint4*>(P.tile_hist + 16 * (size_t)dh[16]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) hp[j] = make_uint4(dh[4 * j], dh[4 * j + 1], dh[4 * j + 2], dh[4 * j + 3]);
+        }
+    }
     __syncthreads();
     if (P.lag_q && tid == 0 && lagw[0] != ~0ull) atomicMin(&P.ctl->wmin[P.phase > 0 ? 1 : 0], lagw[0]);
     const unsigned long long s_act = block_sum<NT>((unsigned long long)active, red);
