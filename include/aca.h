@@ -78,7 +78,7 @@ typedef struct {
                                    tile is chosen by the library (512 threads when a launch has
                                    fewer than two tiles per SM). Environment switches for
                                    ablations only: ACA_TILE_NT, ACA_BULK, ACA_EFF_STREAM,
-                                   ACA_NO_RES, ACA_RES_NT, ACA_NO_TMA_BOX; for tests only:
+                                   ACA_NO_RES, ACA_RES_NT, ACA_NO_TMA_BOX, ACA_TMA_PROMO; for tests only:
                                    ACA_NB_CAP=b caps the counter field at b bits (the words'
                                    high halves then tie often: exercises the exact passes). */
     int32_t early_reject;       /* 1: a cell may also commit arrivals that are rejected for

@@ -409,8 +409,17 @@ void encode_tile_box(aca_sim* S, Shard& sh) {
     cuuint32_t estr[3] = {1, 1, 1};
     if (box[0] > 256 || box[1] > 256 || box[2] > 256) return;
     auto enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    // L2 fetch granule of the box loads: 64 B. The box's rows start 16 B before a tile row (the
+    // 2-word x halo), so a 256 B granule fetched 2 x 240 B of the neighbours per row that no tile
+    // of the launch uses (c3: 1.88 -> 1.37 GB of DRAM reads per launch, +1.4 %; r02g promo A/B)
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    if (const char* e = getenv("ACA_TMA_PROMO")) {   // ablation: 0 (none), 64, 128, 256
+        const int v = atoi(e);
+        promo = v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    }
     CUresult r = enc(&sh.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, (cuuint32_t)nd, sh.words, dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     sh.box_ok = r == CUDA_SUCCESS ? 1 : 0;
 }
