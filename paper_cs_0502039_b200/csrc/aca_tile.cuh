@@ -50,6 +50,9 @@ __host__ __device__ constexpr size_t grp_smem_bytes(int ndim, int tx, int ty, in
            (cls ? (size_t)ng * 2 * (16 + cls_bm_words(ndim, tx, ty)) * 4 : 0);
 }
 
+// compile-time flag for generic lambdas (one copy of a loop per value)
+template <bool B> struct BoolC { static constexpr bool value = B; };
+
 // a10 per-tile class bookkeeping: the BKL class (s, Sigma) of the cell pair (sl, sl + 1) of a
 // tile buffer (words v), from the spins of its neighbours in the buffer, added to the per-lane
 // class counters (8-bit fields: bins 0-7 in c0, 8-13 in c1; bin = (Sigma + z)/2 + (z + 1)(s + 1)/2
@@ -1043,37 +1046,48 @@ __global__ void __launch_bounds__(NTG * NG, 1) tile_grp_kernel(const __grid_cons
                 const int wb0 = wg * CPW;
                 const unsigned long long wT = lagw[1];   // T (termination counts cells below it)
                 unsigned long long wm = ~0ull;
+                // the lag minimum only when a lag window is set: two copies of the loop in the a10
+                // kernels (c5 +1.1 %), the runtime test in the plain ones (c3: the copies cost
+                // 0.4-1.2 %; r02g A/B)
                 const bool lag = P.lag_q != 0;
-                for (int idx = lane; idx < CPW / 2; idx += 32) {
-                    const int oo = wb0 + 2 * idx;
-                    const int lx = oo % TX, ly = (oo / TX) % TY, lz = oo / (TX * TY);
-                    const size_t gi = NDIM == 2 ? (size_t)(o.y0 + ly) * g.nx + o.x0 + lx
-                                                : ((size_t)(o.z0 + lz) * g.ny + (o.y0 + ly)) * g.nx + o.x0 + lx;
-                    const ulonglong2 v = lds128v(&S[slot(lx, ly, lz)]);
-                    if constexpr (BMC) {   // spin bits of the row's even / odd columns
-                        const unsigned int be = __ballot_sync(0xffffffffu, (unsigned int)v.x & 1u);
-                        const unsigned int bo = __ballot_sync(0xffffffffu, (unsigned int)v.y & 1u);
-                        if (lane == 0) {
-                            unsigned int* bm = cbm + (gid * 2 + par) * CBMW;
-                            bm[ly + 1] = be;
-                            bm[TY + 2 + ly + 1] = bo;
+                auto write_back = [&](auto LAGC) {
+                    for (int idx = lane; idx < CPW / 2; idx += 32) {
+                        const int oo = wb0 + 2 * idx;
+                        const int lx = oo % TX, ly = (oo / TX) % TY, lz = oo / (TX * TY);
+                        const size_t gi = NDIM == 2 ? (size_t)(o.y0 + ly) * g.nx + o.x0 + lx
+                                                    : ((size_t)(o.z0 + lz) * g.ny + (o.y0 + ly)) * g.nx + o.x0 + lx;
+                        const ulonglong2 v = lds128v(&S[slot(lx, ly, lz)]);
+                        if constexpr (BMC) {   // spin bits of the row's even / odd columns
+                            const unsigned int be = __ballot_sync(0xffffffffu, (unsigned int)v.x & 1u);
+                            const unsigned int bo = __ballot_sync(0xffffffffu, (unsigned int)v.y & 1u);
+                            if (lane == 0) {
+                                unsigned int* bm = cbm + (gid * 2 + par) * CBMW;
+                                bm[ly + 1] = be;
+                                bm[TY + 2 + ly + 1] = bo;
+                            }
+                        } else if constexpr (CLS) {
+                            cls_pair<NDIM, SX, SXY>(S, slot(lx, ly, lz), v, c0, c1);
                         }
-                    } else if constexpr (CLS) {
-                        cls_pair<NDIM, SX, SXY>(S, slot(lx, ly, lz), v, c0, c1);
-                    }
-                    ACA_CHECK(gi + 1 < (size_t)g.nx * g.ny * g.nz, gi, oo);
-                    *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
-                    active += (v.x < wT) + (v.y < wT);
-                    if (lag) wm = min(wm, min(v.x, v.y));
-                    if (P.push_lo) {
-                        const int a = NDIM == 2 ? o.y0 + ly : o.z0 + lz, n = NDIM == 2 ? g.ny : g.nz;
-                        if (a == 0 || a == n - 1) {
-                            const size_t f = NDIM == 2 ? (size_t)(o.x0 + lx) : (size_t)(o.y0 + ly) * g.nx + o.x0 + lx;
-                            *reinterpret_cast<ulonglong2*>((a == 0 ? P.push_lo : P.push_hi) + f) = v;
-                            if (a == 0 && n == 1) *reinterpret_cast<ulonglong2*>(P.push_hi + f) = v;
+                        ACA_CHECK(gi + 1 < (size_t)g.nx * g.ny * g.nz, gi, oo);
+                        *reinterpret_cast<ulonglong2*>(P.words + gi) = v;
+                        active += (v.x < wT) + (v.y < wT);
+                        if constexpr (EARLY != 0) {
+                            if constexpr (decltype(LAGC)::value) wm = min(wm, min(v.x, v.y));
+                        } else {
+                            if (lag) wm = min(wm, min(v.x, v.y));
+                        }
+                        if (P.push_lo) {
+                            const int a = NDIM == 2 ? o.y0 + ly : o.z0 + lz, n = NDIM == 2 ? g.ny : g.nz;
+                            if (a == 0 || a == n - 1) {
+                                const size_t f = NDIM == 2 ? (size_t)(o.x0 + lx) : (size_t)(o.y0 + ly) * g.nx + o.x0 + lx;
+                                *reinterpret_cast<ulonglong2*>((a == 0 ? P.push_lo : P.push_hi) + f) = v;
+                                if (a == 0 && n == 1) *reinterpret_cast<ulonglong2*>(P.push_hi + f) = v;
+                            }
                         }
                     }
-                }
+                };
+                if (EARLY == 0 || lag) write_back(BoolC<true>{});
+                else write_back(BoolC<false>{});
                 if (P.lag_q) atomicMin(&lagw[0], wm);
                 if constexpr (BMC) {   // the x-halo spins of the warp's rows; the face rows
                     unsigned int* bm = cbm + (gid * 2 + par) * CBMW;
