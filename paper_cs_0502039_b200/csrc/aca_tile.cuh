@@ -311,12 +311,23 @@ __device__ __forceinline__ unsigned int tile_rounds(const KParams& P, unsigned l
             const ulonglong2 up = lds128a(sa0 - 8u * SX);
             unsigned int uh0 = hi32(up.x), uh1 = hi32(up.y);
             ulonglong2 a = lds128a(sa0);
+// the left / right neighbours' high halves: two 32-bit shared loads at a 16-byte stride (4-way
+// bank conflicts: 4 wavefronts each), or (ACA_SHFL_LR, ablation) the neighbour lanes' registers
+// by shuffle, the tile's halo columns loaded by lanes 0 and 31 only
+#ifdef ACA_SHFL_LR
+#define ACA_LR_HALVES                                                                                \
+        unsigned int lh = __shfl_up_sync(0xffffffffu, ah1, 1), rh = __shfl_down_sync(0xffffffffu, ah0, 1); \
+        if (lane == 0) lh = lds32a(ar - 4u);                                                         \
+        if (lane == 31) rh = lds32a(ar + 20u);
+#else
+#define ACA_LR_HALVES const unsigned int lh = lds32a(ar - 4u), rh = lds32a(ar + 20u);
+#endif
 #define ACA_PAIR_ROWS(TEST)                                                                          \
     _Pragma("unroll") for (int rr = 0; rr < RPW; ++rr) {                                             \
         const uint32_t ar = sa0 + 8u * SX * (uint32_t)rr;                                            \
         const ulonglong2 b = lds128a(ar + 8u * SX); /* row rr + 1 (the halo row for the last) */     \
-        const unsigned int lh = lds32a(ar - 4u), rh = lds32a(ar + 20u);                              \
         const unsigned int ah0 = hi32(a.x), ah1 = hi32(a.y);                                         \
+        ACA_LR_HALVES                                                                                \
         const unsigned int m0 = min(min(lh, ah1), min(uh0, hi32(b.x)));                              \
         const unsigned int m1 = min(min(ah0, rh), min(uh1, hi32(b.y)));                              \
         TEST;                                                                                        \
